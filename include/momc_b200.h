@@ -1,0 +1,99 @@
+/*
+ * momc_b200.h — C-ABI of the B200 (sm_100a) hot path of momc (arXiv 2604.26477).
+ *
+ * Plain C: pointers and sizes only, no C++/torch types. Implemented in
+ * paper_2604_26477_b200/csrc/capi.cu, built into paper_2604_26477_b200/libmomc_b200.so.
+ * The reference (/root/reference/proj/include/momc) is a header-only C++ library with no
+ * FFI; each entry point below replaces the reference function cited beside it, and
+ * include/momc_b200/momc_b200.hpp re-exports those functions with the reference's exact
+ * C++ signatures on top of this ABI.
+ *
+ * Conventions
+ *   - Return 0 on success, MOMC_EUSAGE (2) where the reference throws
+ *     std::invalid_argument, MOMC_ERUNTIME (1) where it throws anything else (numerical
+ *     failure, CUDA error). `err` (may be NULL) receives the reference's message text.
+ *   - "host" buffers are ordinary CPU memory; "_dev" entry points take device pointers
+ *     on the context's device and run on the context's stream (asynchronous unless noted).
+ *   - Spin configurations are packed exactly like momc::SamplePool (solver.hpp:288-297):
+ *     wpc = ceil(n/64) uint64 words per config, bit b of word b/64 set iff s_b = +1.
+ *   - Objective values are cut values (maximised), K doubles per vector, row-major.
+ */
+#ifndef MOMC_B200_H
+#define MOMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOMC_OK 0
+#define MOMC_ERUNTIME 1
+#define MOMC_EUSAGE 2
+
+typedef struct momc_ctx momc_ctx; /* one device + one stream + resident buffers */
+
+/* momc::SolverConfig (solver.hpp:46-67); `threads` is accepted and ignored. */
+typedef struct {
+    int variant; /* 0 bsb, 1 dsb, 2 simcim (SolverVariant, solver.hpp:26) */
+    int n_iterations;
+    double dt, a0, alpha;
+    int batch_size;
+    double init_scale;
+    uint64_t seed;
+    int threads;
+} momc_solver_cfg;
+
+/* momc::MultiObjectiveInstance (instance.hpp:102-172) as flat host arrays:
+ * m edges (edge_i[e] < edge_j[e]), weights row-major m x k. */
+typedef struct {
+    int n, k, m;
+    const int32_t* edge_i;
+    const int32_t* edge_j;
+    const double* w;
+} momc_instance_view;
+
+/* ---------------------------------------------------------------- context */
+int momc_b200_ctx_create(int device, momc_ctx** out, char* err, size_t errlen);
+void momc_b200_ctx_destroy(momc_ctx* ctx);
+int momc_b200_ctx_sync(momc_ctx* ctx, char* err, size_t errlen);
+/* the cudaStream_t the context launches on (for external events / NCCL) */
+void* momc_b200_ctx_stream(momc_ctx* ctx);
+/* number of kernel launches issued by this context since creation */
+long long momc_b200_ctx_launches(momc_ctx* ctx);
+
+/* Upload / validate the instance (MultiObjectiveInstance ctor checks, instance.hpp:104-123)
+ * and build the CSR graph on the device. */
+int momc_b200_set_instance(momc_ctx* ctx, const momc_instance_view* inst, char* err, size_t errlen);
+
+/* Upload L interior weight vectors (numerators, row-major L x k, denominator H) and
+ * scalarise every one on the device: build_block_system / scalarize
+ * (scalarize.hpp:22-39, :62-71). Fails with MOMC_EUSAGE and the reference's message on a
+ * degenerate normalisation. Synchronous. */
+int momc_b200_set_weights(momc_ctx* ctx, const int32_t* nums, int L, int H, char* err, size_t errlen);
+/* copy J(c_l) (dense n x n, row-major) and c0 of weight l to host (tests) */
+int momc_b200_get_coupling(momc_ctx* ctx, int l, double* J, double* c0, char* err, size_t errlen);
+
+/* ---------------------------------------------------------------- sampler (solver.hpp) */
+/* run_sampler (solver.hpp:439-529) over the resident instance and weights for the
+ * flattened task range [block_begin, block_end) of (run, weight, 128-trajectory chunk)
+ * blocks (block_end < 0: all runs*L*ceil(batch/128) blocks). The pool stays on the
+ * device in canonical order; timings: [0] sampling seconds (device events). */
+int momc_b200_sample(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long long block_begin,
+                     long long block_end, double* seconds, char* err, size_t errlen);
+/* pool geometry and copies: size = runs*L*batch configs */
+long long momc_b200_pool_size(momc_ctx* ctx);
+int momc_b200_pool_get(momc_ctx* ctx, uint64_t* words, int64_t* stamps_ns, char* err, size_t errlen);
+const uint64_t* momc_b200_pool_device(momc_ctx* ctx);
+
+/* Host-to-host drop-in for run_sampler: instance + weights + sample + copy back. */
+int momc_b200_run_sampler(momc_ctx* ctx, const momc_instance_view* inst, const int32_t* nums, int L, int H,
+                          const momc_solver_cfg* cfg, int runs, uint64_t* out_words, int64_t* out_stamps_ns,
+                          double* out_seconds /* [model_construction, sampling] */, char* err, size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOMC_B200_H */

@@ -1,0 +1,87 @@
+"""ctypes loader of the in-tree CUDA library (libmomc_b200.so) and its C-ABI signatures.
+
+There is no CPU fallback: importing the product API without the built library, or
+creating a context without a B200, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libmomc_b200.so")
+
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+i64p = C.POINTER(C.c_int64)
+i32p = C.POINTER(C.c_int32)
+dp = C.POINTER(C.c_double)
+vp = C.c_void_p
+
+
+class SolverCfgC(C.Structure):
+    """momc_solver_cfg (include/momc_b200.h) == momc::SolverConfig (solver.hpp:46-67)."""
+
+    _fields_ = [
+        ("variant", C.c_int),
+        ("n_iterations", C.c_int),
+        ("dt", C.c_double),
+        ("a0", C.c_double),
+        ("alpha", C.c_double),
+        ("batch_size", C.c_int),
+        ("init_scale", C.c_double),
+        ("seed", C.c_uint64),
+        ("threads", C.c_int),
+    ]
+
+
+class InstanceViewC(C.Structure):
+    """momc_instance_view (include/momc_b200.h)."""
+
+    _fields_ = [
+        ("n", C.c_int),
+        ("k", C.c_int),
+        ("m", C.c_int),
+        ("edge_i", i32p),
+        ("edge_j", i32p),
+        ("w", dp),
+    ]
+
+
+# (name, restype, argtypes) for every symbol declared in include/momc_b200.h
+SIGNATURES = [
+    ("momc_b200_ctx_create", C.c_int, [C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
+    ("momc_b200_ctx_destroy", None, [vp]),
+    ("momc_b200_ctx_sync", C.c_int, [vp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_ctx_stream", vp, [vp]),
+    ("momc_b200_ctx_launches", C.c_longlong, [vp]),
+    ("momc_b200_set_instance", C.c_int, [vp, C.POINTER(InstanceViewC), C.c_char_p, C.c_size_t]),
+    ("momc_b200_set_weights", C.c_int, [vp, i32p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
+    ("momc_b200_get_coupling", C.c_int, [vp, C.c_int, dp, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_sample", C.c_int, [vp, C.POINTER(SolverCfgC), C.c_int, C.c_longlong, C.c_longlong, dp,
+                                   C.c_char_p, C.c_size_t]),
+    ("momc_b200_pool_size", C.c_longlong, [vp]),
+    ("momc_b200_pool_get", C.c_int, [vp, u64p, i64p, C.c_char_p, C.c_size_t]),
+    ("momc_b200_pool_device", vp, [vp]),
+    ("momc_b200_run_sampler", C.c_int, [vp, C.POINTER(InstanceViewC), i32p, C.c_int, C.c_int,
+                                        C.POINTER(SolverCfgC), C.c_int, u64p, i64p, dp, C.c_char_p, C.c_size_t]),
+]
+
+_lib = None
+
+
+def load():
+    """Load libmomc_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the momc_b200 path has no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

@@ -1,0 +1,558 @@
+// C-ABI (include/momc_b200.h): context, instance, scalarisation, sampler entry points.
+// Host-side orchestration only; all per-sample arithmetic runs in the kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/momc_b200.h"
+#include "ctx.cuh"
+#include "sampler.cuh"
+
+using namespace momc_b200;
+
+struct momc_ctx : Ctx {};
+
+namespace momc_b200 {
+
+Ctx::~Ctx()
+{
+    for (auto* b : {&d_ei, &d_ej, &d_rowptr, &d_col, &d_eidx, &d_wi, &d_nums, &d_nan, &d_badstep}) b->release();
+    for (auto* b : {&d_w, &d_vals, &d_c0, &d_dense, &d_gx, &d_gy, &d_gxn, &d_gnoise}) b->release();
+    d_zig.release();
+    d_words.release();
+    d_block_end.release();
+    d_t0.release();
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+namespace {
+
+void put_err(char* err, size_t errlen, const char* msg)
+{
+    if (err && errlen) {
+        std::strncpy(err, msg, errlen - 1);
+        err[errlen - 1] = 0;
+    }
+}
+
+template <class F>
+int guarded(char* err, size_t errlen, F&& f)
+{
+    try {
+        f();
+        return MOMC_OK;
+    } catch (const ApiError& e) {
+        put_err(err, errlen, e.what());
+        return e.code;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return MOMC_ERUNTIME;
+    }
+}
+
+// rng.hpp:62-89 ZigguratTables, same libm calls in the same order (bit-identical tables).
+ZigTables host_ziggurat()
+{
+    ZigTables z;
+    const double m1 = 2147483648.0;
+    const double vn = 9.91256303526217e-3;
+    double dn = 3.442619855899, tn = dn;
+    const double q = vn / std::exp(-0.5 * dn * dn);
+    z.kn[0] = static_cast<uint32_t>((dn / q) * m1);
+    z.kn[1] = 0;
+    z.wn[0] = q / m1;
+    z.wn[127] = dn / m1;
+    z.fn[0] = 1.0;
+    z.fn[127] = std::exp(-0.5 * dn * dn);
+    for (int i = 126; i >= 1; --i) {
+        dn = std::sqrt(-2.0 * std::log(vn / dn + std::exp(-0.5 * dn * dn)));
+        z.kn[i + 1] = static_cast<uint32_t>((dn / tn) * m1);
+        tn = dn;
+        z.fn[i] = std::exp(-0.5 * dn * dn);
+        z.wn[i] = dn / m1;
+    }
+    return z;
+}
+
+// ---- K1 scalarise (scalarize.hpp:22-39), one CTA per weight vector
+__global__ void scalarize_kernel(int n, int k, int nnz, int H, const int* __restrict__ nums, const double* __restrict__ w,
+                                 const int* __restrict__ rowptr, const int* __restrict__ eidx, double* vals,
+                                 double* rowsum_scratch, double* c0, int* degenerate)
+{
+    const int l = blockIdx.x;
+    const int* num = nums + static_cast<long long>(l) * k;
+    double* v = vals + static_cast<long long>(l) * nnz;
+    for (int s = threadIdx.x; s < nnz; s += blockDim.x) {
+        const int e = eidx[s];
+        double acc = 0;  // `double w = 0; for k: w += c[k] * e.w[k]`, c[k] = num_k / H
+        for (int q = 0; q < k; ++q)
+            acc = __dadd_rn(acc, __dmul_rn(__ddiv_rn(static_cast<double>(num[q]), static_cast<double>(H)),
+                                           w[static_cast<long long>(e) * k + q]));
+        v[s] = acc;
+    }
+    __syncthreads();
+    double* rs = rowsum_scratch + static_cast<long long>(l) * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double s = 0.0;  // J.rowwise().sum(): j ascending (zeros of the dense row are exact no-ops)
+        for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) s = __dadd_rn(s, v[e]);
+        rs[i] = fabs(s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // .cwiseAbs().maxCoeff() as the running fold m = max(m, a_i) from a_0
+        double m = rs[0];
+        for (int i = 1; i < n; ++i) m = (m < rs[i]) ? rs[i] : m;
+        if (!(m > 0.0) || !isfinite(m)) {
+            degenerate[l] = 1;
+            c0[l] = 0.0;
+        } else {
+            degenerate[l] = 0;
+            c0[l] = __ddiv_rn(1.0, m);
+        }
+    }
+}
+
+__global__ void densify_kernel(int n, int nnz, const int* __restrict__ rowptr, const int* __restrict__ col,
+                               const double* __restrict__ vals, double* dense)
+{
+    const int l = blockIdx.y;
+    const int i = blockIdx.x;
+    double* row = dense + (static_cast<long long>(l) * n + i) * n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) row[j] = 0.0;
+    __syncthreads();
+    for (int e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x)
+        row[col[e]] = vals[static_cast<long long>(l) * nnz + e];
+}
+
+__global__ void stamp_t0(unsigned long long* t0)
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *t0 = t;
+}
+
+__global__ void first_flag(const int* __restrict__ flags, long long count, unsigned long long* first)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        if (flags[i]) atomicMin(first, static_cast<unsigned long long>(i));
+}
+
+void validate_cfg(const momc_solver_cfg* c)
+{  // SolverConfig::validate (solver.hpp:57-66)
+    if (c->n_iterations < 1) usage("n_iterations must be >= 1");
+    if (!(c->dt > 0.0)) usage("dt must be positive");
+    if (!(c->a0 > 0.0)) usage("a0 must be positive");
+    if (c->alpha < 0.0) usage("alpha must be non-negative");
+    if (c->batch_size < 1) usage("batch_size must be >= 1");
+    if (c->init_scale < 0.0) usage("init_scale must be non-negative");
+    if (c->threads < 0) usage("threads must be non-negative");
+    if (c->variant < 0 || c->variant > 2) usage("unknown solver variant");
+}
+
+void set_instance(Ctx& c, const momc_instance_view* iv)
+{
+    // MultiObjectiveInstance ctor (instance.hpp:104-123)
+    if (iv->n < 1) usage("vertex count must be positive");
+    if (iv->k < 1) usage("objective count must be positive");
+    if (iv->m < 0) usage("edge count must be non-negative");
+    std::unordered_set<long long> seen;
+    seen.reserve(static_cast<size_t>(iv->m) * 2 + 1);
+    for (int e = 0; e < iv->m; ++e) {
+        const int i = iv->edge_i[e], j = iv->edge_j[e];
+        if (i == j) usage("self-loop edge");
+        if (i < 0 || j < 0 || i >= iv->n || j >= iv->n || i >= j) usage("edge endpoints must satisfy 0 <= i < j < n");
+        if (!seen.insert(static_cast<long long>(i) * iv->n + j).second) usage("duplicate edge");
+    }
+    c.n = iv->n;
+    c.k = iv->k;
+    c.m = iv->m;
+    c.h_ei.assign(iv->edge_i, iv->edge_i + iv->m);
+    c.h_ej.assign(iv->edge_j, iv->edge_j + iv->m);
+    c.h_w.assign(iv->w, iv->w + static_cast<size_t>(iv->m) * iv->k);
+    // exact-integer cut path: all weights integral, |sum| < 2^31 per layer
+    bool integral = true;
+    std::vector<double> absum(static_cast<size_t>(c.k), 0.0);
+    for (int e = 0; e < c.m; ++e)
+        for (int q = 0; q < c.k; ++q) {
+            const double v = c.h_w[static_cast<size_t>(e) * c.k + q];
+            if (!(std::floor(v) == v) || !std::isfinite(v)) integral = false;
+            absum[static_cast<size_t>(q)] += std::fabs(v);
+        }
+    for (double a : absum)
+        if (!(a < 2147483647.0)) integral = false;
+    c.integer_weights = integral;
+    // CSR of the symmetric graph, rows i, columns ascending; eidx maps a slot to its edge
+    c.nnz = 2 * c.m;
+    std::vector<int> deg(static_cast<size_t>(c.n) + 1, 0);
+    for (int e = 0; e < c.m; ++e) {
+        ++deg[static_cast<size_t>(c.h_ei[e])];
+        ++deg[static_cast<size_t>(c.h_ej[e])];
+    }
+    std::vector<int> rowptr(static_cast<size_t>(c.n) + 1, 0);
+    for (int i = 0; i < c.n; ++i) rowptr[static_cast<size_t>(i) + 1] = rowptr[static_cast<size_t>(i)] + deg[static_cast<size_t>(i)];
+    std::vector<std::vector<std::pair<int, int>>> rows(static_cast<size_t>(c.n));
+    for (int e = 0; e < c.m; ++e) {
+        rows[static_cast<size_t>(c.h_ei[e])].push_back({c.h_ej[e], e});
+        rows[static_cast<size_t>(c.h_ej[e])].push_back({c.h_ei[e], e});
+    }
+    std::vector<int> col(static_cast<size_t>(c.nnz)), eidx(static_cast<size_t>(c.nnz));
+    for (int i = 0; i < c.n; ++i) {
+        auto& r = rows[static_cast<size_t>(i)];
+        std::sort(r.begin(), r.end());
+        for (size_t q = 0; q < r.size(); ++q) {
+            col[static_cast<size_t>(rowptr[static_cast<size_t>(i)]) + q] = r[q].first;
+            eidx[static_cast<size_t>(rowptr[static_cast<size_t>(i)]) + q] = r[q].second;
+        }
+    }
+    const size_t mk = static_cast<size_t>(c.m) * c.k;
+    c.d_ei.reserve(static_cast<size_t>(c.m));
+    c.d_ej.reserve(static_cast<size_t>(c.m));
+    c.d_w.reserve(mk);
+    c.d_rowptr.reserve(static_cast<size_t>(c.n) + 1);
+    c.d_col.reserve(static_cast<size_t>(c.nnz));
+    c.d_eidx.reserve(static_cast<size_t>(c.nnz));
+    ck(cudaMemcpyAsync(c.d_ei.p, c.h_ei.data(), sizeof(int) * c.m, cudaMemcpyHostToDevice, c.stream), "H2D");
+    ck(cudaMemcpyAsync(c.d_ej.p, c.h_ej.data(), sizeof(int) * c.m, cudaMemcpyHostToDevice, c.stream), "H2D");
+    ck(cudaMemcpyAsync(c.d_w.p, c.h_w.data(), sizeof(double) * mk, cudaMemcpyHostToDevice, c.stream), "H2D");
+    if (integral) {
+        std::vector<int> wi(mk);
+        for (size_t q = 0; q < mk; ++q) wi[q] = static_cast<int>(c.h_w[q]);
+        c.d_wi.reserve(mk);
+        ck(cudaMemcpyAsync(c.d_wi.p, wi.data(), sizeof(int) * mk, cudaMemcpyHostToDevice, c.stream), "H2D");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    }
+    ck(cudaMemcpyAsync(c.d_rowptr.p, rowptr.data(), sizeof(int) * (c.n + 1), cudaMemcpyHostToDevice, c.stream), "H2D");
+    ck(cudaMemcpyAsync(c.d_col.p, col.data(), sizeof(int) * c.nnz, cudaMemcpyHostToDevice, c.stream), "H2D");
+    ck(cudaMemcpyAsync(c.d_eidx.p, eidx.data(), sizeof(int) * c.nnz, cudaMemcpyHostToDevice, c.stream), "H2D");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    c.L = 0;  // weights must be re-scalarised against the new instance
+}
+
+void set_weights(Ctx& c, const int32_t* nums, int L, int H)
+{
+    if (c.n == 0) usage("no instance set");
+    if (L < 1) usage("block system needs at least one weight vector");
+    if (H < 1) usage("lattice resolution must be positive");
+    for (int l = 0; l < L; ++l) {  // WeightVector ctor (weights.hpp:28-40)
+        long long s = 0;
+        for (int q = 0; q < c.k; ++q) {
+            if (nums[static_cast<size_t>(l) * c.k + q] < 0) usage("weight numerators must be non-negative");
+            s += nums[static_cast<size_t>(l) * c.k + q];
+        }
+        if (s != H) usage("weight numerators must sum to the resolution");
+    }
+    c.L = L;
+    c.H = H;
+    c.d_nums.reserve(static_cast<size_t>(L) * c.k);
+    c.d_vals.reserve(static_cast<size_t>(L) * (c.nnz ? c.nnz : 1));
+    c.d_c0.reserve(static_cast<size_t>(L));
+    DevBuf<double> rs;
+    rs.reserve(static_cast<size_t>(L) * c.n);
+    DevBuf<int> degen;
+    degen.reserve(static_cast<size_t>(L));
+    ck(cudaMemcpyAsync(c.d_nums.p, nums, sizeof(int) * L * c.k, cudaMemcpyHostToDevice, c.stream), "H2D");
+    scalarize_kernel<<<L, 256, 0, c.stream>>>(c.n, c.k, c.nnz, H, c.d_nums.p, c.d_w.p, c.d_rowptr.p, c.d_eidx.p,
+                                              c.d_vals.p, rs.p, c.d_c0.p, degen.p);
+    ++c.launches;
+    ck(cudaGetLastError(), "scalarize_kernel");
+    std::vector<int> h_degen(static_cast<size_t>(L));
+    ck(cudaMemcpyAsync(h_degen.data(), degen.p, sizeof(int) * L, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    rs.release();
+    degen.release();
+    for (int l = 0; l < L; ++l) {
+        if (h_degen[static_cast<size_t>(l)]) {
+            c.L = 0;
+            usage("degenerate scalarized coupling: normalization undefined");
+        }
+    }
+    if (c.n > 64) {  // generic path consumes the dense blocks
+        c.d_dense.reserve(static_cast<size_t>(L) * c.n * c.n);
+        densify_kernel<<<dim3(static_cast<unsigned>(c.n), static_cast<unsigned>(L)), 128, 0, c.stream>>>(
+            c.n, c.nnz, c.d_rowptr.p, c.d_col.p, c.d_vals.p, c.d_dense.p);
+        ++c.launches;
+        ck(cudaGetLastError(), "densify_kernel");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    }
+}
+
+void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, long long b_end, double* seconds)
+{
+    validate_cfg(cfg);
+    if (c.n == 0) usage("no instance set");
+    if (c.L < 1) usage("run_sampler needs at least one weight vector");
+    if (runs < 1) usage("runs must be >= 1");
+    const int batch = cfg->batch_size;
+    const int chunks = (batch + kSampleBlock - 1) / kSampleBlock;
+    const long long total_blocks = static_cast<long long>(runs) * c.L * chunks;
+    if (b_end < 0 || b_end > total_blocks) b_end = total_blocks;
+    if (b_begin < 0 || b_begin > b_end) usage("invalid block range");
+    const long long nblocks = b_end - b_begin;
+    const int wpc = (c.n + 63) / 64;
+    c.pool_size = static_cast<long long>(runs) * c.L * batch;
+    c.pool_runs = runs;
+    c.pool_batch = batch;
+    c.pool_block_begin = b_begin;
+    c.pool_blocks = nblocks;
+    c.d_words.reserve(static_cast<size_t>(c.pool_size) * wpc);
+    c.d_nan.reserve(static_cast<size_t>(nblocks) + 1);
+    c.d_badstep.reserve(static_cast<size_t>(nblocks) + 1);
+    c.d_block_end.reserve(static_cast<size_t>(nblocks) + 1);
+    c.d_t0.reserve(2);
+    if (!c.d_zig.p) {
+        c.d_zig.reserve(1);
+        const ZigTables z = host_ziggurat();
+        ck(cudaMemcpyAsync(c.d_zig.p, &z, sizeof z, cudaMemcpyHostToDevice, c.stream), "H2D");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    }
+    ck(cudaMemsetAsync(c.d_nan.p, 0, sizeof(int) * (nblocks + 1), c.stream), "memset");
+    ck(cudaMemsetAsync(c.d_block_end.p, 0, sizeof(unsigned long long) * (nblocks + 1), c.stream), "memset");
+
+    SamplerParams p{};
+    p.n = c.n;
+    p.nnz = c.nnz;
+    p.T = cfg->n_iterations;
+    p.variant = cfg->variant;
+    p.dt = cfg->dt;
+    p.a0 = cfg->a0;
+    p.alpha = cfg->alpha;
+    p.init_scale = cfg->init_scale;
+    p.s_dt_a0 = cfg->dt * cfg->a0;
+    p.L = c.L;
+    p.batch = batch;
+    p.runs = runs;
+    p.chunks = chunks;
+    p.block_begin = b_begin;
+    p.seed = cfg->seed;
+    p.row_ptr = c.d_rowptr.p;
+    p.col = c.d_col.p;
+    p.vals = c.d_vals.p;
+    p.c0 = c.d_c0.p;
+    p.dense = c.d_dense.p;
+    p.zig = c.d_zig.p;
+    p.words = c.d_words.p;
+    p.block_end_ns = c.d_block_end.p;
+    p.nan_block = c.d_nan.p;
+    p.first_bad_step_task = -1;
+    p.bad_step = c.d_badstep.p;
+
+    GenericScratch g{};
+    if (c.n > 64) {
+        long long cap = std::min<long long>(nblocks, 4096) * kSampleBlock;
+        if (cap < kSampleBlock) cap = kSampleBlock;
+        c.d_gx.reserve(static_cast<size_t>(cap) * c.n);
+        c.d_gy.reserve(static_cast<size_t>(cap) * c.n);
+        c.d_gxn.reserve(static_cast<size_t>(cap) * c.n);
+        c.d_gnoise.reserve(static_cast<size_t>(cap) * c.n);
+        g = GenericScratch{c.d_gx.p, c.d_gy.p, c.d_gxn.p, c.d_gnoise.p, cap};
+    }
+
+    stamp_t0<<<1, 1, 0, c.stream>>>(c.d_t0.p);
+    ++c.launches;
+    ck(cudaEventRecord(c.ev0, c.stream), "event");
+    if (nblocks > 0) {
+        const int rc = c.n <= 64 ? launch_sampler(p, nblocks, c.stream, 0) : launch_sampler_generic(p, nblocks, g, c.stream);
+        ck(static_cast<cudaError_t>(rc), "sampler launch");
+        c.launches += c.n <= 64 ? 1 : 2 + (long long)p.T * (cfg->alpha > 0 ? 2 : 1);
+    }
+    ck(cudaEventRecord(c.ev1, c.stream), "event");
+    // numerical failure (solver.hpp:138-143, :503-523): NaN is sticky through the wall and
+    // the clamp, so a final-state scan finds every failing trajectory; the step index is
+    // recovered by re-running the first failing 512-trajectory task with per-step checks.
+    DevBuf<unsigned long long> first;
+    first.reserve(1);
+    const unsigned long long none = ~0ull;
+    ck(cudaMemcpyAsync(first.p, &none, sizeof none, cudaMemcpyHostToDevice, c.stream), "H2D");
+    first_flag<<<64, 256, 0, c.stream>>>(c.d_nan.p, nblocks, first.p);
+    ++c.launches;
+    unsigned long long h_first = none;
+    ck(cudaMemcpyAsync(&h_first, first.p, sizeof h_first, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "sampler");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c.ev0, c.ev1), "event");
+    if (seconds) seconds[0] = ms * 1e-3;
+    first.release();
+    if (h_first != none) {
+        const long long gb = b_begin + static_cast<long long>(h_first);
+        const int chunk128 = static_cast<int>(gb % chunks);
+        const long long rl = gb / chunks;
+        const int l = static_cast<int>(rl % c.L), run = static_cast<int>(rl / c.L);
+        const int c512 = chunk128 / 4;
+        const long long rb = rl * chunks + 4ll * c512;
+        const long long re = std::min<long long>(rl * chunks + chunks, rb + 4);
+        SamplerParams q = p;
+        q.block_begin = rb;
+        q.first_bad_step_task = 1;
+        q.block_end_ns = nullptr;
+        ck(cudaMemsetAsync(c.d_badstep.p, 0x7f, sizeof(int) * (re - rb), c.stream), "memset");
+        // scratch outputs so the pool / flags of the real run are untouched
+        DevBuf<uint64_t> wtmp;
+        wtmp.reserve(static_cast<size_t>(c.pool_size) * wpc);
+        DevBuf<int> ntmp;
+        ntmp.reserve(static_cast<size_t>(re - rb));
+        q.words = wtmp.p;
+        q.nan_block = ntmp.p;
+        const int rc = c.n <= 64 ? launch_sampler(q, re - rb, c.stream, 1) : launch_sampler_generic(q, re - rb, g, c.stream);
+        ck(static_cast<cudaError_t>(rc), "sampler debug launch");
+        std::vector<int> bs(static_cast<size_t>(re - rb));
+        ck(cudaMemcpyAsync(bs.data(), c.d_badstep.p, sizeof(int) * (re - rb), cudaMemcpyDeviceToHost, c.stream), "D2H");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+        int step = *std::min_element(bs.begin(), bs.end());
+        runtime("numerical failure at step " + std::to_string(step) + " (run " + std::to_string(run) + ", weight " +
+                std::to_string(l) + ")");
+    }
+}
+
+void pool_get(Ctx& c, uint64_t* words, int64_t* stamps)
+{
+    const int wpc = (c.n + 63) / 64;
+    if (words)
+        ck(cudaMemcpyAsync(words, c.d_words.p, sizeof(uint64_t) * c.pool_size * wpc, cudaMemcpyDeviceToHost, c.stream),
+           "D2H");
+    if (stamps) {
+        std::vector<unsigned long long> be(static_cast<size_t>(c.pool_blocks) + 1);
+        unsigned long long t0 = 0;
+        ck(cudaMemcpyAsync(be.data(), c.d_block_end.p, sizeof(unsigned long long) * c.pool_blocks,
+                           cudaMemcpyDeviceToHost, c.stream),
+           "D2H");
+        ck(cudaMemcpyAsync(&t0, c.d_t0.p, sizeof t0, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+        const int chunks = (c.pool_batch + kSampleBlock - 1) / kSampleBlock;
+        for (long long i = 0; i < c.pool_size; ++i) stamps[i] = 0;
+        for (long long b = 0; b < c.pool_blocks; ++b) {
+            const long long gb = c.pool_block_begin + b;
+            const int chunk = static_cast<int>(gb % chunks);
+            const long long rl = gb / chunks;
+            const long long base = rl * c.pool_batch + static_cast<long long>(chunk) * kSampleBlock;
+            const long long stamp = be[static_cast<size_t>(b)] > t0 ? static_cast<long long>(be[static_cast<size_t>(b)] - t0) : 0;
+            for (int t = 0; t < kSampleBlock && chunk * kSampleBlock + t < c.pool_batch; ++t) stamps[base + t] = stamp;
+        }
+    }
+    ck(cudaStreamSynchronize(c.stream), "sync");
+}
+
+}  // namespace
+}  // namespace momc_b200
+
+extern "C" {
+
+int momc_b200_ctx_create(int device, momc_ctx** out, char* err, size_t errlen)
+{
+    *out = nullptr;
+    return guarded(err, errlen, [&] {
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1)
+            runtime("no CUDA device available: the momc_b200 path has no CPU fallback");
+        if (device < 0 || device >= count) usage("device index out of range");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10) runtime("momc_b200 is built for sm_100a (B200); device is sm_" +
+                                      std::to_string(prop.major) + std::to_string(prop.minor));
+        auto* c = new momc_ctx();
+        c->device = device;
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreate(&c->ev0), "event");
+        ck(cudaEventCreate(&c->ev1), "event");
+        *out = c;
+    });
+}
+
+void momc_b200_ctx_destroy(momc_ctx* ctx) { delete ctx; }
+
+int momc_b200_ctx_sync(momc_ctx* ctx, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] { ck(cudaStreamSynchronize(ctx->stream), "sync"); });
+}
+
+void* momc_b200_ctx_stream(momc_ctx* ctx) { return ctx->stream; }
+long long momc_b200_ctx_launches(momc_ctx* ctx) { return ctx->launches; }
+
+int momc_b200_set_instance(momc_ctx* ctx, const momc_instance_view* inst, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        set_instance(*ctx, inst);
+    });
+}
+
+int momc_b200_set_weights(momc_ctx* ctx, const int32_t* nums, int L, int H, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        set_weights(*ctx, nums, L, H);
+    });
+}
+
+int momc_b200_get_coupling(momc_ctx* ctx, int l, double* J, double* c0, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        if (l < 0 || l >= ctx->L) usage("weight index out of range");
+        const int n = ctx->n, nnz = ctx->nnz;
+        std::vector<double> v(static_cast<size_t>(nnz));
+        std::vector<int> rp(static_cast<size_t>(n) + 1), col(static_cast<size_t>(nnz));
+        ck(cudaMemcpyAsync(v.data(), ctx->d_vals.p + static_cast<size_t>(l) * nnz, sizeof(double) * nnz,
+                           cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaMemcpyAsync(rp.data(), ctx->d_rowptr.p, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaMemcpyAsync(col.data(), ctx->d_col.p, sizeof(int) * nnz, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaMemcpyAsync(c0, ctx->d_c0.p + l, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        std::fill(J, J + static_cast<size_t>(n) * n, 0.0);
+        for (int i = 0; i < n; ++i)
+            for (int e = rp[static_cast<size_t>(i)]; e < rp[static_cast<size_t>(i) + 1]; ++e)
+                J[static_cast<size_t>(i) * n + col[static_cast<size_t>(e)]] = v[static_cast<size_t>(e)];
+    });
+}
+
+int momc_b200_sample(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long long block_begin, long long block_end,
+                     double* seconds, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        sample(*ctx, cfg, runs, block_begin, block_end, seconds);
+    });
+}
+
+long long momc_b200_pool_size(momc_ctx* ctx) { return ctx->pool_size; }
+
+int momc_b200_pool_get(momc_ctx* ctx, uint64_t* words, int64_t* stamps_ns, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] { pool_get(*ctx, words, stamps_ns); });
+}
+
+const uint64_t* momc_b200_pool_device(momc_ctx* ctx) { return ctx->d_words.p; }
+
+int momc_b200_run_sampler(momc_ctx* ctx, const momc_instance_view* inst, const int32_t* nums, int L, int H,
+                          const momc_solver_cfg* cfg, int runs, uint64_t* out_words, int64_t* out_stamps_ns,
+                          double* out_seconds, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        validate_cfg(cfg);
+        if (L < 1) usage("run_sampler needs at least one weight vector");
+        if (runs < 1) usage("runs must be >= 1");
+        const auto t0 = std::chrono::steady_clock::now();
+        set_instance(*ctx, inst);
+        set_weights(*ctx, nums, L, H);
+        const auto t1 = std::chrono::steady_clock::now();
+        double s = 0;
+        sample(*ctx, cfg, runs, 0, -1, &s);
+        pool_get(*ctx, out_words, out_stamps_ns);
+        const auto t2 = std::chrono::steady_clock::now();
+        if (out_seconds) {
+            out_seconds[0] = std::chrono::duration<double>(t1 - t0).count();
+            out_seconds[1] = std::chrono::duration<double>(t2 - t1).count();
+        }
+    });
+}
+
+}  // extern "C"

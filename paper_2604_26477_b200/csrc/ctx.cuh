@@ -1,0 +1,82 @@
+// Context object behind momc_b200.h: one device, one stream, resident device buffers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rng.cuh"
+
+namespace momc_b200 {
+
+// Error carrying the C-ABI code (2 = usage / std::invalid_argument, 1 = runtime).
+struct ApiError : std::runtime_error {
+    int code;
+    ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void usage(const std::string& m) { throw ApiError(2, m); }
+[[noreturn]] inline void runtime(const std::string& m) { throw ApiError(1, m); }
+
+inline void ck(cudaError_t e, const char* what)
+{
+    if (e != cudaSuccess) runtime(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+// Growable device buffer.
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;  // elements
+    void reserve(size_t n)
+    {
+        if (n <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        ck(cudaMalloc(&p, sizeof(T) * (n ? n : 1)), "cudaMalloc");
+        cap = n;
+    }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    long long launches = 0;
+
+    // instance
+    int n = 0, k = 0, m = 0, nnz = 0;
+    bool integer_weights = false;  // every weight integral and sum |w| < 2^31 (exact int32 cut path)
+    std::vector<int> h_ei, h_ej;
+    std::vector<double> h_w;
+    DevBuf<int> d_ei, d_ej, d_rowptr, d_col, d_eidx;
+    DevBuf<double> d_w;
+    DevBuf<int> d_wi;  // integer weights (m x k) when integer_weights
+
+    // weights / scalarisation
+    int L = 0, H = 0;
+    DevBuf<int> d_nums;
+    DevBuf<double> d_vals, d_c0, d_dense;
+    DevBuf<ZigTables> d_zig;
+
+    // pool
+    long long pool_size = 0;
+    int pool_runs = 0, pool_batch = 0;
+    long long pool_block_begin = 0, pool_blocks = 0;
+    DevBuf<uint64_t> d_words;
+    DevBuf<int> d_nan, d_badstep;
+    DevBuf<unsigned long long> d_block_end, d_t0;
+    DevBuf<double> d_gx, d_gy, d_gxn, d_gnoise;  // generic-n scratch
+
+    ~Ctx();
+};
+
+}  // namespace momc_b200

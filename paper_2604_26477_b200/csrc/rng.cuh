@@ -1,0 +1,122 @@
+// Device-side counter RNG: bit-exact restatement of momc::rng (rng.hpp) for sm_100a.
+//
+//   philox4x32_10   rng.hpp:22-38   (Random123 Philox4x32-10; round keys are warp-uniform)
+//   derive_key      rng.hpp:54-57   (SplitMix64 finaliser mix64, rng.hpp:42-50)
+//   stream ids      rng.hpp:107-111 counter = {block#, id_lo, id_mid, id_hi}
+//   u01 / symmetric rng.hpp:131-146 (u64 >> 11) * 2^-53, h * (2u - 1)
+//   normal          rng.hpp:156-185 128-layer ziggurat; tables are computed on the host by
+//                   the same libm calls as rng.hpp:62-89 and uploaded (bit-identical).
+// No cuRAND: its Philox state layout differs from the reference's counter layout.
+#pragma once
+#include <cstdint>
+
+namespace momc_b200 {
+
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
+constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kWeyl0 = 0x9E3779B9u;
+constexpr uint32_t kWeyl1 = 0xBB67AE85u;
+
+constexpr uint32_t kTagInitX = 1, kTagInitY = 2, kTagStepNoise = 3, kTagEdgePresence = 4,
+                   kTagEdgeWeight = 5, kTagReferenceSample = 8;
+
+__host__ __device__ __forceinline__ uint32_t tag_word(uint32_t tag, uint32_t step)
+{
+    return (tag << 26) | (step & 0x03FFFFFFu);
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z)
+{
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+__host__ __device__ __forceinline__ uint64_t derive_key(uint64_t seed, uint64_t ctx)
+{
+    return mix64(seed + 0x9E3779B97F4A7C15ull) ^ mix64(ctx * 0x9E3779B97F4A7C15ull + 1);
+}
+
+// solver.hpp:98-104
+__host__ __device__ __forceinline__ uint64_t run_key(uint64_t seed, uint32_t run)
+{
+    return derive_key(derive_key(seed, 0x736F6C76u), run);
+}
+
+// One Philox4x32-10 block. ctr = {c0 (block#), c1 (id_lo), c2 (id_mid), c3 (id_hi)}.
+__device__ __forceinline__ uint4 philox(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
+                                        uint32_t c3)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = static_cast<uint64_t>(kPhiloxM0) * c0;
+        const uint64_t p1 = static_cast<uint64_t>(kPhiloxM1) * c2;
+        const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ (k0 + kWeyl0 * r);
+        const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ (k1 + kWeyl1 * r);
+        c1 = static_cast<uint32_t>(p1);
+        c3 = static_cast<uint32_t>(p0);
+        c0 = n0;
+        c2 = n2;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+__device__ __forceinline__ double u01_from(uint32_t lo, uint32_t hi)
+{
+    const uint64_t v = (static_cast<uint64_t>(hi) << 32) | lo;
+    return static_cast<double>(v >> 11) * 0x1.0p-53;
+}
+__device__ __forceinline__ double u01_open_from(uint32_t lo, uint32_t hi)
+{
+    const uint64_t v = (static_cast<uint64_t>(hi) << 32) | lo;
+    return static_cast<double>((v >> 11) + 1) * 0x1.0p-53;
+}
+
+// Sequential reader of one reference Stream (rng.hpp:113-121), for the cold paths.
+struct DevStream {
+    uint32_t k0, k1, lo, mid, hi;
+    uint32_t block;  // next block index to generate
+    uint32_t buf[4];
+    int pos;
+    __device__ __forceinline__ void init(uint64_t key, uint32_t id_hi, uint32_t id_mid, uint32_t id_lo)
+    {
+        k0 = static_cast<uint32_t>(key);
+        k1 = static_cast<uint32_t>(key >> 32);
+        hi = id_hi;
+        mid = id_mid;
+        lo = id_lo;
+        block = 0;
+        pos = 4;
+    }
+    __device__ __forceinline__ uint32_t next_u32()
+    {
+        if (pos == 4) {
+            const uint4 b = philox(k0, k1, block, lo, mid, hi);
+            buf[0] = b.x;
+            buf[1] = b.y;
+            buf[2] = b.z;
+            buf[3] = b.w;
+            ++block;
+            pos = 0;
+        }
+        return buf[pos++];
+    }
+    __device__ __forceinline__ uint64_t next_u64()
+    {
+        const uint64_t a = next_u32();
+        const uint64_t b = next_u32();
+        return a | (b << 32);
+    }
+};
+
+// Ziggurat tables (rng.hpp:62-89), uploaded from the host.
+struct ZigTables {
+    uint32_t kn[128];
+    double wn[128];
+    double fn[128];
+};
+
+}  // namespace momc_b200

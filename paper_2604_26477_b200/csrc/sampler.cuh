@@ -1,0 +1,51 @@
+// Batched noise-injected SB sampler (bSB / dSB / SimCIM) on sm_100a.
+// Restates momc::run_sampler (solver.hpp:439-529) / integrate_block (:221-234) /
+// sb_step (:152-183) / simcim_step (:188-214) / init_state (:108-124) /
+// fill_step_noise (:128-136) / read_spins (:237-244), FP64, in the reference's exact
+// per-element operation order (no FMA contraction), so final spins are bit-identical
+// to the oracle build of the reference.
+#pragma once
+#include <cstdint>
+
+#include "rng.cuh"
+
+namespace momc_b200 {
+
+constexpr int kSampleBlock = 128;  // trajectories per CTA (one per thread)
+
+struct SamplerParams {
+    int n;            // spins
+    int nnz;          // CSR entries (2m)
+    int T;            // n_iterations
+    int variant;      // 0 bsb, 1 dsb, 2 simcim
+    double dt, a0, alpha, init_scale, s_dt_a0;  // s_dt_a0 = dt * a0 (host-rounded, solver.hpp:176)
+    int L, batch, runs, chunks;                 // chunks = ceil(batch / kSampleBlock)
+    long long block_begin;                      // first flattened (run, weight, chunk) block
+    uint64_t seed;
+    const int* row_ptr;       // n + 1
+    const int* col;           // nnz, ascending within a row
+    const double* vals;       // L * nnz, J(c_l) in CSR order
+    const double* c0;         // L
+    const double* dense;      // L * n * n row-major J(c_l) (generic path only)
+    const ZigTables* zig;
+    uint64_t* words;          // (runs * L * batch) * wpc, canonical order
+    unsigned long long* block_end_ns;  // per launched block (optional)
+    int* nan_block;           // per launched block: 1 if any trajectory went non-finite
+    int first_bad_step_task;  // debug rerun: -1, else records first bad step per block
+    int* bad_step;            // per launched block: min first non-finite step (debug rerun)
+};
+
+// Launch the register-resident path (n <= 64) or the generic path; returns a CUDA error.
+int launch_sampler(const SamplerParams& p, long long nblocks, void* stream, int check_steps);
+
+// Generic-n state buffers (x, y, noise) are owned by the caller.
+struct GenericScratch {
+    double* x;      // [chunk_traj][n]
+    double* y;
+    double* xn;     // next x (double buffer)
+    double* noise;  // [chunk_traj][n]
+    long long cap_traj;
+};
+int launch_sampler_generic(const SamplerParams& p, long long nblocks, const GenericScratch& g, void* stream);
+
+}  // namespace momc_b200

@@ -1,0 +1,213 @@
+// Generic-n SB sampler (n > 64): state in HBM, one wave of 128-trajectory blocks at a time.
+// Same arithmetic contract as the register-resident kernel (sampler_impl.cuh): dense
+// J(c_l) row i summed over j = 0..n-1 in order from +0.0 with separately rounded
+// products (the shim GEMM order, oracle/eigen_shim/Eigen/Dense), then the sb_step /
+// simcim_step element update (solver.hpp:167-179, :199-210).
+// Layout of the state buffers: [spin i][wave trajectory] so that every per-spin access
+// across a warp is a coalesced 256-B line.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "sampler.cuh"
+
+namespace momc_b200 {
+
+namespace {
+
+struct WaveCtx {
+    SamplerParams p;
+    long long wave_block0;  // first block (relative to p.block_begin) of this wave
+    long long wave_blocks;
+    long long W;            // wave_blocks * kSampleBlock
+};
+
+__device__ __forceinline__ void decode(const WaveCtx& w, long long wt, int& run, int& l, int& traj, bool& active)
+{
+    const long long gblock = w.p.block_begin + w.wave_block0 + wt / kSampleBlock;
+    const int chunk = static_cast<int>(gblock % w.p.chunks);
+    const long long rl = gblock / w.p.chunks;
+    l = static_cast<int>(rl % w.p.L);
+    run = static_cast<int>(rl / w.p.L);
+    traj = chunk * kSampleBlock + static_cast<int>(wt % kSampleBlock);
+    active = traj < w.p.batch;
+}
+
+__global__ void gen_init(WaveCtx w, double* x, double* y)
+{
+    const long long wt = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (wt >= w.W) return;
+    int run, l, traj;
+    bool active;
+    decode(w, wt, run, l, traj, active);
+    if (!active) return;
+    const uint64_t key = run_key(w.p.seed, static_cast<uint32_t>(run));
+    DevStream sx, sy;
+    sx.init(key, l, traj, tag_word(kTagInitX, 0));
+    sy.init(key, l, traj, tag_word(kTagInitY, 0));
+    const double h = w.p.init_scale;
+    for (int i = 0; i < w.p.n; ++i) {
+        const uint64_t v = sx.next_u64();
+        const double u = static_cast<double>(v >> 11) * 0x1.0p-53;
+        x[i * w.W + wt] = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, u), 1.0));
+    }
+    for (int i = 0; i < w.p.n; ++i) {
+        const uint64_t v = sy.next_u64();
+        const double u = static_cast<double>(v >> 11) * 0x1.0p-53;
+        y[i * w.W + wt] = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, u), 1.0));
+    }
+}
+
+// rng.hpp:156-185 over a DevStream (sequential; this path is not throughput-critical)
+__device__ double normal_seq(DevStream& s, const ZigTables* __restrict__ z)
+{
+    for (;;) {
+        const uint32_t u = s.next_u32();
+        const int32_t hz = static_cast<int32_t>(u);
+        const uint32_t iz = u & 127u;
+        const uint32_t mag = hz < 0 ? static_cast<uint32_t>(-static_cast<int64_t>(hz)) : static_cast<uint32_t>(hz);
+        if (mag < z->kn[iz]) return __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        if (iz == 0) {
+            const double r = 3.442619855899;
+            for (;;) {
+                const uint64_t a = s.next_u64();
+                const double x = __ddiv_rn(-log(static_cast<double>((a >> 11) + 1) * 0x1.0p-53), r);
+                const uint64_t b = s.next_u64();
+                const double y = -log(static_cast<double>((b >> 11) + 1) * 0x1.0p-53);
+                if (__dadd_rn(y, y) >= __dmul_rn(x, x)) return hz > 0 ? __dadd_rn(r, x) : -__dadd_rn(r, x);
+            }
+        }
+        const double x = __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        const uint64_t a = s.next_u64();
+        const double u01 = static_cast<double>(a >> 11) * 0x1.0p-53;
+        if (__dadd_rn(z->fn[iz], __dmul_rn(u01, __dsub_rn(z->fn[iz - 1], z->fn[iz]))) <
+            exp(__dmul_rn(__dmul_rn(-0.5, x), x)))
+            return x;
+    }
+}
+
+__global__ void gen_noise(WaveCtx w, int t, double* noise)
+{
+    const long long wt = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (wt >= w.W) return;
+    int run, l, traj;
+    bool active;
+    decode(w, wt, run, l, traj, active);
+    if (!active) return;
+    DevStream s;
+    s.init(run_key(w.p.seed, static_cast<uint32_t>(run)), l, traj, tag_word(kTagStepNoise, static_cast<uint32_t>(t)));
+    for (int i = 0; i < w.p.n; ++i) noise[i * w.W + wt] = normal_seq(s, w.p.zig);
+}
+
+// grid: (wave_blocks, n); block: 128 trajectories of one (run, weight); thread = (spin i, traj)
+__global__ void gen_step(WaveCtx w, int t, const double* __restrict__ x, double* __restrict__ xn, double* y,
+                         const double* __restrict__ noise)
+{
+    const long long wb = blockIdx.x;
+    const int i = blockIdx.y;
+    const long long wt = wb * kSampleBlock + threadIdx.x;
+    int run, l, traj;
+    bool active;
+    decode(w, wt, run, l, traj, active);
+    if (!active) return;
+    const int n = w.p.n;
+    const double* Jrow = w.p.dense + (static_cast<long long>(l) * n + i) * n;
+    const bool dsb = w.p.variant == 1;
+    double coupled = 0.0;
+    for (int j = 0; j < n; ++j) {
+        const double xj = x[j * w.W + wt];
+        const double phi = dsb ? (xj < 0.0 ? -1.0 : 1.0) : xj;
+        coupled = __dadd_rn(coupled, __dmul_rn(Jrow[j], phi));
+    }
+    const double c0 = w.p.c0[l];
+    const double a_t = __ddiv_rn(static_cast<double>(t + 1), static_cast<double>(w.p.T));
+    const bool noisy = w.p.alpha > 0.0;
+    const double eta = noisy ? noise[i * w.W + wt] : 0.0;
+    double xi = x[i * w.W + wt];
+    double yi = y[i * w.W + wt];
+    if (w.p.variant == 2) {
+        const double pump = __dmul_rn(-0.5, __dsub_rn(1.0, a_t));
+        double d = __dsub_rn(__dmul_rn(pump, xi), __dmul_rn(c0, coupled));
+        if (noisy) d = __dadd_rn(d, __dmul_rn(w.p.alpha, eta));
+        yi = __dadd_rn(__dmul_rn(0.9, yi), __dmul_rn(1.0 - 0.9, d));
+        xi = __dadd_rn(xi, __dmul_rn(w.p.dt, yi));
+    } else {
+        const double neg_drift = -__dsub_rn(w.p.a0, a_t);
+        double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled));
+        if (noisy) d = __dadd_rn(d, __dmul_rn(w.p.alpha, eta));
+        yi = __dadd_rn(yi, __dmul_rn(w.p.dt, d));
+        xi = __dadd_rn(xi, __dmul_rn(w.p.s_dt_a0, yi));
+        yi = fabs(xi) > 1.0 ? 0.0 : yi;
+    }
+    xi = (xi < -1.0) ? -1.0 : xi;
+    xi = (1.0 < xi) ? 1.0 : xi;
+    xn[i * w.W + wt] = xi;
+    y[i * w.W + wt] = yi;
+    if (w.p.first_bad_step_task >= 0 && (!isfinite(xi) || !isfinite(yi)))
+        atomicMin(&w.p.bad_step[w.wave_block0 + wb], t + 1);
+}
+
+__global__ void gen_readout(WaveCtx w, const double* __restrict__ x)
+{
+    const long long wt = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (wt >= w.W) return;
+    int run, l, traj;
+    bool active;
+    decode(w, wt, run, l, traj, active);
+    if (!active) return;
+    const int n = w.p.n;
+    const int wpc = (n + 63) / 64;
+    const long long idx = (static_cast<long long>(run) * w.p.L + l) * w.p.batch + traj;
+    bool bad = false;
+    for (int wd = 0; wd < wpc; ++wd) {
+        uint64_t word = 0;
+        for (int b = 0; b < 64 && wd * 64 + b < n; ++b) {
+            const double v = x[(wd * 64 + b) * w.W + wt];
+            word |= static_cast<uint64_t>(!(v < 0.0)) << b;
+            bad |= v != v;
+        }
+        w.p.words[idx * wpc + wd] = word;
+    }
+    const long long blk = w.wave_block0 + wt / kSampleBlock;
+    if (bad) w.p.nan_block[blk] = 1;
+    if (w.p.block_end_ns && (threadIdx.x & 31) == 0) {
+        unsigned long long tnow;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+        atomicMax(&w.p.block_end_ns[blk], tnow);
+    }
+}
+
+}  // namespace
+
+int launch_sampler_generic(const SamplerParams& p, long long nblocks, const GenericScratch& g, void* stream)
+{
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const long long wave_cap = g.cap_traj / kSampleBlock;
+    if (wave_cap < 1) return cudaErrorInvalidValue;
+    for (long long b0 = 0; b0 < nblocks; b0 += wave_cap) {
+        WaveCtx w;
+        w.p = p;
+        w.wave_block0 = b0;
+        w.wave_blocks = nblocks - b0 < wave_cap ? nblocks - b0 : wave_cap;
+        w.W = w.wave_blocks * kSampleBlock;
+        const unsigned grid1 = static_cast<unsigned>((w.W + 127) / 128);
+        gen_init<<<grid1, 128, 0, st>>>(w, g.x, g.y);
+        double* xa = g.x;
+        double* xb = g.xn;
+        for (int t = 0; t < p.T; ++t) {
+            if (p.alpha > 0.0) gen_noise<<<grid1, 128, 0, st>>>(w, t, g.noise);
+            dim3 grid2(static_cast<unsigned>(w.wave_blocks), static_cast<unsigned>(p.n));
+            gen_step<<<grid2, kSampleBlock, 0, st>>>(w, t, xa, xb, g.y, g.noise);
+            double* tmp = xa;
+            xa = xb;
+            xb = tmp;
+        }
+        gen_readout<<<grid1, 128, 0, st>>>(w, xa);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace momc_b200
