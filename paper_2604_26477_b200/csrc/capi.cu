@@ -23,7 +23,7 @@ namespace momc_b200 {
 Ctx::~Ctx()
 {
     for (auto* b : {&d_ei, &d_ej, &d_rowptr, &d_col, &d_eidx, &d_wi, &d_nums, &d_nan, &d_badstep}) b->release();
-    for (auto* b : {&d_w, &d_vals, &d_c0, &d_dense, &d_gx, &d_gy, &d_gxn, &d_gnoise}) b->release();
+    for (auto* b : {&d_w, &d_vals, &d_c0, &d_padv, &d_gx, &d_gy, &d_gxn, &d_gnoise}) b->release();
     d_zig.release();
     d_words.release();
     d_block_end.release();
@@ -120,16 +120,16 @@ __global__ void scalarize_kernel(int n, int k, int nnz, int H, const int* __rest
     }
 }
 
-__global__ void densify_kernel(int n, int nnz, const int* __restrict__ rowptr, const int* __restrict__ col,
-                               const double* __restrict__ vals, double* dense)
+// rows of J(c_l) padded to `dmax` entries with exact zeros (sampler DMAX > 0 path)
+__global__ void pad_rows_kernel(int n, int nnz, int dmax, const int* __restrict__ rowptr,
+                                const double* __restrict__ vals, double* padv)
 {
-    const int l = blockIdx.y;
-    const int i = blockIdx.x;
-    double* row = dense + (static_cast<long long>(l) * n + i) * n;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) row[j] = 0.0;
-    __syncthreads();
-    for (int e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x)
-        row[col[e]] = vals[static_cast<long long>(l) * nnz + e];
+    const int l = blockIdx.x;
+    for (int s = threadIdx.x; s < n * dmax; s += blockDim.x) {
+        const int i = s / dmax, d = s % dmax;
+        const int e = rowptr[i] + d;
+        padv[static_cast<long long>(l) * n * dmax + s] = e < rowptr[i + 1] ? vals[static_cast<long long>(l) * nnz + e] : 0.0;
+    }
 }
 
 __global__ void stamp_t0(unsigned long long* t0)
@@ -137,13 +137,6 @@ __global__ void stamp_t0(unsigned long long* t0)
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     *t0 = t;
-}
-
-__global__ void first_flag(const int* __restrict__ flags, long long count, unsigned long long* first)
-{
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < count;
-         i += static_cast<long long>(gridDim.x) * blockDim.x)
-        if (flags[i]) atomicMin(first, static_cast<unsigned long long>(i));
 }
 
 void validate_cfg(const momc_solver_cfg* c)
@@ -213,6 +206,16 @@ void set_instance(Ctx& c, const momc_instance_view* iv)
             eidx[static_cast<size_t>(rowptr[static_cast<size_t>(i)]) + q] = r[q].second;
         }
     }
+    int maxdeg = 0;
+    for (int i = 0; i < c.n; ++i) maxdeg = std::max(maxdeg, deg[static_cast<size_t>(i)]);
+    c.pad_dmax = (c.n <= 64 && maxdeg <= 3) ? 3 : 0;  // instantiated padded row length
+    c.h_pad_col.assign(64 * kMaxPadDeg, 0);
+    if (c.pad_dmax > 0) {
+        for (int i = 0; i < c.n; ++i)
+            for (int d = 0; d < c.pad_dmax; ++d)
+                c.h_pad_col[static_cast<size_t>(i * c.pad_dmax + d)] =
+                    d < deg[static_cast<size_t>(i)] ? col[static_cast<size_t>(rowptr[static_cast<size_t>(i)] + d)] : i;
+    }
     const size_t mk = static_cast<size_t>(c.m) * c.k;
     c.d_ei.reserve(static_cast<size_t>(c.m));
     c.d_ej.reserve(static_cast<size_t>(c.m));
@@ -275,12 +278,11 @@ void set_weights(Ctx& c, const int32_t* nums, int L, int H)
             usage("degenerate scalarized coupling: normalization undefined");
         }
     }
-    if (c.n > 64) {  // generic path consumes the dense blocks
-        c.d_dense.reserve(static_cast<size_t>(L) * c.n * c.n);
-        densify_kernel<<<dim3(static_cast<unsigned>(c.n), static_cast<unsigned>(L)), 128, 0, c.stream>>>(
-            c.n, c.nnz, c.d_rowptr.p, c.d_col.p, c.d_vals.p, c.d_dense.p);
+    if (c.pad_dmax > 0) {
+        c.d_padv.reserve(static_cast<size_t>(L) * c.n * c.pad_dmax);
+        pad_rows_kernel<<<L, 128, 0, c.stream>>>(c.n, c.nnz, c.pad_dmax, c.d_rowptr.p, c.d_vals.p, c.d_padv.p);
         ++c.launches;
-        ck(cudaGetLastError(), "densify_kernel");
+        ck(cudaGetLastError(), "pad_rows_kernel");
         ck(cudaStreamSynchronize(c.stream), "sync");
     }
 }
@@ -337,7 +339,9 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     p.col = c.d_col.p;
     p.vals = c.d_vals.p;
     p.c0 = c.d_c0.p;
-    p.dense = c.d_dense.p;
+    p.pad_vals = c.d_padv.p;
+    p.pad_dmax = c.pad_dmax;
+    std::copy(c.h_pad_col.begin(), c.h_pad_col.end(), p.pad_col);
     p.zig = c.d_zig.p;
     p.words = c.d_words.p;
     p.block_end_ns = c.d_block_end.p;
@@ -345,16 +349,17 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     p.first_bad_step_task = -1;
     p.bad_step = c.d_badstep.p;
 
-    GenericScratch g{};
-    if (c.n > 64) {
-        long long cap = std::min<long long>(nblocks, 4096) * kSampleBlock;
+    auto scratch = [&](long long blocks) {
+        long long cap = std::min<long long>(blocks, 4096) * kSampleBlock;
         if (cap < kSampleBlock) cap = kSampleBlock;
         c.d_gx.reserve(static_cast<size_t>(cap) * c.n);
         c.d_gy.reserve(static_cast<size_t>(cap) * c.n);
         c.d_gxn.reserve(static_cast<size_t>(cap) * c.n);
         c.d_gnoise.reserve(static_cast<size_t>(cap) * c.n);
-        g = GenericScratch{c.d_gx.p, c.d_gy.p, c.d_gxn.p, c.d_gnoise.p, cap};
-    }
+        return GenericScratch{c.d_gx.p, c.d_gy.p, c.d_gxn.p, c.d_gnoise.p, cap};
+    };
+    GenericScratch g{};
+    if (c.n > 64) g = scratch(nblocks);
 
     stamp_t0<<<1, 1, 0, c.stream>>>(c.d_t0.p);
     ++c.launches;
@@ -365,24 +370,42 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         c.launches += c.n <= 64 ? 1 : 2 + (long long)p.T * (cfg->alpha > 0 ? 2 : 1);
     }
     ck(cudaEventRecord(c.ev1, c.stream), "event");
-    // numerical failure (solver.hpp:138-143, :503-523): NaN is sticky through the wall and
-    // the clamp, so a final-state scan finds every failing trajectory; the step index is
-    // recovered by re-running the first failing 512-trajectory task with per-step checks.
-    DevBuf<unsigned long long> first;
-    first.reserve(1);
-    const unsigned long long none = ~0ull;
-    ck(cudaMemcpyAsync(first.p, &none, sizeof none, cudaMemcpyHostToDevice, c.stream), "H2D");
-    first_flag<<<64, 256, 0, c.stream>>>(c.d_nan.p, nblocks, first.p);
-    ++c.launches;
-    unsigned long long h_first = none;
-    ck(cudaMemcpyAsync(&h_first, first.p, sizeof h_first, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    // Per-block flags: bit 2 = the register path's noise-event buffer overflowed (re-run the
+    // block on the exact sequential path); bit 1 = some trajectory went non-finite.
+    std::vector<int> flags(static_cast<size_t>(nblocks));
+    if (nblocks > 0)
+        ck(cudaMemcpyAsync(flags.data(), c.d_nan.p, sizeof(int) * nblocks, cudaMemcpyDeviceToHost, c.stream), "D2H");
     ck(cudaStreamSynchronize(c.stream), "sampler");
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, c.ev0, c.ev1), "event");
+    bool refixed = false;
+    for (long long b = 0; b < nblocks; ++b) {
+        if (!(flags[static_cast<size_t>(b)] & 2)) continue;
+        if (!refixed) g = scratch(1);
+        refixed = true;
+        SamplerParams q = p;
+        q.block_begin = b_begin + b;
+        q.block_end_ns = nullptr;
+        q.nan_block = c.d_nan.p + b;
+        ck(cudaMemsetAsync(q.nan_block, 0, sizeof(int), c.stream), "memset");
+        ck(static_cast<cudaError_t>(launch_sampler_generic(q, 1, g, c.stream)), "sampler fallback");
+        c.launches += 3 + 2ll * p.T;
+        ck(cudaMemcpyAsync(&flags[static_cast<size_t>(b)], q.nan_block, sizeof(int), cudaMemcpyDeviceToHost, c.stream),
+           "D2H");
+    }
+    if (refixed) ck(cudaStreamSynchronize(c.stream), "sampler fallback");
     if (seconds) seconds[0] = ms * 1e-3;
-    first.release();
-    if (h_first != none) {
-        const long long gb = b_begin + static_cast<long long>(h_first);
+    // numerical failure (solver.hpp:138-143, :503-523): NaN is sticky through the wall and
+    // the clamp, so a final-state scan finds every failing trajectory; the step index is
+    // recovered by re-running the first failing 512-trajectory task with per-step checks.
+    long long h_first = -1;
+    for (long long b = 0; b < nblocks; ++b)
+        if (flags[static_cast<size_t>(b)] & 1) {
+            h_first = b;
+            break;
+        }
+    if (h_first >= 0) {
+        const long long gb = b_begin + h_first;
         const int chunk128 = static_cast<int>(gb % chunks);
         const long long rl = gb / chunks;
         const int l = static_cast<int>(rl % c.L), run = static_cast<int>(rl / c.L);
@@ -401,7 +424,8 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         ntmp.reserve(static_cast<size_t>(re - rb));
         q.words = wtmp.p;
         q.nan_block = ntmp.p;
-        const int rc = c.n <= 64 ? launch_sampler(q, re - rb, c.stream, 1) : launch_sampler_generic(q, re - rb, g, c.stream);
+        g = scratch(re - rb);  // the sequential path carries the per-step finiteness check
+        const int rc = launch_sampler_generic(q, re - rb, g, c.stream);
         ck(static_cast<cudaError_t>(rc), "sampler debug launch");
         std::vector<int> bs(static_cast<size_t>(re - rb));
         ck(cudaMemcpyAsync(bs.data(), c.d_badstep.p, sizeof(int) * (re - rb), cudaMemcpyDeviceToHost, c.stream), "D2H");

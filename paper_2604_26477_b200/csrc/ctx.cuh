@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "rng.cuh"
+#include "sampler.cuh"
 
 namespace momc_b200 {
 
@@ -64,7 +65,9 @@ struct Ctx {
     // weights / scalarisation
     int L = 0, H = 0;
     DevBuf<int> d_nums;
-    DevBuf<double> d_vals, d_c0, d_dense;
+    DevBuf<double> d_vals, d_c0, d_padv;
+    int pad_dmax = 0;               // padded row length of the register-resident sampler (0: CSR rows)
+    std::vector<int> h_pad_col;     // 64 * kMaxPadDeg padded column indices
     DevBuf<ZigTables> d_zig;
 
     // pool

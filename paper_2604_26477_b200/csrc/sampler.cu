@@ -9,10 +9,17 @@ int launch_sampler(const SamplerParams& p, long long nblocks, void* stream, int 
 {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int n = p.n;
-    if (n <= 16) return launch_small_n16(p, nblocks, st);
-    if (n <= 32) return launch_small_n32(p, nblocks, st);
-    if (n <= 42) return launch_small_n42(p, nblocks, st);
-    if (n <= 64) return launch_small_n64(p, nblocks, st);
+    if (p.pad_dmax == 3) {
+        if (n <= 16) return launch_small_n16_d3(p, nblocks, st);
+        if (n <= 32) return launch_small_n32_d3(p, nblocks, st);
+        if (n <= 42) return launch_small_n42_d3(p, nblocks, st);
+        if (n <= 64) return launch_small_n64_d3(p, nblocks, st);
+    } else {
+        if (n <= 16) return launch_small_n16_d0(p, nblocks, st);
+        if (n <= 32) return launch_small_n32_d0(p, nblocks, st);
+        if (n <= 42) return launch_small_n42_d0(p, nblocks, st);
+        if (n <= 64) return launch_small_n64_d0(p, nblocks, st);
+    }
     return cudaErrorInvalidValue;  // n > 64: launch_sampler_generic
 }
 

@@ -12,6 +12,7 @@
 namespace momc_b200 {
 
 constexpr int kSampleBlock = 128;  // trajectories per CTA (one per thread)
+constexpr int kMaxPadDeg = 4;      // max padded row length of the register-resident path
 
 struct SamplerParams {
     int n;            // spins
@@ -26,7 +27,9 @@ struct SamplerParams {
     const int* col;           // nnz, ascending within a row
     const double* vals;       // L * nnz, J(c_l) in CSR order
     const double* c0;         // L
-    const double* dense;      // L * n * n row-major J(c_l) (generic path only)
+    const double* pad_vals;   // L * n * DMAX: rows padded with exact zeros (DMAX > 0 path)
+    int pad_dmax;             // 0: runtime CSR rows; else the padded row length
+    int pad_col[64 * kMaxPadDeg];  // padded column indices (pad = the row's own index)
     const ZigTables* zig;
     uint64_t* words;          // (runs * L * batch) * wpc, canonical order
     unsigned long long* block_end_ns;  // per launched block (optional)
@@ -38,7 +41,8 @@ struct SamplerParams {
 // Launch the register-resident path (n <= 64) or the generic path; returns a CUDA error.
 int launch_sampler(const SamplerParams& p, long long nblocks, void* stream, int check_steps);
 
-// Generic-n state buffers (x, y, noise) are owned by the caller.
+// Generic path (any n; also the exact fallback for blocks flagged by the fast kernel).
+// State buffers (x, y, noise) are owned by the caller.
 struct GenericScratch {
     double* x;      // [chunk_traj][n]
     double* y;

@@ -1,8 +1,10 @@
-// Generic-n SB sampler (n > 64): state in HBM, one wave of 128-trajectory blocks at a time.
-// Same arithmetic contract as the register-resident kernel (sampler_impl.cuh): dense
-// J(c_l) row i summed over j = 0..n-1 in order from +0.0 with separately rounded
-// products (the shim GEMM order, oracle/eigen_shim/Eigen/Dense), then the sb_step /
-// simcim_step element update (solver.hpp:167-179, :199-210).
+// Generic-n SB sampler: state in HBM, one wave of 128-trajectory blocks at a time. Used
+// for n > 64 and as the exact sequential fallback for any block the register-resident
+// kernel flags (noise-stream event overflow). Same arithmetic contract as
+// sampler_impl.cuh: row i of J(c_l) summed over its CSR columns in ascending order from
+// +0.0 with separately rounded products (equal to the shim's dense k-ordered GEMM, since
+// the omitted zero products are exact no-ops), then the sb_step / simcim_step element
+// update (solver.hpp:167-179, :199-210); noise drawn sequentially per rng.hpp:156-185.
 // Layout of the state buffers: [spin i][wave trajectory] so that every per-spin access
 // across a warp is a coalesced 256-B line.
 #include <cuda_runtime.h>
@@ -111,14 +113,13 @@ __global__ void gen_step(WaveCtx w, int t, const double* __restrict__ x, double*
     bool active;
     decode(w, wt, run, l, traj, active);
     if (!active) return;
-    const int n = w.p.n;
-    const double* Jrow = w.p.dense + (static_cast<long long>(l) * n + i) * n;
+    const double* Jv = w.p.vals + static_cast<long long>(l) * w.p.nnz;
     const bool dsb = w.p.variant == 1;
     double coupled = 0.0;
-    for (int j = 0; j < n; ++j) {
-        const double xj = x[j * w.W + wt];
+    for (int e = w.p.row_ptr[i]; e < w.p.row_ptr[i + 1]; ++e) {
+        const double xj = x[w.p.col[e] * w.W + wt];
         const double phi = dsb ? (xj < 0.0 ? -1.0 : 1.0) : xj;
-        coupled = __dadd_rn(coupled, __dmul_rn(Jrow[j], phi));
+        coupled = __dadd_rn(coupled, __dmul_rn(Jv[e], phi));
     }
     const double c0 = w.p.c0[l];
     const double a_t = __ddiv_rn(static_cast<double>(t + 1), static_cast<double>(w.p.T));

@@ -1,16 +1,28 @@
 #pragma once
-// SB sampler kernel implementation (see sampler.cuh), included by sampler_n*.cu. Design:
-//   * one trajectory per thread, 128 trajectories of one (run, weight) per CTA;
-//   * x (and y for n <= 42) live in registers, fully unrolled over NMAX spins;
-//   * the coupling J(c_l) is a CSR row list in shared memory (broadcast reads); bSB/SimCIM
-//     gather phi(x_j) = x_j from a per-thread column of shared memory, dSB gathers
-//     sgn(x_j) from a 64-bit sign mask held in a register;
-//   * per step, the Philox blocks of the (trajectory, step) noise stream are generated
-//     up-front into shared memory (uniform work, no divergence), then the ziggurat
-//     consumes them sequentially (rng.hpp:156-185) in groups of 8 spins, each group
-//     immediately feeding its 8 spin updates;
-//   * every FP64 operation uses an explicitly rounded intrinsic (__dmul_rn/__dadd_rn/
-//     __dsub_rn) in the reference's order, so nvcc cannot contract into FMA.
+// SB sampler kernel implementation (see sampler.cuh), included by sampler_n*.cu.
+//
+// Design. A CTA integrates 128 trajectories of one (run, weight) with
+// 256 threads: the two lanes 2t, 2t+1 of a warp own trajectory t and each keeps half of
+// its spins (x, y) in registers, fully unrolled over NH = NMAX/2 spins. Halving the
+// per-thread state halves registers (4 warps per scheduler instead of 2) and the
+// unrolled code (the step loop fits the 32 KB L1.5 instruction cache; the first
+// version thrashed it). Per step t, the (trajectory, t) noise stream (solver.hpp:128-136)
+// is handled in three branch-light phases instead of the reference's sequential
+// next_normal():
+//   A1  the pair generates the Philox blocks of the stream (even blocks on lane 0, odd
+//       on lane 1) into shared memory and marks, per word, whether a ziggurat attempt
+//       starting there takes the fast path (|hz| < kn[iz]) -> 128-bit mask F;
+//   A2  both lanes walk only the slow attempts (~0.5 per thread-step) -- wedge
+//       accept/reject and tail draws exactly as rng.hpp:156-185 -- producing a short list
+//       of "offset changes" / "special values" for the normal indices they affect;
+//   B   the unrolled spin update reconstructs normal i as hz*wn[iz] of word i + off(i)
+//       (or the special value): every fast normal is independent of the others.
+// The coupling phi(x_j) (x_j for bSB/SimCIM, sgn(x_j) for dSB) is gathered from a
+// per-trajectory shared-memory column written once per step. Rows of J(c_l) are runtime
+// CSR rows (DMAX = 0) or rows padded to DMAX entries with exact zeros (DMAX > 0) whose
+// column indices are kernel parameters (constant bank). All FP64 arithmetic is explicitly
+// rounded (__dmul_rn/__dadd_rn/__dsub_rn) in the reference's order: final spins are
+// bit-identical to the shim build of the reference.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -22,7 +34,7 @@ namespace momc_b200 {
 
 namespace sbimpl {
 
-constexpr int kGroup = 8;  // spins whose normals are produced, then consumed, together
+constexpr int kThreads = 2 * kSampleBlock;  // two lanes per trajectory
 
 __device__ __forceinline__ unsigned long long globaltimer()
 {
@@ -31,89 +43,81 @@ __device__ __forceinline__ unsigned long long globaltimer()
     return t;
 }
 
-struct NoiseCursor {
-    const uint32_t* ubuf;  // [NU][kSampleBlock] u32 of the current stream (this thread's column)
-    int nu;                // pre-generated words
-    int pos;               // next word
-    uint32_t k0, k1, lo, mid, hi;
+// exact int32 -> double without the XU conversion pipe: (2^52 + 2^31 + v) - (2^52 + 2^31)
+__device__ __forceinline__ double i32_to_f64(int32_t v)
+{
+    return __dsub_rn(__hiloint2double(0x43300000, static_cast<uint32_t>(v) ^ 0x80000000u), 4503601774854144.0);
+}
 
-    __device__ __forceinline__ uint32_t fetch()
-    {
-        const int p = pos++;
-        if (p < nu) return ubuf[p * kSampleBlock];
-        // overflow past the pre-generated blocks (several slow draws in one step): recompute
-        const uint4 b = philox(k0, k1, static_cast<uint32_t>(p >> 2), lo, mid, hi);
-        const int q = p & 3;
-        return q == 0 ? b.x : (q == 1 ? b.y : (q == 2 ? b.z : b.w));
-    }
+// |hz| as in rng.hpp:161-163 (INT_MIN -> 2^31)
+__device__ __forceinline__ uint32_t zmag(uint32_t u)
+{
+    return static_cast<int32_t>(u) < 0 ? 0u - u : u;
+}
+
+template <int NMAX>
+struct Geo {
+    static constexpr int kNH = NMAX / 2;            // spins per lane
+    static constexpr int kNB = (NMAX + 3) / 4 + 2;  // Philox blocks pre-generated per step (even count below)
+    static constexpr int kNBe = (kNB + 1) / 2 * 2;
+    static constexpr int kNU = 4 * kNBe;            // words covered by the fast mask (<= 128)
+    static constexpr int kNA = kNU + 16;            // allocated words (A2 extends on demand)
+    static constexpr int kUS = kSampleBlock + 1;    // word-row stride (odd: pair lanes hit distinct banks)
+    static constexpr int kECAP = 8;                 // event entries per lane-step
+    static constexpr int zig = 0;                                  // ZigTables (2560 B)
+    static constexpr int ubuf = 2560;                              // kNA x kUS u32
+    static constexpr int ent = ubuf + (kNA * kUS * 4 + 15) / 16 * 16;  // kECAP x 256 u32
+    static constexpr int entv = ent + kECAP * kThreads * 4;        // kECAP x 256 f64
+    static constexpr int phi = entv + kECAP * kThreads * 8;        // NMAX x 128 f64
+    static constexpr int csr = phi + NMAX * kSampleBlock * 8;
+    static_assert(kNU <= 128, "mask covers at most 128 words");
 };
 
-// rng.hpp:156-185 Stream::next_normal, words taken from the cursor in stream order.
-__device__ __forceinline__ double next_normal(NoiseCursor& c, const uint32_t* __restrict__ kn,
-                                              const double* __restrict__ wn, const double* __restrict__ fn)
+// first p in [from, kNU) whose mask bit is clear, else kNU
+template <int kNU>
+__device__ __forceinline__ int next_slow(uint64_t F0, uint64_t F1, int from)
 {
-    for (;;) {
-        const uint32_t u = c.fetch();
-        const int32_t hz = static_cast<int32_t>(u);
-        const uint32_t iz = u & 127u;
-        const uint32_t mag = hz < 0 ? static_cast<uint32_t>(-static_cast<int64_t>(hz)) : static_cast<uint32_t>(hz);
-        if (mag < kn[iz]) return __dmul_rn(static_cast<double>(hz), wn[iz]);
-        if (iz == 0) {
-            const double r = 3.442619855899;
-            for (;;) {
-                const uint32_t a0 = c.fetch(), a1 = c.fetch();
-                const double x = __ddiv_rn(-log(u01_open_from(a0, a1)), r);
-                const uint32_t b0 = c.fetch(), b1 = c.fetch();
-                const double y = -log(u01_open_from(b0, b1));
-                if (__dadd_rn(y, y) >= __dmul_rn(x, x)) return hz > 0 ? __dadd_rn(r, x) : -__dadd_rn(r, x);
-            }
+    constexpr uint64_t v0 = kNU >= 64 ? ~0ull : ((1ull << (kNU & 63)) - 1);
+    constexpr uint64_t v1 = kNU >= 128 ? ~0ull : (kNU > 64 ? ((1ull << ((kNU - 64) & 63)) - 1) : 0ull);
+    if (from < 64) {
+        const uint64_t s0 = ~F0 & v0 & (~0ull << from);
+        if (s0) return __ffsll(static_cast<long long>(s0)) - 1;
+    }
+    if (kNU > 64) {
+        const int f1 = from > 64 ? from - 64 : 0;
+        if (f1 < 64) {
+            const uint64_t s1 = ~F1 & v1 & (~0ull << f1);
+            if (s1) return 64 + __ffsll(static_cast<long long>(s1)) - 1;
         }
-        const double x = __dmul_rn(static_cast<double>(hz), wn[iz]);
-        const uint32_t a0 = c.fetch(), a1 = c.fetch();
-        const double lhs = __dadd_rn(fn[iz], __dmul_rn(u01_from(a0, a1), __dsub_rn(fn[iz - 1], fn[iz])));
-        if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) return x;
     }
+    return kNU;
 }
 
-// Shared-memory carve-up for one CTA.
 template <int NMAX>
-struct SmemLayout {
-    static constexpr int kNU = 4 * ((NMAX + 3) / 4 + 1);  // pre-generated u32 per step
-    // byte offsets (all 16-B aligned)
-    static constexpr int zig = 0;                                            // ZigTables (2560 B)
-    static constexpr int ubuf = 2560;                                        // kNU * 128 * 4
-    static constexpr int noise = ubuf + kNU * kSampleBlock * 4;              // kGroup * 128 * 8
-    static constexpr int xs = noise + kGroup * kSampleBlock * 8;             // NMAX * 128 * 8 (bsb/simcim)
-    __host__ __device__ static constexpr int ys_of(bool gather) { return xs + (gather ? NMAX * kSampleBlock * 8 : 0); }
-    __host__ __device__ static constexpr int csr_of(bool gather, bool ys)
-    {
-        return ys_of(gather) + (ys ? NMAX * kSampleBlock * 8 : 0);
-    }
-};
-
-template <int NMAX>
-__host__ __device__ constexpr bool y_in_smem()
+constexpr int min_blocks()
 {
-    return NMAX > 42;
+    return NMAX <= 42 ? 2 : 1;
 }
 
-// Register-resident integrator for n <= NMAX <= 64.
-template <int NMAX, int VAR>
-__global__ void __launch_bounds__(kSampleBlock, 2) sb_small_kernel(const SamplerParams p)
+// Register-resident integrator for n <= NMAX <= 64, two lanes per trajectory.
+template <int NMAX, int VAR, int DMAX>
+__global__ void __launch_bounds__(kThreads, min_blocks<NMAX>()) sb_small_kernel(const SamplerParams p)
 {
-    constexpr bool kGather = VAR != 1;  // bsb / simcim gather x_j values; dsb uses a sign mask
-    constexpr bool kYS = y_in_smem<NMAX>();
-    using SL = SmemLayout<NMAX>;
+    using G = Geo<NMAX>;
+    constexpr int NH = G::kNH;
+    constexpr int US = G::kUS;
     extern __shared__ __align__(16) unsigned char smem[];
-    ZigTables* zig = reinterpret_cast<ZigTables*>(smem + SL::zig);
-    uint32_t* ubuf = reinterpret_cast<uint32_t*>(smem + SL::ubuf);
-    double* noise_s = reinterpret_cast<double*>(smem + SL::noise);
-    double* xs = reinterpret_cast<double*>(smem + SL::xs);
-    double* ys = reinterpret_cast<double*>(smem + SL::ys_of(kGather));
-    unsigned char* csr = smem + SL::csr_of(kGather, kYS);
-    int* rp = reinterpret_cast<int*>(csr);                                         // NMAX + 1
-    double* cv = reinterpret_cast<double*>(csr + ((NMAX + 1) * 4 + 15) / 16 * 16);  // nnz
-    int* cc = reinterpret_cast<int*>(cv + p.nnz);                                   // nnz
+    ZigTables* zig = reinterpret_cast<ZigTables*>(smem + G::zig);
+    uint32_t* ubuf = reinterpret_cast<uint32_t*>(smem + G::ubuf);
+    uint32_t* ent = reinterpret_cast<uint32_t*>(smem + G::ent);
+    double* entv = reinterpret_cast<double*>(smem + G::entv);
+    double* phis = reinterpret_cast<double*>(smem + G::phi);
+    unsigned char* csr = smem + G::csr;
+    // DMAX == 0: rp[n+1] | cv[nnz] | cc[nnz];  DMAX > 0: pv[n*DMAX] (columns in p.pad_col)
+    int* rp = reinterpret_cast<int*>(csr);
+    double* cv = reinterpret_cast<double*>(csr + ((NMAX + 1) * 4 + 15) / 16 * 16);
+    int* cc = reinterpret_cast<int*>(cv + p.nnz);
+    double* pv = reinterpret_cast<double*>(csr);
 
     const int n = p.n;
     const long long gblock = p.block_begin + blockIdx.x;
@@ -122,194 +126,331 @@ __global__ void __launch_bounds__(kSampleBlock, 2) sb_small_kernel(const Sampler
     const int l = static_cast<int>(rl % p.L);
     const int run = static_cast<int>(rl / p.L);
     const int tid = threadIdx.x;
+    const int t_loc = tid >> 1;  // trajectory within the CTA
+    const int h = tid & 1;       // which half of the spins this lane owns
 
-    // ---- CTA setup: ziggurat tables, CSR of J(c_l)
-    {
+    {  // CTA setup: ziggurat tables, coupling rows of J(c_l)
         const uint32_t* src = reinterpret_cast<const uint32_t*>(p.zig);
         uint32_t* dst = reinterpret_cast<uint32_t*>(zig);
-        for (int i = tid; i < static_cast<int>(sizeof(ZigTables) / 4); i += kSampleBlock) dst[i] = src[i];
-        for (int i = tid; i <= n; i += kSampleBlock) rp[i] = p.row_ptr[i];
-        const double* v = p.vals + static_cast<long long>(l) * p.nnz;
-        for (int i = tid; i < p.nnz; i += kSampleBlock) {
-            cv[i] = v[i];
-            cc[i] = p.col[i];
+        for (int i = tid; i < static_cast<int>(sizeof(ZigTables) / 4); i += kThreads) dst[i] = src[i];
+        if constexpr (DMAX == 0) {
+            for (int i = tid; i <= n; i += kThreads) rp[i] = p.row_ptr[i];
+            const double* v = p.vals + static_cast<long long>(l) * p.nnz;
+            for (int i = tid; i < p.nnz; i += kThreads) {
+                cv[i] = v[i];
+                cc[i] = p.col[i];
+            }
+        } else {
+            const double* v = p.pad_vals + static_cast<long long>(l) * n * DMAX;
+            for (int i = tid; i < n * DMAX; i += kThreads) pv[i] = v[i];
         }
     }
     __syncthreads();
 
-    const int traj = chunk * kSampleBlock + tid;
+    const int traj = chunk * kSampleBlock + t_loc;
+    const unsigned wmask = __ballot_sync(0xffffffffu, traj < p.batch);  // pairs are never split
     if (traj >= p.batch) return;  // no CTA-wide barrier below this point
 
     const uint64_t key = run_key(p.seed, static_cast<uint32_t>(run));
     const uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
     const uint32_t wl = static_cast<uint32_t>(l), tr = static_cast<uint32_t>(traj);
     const double c0 = p.c0[l];
+    const int s0 = h * NH;  // first spin of this lane
 
-    // ---- init_state (solver.hpp:108-124): x then y, one next_symmetric per spin
-    double x[NMAX];
-    double y[kYS ? 1 : NMAX];
+    // ---- init_state (solver.hpp:108-124): spin i uses words 2i, 2i+1 of the init_x / init_y
+    //      streams, i.e. block i/2, half i%2
+    double x[NH];
+    double y[NH];
 #pragma unroll
-    for (int b = 0; b < (NMAX + 1) / 2; ++b) {
-        if (2 * b < n) {
-            const uint4 rx = philox(k0, k1, b, tag_word(kTagInitX, 0), tr, wl);
-            x[2 * b] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(rx.x, rx.y)), 1.0));
-            if (2 * b + 1 < NMAX)
-                x[2 * b + 1] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(rx.z, rx.w)), 1.0));
-            const uint4 ry = philox(k0, k1, b, tag_word(kTagInitY, 0), tr, wl);
-            const double y0 = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(ry.x, ry.y)), 1.0));
-            const double y1 = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(ry.z, ry.w)), 1.0));
-            if constexpr (kYS) {
-                ys[(2 * b) * kSampleBlock + tid] = y0;
-                if (2 * b + 1 < NMAX) ys[(2 * b + 1) * kSampleBlock + tid] = y1;
-            } else {
-                y[2 * b] = y0;
-                if (2 * b + 1 < NMAX) y[2 * b + 1] = y1;
+    for (int s = 0; s < NH; s += 2) {
+        const int i = s0 + s;  // even
+        if (i < n) {
+            const uint4 rx = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitX, 0), tr, wl);
+            const uint4 ry = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitY, 0), tr, wl);
+            x[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(rx.x, rx.y)), 1.0));
+            y[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(ry.x, ry.y)), 1.0));
+            if (s + 1 < NH) {
+                x[s + 1] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(rx.z, rx.w)), 1.0));
+                y[s + 1] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(ry.z, ry.w)), 1.0));
             }
         } else {
-            x[2 * b] = 0.0;
-            if (2 * b + 1 < NMAX) x[2 * b + 1] = 0.0;
-            if constexpr (!kYS) {
-                y[2 * b] = 0.0;
-                if (2 * b + 1 < NMAX) y[2 * b + 1] = 0.0;
+            x[s] = y[s] = 0.0;
+            if (s + 1 < NH) x[s + 1] = y[s + 1] = 0.0;
+        }
+    }
+    // NH odd (e.g. 21): lane 1's first spin is odd -> the loop above paired (i, i+1) from
+    // block i/2 assuming i even; recompute the odd-start case exactly
+    if constexpr ((NH & 1) != 0) {
+        if (h == 1) {
+#pragma unroll
+            for (int s = 0; s < NH; ++s) {
+                const int i = s0 + s;
+                if (i < n) {
+                    const uint4 rx = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitX, 0), tr, wl);
+                    const uint4 ry = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitY, 0), tr, wl);
+                    const bool hi = i & 1;
+                    x[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, hi ? u01_from(rx.z, rx.w) : u01_from(rx.x, rx.y)), 1.0));
+                    y[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, hi ? u01_from(ry.z, ry.w) : u01_from(ry.x, ry.y)), 1.0));
+                } else {
+                    x[s] = y[s] = 0.0;
+                }
             }
         }
     }
-    // spins past n stay exactly 0 and are never read
 
-    uint64_t negmask = 0;  // dsb: bit j set iff x_j < 0 (phi_j = -1)
+    double* ph = phis + t_loc;  // phi_j of this trajectory at ph[j * 128]
 #pragma unroll
-    for (int i = 0; i < NMAX; ++i) {
-        if (i < n) {
-            if constexpr (kGather) xs[i * kSampleBlock + tid] = x[i];
-            negmask |= static_cast<uint64_t>(x[i] < 0.0) << i;
-        }
+    for (int s = 0; s < NH; ++s) {
+        const int i = s0 + s;
+        if (i < n) ph[i * kSampleBlock] = VAR == 1 ? (x[s] < 0.0 ? -1.0 : 1.0) : x[s];
     }
 
     const uint32_t* kn = zig->kn;
     const double* wn = zig->wn;
     const double* fn = zig->fn;
     const bool noisy = p.alpha > 0.0;
-    int first_bad = 0;
+    uint32_t* ub = ubuf + t_loc;  // this trajectory's word column, stride US
+    uint32_t* en = ent + tid;     // this lane's event column, stride kThreads
+    double* ev = entv + tid;
+    bool overflow = false;
+    __syncwarp(wmask);
 
     for (int t = 0; t < p.T; ++t) {
         const double a_t = __ddiv_rn(static_cast<double>(t + 1), static_cast<double>(p.T));
-        const double neg_drift = -__dsub_rn(p.a0, a_t);             // -(a0 - a_t)
-        const double pump = __dmul_rn(-0.5, __dsub_rn(1.0, a_t));   // simcim_schedule
+        const double neg_drift = -__dsub_rn(p.a0, a_t);            // -(a0 - a_t)
+        const double pump = __dmul_rn(-0.5, __dsub_rn(1.0, a_t));  // simcim_schedule
         const uint32_t lo = tag_word(kTagStepNoise, static_cast<uint32_t>(t));
 
-        NoiseCursor cur;
+        int ne = 0;     // events this step
+        int e = 0;      // next event to apply
+        int nxt = 255;  // normal index of the next event
+        int off = 0;    // current word offset of the fast normals
         if (noisy) {
-            // fill_step_noise (solver.hpp:128-136): stream (key, l, traj, tag_word(step_noise, t))
-#pragma unroll
-            for (int b = 0; b < SL::kNU / 4; ++b) {
-                const uint4 r = philox(k0, k1, b, lo, tr, wl);
-                ubuf[(4 * b + 0) * kSampleBlock + tid] = r.x;
-                ubuf[(4 * b + 1) * kSampleBlock + tid] = r.y;
-                ubuf[(4 * b + 2) * kSampleBlock + tid] = r.z;
-                ubuf[(4 * b + 3) * kSampleBlock + tid] = r.w;
+            // ---- A1: Philox blocks (lane h: blocks h, h+2, ...) + fast-attempt mask
+            uint64_t F0 = 0, F1 = 0;
+#pragma unroll 1
+            for (int b = h; b < G::kNBe; b += 2) {
+                const uint4 r = philox(k0, k1, static_cast<uint32_t>(b), lo, tr, wl);
+                ub[(4 * b + 0) * US] = r.x;
+                ub[(4 * b + 1) * US] = r.y;
+                ub[(4 * b + 2) * US] = r.z;
+                ub[(4 * b + 3) * US] = r.w;
+                const uint64_t f = static_cast<uint64_t>(zmag(r.x) < kn[r.x & 127u]) |
+                                   static_cast<uint64_t>(zmag(r.y) < kn[r.y & 127u]) << 1 |
+                                   static_cast<uint64_t>(zmag(r.z) < kn[r.z & 127u]) << 2 |
+                                   static_cast<uint64_t>(zmag(r.w) < kn[r.w & 127u]) << 3;
+                const int pp = 4 * b;
+                if (pp < 64) F0 |= f << pp;
+                else F1 |= f << (pp - 64);
             }
-            cur.ubuf = ubuf + tid;
-            cur.nu = SL::kNU;
-            cur.pos = 0;
-            cur.k0 = k0;
-            cur.k1 = k1;
-            cur.lo = lo;
-            cur.mid = tr;
-            cur.hi = wl;
-        }
-
-        uint64_t newmask = 0;
-#pragma unroll
-        for (int g = 0; g < (NMAX + kGroup - 1) / kGroup; ++g) {
-            if (g * kGroup < n) {
-                if (noisy) {
-                    const int cnt = min(kGroup, n - g * kGroup);
-                    for (int q = 0; q < cnt; ++q) noise_s[q * kSampleBlock + tid] = next_normal(cur, kn, wn, fn);
-                }
-#pragma unroll
-                for (int q = 0; q < kGroup; ++q) {
-                    const int i = g * kGroup + q;
-                    if (i < NMAX && i < n) {
-                        // coupled_i = sum_j J_ij phi(x_j), j ascending, from +0.0 (shim GEMM order)
-                        double coupled = 0.0;
-                        const int e1 = rp[i + 1];
-                        for (int e = rp[i]; e < e1; ++e) {
-                            const int j = cc[e];
-                            const double v = cv[e];
-                            double term;
-                            if constexpr (VAR == 1) {
-                                term = ((negmask >> j) & 1ull) ? -v : v;  // J * (+-1) is exact
-                            } else {
-                                term = __dmul_rn(v, xs[j * kSampleBlock + tid]);
-                            }
-                            coupled = __dadd_rn(coupled, term);
+            F0 |= __shfl_xor_sync(wmask, F0, 1);
+            F1 |= __shfl_xor_sync(wmask, F1, 1);
+            __syncwarp(wmask);  // partner's words visible
+            // ---- A2: resolve the slow attempts (rng.hpp:164-184), redundantly on both lanes
+            int gen = G::kNU;  // words present in ub
+            int pos = 0, i = 0;
+            for (;;) {
+                const int last = pos + (n - 1 - i);  // position of normal n-1 if the rest is fast
+                int q = next_slow<G::kNU>(F0, F1, pos);
+                if (q >= G::kNU) {  // beyond the mask: extend the word buffer, test on demand
+                    q = pos > G::kNU ? pos : G::kNU;
+                    for (; q <= last; ++q) {
+                        if (q >= G::kNA) break;
+                        while (gen <= q) {  // both lanes write identical words
+                            const uint4 r = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
+                            ub[(gen + 0) * US] = r.x;
+                            ub[(gen + 1) * US] = r.y;
+                            ub[(gen + 2) * US] = r.z;
+                            ub[(gen + 3) * US] = r.w;
+                            gen += 4;
                         }
-                        double yi;
-                        if constexpr (kYS) yi = ys[i * kSampleBlock + tid];
-                        else yi = y[i];
-                        double xi = x[i];
-                        const double eta = noisy ? noise_s[q * kSampleBlock + tid] : 0.0;
-                        if constexpr (VAR == 2) {
-                            // simcim_step (solver.hpp:199-210)
-                            double d = __dsub_rn(__dmul_rn(pump, xi), __dmul_rn(c0, coupled));
-                            if (noisy) d = __dadd_rn(d, __dmul_rn(p.alpha, eta));
-                            yi = __dadd_rn(__dmul_rn(0.9, yi), __dmul_rn(1.0 - 0.9, d));
-                            xi = __dadd_rn(xi, __dmul_rn(p.dt, yi));
-                        } else {
-                            // sb_step (solver.hpp:167-178)
-                            double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled));
-                            if (noisy) d = __dadd_rn(d, __dmul_rn(p.alpha, eta));
-                            yi = __dadd_rn(yi, __dmul_rn(p.dt, d));
-                            xi = __dadd_rn(xi, __dmul_rn(p.s_dt_a0, yi));
-                            yi = fabs(xi) > 1.0 ? 0.0 : yi;
-                        }
-                        // cwiseMax(-1).cwiseMin(1) == std::max/std::min (NaN propagates)
-                        xi = (xi < -1.0) ? -1.0 : xi;
-                        xi = (1.0 < xi) ? 1.0 : xi;
-                        x[i] = xi;
-                        if constexpr (kYS) ys[i * kSampleBlock + tid] = yi;
-                        else y[i] = yi;
-                        newmask |= static_cast<uint64_t>(xi < 0.0) << i;
-                        if (p.first_bad_step_task >= 0 && first_bad == 0 &&
-                            (!isfinite(xi) || !isfinite(yi)))
-                            first_bad = t + 1;
+                        const uint32_t w = ub[q * US];
+                        if (!(zmag(w) < kn[w & 127u])) break;
                     }
                 }
+                if (q > last) break;  // every remaining normal is a fast attempt
+                if (q + 9 >= G::kNA) {
+                    overflow = true;
+                    break;
+                }
+                while (gen <= q + 8) {  // words a wedge attempt may consume
+                    const uint4 r = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
+                    ub[(gen + 0) * US] = r.x;
+                    ub[(gen + 1) * US] = r.y;
+                    ub[(gen + 2) * US] = r.z;
+                    ub[(gen + 3) * US] = r.w;
+                    gen += 4;
+                }
+                const int iq = i + (q - pos);  // normal index of the attempt at q
+                const uint32_t u = ub[q * US];
+                const int32_t hz = static_cast<int32_t>(u);
+                const uint32_t iz = u & 127u;
+                int new_i, new_pos;
+                bool special = false;
+                double sval = 0.0;
+                if (iz == 0) {  // tail: 4 words per (x, y) trial
+                    const double r = 3.442619855899;
+                    int qq = q + 1;
+                    for (;;) {
+                        if (qq + 4 > G::kNA) {
+                            overflow = true;
+                            break;
+                        }
+                        while (gen < qq + 4) {
+                            const uint4 rr = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
+                            ub[(gen + 0) * US] = rr.x;
+                            ub[(gen + 1) * US] = rr.y;
+                            ub[(gen + 2) * US] = rr.z;
+                            ub[(gen + 3) * US] = rr.w;
+                            gen += 4;
+                        }
+                        const double xx = __ddiv_rn(-log(u01_open_from(ub[qq * US], ub[(qq + 1) * US])), r);
+                        const double yy = -log(u01_open_from(ub[(qq + 2) * US], ub[(qq + 3) * US]));
+                        qq += 4;
+                        if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) {
+                            sval = hz > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
+                            break;
+                        }
+                    }
+                    if (overflow) break;
+                    special = true;
+                    new_i = iq + 1;
+                    new_pos = qq;
+                } else {  // wedge: accept iff fn[iz] + u01 (fn[iz-1] - fn[iz]) < exp(-x^2 / 2)
+                    const double xv = __dmul_rn(i32_to_f64(hz), wn[iz]);
+                    const double lhs = __dadd_rn(
+                        fn[iz], __dmul_rn(u01_from(ub[(q + 1) * US], ub[(q + 2) * US]), __dsub_rn(fn[iz - 1], fn[iz])));
+                    const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
+                    // FP32 exp brackets the FP64 one within 1e-6 relative on [-6, 0]; decide
+                    // from it unless lhs falls in the +-1e-5 band, then use the FP64 exp
+                    const float ef = __expf(static_cast<float>(targ));
+                    bool accept;
+                    if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) accept = true;
+                    else if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) accept = false;
+                    else accept = lhs < exp(targ);
+                    new_pos = q + 3;
+                    new_i = accept ? iq + 1 : iq;
+                }
+                // event: from normal new_i on, words continue at offset new_pos - new_i; a tail
+                // also pins normal iq to sval (one event per normal index: later ones replace)
+                const int idx = special ? iq : new_i;
+                if (ne > 0 && static_cast<int>(en[(ne - 1) * kThreads] & 0xFFu) == idx) --ne;
+                if (ne >= G::kECAP) {
+                    overflow = true;
+                    break;
+                }
+                en[ne * kThreads] = static_cast<uint32_t>(idx) | (static_cast<uint32_t>(new_pos - new_i) << 8) |
+                                    (special ? 1u << 16 : 0u);
+                if (special) ev[ne * kThreads] = sval;
+                ++ne;
+                pos = new_pos;
+                i = new_i;
+                if (i >= n) break;
+            }
+            // lane 1 starts at normal NH: apply the events of earlier normals
+            while (e < ne) {
+                const uint32_t w = en[e * kThreads];
+                if (static_cast<int>(w & 0xFFu) >= s0) break;
+                off = static_cast<int>((w >> 8) & 0xFFu);
+                ++e;
+            }
+            nxt = e < ne ? static_cast<int>(en[e * kThreads] & 0xFFu) : 255;
+        }
+
+        // ---- B: spin updates (sb_step solver.hpp:159-181 / simcim_step :196-210)
+#pragma unroll
+        for (int s = 0; s < NH; ++s) {
+            const int i = s0 + s;
+            if (i < n) {
+                double eta = 0.0;
+                if (noisy) {
+                    bool sp = false;
+                    double spv = 0.0;
+                    if (i == nxt) {
+                        const uint32_t w = en[e * kThreads];
+                        off = static_cast<int>((w >> 8) & 0xFFu);
+                        if (w >> 16) {
+                            sp = true;
+                            spv = ev[e * kThreads];
+                        }
+                        ++e;
+                        nxt = e < ne ? static_cast<int>(en[e * kThreads] & 0xFFu) : 255;
+                    }
+                    const uint32_t u = ub[(sp ? 0 : i + off) * US];
+                    const double v = __dmul_rn(i32_to_f64(static_cast<int32_t>(u)), wn[u & 127u]);
+                    eta = sp ? spv : v;
+                }
+                // coupled_i = sum_j J_ij phi(x_j), j ascending, from +0.0 (shim GEMM order)
+                double coupled = 0.0;
+                if constexpr (DMAX > 0) {
+#pragma unroll
+                    for (int d = 0; d < DMAX; ++d) {
+                        const int j = p.pad_col[i * DMAX + d];  // constant-bank operand
+                        coupled = __dadd_rn(coupled, __dmul_rn(pv[i * DMAX + d], ph[j * kSampleBlock]));
+                    }
+                } else {
+                    const int e1 = rp[i + 1];
+                    for (int q = rp[i]; q < e1; ++q) coupled = __dadd_rn(coupled, __dmul_rn(cv[q], ph[cc[q] * kSampleBlock]));
+                }
+                double xi = x[s], yi = y[s];
+                if constexpr (VAR == 2) {
+                    double d = __dsub_rn(__dmul_rn(pump, xi), __dmul_rn(c0, coupled));
+                    if (noisy) d = __dadd_rn(d, __dmul_rn(p.alpha, eta));
+                    yi = __dadd_rn(__dmul_rn(0.9, yi), __dmul_rn(1.0 - 0.9, d));
+                    xi = __dadd_rn(xi, __dmul_rn(p.dt, yi));
+                } else {
+                    double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled));
+                    if (noisy) d = __dadd_rn(d, __dmul_rn(p.alpha, eta));
+                    yi = __dadd_rn(yi, __dmul_rn(p.dt, d));
+                    xi = __dadd_rn(xi, __dmul_rn(p.s_dt_a0, yi));
+                    yi = fabs(xi) > 1.0 ? 0.0 : yi;
+                }
+                // cwiseMax(-1).cwiseMin(1) == std::max/std::min (NaN propagates)
+                xi = (xi < -1.0) ? -1.0 : xi;
+                xi = (1.0 < xi) ? 1.0 : xi;
+                x[s] = xi;
+                y[s] = yi;
             }
         }
-        negmask = newmask;
-        if constexpr (kGather) {
+        __syncwarp(wmask);  // the pair has finished reading phi(t) and this step's words
 #pragma unroll
-            for (int i = 0; i < NMAX; ++i)
-                if (i < n) xs[i * kSampleBlock + tid] = x[i];
+        for (int s = 0; s < NH; ++s) {
+            const int i = s0 + s;
+            if (i < n) ph[i * kSampleBlock] = VAR == 1 ? (x[s] < 0.0 ? -1.0 : 1.0) : x[s];
         }
+        __syncwarp(wmask);  // phi(t+1) complete
     }
 
     // ---- read_spins + pack (solver.hpp:237-244, :288-297): bit i set iff !(x_i < 0)
     uint64_t word = 0;
     bool bad = false;
 #pragma unroll
-    for (int i = 0; i < NMAX; ++i) {
+    for (int s = 0; s < NH; ++s) {
+        const int i = s0 + s;
         if (i < n) {
-            word |= static_cast<uint64_t>(!(x[i] < 0.0)) << i;
-            bad |= x[i] != x[i];
+            word |= static_cast<uint64_t>(!(x[s] < 0.0)) << i;
+            bad |= x[s] != x[s];
         }
     }
-    const long long idx = (static_cast<long long>(run) * p.L + l) * p.batch + traj;
-    p.words[idx] = word;
-    if (bad) p.nan_block[blockIdx.x] = 1;
-    if (p.first_bad_step_task >= 0 && first_bad) atomicMin(&p.bad_step[blockIdx.x], first_bad);
+    word |= __shfl_xor_sync(wmask, word, 1);
+    if (h == 0) {
+        const long long idx = (static_cast<long long>(run) * p.L + l) * p.batch + traj;
+        p.words[idx] = word;
+    }
+    // NaN (numerical failure) -> bit 1; noise-event buffer overflow (re-run on the exact
+    // sequential path) -> bit 2
+    if (bad) atomicOr(&p.nan_block[blockIdx.x], 1);
+    if (overflow) atomicOr(&p.nan_block[blockIdx.x], 2);
     if (p.block_end_ns && (tid & 31) == 0) atomicMax(&p.block_end_ns[blockIdx.x], globaltimer());
 }
 
-template <int NMAX, int VAR>
+template <int NMAX, int VAR, int DMAX>
 int launch_small(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
-    using SL = SmemLayout<NMAX>;
-    constexpr bool kGather = VAR != 1;
-    constexpr bool kYS = y_in_smem<NMAX>();
-    const int smem = SL::csr_of(kGather, kYS) + ((NMAX + 1) * 4 + 15) / 16 * 16 + p.nnz * 12 + 16;
-    auto kern = sb_small_kernel<NMAX, VAR>;
+    using G = Geo<NMAX>;
+    const int csr_bytes = DMAX == 0 ? ((NMAX + 1) * 4 + 15) / 16 * 16 + p.nnz * 12 : p.n * DMAX * 8;
+    const int smem = G::csr + csr_bytes + 16;
+    auto kern = sb_small_kernel<NMAX, VAR, DMAX>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const long long kMaxGrid = 1ll << 30;
@@ -317,33 +458,37 @@ int launch_small(const SamplerParams& p, long long nblocks, cudaStream_t st)
         SamplerParams q = p;
         q.block_begin = p.block_begin + b0;
         const long long nb = nblocks - b0 < kMaxGrid ? nblocks - b0 : kMaxGrid;
-        // per-block outputs are indexed by blockIdx.x: shift them for later slices
         q.nan_block = p.nan_block + b0;
         if (p.block_end_ns) q.block_end_ns = p.block_end_ns + b0;
-        if (p.bad_step) q.bad_step = p.bad_step + b0;
-        kern<<<static_cast<unsigned>(nb), kSampleBlock, smem, st>>>(q);
+        kern<<<static_cast<unsigned>(nb), kThreads, smem, st>>>(q);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
 }
 
-template <int NMAX>
+template <int NMAX, int DMAX>
 int launch_variant(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
     switch (p.variant) {
-        case 0: return launch_small<NMAX, 0>(p, nblocks, st);
-        case 1: return launch_small<NMAX, 1>(p, nblocks, st);
-        default: return launch_small<NMAX, 2>(p, nblocks, st);
+        case 0: return launch_small<NMAX, 0, DMAX>(p, nblocks, st);
+        case 1: return launch_small<NMAX, 1, DMAX>(p, nblocks, st);
+        default: return launch_small<NMAX, 2, DMAX>(p, nblocks, st);
     }
 }
 
 }  // namespace sbimpl
 
-// explicit instantiation units: sampler_n<NMAX>.cu
-int launch_small_n16(const SamplerParams&, long long, cudaStream_t);
-int launch_small_n32(const SamplerParams&, long long, cudaStream_t);
-int launch_small_n42(const SamplerParams&, long long, cudaStream_t);
-int launch_small_n64(const SamplerParams&, long long, cudaStream_t);
+// instantiation units sampler_n<NMAX>_d<DMAX>.cu
+#define MOMC_SB_DECL(N, D) int launch_small_n##N##_d##D(const SamplerParams&, long long, cudaStream_t);
+MOMC_SB_DECL(16, 0)
+MOMC_SB_DECL(32, 0)
+MOMC_SB_DECL(42, 0)
+MOMC_SB_DECL(64, 0)
+MOMC_SB_DECL(16, 3)
+MOMC_SB_DECL(32, 3)
+MOMC_SB_DECL(42, 3)
+MOMC_SB_DECL(64, 3)
+#undef MOMC_SB_DECL
 
 }  // namespace momc_b200

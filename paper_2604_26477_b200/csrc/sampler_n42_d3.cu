@@ -1,0 +1,9 @@
+// Instantiation unit for the register-resident SB kernel, NMAX = 42, DMAX = 3 (parallel build).
+#include "sampler_impl.cuh"
+
+namespace momc_b200 {
+int launch_small_n42_d3(const SamplerParams& p, long long nblocks, cudaStream_t st)
+{
+    return sbimpl::launch_variant<42, 3>(p, nblocks, st);
+}
+}  // namespace momc_b200
