@@ -294,7 +294,9 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     if (c.L < 1) usage("run_sampler needs at least one weight vector");
     if (runs < 1) usage("runs must be >= 1");
     const int batch = cfg->batch_size;
-    const int chunks = (batch + kSampleBlock - 1) / kSampleBlock;
+    const bool regpath = sampler_uses_register_path(c.n, cfg->alpha);
+    const int bt = sampler_block_traj(c.n, cfg->alpha);
+    const int chunks = (batch + bt - 1) / bt;
     const long long total_blocks = static_cast<long long>(runs) * c.L * chunks;
     if (b_end < 0 || b_end > total_blocks) b_end = total_blocks;
     if (b_begin < 0 || b_begin > b_end) usage("invalid block range");
@@ -305,6 +307,7 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     c.pool_batch = batch;
     c.pool_block_begin = b_begin;
     c.pool_blocks = nblocks;
+    c.pool_block_traj = bt;
     c.d_words.reserve(static_cast<size_t>(c.pool_size) * wpc);
     c.d_nan.reserve(static_cast<size_t>(nblocks) + 1);
     c.d_badstep.reserve(static_cast<size_t>(nblocks) + 1);
@@ -333,6 +336,7 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     p.batch = batch;
     p.runs = runs;
     p.chunks = chunks;
+    p.block_traj = bt;
     p.block_begin = b_begin;
     p.seed = cfg->seed;
     p.row_ptr = c.d_rowptr.p;
@@ -350,8 +354,8 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     p.bad_step = c.d_badstep.p;
 
     auto scratch = [&](long long blocks) {
-        long long cap = std::min<long long>(blocks, 4096) * kSampleBlock;
-        if (cap < kSampleBlock) cap = kSampleBlock;
+        long long cap = std::min<long long>(blocks, 4096) * bt;
+        if (cap < bt) cap = bt;
         c.d_gx.reserve(static_cast<size_t>(cap) * c.n);
         c.d_gy.reserve(static_cast<size_t>(cap) * c.n);
         c.d_gxn.reserve(static_cast<size_t>(cap) * c.n);
@@ -359,15 +363,15 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         return GenericScratch{c.d_gx.p, c.d_gy.p, c.d_gxn.p, c.d_gnoise.p, cap};
     };
     GenericScratch g{};
-    if (c.n > 64) g = scratch(nblocks);
+    if (!regpath) g = scratch(nblocks);
 
     stamp_t0<<<1, 1, 0, c.stream>>>(c.d_t0.p);
     ++c.launches;
     ck(cudaEventRecord(c.ev0, c.stream), "event");
     if (nblocks > 0) {
-        const int rc = c.n <= 64 ? launch_sampler(p, nblocks, c.stream, 0) : launch_sampler_generic(p, nblocks, g, c.stream);
+        const int rc = regpath ? launch_sampler(p, nblocks, c.stream) : launch_sampler_generic(p, nblocks, g, c.stream);
         ck(static_cast<cudaError_t>(rc), "sampler launch");
-        c.launches += c.n <= 64 ? 1 : 2 + (long long)p.T * (cfg->alpha > 0 ? 2 : 1);
+        c.launches += regpath ? 1 : 2 + (long long)p.T * (cfg->alpha > 0 ? 2 : 1);
     }
     ck(cudaEventRecord(c.ev1, c.stream), "event");
     // Per-block flags: bit 2 = the register path's noise-event buffer overflowed (re-run the
@@ -406,12 +410,13 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         }
     if (h_first >= 0) {
         const long long gb = b_begin + h_first;
-        const int chunk128 = static_cast<int>(gb % chunks);
+        const int chunkb = static_cast<int>(gb % chunks);
         const long long rl = gb / chunks;
         const int l = static_cast<int>(rl % c.L), run = static_cast<int>(rl / c.L);
-        const int c512 = chunk128 / 4;
-        const long long rb = rl * chunks + 4ll * c512;
-        const long long re = std::min<long long>(rl * chunks + chunks, rb + 4);
+        const int per512 = 512 / bt;  // blocks per reference task (kTrajectoryChunk, solver.hpp:99)
+        const int c512 = chunkb / per512;
+        const long long rb = rl * chunks + static_cast<long long>(per512) * c512;
+        const long long re = std::min<long long>(rl * chunks + chunks, rb + per512);
         SamplerParams q = p;
         q.block_begin = rb;
         q.first_bad_step_task = 1;
@@ -450,15 +455,16 @@ void pool_get(Ctx& c, uint64_t* words, int64_t* stamps)
            "D2H");
         ck(cudaMemcpyAsync(&t0, c.d_t0.p, sizeof t0, cudaMemcpyDeviceToHost, c.stream), "D2H");
         ck(cudaStreamSynchronize(c.stream), "sync");
-        const int chunks = (c.pool_batch + kSampleBlock - 1) / kSampleBlock;
+        const int bt = c.pool_block_traj;
+        const int chunks = (c.pool_batch + bt - 1) / bt;
         for (long long i = 0; i < c.pool_size; ++i) stamps[i] = 0;
         for (long long b = 0; b < c.pool_blocks; ++b) {
             const long long gb = c.pool_block_begin + b;
             const int chunk = static_cast<int>(gb % chunks);
             const long long rl = gb / chunks;
-            const long long base = rl * c.pool_batch + static_cast<long long>(chunk) * kSampleBlock;
+            const long long base = rl * c.pool_batch + static_cast<long long>(chunk) * bt;
             const long long stamp = be[static_cast<size_t>(b)] > t0 ? static_cast<long long>(be[static_cast<size_t>(b)] - t0) : 0;
-            for (int t = 0; t < kSampleBlock && chunk * kSampleBlock + t < c.pool_batch; ++t) stamps[base + t] = stamp;
+            for (int t = 0; t < bt && chunk * bt + t < c.pool_batch; ++t) stamps[base + t] = stamp;
         }
     }
     ck(cudaStreamSynchronize(c.stream), "sync");

@@ -74,6 +74,7 @@ struct Ctx {
     long long pool_size = 0;
     int pool_runs = 0, pool_batch = 0;
     long long pool_block_begin = 0, pool_blocks = 0;
+    int pool_block_traj = 128;
     DevBuf<uint64_t> d_words;
     DevBuf<int> d_nan, d_badstep;
     DevBuf<unsigned long long> d_block_end, d_t0;

@@ -5,7 +5,14 @@
 
 namespace momc_b200 {
 
-int launch_sampler(const SamplerParams& p, long long nblocks, void* stream, int /*check_steps*/)
+bool sampler_uses_register_path(int n, double alpha) { return n >= 1 && n <= 64 && alpha > 0.0; }
+
+int sampler_block_traj(int n, double alpha)
+{
+    return sampler_uses_register_path(n, alpha) ? sbimpl::kThreads / 4 : kSampleBlock;
+}
+
+int launch_sampler(const SamplerParams& p, long long nblocks, void* stream)
 {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int n = p.n;
@@ -20,7 +27,7 @@ int launch_sampler(const SamplerParams& p, long long nblocks, void* stream, int 
         if (n <= 42) return launch_small_n42_d0(p, nblocks, st);
         if (n <= 64) return launch_small_n64_d0(p, nblocks, st);
     }
-    return cudaErrorInvalidValue;  // n > 64: launch_sampler_generic
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace momc_b200

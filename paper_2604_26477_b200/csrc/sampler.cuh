@@ -11,7 +11,7 @@
 
 namespace momc_b200 {
 
-constexpr int kSampleBlock = 128;  // trajectories per CTA (one per thread)
+constexpr int kSampleBlock = 128;  // trajectories per block of the sequential (generic) path
 constexpr int kMaxPadDeg = 4;      // max padded row length of the register-resident path
 
 struct SamplerParams {
@@ -20,7 +20,8 @@ struct SamplerParams {
     int T;            // n_iterations
     int variant;      // 0 bsb, 1 dsb, 2 simcim
     double dt, a0, alpha, init_scale, s_dt_a0;  // s_dt_a0 = dt * a0 (host-rounded, solver.hpp:176)
-    int L, batch, runs, chunks;                 // chunks = ceil(batch / kSampleBlock)
+    int L, batch, runs, chunks;                 // chunks = ceil(batch / block_traj)
+    int block_traj;                             // trajectories per block (sampler_block_traj)
     long long block_begin;                      // first flattened (run, weight, chunk) block
     uint64_t seed;
     const int* row_ptr;       // n + 1
@@ -38,8 +39,13 @@ struct SamplerParams {
     int* bad_step;            // per launched block: min first non-finite step (debug rerun)
 };
 
-// Launch the register-resident path (n <= 64) or the generic path; returns a CUDA error.
-int launch_sampler(const SamplerParams& p, long long nblocks, void* stream, int check_steps);
+// Trajectories per flattened block for this problem: the register-resident path
+// (n <= 64, alpha > 0) uses 256 / lanes-per-trajectory, the sequential path 128.
+int sampler_block_traj(int n, double alpha);
+bool sampler_uses_register_path(int n, double alpha);
+
+// Launch the register-resident path (n <= 64, alpha > 0); returns a CUDA error.
+int launch_sampler(const SamplerParams& p, long long nblocks, void* stream);
 
 // Generic path (any n; also the exact fallback for blocks flagged by the fast kernel).
 // State buffers (x, y, noise) are owned by the caller.

@@ -22,17 +22,18 @@ struct WaveCtx {
     SamplerParams p;
     long long wave_block0;  // first block (relative to p.block_begin) of this wave
     long long wave_blocks;
-    long long W;            // wave_blocks * kSampleBlock
+    long long W;            // wave_blocks * p.block_traj
 };
 
 __device__ __forceinline__ void decode(const WaveCtx& w, long long wt, int& run, int& l, int& traj, bool& active)
 {
-    const long long gblock = w.p.block_begin + w.wave_block0 + wt / kSampleBlock;
+    const int bt = w.p.block_traj;
+    const long long gblock = w.p.block_begin + w.wave_block0 + wt / bt;
     const int chunk = static_cast<int>(gblock % w.p.chunks);
     const long long rl = gblock / w.p.chunks;
     l = static_cast<int>(rl % w.p.L);
     run = static_cast<int>(rl / w.p.L);
-    traj = chunk * kSampleBlock + static_cast<int>(wt % kSampleBlock);
+    traj = chunk * bt + static_cast<int>(wt % bt);
     active = traj < w.p.batch;
 }
 
@@ -108,7 +109,7 @@ __global__ void gen_step(WaveCtx w, int t, const double* __restrict__ x, double*
 {
     const long long wb = blockIdx.x;
     const int i = blockIdx.y;
-    const long long wt = wb * kSampleBlock + threadIdx.x;
+    const long long wt = wb * w.p.block_traj + threadIdx.x;
     int run, l, traj;
     bool active;
     decode(w, wt, run, l, traj, active);
@@ -170,7 +171,7 @@ __global__ void gen_readout(WaveCtx w, const double* __restrict__ x)
         }
         w.p.words[idx * wpc + wd] = word;
     }
-    const long long blk = w.wave_block0 + wt / kSampleBlock;
+    const long long blk = w.wave_block0 + wt / w.p.block_traj;
     if (bad) w.p.nan_block[blk] = 1;
     if (w.p.block_end_ns && (threadIdx.x & 31) == 0) {
         unsigned long long tnow;
@@ -184,14 +185,14 @@ __global__ void gen_readout(WaveCtx w, const double* __restrict__ x)
 int launch_sampler_generic(const SamplerParams& p, long long nblocks, const GenericScratch& g, void* stream)
 {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const long long wave_cap = g.cap_traj / kSampleBlock;
+    const long long wave_cap = g.cap_traj / p.block_traj;
     if (wave_cap < 1) return cudaErrorInvalidValue;
     for (long long b0 = 0; b0 < nblocks; b0 += wave_cap) {
         WaveCtx w;
         w.p = p;
         w.wave_block0 = b0;
         w.wave_blocks = nblocks - b0 < wave_cap ? nblocks - b0 : wave_cap;
-        w.W = w.wave_blocks * kSampleBlock;
+        w.W = w.wave_blocks * p.block_traj;
         const unsigned grid1 = static_cast<unsigned>((w.W + 127) / 128);
         gen_init<<<grid1, 128, 0, st>>>(w, g.x, g.y);
         double* xa = g.x;
@@ -199,7 +200,7 @@ int launch_sampler_generic(const SamplerParams& p, long long nblocks, const Gene
         for (int t = 0; t < p.T; ++t) {
             if (p.alpha > 0.0) gen_noise<<<grid1, 128, 0, st>>>(w, t, g.noise);
             dim3 grid2(static_cast<unsigned>(w.wave_blocks), static_cast<unsigned>(p.n));
-            gen_step<<<grid2, kSampleBlock, 0, st>>>(w, t, xa, xb, g.y, g.noise);
+            gen_step<<<grid2, p.block_traj, 0, st>>>(w, t, xa, xb, g.y, g.noise);
             double* tmp = xa;
             xa = xb;
             xb = tmp;

@@ -1,28 +1,31 @@
 #pragma once
 // SB sampler kernel implementation (see sampler.cuh), included by sampler_n*.cu.
 //
-// Design. A CTA integrates 128 trajectories of one (run, weight) with
-// 256 threads: the two lanes 2t, 2t+1 of a warp own trajectory t and each keeps half of
-// its spins (x, y) in registers, fully unrolled over NH = NMAX/2 spins. Halving the
-// per-thread state halves registers (4 warps per scheduler instead of 2) and the
-// unrolled code (the step loop fits the 32 KB L1.5 instruction cache; the first
-// version thrashed it). Per step t, the (trajectory, t) noise stream (solver.hpp:128-136)
-// is handled in three branch-light phases instead of the reference's sequential
-// next_normal():
-//   A1  the pair generates the Philox blocks of the stream (even blocks on lane 0, odd
-//       on lane 1) into shared memory and marks, per word, whether a ziggurat attempt
-//       starting there takes the fast path (|hz| < kn[iz]) -> 128-bit mask F;
-//   A2  both lanes walk only the slow attempts (~0.5 per thread-step) -- wedge
-//       accept/reject and tail draws exactly as rng.hpp:156-185 -- producing a short list
+// Design. A CTA of 256 threads integrates TPC = 256/LANES trajectories
+// of one (run, weight). The LANES consecutive lanes of a warp that own a trajectory each
+// keep NQ = ceil(NMAX/LANES) of its spins (x, y) in registers, fully unrolled. Splitting a
+// trajectory over lanes cuts the per-thread state and the unrolled step loop (which must
+// stay inside the 32 KB L1.5 instruction cache; a one-thread-per-trajectory version
+// thrashed it) and raises the number of resident warps. Spins past n ("phantoms", when
+// LANES*NQ > n) are integrated too: they have no couplings, draw their normals after the
+// n real ones, and are masked out of the readout, so no per-spin bound checks are needed.
+//
+// Per step t the (trajectory, t) noise stream (solver.hpp:128-136) is handled in three
+// branch-light phases instead of the reference's sequential next_normal():
+//   A1  the lanes generate the Philox blocks of the stream (block b on lane b % LANES)
+//       into shared memory and mark, per word, whether a ziggurat attempt starting there
+//       takes the fast path (|hz| < kn[iz]) -> 128-bit mask F (OR-reduced over the lanes);
+//   A2  every lane walks only the slow attempts (~0.5 per trajectory-step): wedge
+//       accept/reject and tail draws exactly as rng.hpp:156-185, producing a short list
 //       of "offset changes" / "special values" for the normal indices they affect;
 //   B   the unrolled spin update reconstructs normal i as hz*wn[iz] of word i + off(i)
 //       (or the special value): every fast normal is independent of the others.
-// The coupling phi(x_j) (x_j for bSB/SimCIM, sgn(x_j) for dSB) is gathered from a
-// per-trajectory shared-memory column written once per step. Rows of J(c_l) are runtime
-// CSR rows (DMAX = 0) or rows padded to DMAX entries with exact zeros (DMAX > 0) whose
-// column indices are kernel parameters (constant bank). All FP64 arithmetic is explicitly
-// rounded (__dmul_rn/__dadd_rn/__dsub_rn) in the reference's order: final spins are
-// bit-identical to the shim build of the reference.
+// phi(x_j) (x_j for bSB/SimCIM, sgn(x_j) for dSB) is gathered from the trajectory's
+// shared-memory column, rewritten once per step. Rows of J(c_l) are runtime CSR rows
+// (DMAX = 0) or rows padded to DMAX entries with exact zeros (DMAX > 0). All FP64
+// arithmetic is explicitly rounded (__dmul_rn/__dadd_rn/__dsub_rn) in the reference's
+// order: final spins are bit-identical to the shim build of the reference.
+// Noise-free runs (alpha = 0) take the sequential path (sampler_generic.cu).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -34,7 +37,7 @@ namespace momc_b200 {
 
 namespace sbimpl {
 
-constexpr int kThreads = 2 * kSampleBlock;  // two lanes per trajectory
+constexpr int kThreads = 256;
 
 __device__ __forceinline__ unsigned long long globaltimer()
 {
@@ -55,21 +58,22 @@ __device__ __forceinline__ uint32_t zmag(uint32_t u)
     return static_cast<int32_t>(u) < 0 ? 0u - u : u;
 }
 
-template <int NMAX>
+template <int NMAX, int LANES>
 struct Geo {
-    static constexpr int kNH = NMAX / 2;            // spins per lane
-    static constexpr int kNB = (NMAX + 3) / 4 + 2;  // Philox blocks pre-generated per step (even count below)
-    static constexpr int kNBe = (kNB + 1) / 2 * 2;
-    static constexpr int kNU = 4 * kNBe;            // words covered by the fast mask (<= 128)
-    static constexpr int kNA = kNU + 16;            // allocated words (A2 extends on demand)
-    static constexpr int kUS = kSampleBlock + 1;    // word-row stride (odd: pair lanes hit distinct banks)
-    static constexpr int kECAP = 8;                 // event entries per lane-step
-    static constexpr int zig = 0;                                  // ZigTables (2560 B)
-    static constexpr int ubuf = 2560;                              // kNA x kUS u32
-    static constexpr int ent = ubuf + (kNA * kUS * 4 + 15) / 16 * 16;  // kECAP x 256 u32
-    static constexpr int entv = ent + kECAP * kThreads * 4;        // kECAP x 256 f64
-    static constexpr int phi = entv + kECAP * kThreads * 8;        // NMAX x 128 f64
-    static constexpr int csr = phi + NMAX * kSampleBlock * 8;
+    static constexpr int kTPC = kThreads / LANES;           // trajectories per CTA
+    static constexpr int kNQ = (NMAX + LANES - 1) / LANES;  // spins per lane
+    static constexpr int kNP = kNQ * LANES;                 // integrated spins (>= n)
+    static constexpr int kNB = ((kNP + 3) / 4 + 2 + LANES - 1) / LANES * LANES;  // Philox blocks per step
+    static constexpr int kNU = 4 * kNB;                     // words covered by the fast mask
+    static constexpr int kNA = kNU + 16;                    // allocated words (A2 extends on demand)
+    static constexpr int kUS = kTPC + 1;                    // word-row stride (odd: lanes of a trajectory hit distinct banks)
+    static constexpr int kECAP = 8;                         // event entries per trajectory-step
+    static constexpr int zig = 0;                                           // ZigTables (2560 B)
+    static constexpr int ubuf = 2560;                                       // kNA x kUS u32
+    static constexpr int ent = ubuf + (kNA * kUS * 4 + 15) / 16 * 16;       // kECAP x kTPC u32
+    static constexpr int entv = ent + kECAP * kTPC * 4;                     // kECAP x kTPC f64
+    static constexpr int phi = entv + kECAP * kTPC * 8;                     // kNP x kTPC f64
+    static constexpr int csr = phi + kNP * kTPC * 8;
     static_assert(kNU <= 128, "mask covers at most 128 words");
 };
 
@@ -93,18 +97,28 @@ __device__ __forceinline__ int next_slow(uint64_t F0, uint64_t F1, int from)
     return kNU;
 }
 
-template <int NMAX>
+template <int LANES>
 constexpr int min_blocks()
 {
-    return NMAX <= 42 ? 2 : 1;
+    return LANES == 4 ? 3 : 2;
 }
 
-// Register-resident integrator for n <= NMAX <= 64, two lanes per trajectory.
-template <int NMAX, int VAR, int DMAX>
-__global__ void __launch_bounds__(kThreads, min_blocks<NMAX>()) sb_small_kernel(const SamplerParams p)
+template <int LANES>
+__device__ __forceinline__ uint64_t lane_or(unsigned mask, uint64_t v)
 {
-    using G = Geo<NMAX>;
-    constexpr int NH = G::kNH;
+#pragma unroll
+    for (int o = 1; o < LANES; o <<= 1) v |= __shfl_xor_sync(mask, v, o);
+    return v;
+}
+
+// Register-resident integrator for n <= NMAX <= 64, LANES lanes per trajectory.
+template <int NMAX, int LANES, int VAR, int DMAX>
+__global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel(const SamplerParams p)
+{
+    using G = Geo<NMAX, LANES>;
+    constexpr int TPC = G::kTPC;
+    constexpr int NQ = G::kNQ;
+    constexpr int NP = G::kNP;
     constexpr int US = G::kUS;
     extern __shared__ __align__(16) unsigned char smem[];
     ZigTables* zig = reinterpret_cast<ZigTables*>(smem + G::zig);
@@ -113,11 +127,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NMAX>()) sb_small_kernel(
     double* entv = reinterpret_cast<double*>(smem + G::entv);
     double* phis = reinterpret_cast<double*>(smem + G::phi);
     unsigned char* csr = smem + G::csr;
-    // DMAX == 0: rp[n+1] | cv[nnz] | cc[nnz];  DMAX > 0: pv[n*DMAX] (columns in p.pad_col)
+    // DMAX == 0: rp[NP+1] | cv[nnz] | cc[nnz];  DMAX > 0: pc[NP*DMAX] int | pv[NP*DMAX] f64
     int* rp = reinterpret_cast<int*>(csr);
-    double* cv = reinterpret_cast<double*>(csr + ((NMAX + 1) * 4 + 15) / 16 * 16);
+    double* cv = reinterpret_cast<double*>(csr + ((NP + 1) * 4 + 15) / 16 * 16);
     int* cc = reinterpret_cast<int*>(cv + p.nnz);
-    double* pv = reinterpret_cast<double*>(csr);
+    int* pc = reinterpret_cast<int*>(csr);
+    double* pv = reinterpret_cast<double*>(csr + (NP * DMAX * 4 + 15) / 16 * 16);
 
     const int n = p.n;
     const long long gblock = p.block_begin + blockIdx.x;
@@ -126,15 +141,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NMAX>()) sb_small_kernel(
     const int l = static_cast<int>(rl % p.L);
     const int run = static_cast<int>(rl / p.L);
     const int tid = threadIdx.x;
-    const int t_loc = tid >> 1;  // trajectory within the CTA
-    const int h = tid & 1;       // which half of the spins this lane owns
+    const int t_loc = tid / LANES;  // trajectory within the CTA
+    const int h = tid % LANES;      // which quarter/half of the spins this lane owns
 
-    {  // CTA setup: ziggurat tables, coupling rows of J(c_l)
+    {  // CTA setup: ziggurat tables, coupling rows of J(c_l) (phantom rows: empty / zero)
         const uint32_t* src = reinterpret_cast<const uint32_t*>(p.zig);
         uint32_t* dst = reinterpret_cast<uint32_t*>(zig);
         for (int i = tid; i < static_cast<int>(sizeof(ZigTables) / 4); i += kThreads) dst[i] = src[i];
         if constexpr (DMAX == 0) {
-            for (int i = tid; i <= n; i += kThreads) rp[i] = p.row_ptr[i];
+            for (int i = tid; i <= NP; i += kThreads) rp[i] = p.row_ptr[i < n ? i : n];
             const double* v = p.vals + static_cast<long long>(l) * p.nnz;
             for (int i = tid; i < p.nnz; i += kThreads) {
                 cv[i] = v[i];
@@ -142,76 +157,53 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NMAX>()) sb_small_kernel(
             }
         } else {
             const double* v = p.pad_vals + static_cast<long long>(l) * n * DMAX;
-            for (int i = tid; i < n * DMAX; i += kThreads) pv[i] = v[i];
+            for (int q = tid; q < NP * DMAX; q += kThreads) {
+                const int i = q / DMAX;
+                pc[q] = (i < n ? p.pad_col[q] : i) * TPC * 8;  // byte offset of phi row j
+                pv[q] = i < n ? v[q] : 0.0;
+            }
         }
     }
     __syncthreads();
 
-    const int traj = chunk * kSampleBlock + t_loc;
-    const unsigned wmask = __ballot_sync(0xffffffffu, traj < p.batch);  // pairs are never split
+    const int traj = chunk * TPC + t_loc;
+    const unsigned wmask = __ballot_sync(0xffffffffu, traj < p.batch);  // trajectories never split
     if (traj >= p.batch) return;  // no CTA-wide barrier below this point
 
     const uint64_t key = run_key(p.seed, static_cast<uint32_t>(run));
     const uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
     const uint32_t wl = static_cast<uint32_t>(l), tr = static_cast<uint32_t>(traj);
     const double c0 = p.c0[l];
-    const int s0 = h * NH;  // first spin of this lane
+    const double alpha = p.alpha, dt = p.dt, sdt = p.s_dt_a0;
+    const int s0 = h * NQ;  // first spin of this lane
 
-    // ---- init_state (solver.hpp:108-124): spin i uses words 2i, 2i+1 of the init_x / init_y
-    //      streams, i.e. block i/2, half i%2
-    double x[NH];
-    double y[NH];
+    // ---- init_state (solver.hpp:108-124): spin i uses words 2i, 2i+1 of the init_x /
+    //      init_y streams (block i/2, half i%2)
+    double x[NQ];
+    double y[NQ];
 #pragma unroll
-    for (int s = 0; s < NH; s += 2) {
-        const int i = s0 + s;  // even
-        if (i < n) {
-            const uint4 rx = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitX, 0), tr, wl);
-            const uint4 ry = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitY, 0), tr, wl);
-            x[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(rx.x, rx.y)), 1.0));
-            y[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(ry.x, ry.y)), 1.0));
-            if (s + 1 < NH) {
-                x[s + 1] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(rx.z, rx.w)), 1.0));
-                y[s + 1] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(ry.z, ry.w)), 1.0));
-            }
-        } else {
-            x[s] = y[s] = 0.0;
-            if (s + 1 < NH) x[s + 1] = y[s + 1] = 0.0;
-        }
-    }
-    // NH odd (e.g. 21): lane 1's first spin is odd -> the loop above paired (i, i+1) from
-    // block i/2 assuming i even; recompute the odd-start case exactly
-    if constexpr ((NH & 1) != 0) {
-        if (h == 1) {
-#pragma unroll
-            for (int s = 0; s < NH; ++s) {
-                const int i = s0 + s;
-                if (i < n) {
-                    const uint4 rx = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitX, 0), tr, wl);
-                    const uint4 ry = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitY, 0), tr, wl);
-                    const bool hi = i & 1;
-                    x[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, hi ? u01_from(rx.z, rx.w) : u01_from(rx.x, rx.y)), 1.0));
-                    y[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, hi ? u01_from(ry.z, ry.w) : u01_from(ry.x, ry.y)), 1.0));
-                } else {
-                    x[s] = y[s] = 0.0;
-                }
-            }
-        }
-    }
-
-    double* ph = phis + t_loc;  // phi_j of this trajectory at ph[j * 128]
-#pragma unroll
-    for (int s = 0; s < NH; ++s) {
+    for (int s = 0; s < NQ; ++s) {
         const int i = s0 + s;
-        if (i < n) ph[i * kSampleBlock] = VAR == 1 ? (x[s] < 0.0 ? -1.0 : 1.0) : x[s];
+        const uint4 rx = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitX, 0), tr, wl);
+        const uint4 ry = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitY, 0), tr, wl);
+        const bool odd = i & 1;
+        x[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(rx.z, rx.w) : u01_from(rx.x, rx.y)), 1.0));
+        y[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(ry.z, ry.w) : u01_from(ry.x, ry.y)), 1.0));
     }
+
+    double* ph = phis + t_loc;  // phi_j of this trajectory at ph[j * TPC]
+    const unsigned char* phb = reinterpret_cast<const unsigned char*>(ph);
+#pragma unroll
+    for (int s = 0; s < NQ; ++s) ph[(s0 + s) * TPC] = VAR == 1 ? (x[s] < 0.0 ? -1.0 : 1.0) : x[s];
 
     const uint32_t* kn = zig->kn;
     const double* wn = zig->wn;
     const double* fn = zig->fn;
-    const bool noisy = p.alpha > 0.0;
     uint32_t* ub = ubuf + t_loc;  // this trajectory's word column, stride US
-    uint32_t* en = ent + tid;     // this lane's event column, stride kThreads
-    double* ev = entv + tid;
+    uint32_t* en = ent + t_loc;   // this trajectory's event column, stride TPC
+    double* ev = entv + t_loc;
+    const int* pcs = pc + s0 * DMAX;
+    const double* pvs = pv + s0 * DMAX;
     bool overflow = false;
     __syncwarp(wmask);
 
@@ -221,42 +213,40 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NMAX>()) sb_small_kernel(
         const double pump = __dmul_rn(-0.5, __dsub_rn(1.0, a_t));  // simcim_schedule
         const uint32_t lo = tag_word(kTagStepNoise, static_cast<uint32_t>(t));
 
-        int ne = 0;     // events this step
-        int e = 0;      // next event to apply
-        int nxt = 255;  // normal index of the next event
-        int off = 0;    // current word offset of the fast normals
-        if (noisy) {
-            // ---- A1: Philox blocks (lane h: blocks h, h+2, ...) + fast-attempt mask
-            uint64_t F0 = 0, F1 = 0;
+        // ---- A1: Philox blocks (lane h: blocks h, h+LANES, ...) + fast-attempt mask
+        uint64_t F0 = 0, F1 = 0;
 #pragma unroll 1
-            for (int b = h; b < G::kNBe; b += 2) {
-                const uint4 r = philox(k0, k1, static_cast<uint32_t>(b), lo, tr, wl);
-                ub[(4 * b + 0) * US] = r.x;
-                ub[(4 * b + 1) * US] = r.y;
-                ub[(4 * b + 2) * US] = r.z;
-                ub[(4 * b + 3) * US] = r.w;
-                const uint64_t f = static_cast<uint64_t>(zmag(r.x) < kn[r.x & 127u]) |
-                                   static_cast<uint64_t>(zmag(r.y) < kn[r.y & 127u]) << 1 |
-                                   static_cast<uint64_t>(zmag(r.z) < kn[r.z & 127u]) << 2 |
-                                   static_cast<uint64_t>(zmag(r.w) < kn[r.w & 127u]) << 3;
-                const int pp = 4 * b;
-                if (pp < 64) F0 |= f << pp;
-                else F1 |= f << (pp - 64);
-            }
-            F0 |= __shfl_xor_sync(wmask, F0, 1);
-            F1 |= __shfl_xor_sync(wmask, F1, 1);
-            __syncwarp(wmask);  // partner's words visible
-            // ---- A2: resolve the slow attempts (rng.hpp:164-184), redundantly on both lanes
+        for (int b = h; b < G::kNB; b += LANES) {
+            const uint4 r = philox(k0, k1, static_cast<uint32_t>(b), lo, tr, wl);
+            ub[(4 * b + 0) * US] = r.x;
+            ub[(4 * b + 1) * US] = r.y;
+            ub[(4 * b + 2) * US] = r.z;
+            ub[(4 * b + 3) * US] = r.w;
+            const uint64_t f = static_cast<uint64_t>(zmag(r.x) < kn[r.x & 127u]) |
+                               static_cast<uint64_t>(zmag(r.y) < kn[r.y & 127u]) << 1 |
+                               static_cast<uint64_t>(zmag(r.z) < kn[r.z & 127u]) << 2 |
+                               static_cast<uint64_t>(zmag(r.w) < kn[r.w & 127u]) << 3;
+            const int pp = 4 * b;
+            if (pp < 64) F0 |= f << pp;
+            else F1 |= f << (pp - 64);
+        }
+        F0 = lane_or<LANES>(wmask, F0);
+        F1 = lane_or<LANES>(wmask, F1);
+        __syncwarp(wmask);  // the other lanes' words are visible
+
+        // ---- A2: resolve the slow attempts (rng.hpp:164-184), identically on every lane
+        int ne = 0;
+        {
             int gen = G::kNU;  // words present in ub
             int pos = 0, i = 0;
             for (;;) {
-                const int last = pos + (n - 1 - i);  // position of normal n-1 if the rest is fast
+                const int last = pos + (NP - 1 - i);  // position of normal NP-1 if the rest is fast
                 int q = next_slow<G::kNU>(F0, F1, pos);
                 if (q >= G::kNU) {  // beyond the mask: extend the word buffer, test on demand
                     q = pos > G::kNU ? pos : G::kNU;
                     for (; q <= last; ++q) {
                         if (q >= G::kNA) break;
-                        while (gen <= q) {  // both lanes write identical words
+                        while (gen <= q) {  // every lane writes the same words
                             const uint4 r = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
                             ub[(gen + 0) * US] = r.x;
                             ub[(gen + 1) * US] = r.y;
@@ -334,90 +324,83 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NMAX>()) sb_small_kernel(
                 // event: from normal new_i on, words continue at offset new_pos - new_i; a tail
                 // also pins normal iq to sval (one event per normal index: later ones replace)
                 const int idx = special ? iq : new_i;
-                if (ne > 0 && static_cast<int>(en[(ne - 1) * kThreads] & 0xFFu) == idx) --ne;
+                if (ne > 0 && static_cast<int>(en[(ne - 1) * TPC] & 0xFFu) == idx) --ne;
                 if (ne >= G::kECAP) {
                     overflow = true;
                     break;
                 }
-                en[ne * kThreads] = static_cast<uint32_t>(idx) | (static_cast<uint32_t>(new_pos - new_i) << 8) |
-                                    (special ? 1u << 16 : 0u);
-                if (special) ev[ne * kThreads] = sval;
+                en[ne * TPC] = static_cast<uint32_t>(idx) | (static_cast<uint32_t>(new_pos - new_i) << 8) |
+                               (special ? 1u << 16 : 0u);
+                if (special) ev[ne * TPC] = sval;
                 ++ne;
                 pos = new_pos;
                 i = new_i;
-                if (i >= n) break;
+                if (i >= NP) break;
             }
-            // lane 1 starts at normal NH: apply the events of earlier normals
-            while (e < ne) {
-                const uint32_t w = en[e * kThreads];
-                if (static_cast<int>(w & 0xFFu) >= s0) break;
-                off = static_cast<int>((w >> 8) & 0xFFu);
-                ++e;
-            }
-            nxt = e < ne ? static_cast<int>(en[e * kThreads] & 0xFFu) : 255;
         }
+        // lanes h > 0 start at normal s0: apply the events of earlier normals
+        int e = 0, off = 0;
+        while (e < ne) {
+            const uint32_t w = en[e * TPC];
+            if (static_cast<int>(w & 0xFFu) >= s0) break;
+            off = static_cast<int>((w >> 8) & 0xFFu);
+            ++e;
+        }
+        int nxt = e < ne ? static_cast<int>(en[e * TPC] & 0xFFu) - s0 : 255;  // lane-local spin index
 
         // ---- B: spin updates (sb_step solver.hpp:159-181 / simcim_step :196-210)
+        const uint32_t* ubs = ub + s0 * US;
 #pragma unroll
-        for (int s = 0; s < NH; ++s) {
-            const int i = s0 + s;
-            if (i < n) {
-                double eta = 0.0;
-                if (noisy) {
-                    bool sp = false;
-                    double spv = 0.0;
-                    if (i == nxt) {
-                        const uint32_t w = en[e * kThreads];
-                        off = static_cast<int>((w >> 8) & 0xFFu);
-                        if (w >> 16) {
-                            sp = true;
-                            spv = ev[e * kThreads];
-                        }
-                        ++e;
-                        nxt = e < ne ? static_cast<int>(en[e * kThreads] & 0xFFu) : 255;
-                    }
-                    const uint32_t u = ub[(sp ? 0 : i + off) * US];
-                    const double v = __dmul_rn(i32_to_f64(static_cast<int32_t>(u)), wn[u & 127u]);
-                    eta = sp ? spv : v;
+        for (int s = 0; s < NQ; ++s) {
+            bool sp = false;
+            double spv = 0.0;
+            if (s == nxt) {  // rare: an event changes the word offset at this normal
+                const uint32_t w = en[e * TPC];
+                off = static_cast<int>((w >> 8) & 0xFFu);
+                if (w >> 16) {
+                    sp = true;
+                    spv = ev[e * TPC];
                 }
-                // coupled_i = sum_j J_ij phi(x_j), j ascending, from +0.0 (shim GEMM order)
-                double coupled = 0.0;
-                if constexpr (DMAX > 0) {
-#pragma unroll
-                    for (int d = 0; d < DMAX; ++d) {
-                        const int j = p.pad_col[i * DMAX + d];  // constant-bank operand
-                        coupled = __dadd_rn(coupled, __dmul_rn(pv[i * DMAX + d], ph[j * kSampleBlock]));
-                    }
-                } else {
-                    const int e1 = rp[i + 1];
-                    for (int q = rp[i]; q < e1; ++q) coupled = __dadd_rn(coupled, __dmul_rn(cv[q], ph[cc[q] * kSampleBlock]));
-                }
-                double xi = x[s], yi = y[s];
-                if constexpr (VAR == 2) {
-                    double d = __dsub_rn(__dmul_rn(pump, xi), __dmul_rn(c0, coupled));
-                    if (noisy) d = __dadd_rn(d, __dmul_rn(p.alpha, eta));
-                    yi = __dadd_rn(__dmul_rn(0.9, yi), __dmul_rn(1.0 - 0.9, d));
-                    xi = __dadd_rn(xi, __dmul_rn(p.dt, yi));
-                } else {
-                    double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled));
-                    if (noisy) d = __dadd_rn(d, __dmul_rn(p.alpha, eta));
-                    yi = __dadd_rn(yi, __dmul_rn(p.dt, d));
-                    xi = __dadd_rn(xi, __dmul_rn(p.s_dt_a0, yi));
-                    yi = fabs(xi) > 1.0 ? 0.0 : yi;
-                }
-                // cwiseMax(-1).cwiseMin(1) == std::max/std::min (NaN propagates)
-                xi = (xi < -1.0) ? -1.0 : xi;
-                xi = (1.0 < xi) ? 1.0 : xi;
-                x[s] = xi;
-                y[s] = yi;
+                ++e;
+                nxt = e < ne ? static_cast<int>(en[e * TPC] & 0xFFu) - s0 : 255;
             }
-        }
-        __syncwarp(wmask);  // the pair has finished reading phi(t) and this step's words
+            const uint32_t u = ubs[(s + off) * US];
+            double eta = __dmul_rn(i32_to_f64(static_cast<int32_t>(u)), wn[u & 127u]);
+            eta = sp ? spv : eta;
+            // coupled_i = sum_j J_ij phi(x_j), j ascending, from +0.0 (shim GEMM order)
+            double coupled = 0.0;
+            if constexpr (DMAX > 0) {
 #pragma unroll
-        for (int s = 0; s < NH; ++s) {
-            const int i = s0 + s;
-            if (i < n) ph[i * kSampleBlock] = VAR == 1 ? (x[s] < 0.0 ? -1.0 : 1.0) : x[s];
+                for (int d = 0; d < DMAX; ++d) {
+                    const double phj = *reinterpret_cast<const double*>(phb + pcs[s * DMAX + d]);
+                    coupled = __dadd_rn(coupled, __dmul_rn(pvs[s * DMAX + d], phj));
+                }
+            } else {
+                const int i = s0 + s;
+                const int e1 = rp[i + 1];
+                for (int q = rp[i]; q < e1; ++q) coupled = __dadd_rn(coupled, __dmul_rn(cv[q], ph[cc[q] * TPC]));
+            }
+            double xi = x[s], yi = y[s];
+            if constexpr (VAR == 2) {
+                const double d = __dadd_rn(__dsub_rn(__dmul_rn(pump, xi), __dmul_rn(c0, coupled)), __dmul_rn(alpha, eta));
+                yi = __dadd_rn(__dmul_rn(0.9, yi), __dmul_rn(1.0 - 0.9, d));
+                xi = __dadd_rn(xi, __dmul_rn(dt, yi));
+            } else {
+                const double d =
+                    __dadd_rn(__dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled)), __dmul_rn(alpha, eta));
+                yi = __dadd_rn(yi, __dmul_rn(dt, d));
+                xi = __dadd_rn(xi, __dmul_rn(sdt, yi));
+                yi = fabs(xi) > 1.0 ? 0.0 : yi;
+            }
+            // cwiseMax(-1).cwiseMin(1) == std::max/std::min (NaN propagates)
+            xi = (xi < -1.0) ? -1.0 : xi;
+            xi = (1.0 < xi) ? 1.0 : xi;
+            x[s] = xi;
+            y[s] = yi;
         }
+        __syncwarp(wmask);  // every lane has finished reading phi(t) and this step's words
+#pragma unroll
+        for (int s = 0; s < NQ; ++s) ph[(s0 + s) * TPC] = VAR == 1 ? (x[s] < 0.0 ? -1.0 : 1.0) : x[s];
         __syncwarp(wmask);  // phi(t+1) complete
     }
 
@@ -425,14 +408,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NMAX>()) sb_small_kernel(
     uint64_t word = 0;
     bool bad = false;
 #pragma unroll
-    for (int s = 0; s < NH; ++s) {
+    for (int s = 0; s < NQ; ++s) {
         const int i = s0 + s;
         if (i < n) {
             word |= static_cast<uint64_t>(!(x[s] < 0.0)) << i;
             bad |= x[s] != x[s];
         }
     }
-    word |= __shfl_xor_sync(wmask, word, 1);
+    word = lane_or<LANES>(wmask, word);
     if (h == 0) {
         const long long idx = (static_cast<long long>(run) * p.L + l) * p.batch + traj;
         p.words[idx] = word;
@@ -444,13 +427,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NMAX>()) sb_small_kernel(
     if (p.block_end_ns && (tid & 31) == 0) atomicMax(&p.block_end_ns[blockIdx.x], globaltimer());
 }
 
-template <int NMAX, int VAR, int DMAX>
+template <int NMAX, int LANES, int VAR, int DMAX>
 int launch_small(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
-    using G = Geo<NMAX>;
-    const int csr_bytes = DMAX == 0 ? ((NMAX + 1) * 4 + 15) / 16 * 16 + p.nnz * 12 : p.n * DMAX * 8;
+    using G = Geo<NMAX, LANES>;
+    const int csr_bytes = DMAX == 0 ? ((G::kNP + 1) * 4 + 15) / 16 * 16 + p.nnz * 12
+                                    : (G::kNP * DMAX * 4 + 15) / 16 * 16 + G::kNP * DMAX * 8;
     const int smem = G::csr + csr_bytes + 16;
-    auto kern = sb_small_kernel<NMAX, VAR, DMAX>;
+    auto kern = sb_small_kernel<NMAX, LANES, VAR, DMAX>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const long long kMaxGrid = 1ll << 30;
@@ -467,13 +451,13 @@ int launch_small(const SamplerParams& p, long long nblocks, cudaStream_t st)
     return cudaSuccess;
 }
 
-template <int NMAX, int DMAX>
+template <int NMAX, int LANES, int DMAX>
 int launch_variant(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
     switch (p.variant) {
-        case 0: return launch_small<NMAX, 0, DMAX>(p, nblocks, st);
-        case 1: return launch_small<NMAX, 1, DMAX>(p, nblocks, st);
-        default: return launch_small<NMAX, 2, DMAX>(p, nblocks, st);
+        case 0: return launch_small<NMAX, LANES, 0, DMAX>(p, nblocks, st);
+        case 1: return launch_small<NMAX, LANES, 1, DMAX>(p, nblocks, st);
+        default: return launch_small<NMAX, LANES, 2, DMAX>(p, nblocks, st);
     }
 }
 

@@ -4,6 +4,6 @@
 namespace momc_b200 {
 int launch_small_n16_d3(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
-    return sbimpl::launch_variant<16, 3>(p, nblocks, st);
+    return sbimpl::launch_variant<16, 4, 3>(p, nblocks, st);
 }
 }  // namespace momc_b200

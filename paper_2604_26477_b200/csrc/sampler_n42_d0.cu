@@ -4,6 +4,6 @@
 namespace momc_b200 {
 int launch_small_n42_d0(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
-    return sbimpl::launch_variant<42, 0>(p, nblocks, st);
+    return sbimpl::launch_variant<42, 4, 0>(p, nblocks, st);
 }
 }  // namespace momc_b200
