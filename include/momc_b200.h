@@ -92,6 +92,60 @@ int momc_b200_run_sampler(momc_ctx* ctx, const momc_instance_view* inst, const i
                           const momc_solver_cfg* cfg, int runs, uint64_t* out_words, int64_t* out_stamps_ns,
                           double* out_seconds /* [model_construction, sampling] */, char* err, size_t errlen);
 
+
+/* ---------------------------------------------------------------- Pareto stage (pareto.hpp) */
+/* non_dominated_filter(pool, inst) (pareto.hpp:370-410) on the pool resident in the context
+ * (after momc_b200_sample). The archive (lexicographically descending, one lex-smallest
+ * configuration per vector) stays resident. seconds (nullable, 5 entries): dedup, eval,
+ * collapse, front, archive order. Synchronous. */
+int momc_b200_filter(momc_ctx* ctx, int64_t* out_F, double* seconds, char* err, size_t errlen);
+/* the same over M host configs (M x wpc words) for the resident instance */
+int momc_b200_filter_pool(momc_ctx* ctx, const uint64_t* words, size_t M, int64_t* out_F, double* filtering_s,
+                          char* err, size_t errlen);
+/* non_dominated_filter(vector<ObjectiveVector>) (pareto.hpp:253-293); sense 0 = cut (max),
+ * 1 = hamiltonian (min). Host values M x k. */
+int momc_b200_filter_values(momc_ctx* ctx, const double* vals, size_t M, int k, int sense, int64_t* out_F,
+                            char* err, size_t errlen);
+/* merge of configuration-carrying archives (multi-GPU allgather): device values M x k and
+ * device configs M x wpc; equal vectors keep the lexicographically smallest config. */
+int momc_b200_filter_values_dev(momc_ctx* ctx, const double* d_vals, const uint64_t* d_words, int wpc, size_t M,
+                                int k, int64_t* out_F, char* err, size_t errlen);
+/* resident archive: size, host copy, device pointers, device-to-device copy */
+int64_t momc_b200_archive_size(momc_ctx* ctx);
+int momc_b200_archive_get(momc_ctx* ctx, double* vals, uint64_t* words, char* err, size_t errlen);
+int momc_b200_archive_copy_device(momc_ctx* ctx, double* d_vals, uint64_t* d_words, char* err, size_t errlen);
+
+/* hypervolume(archive, r) (pareto.hpp:540-552) of F host vectors, or of the resident archive */
+int momc_b200_hypervolume(momc_ctx* ctx, const double* vals, int64_t F, int k, const double* r, double* out,
+                          char* err, size_t errlen);
+int momc_b200_archive_hypervolume(momc_ctx* ctx, const double* r, double* out, char* err, size_t errlen);
+/* detail::evaluate_cuts (pareto.hpp:330-363): U host configs -> U x k cut values */
+int momc_b200_evaluate_cuts(momc_ctx* ctx, const uint64_t* words, size_t U, double* out, char* err, size_t errlen);
+/* reference_point_sampled (pareto.hpp:620-642) and clamp_reference under the resident archive (:647-655) */
+int momc_b200_reference_point_sampled(momc_ctx* ctx, int count, uint64_t seed, double* r, char* err, size_t errlen);
+int momc_b200_clamp_reference(momc_ctx* ctx, double* r, char* err, size_t errlen);
+
+/* ---------------------------------------------------------------- pipeline (pipeline.hpp:309-393) */
+typedef struct {
+    double model_construction_s; /* instance + lattice scalarisation (build_block_system) */
+    double sampling_s;           /* run_sampler integration + readout (device events) */
+    double pareto_filtering_s;   /* dedup + eval + collapse + front + order + reference + HV */
+    double end_to_end_s;         /* wall clock of the whole call, host copies included */
+    int64_t pool_size, unique_configs, unique_vectors, archive_size;
+    double hv;
+    double reference[16];
+    double dedup_s, eval_s, collapse_s, front_s, order_s, reference_s, hv_s;
+    int front_method; /* 1 compressed grid, 2 all-pairs */
+} momc_bench_report;
+
+/* bench(): instance -> scalarise L weight vectors -> sample runs*L*batch -> filter ->
+ * reference point (sampled:ref_count with the solver seed, clamped under the archive, or
+ * `fixed_ref` when non-NULL) -> hypervolume. The pool is copied to out_pool when non-NULL
+ * (momc::BenchResult::pool); the archive stays resident (momc_b200_archive_get). */
+int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t* nums, int L, int H,
+                    const momc_solver_cfg* cfg, int runs, int ref_count, const double* fixed_ref, uint64_t* out_pool,
+                    momc_bench_report* report, char* err, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

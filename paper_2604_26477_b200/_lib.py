@@ -35,6 +35,31 @@ class SolverCfgC(C.Structure):
     ]
 
 
+class BenchReportC(C.Structure):
+    """momc_bench_report (include/momc_b200.h)."""
+
+    _fields_ = [
+        ("model_construction_s", C.c_double),
+        ("sampling_s", C.c_double),
+        ("pareto_filtering_s", C.c_double),
+        ("end_to_end_s", C.c_double),
+        ("pool_size", C.c_int64),
+        ("unique_configs", C.c_int64),
+        ("unique_vectors", C.c_int64),
+        ("archive_size", C.c_int64),
+        ("hv", C.c_double),
+        ("reference", C.c_double * 16),
+        ("dedup_s", C.c_double),
+        ("eval_s", C.c_double),
+        ("collapse_s", C.c_double),
+        ("front_s", C.c_double),
+        ("order_s", C.c_double),
+        ("reference_s", C.c_double),
+        ("hv_s", C.c_double),
+        ("front_method", C.c_int),
+    ]
+
+
 class InstanceViewC(C.Structure):
     """momc_instance_view (include/momc_b200.h)."""
 
@@ -65,6 +90,21 @@ SIGNATURES = [
     ("momc_b200_pool_device", vp, [vp]),
     ("momc_b200_run_sampler", C.c_int, [vp, C.POINTER(InstanceViewC), i32p, C.c_int, C.c_int,
                                         C.POINTER(SolverCfgC), C.c_int, u64p, i64p, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_filter", C.c_int, [vp, i64p, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_filter_pool", C.c_int, [vp, u64p, C.c_size_t, i64p, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_filter_values", C.c_int, [vp, dp, C.c_size_t, C.c_int, C.c_int, i64p, C.c_char_p, C.c_size_t]),
+    ("momc_b200_filter_values_dev", C.c_int, [vp, vp, vp, C.c_int, C.c_size_t, C.c_int, i64p, C.c_char_p,
+                                              C.c_size_t]),
+    ("momc_b200_archive_size", C.c_int64, [vp]),
+    ("momc_b200_archive_get", C.c_int, [vp, dp, u64p, C.c_char_p, C.c_size_t]),
+    ("momc_b200_archive_copy_device", C.c_int, [vp, vp, vp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_hypervolume", C.c_int, [vp, dp, C.c_int64, C.c_int, dp, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_archive_hypervolume", C.c_int, [vp, dp, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_evaluate_cuts", C.c_int, [vp, u64p, C.c_size_t, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_reference_point_sampled", C.c_int, [vp, C.c_int, C.c_uint64, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_clamp_reference", C.c_int, [vp, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_bench", C.c_int, [vp, C.POINTER(InstanceViewC), i32p, C.c_int, C.c_int, C.POINTER(SolverCfgC),
+                                  C.c_int, C.c_int, dp, u64p, C.POINTER(BenchReportC), C.c_char_p, C.c_size_t]),
 ]
 
 _lib = None

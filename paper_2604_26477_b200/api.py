@@ -11,6 +11,13 @@ Same names, argument meaning and error behaviour as the reference, on top of the
   SolverVariant / SolverConfig  solver.hpp:26-67    SolverVariant / SolverConfig
   SamplePool  solver.hpp:258-338                    SamplePool
   run_sampler  solver.hpp:439-529                   run_sampler (CUDA)
+  ObjectiveVector / Sense  instance.hpp:73-98       ObjectiveVector / Sense
+  ParetoArchive  pareto.hpp:64-119                  ParetoArchive
+  non_dominated_filter  pareto.hpp:253-293, :370-410  non_dominated_filter (CUDA)
+  detail::evaluate_cuts  pareto.hpp:330-363        evaluate_cuts (CUDA)
+  hypervolume  pareto.hpp:540-552                   hypervolume (CUDA)
+  reference_point_sampled / clamp_reference  pareto.hpp:620-655   same names (CUDA / host)
+  bench  pipeline.hpp:309-393                       bench (CUDA)
 
 ``std::invalid_argument`` maps to :class:`InvalidArgument` (a ValueError), any other
 reference exception to :class:`MomcRuntimeError` (a RuntimeError).
@@ -551,3 +558,219 @@ def run_sampler(inst: MultiObjectiveInstance, weights, config: SolverConfig, run
     pool.model_construction_seconds = float(secs[0])
     pool.sampling_seconds = float(secs[1])
     return pool
+
+
+# ----------------------------------------------------------------------------- pareto
+class Sense(enum.IntEnum):
+    """instance.hpp:73"""
+
+    cut = 0
+    hamiltonian = 1
+
+
+class ObjectiveVector:
+    """instance.hpp:78-98"""
+
+    def __init__(self, values, sense: Sense = Sense.cut):
+        if len(values) == 0:
+            raise InvalidArgument("objective vector must be non-empty")
+        self._v = [float(x) for x in values]
+        self._sense = Sense(sense)
+
+    def size(self):
+        return len(self._v)
+
+    def __getitem__(self, k):
+        return self._v[k]
+
+    def values(self):
+        return list(self._v)
+
+    def sense(self):
+        return self._sense
+
+    def __eq__(self, o):
+        return isinstance(o, ObjectiveVector) and self._v == o._v and self._sense == o._sense
+
+
+class ParetoArchive:
+    """pareto.hpp:64-119: entries sorted lexicographically descending by value."""
+
+    def __init__(self, values=None, configs=None, n: int = 0):
+        self.values = np.zeros((0, 0), np.float64) if values is None else np.asarray(values, np.float64)
+        self.configs = configs  # F x wpc packed words, or None for objective-only archives
+        self.n = n
+        self.reference = []
+        self.filtering_seconds = 0.0
+
+    def k(self):
+        return 0 if self.values.shape[0] == 0 else int(self.values.shape[1])
+
+    def size(self):
+        return int(self.values.shape[0])
+
+    def __len__(self):
+        return self.size()
+
+    def contains_value(self, v):
+        return bool(np.any(np.all(self.values == np.asarray(v, np.float64), axis=1)))
+
+    def config(self, i):
+        w = self.configs[i]
+        return np.array([1 if (int(w[b // 64]) >> (b % 64)) & 1 else -1 for b in range(self.n)], dtype=np.int8)
+
+    def validate_reference(self, r):
+        r = list(r)
+        for i in range(self.size()):
+            if len(r) != self.k():
+                raise InvalidArgument("reference point length does not match archive")
+            for k in range(len(r)):
+                if r[k] > self.values[i, k]:
+                    raise InvalidArgument(f"reference point not dominated by archive entry {i} (objective {k})")
+
+    def set_reference(self, r):
+        self.validate_reference(r)
+        self.reference = list(r)
+
+
+def _session_for(inst, session):
+    s = session or default_session()
+    if s.inst is not inst:
+        s.set_instance(inst)
+    return s
+
+
+def _fetch_archive(s: Session, k: int, n: int, with_configs: bool) -> ParetoArchive:
+    F = int(s.lib.momc_b200_archive_size(s.h))
+    vals = np.zeros((F, k), np.float64)
+    wpc = (n + 63) // 64
+    words = np.zeros((F, wpc), np.uint64) if with_configs else None
+    err = _errbuf()
+    _raise(s.lib.momc_b200_archive_get(s.h, vals.ctypes.data_as(_lib.dp),
+                                       words.ctypes.data_as(_lib.u64p) if with_configs else None, err, 2048), err)
+    return ParetoArchive(vals, words, n if with_configs else 0)
+
+
+def non_dominated_filter(pool, inst=None, algo: str = "fast", session: Session | None = None) -> ParetoArchive:
+    """pareto.hpp:370-410 (pool + instance) or pareto.hpp:253-293 (list of ObjectiveVector).
+
+    ``algo`` is accepted for signature parity; the GPU front is exact for both."""
+    if inst is None:
+        vecs = list(pool)
+        if not vecs:
+            raise InvalidArgument("non-dominated filter needs a non-empty pool")
+        sense, k = vecs[0].sense(), vecs[0].size()
+        for v in vecs:
+            if v.sense() != sense or v.size() != k:
+                raise InvalidArgument("pool mixes objective senses or lengths")
+        vals = np.ascontiguousarray([v.values() for v in vecs], np.float64)
+        s = session or default_session()
+        F = C.c_int64()
+        err = _errbuf()
+        _raise(s.lib.momc_b200_filter_values(s.h, vals.ctypes.data_as(_lib.dp), vals.shape[0], k, int(sense),
+                                             C.byref(F), err, 2048), err)
+        return _fetch_archive(s, k, 0, False)
+    if pool.empty():
+        raise InvalidArgument("non-dominated filter needs a non-empty pool")
+    if pool.n() != inst.n():
+        raise InvalidArgument("pool does not match instance")
+    s = _session_for(inst, session)
+    words = np.ascontiguousarray(pool.words, np.uint64)
+    F = C.c_int64()
+    secs = C.c_double()
+    err = _errbuf()
+    _raise(s.lib.momc_b200_filter_pool(s.h, words.ctypes.data_as(_lib.u64p), words.shape[0], C.byref(F),
+                                       C.byref(secs), err, 2048), err)
+    a = _fetch_archive(s, inst.k(), inst.n(), True)
+    a.filtering_seconds = secs.value
+    return a
+
+
+def hypervolume(archive: ParetoArchive, r, session: Session | None = None) -> float:
+    """pareto.hpp:540-552 (exact; integer-valued inputs give the exact integer volume)."""
+    if archive.size() == 0:
+        raise InvalidArgument("hypervolume of an empty archive")
+    r = np.ascontiguousarray(r, np.float64)
+    if r.shape[0] != archive.k():
+        raise InvalidArgument("reference point length does not match archive")
+    s = session or default_session()
+    vals = np.ascontiguousarray(archive.values, np.float64)
+    out = C.c_double()
+    err = _errbuf()
+    _raise(s.lib.momc_b200_hypervolume(s.h, vals.ctypes.data_as(_lib.dp), vals.shape[0], vals.shape[1],
+                                       r.ctypes.data_as(_lib.dp), C.byref(out), err, 2048), err)
+    return out.value
+
+
+def evaluate_cuts(inst: MultiObjectiveInstance, words, session: Session | None = None) -> np.ndarray:
+    """detail::evaluate_cuts (pareto.hpp:330-363) of packed configurations."""
+    s = _session_for(inst, session)
+    words = np.ascontiguousarray(words, np.uint64).reshape(-1, (inst.n() + 63) // 64)
+    out = np.zeros((words.shape[0], inst.k()), np.float64)
+    err = _errbuf()
+    _raise(s.lib.momc_b200_evaluate_cuts(s.h, words.ctypes.data_as(_lib.u64p), words.shape[0],
+                                         out.ctypes.data_as(_lib.dp), err, 2048), err)
+    return out
+
+
+def reference_point_sampled(inst: MultiObjectiveInstance, count: int, seed: int,
+                            session: Session | None = None) -> list:
+    """pareto.hpp:620-642"""
+    if count < 1:
+        raise InvalidArgument("sampled reference needs count >= 1")
+    s = _session_for(inst, session)
+    r = np.zeros(inst.k(), np.float64)
+    err = _errbuf()
+    _raise(s.lib.momc_b200_reference_point_sampled(s.h, count, seed, r.ctypes.data_as(_lib.dp), err, 2048), err)
+    return r.tolist()
+
+
+def clamp_reference(r, archive: ParetoArchive):
+    """pareto.hpp:647-655 (host; the archive is small)."""
+    out = list(r)
+    for row in archive.values:
+        if len(row) != len(out):
+            raise InvalidArgument("reference point length does not match archive")
+        out = [min(a, b) for a, b in zip(out, row)]
+    return out
+
+
+@dataclass
+class BenchResult:
+    """pipeline.hpp:297-302 (report fields as a dict)."""
+
+    report: dict
+    pool: SamplePool
+    archive: ParetoArchive
+
+
+def bench(inst: MultiObjectiveInstance, weights, config: SolverConfig, runs: int = 1, ref_count: int = 1000,
+          fixed_reference=None, keep_pool: bool = True, session: Session | None = None) -> BenchResult:
+    """pipeline.hpp:309-393 on the GPU: scalarise -> sample -> filter -> reference -> HV."""
+    config.validate()
+    if runs < 1:
+        raise InvalidArgument("runs must be >= 1")
+    s = session or default_session()
+    nums, H = _weights_array(weights, inst.k())
+    L = nums.shape[0]
+    M = runs * L * config.batch_size
+    wpc = (inst.n() + 63) // 64
+    words = np.zeros((M, wpc), np.uint64) if keep_pool else None
+    rep = _lib.BenchReportC()
+    cfg = config.c()
+    v = inst.view()
+    fr = np.ascontiguousarray(fixed_reference, np.float64) if fixed_reference is not None else None
+    err = _errbuf()
+    rc = s.lib.momc_b200_bench(s.h, C.byref(v), nums.ctypes.data_as(_lib.i32p), L, H, C.byref(cfg), runs, ref_count,
+                               fr.ctypes.data_as(_lib.dp) if fr is not None else None,
+                               words.ctypes.data_as(_lib.u64p) if keep_pool else None, C.byref(rep), err, 2048)
+    _raise(rc, err)
+    s.inst = inst
+    s.L = L
+    s._pool_geom = (runs, L, config.batch_size)
+    report = {name: getattr(rep, name) for name, _ in _lib.BenchReportC._fields_}
+    report["reference"] = list(rep.reference)[: inst.k()]
+    archive = _fetch_archive(s, inst.k(), inst.n(), True)
+    archive.reference = report["reference"]
+    pool = SamplePool(inst.n(), words, runs, L, config.batch_size) if keep_pool else None
+    return BenchResult(report, pool, archive)

@@ -12,6 +12,7 @@
 
 #include "../../include/momc_b200.h"
 #include "ctx.cuh"
+#include "pareto.cuh"
 #include "sampler.cuh"
 
 using namespace momc_b200;
@@ -470,6 +471,24 @@ void pool_get(Ctx& c, uint64_t* words, int64_t* stamps)
     ck(cudaStreamSynchronize(c.stream), "sync");
 }
 
+DevArchive& resident_archive(Ctx& c)
+{
+    if (!c.archive) c.archive = std::shared_ptr<void>(new DevArchive(), [](void* p) {
+        auto* a = static_cast<DevArchive*>(p);
+        a->vals.release();
+        a->words.release();
+        delete a;
+    });
+    return *static_cast<DevArchive*>(c.archive.get());
+}
+
+void upload_words(Ctx& c, const uint64_t* words, size_t M)
+{
+    const int wpc = (c.n + 63) / 64;
+    c.d_upload.reserve(M * wpc + 1);
+    ck(cudaMemcpyAsync(c.d_upload.p, words, sizeof(uint64_t) * M * wpc, cudaMemcpyHostToDevice, c.stream), "H2D");
+}
+
 }  // namespace
 }  // namespace momc_b200
 
@@ -582,6 +601,231 @@ int momc_b200_run_sampler(momc_ctx* ctx, const momc_instance_view* inst, const i
             out_seconds[0] = std::chrono::duration<double>(t1 - t0).count();
             out_seconds[1] = std::chrono::duration<double>(t2 - t1).count();
         }
+    });
+}
+
+int momc_b200_filter(momc_ctx* ctx, int64_t* out_F, double* seconds, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (ctx->pool_size <= 0) usage("non-dominated filter needs a non-empty pool");
+        ParetoTimings tm;
+        DevArchive& a = resident_archive(*ctx);
+        filter_pool_device(*ctx, ctx->d_words.p, ctx->pool_size, a, &tm);
+        if (out_F) *out_F = a.F;
+        if (seconds) {
+            seconds[0] = tm.dedup_s;
+            seconds[1] = tm.eval_s;
+            seconds[2] = tm.collapse_s;
+            seconds[3] = tm.front_s;
+            seconds[4] = tm.order_s;
+        }
+    });
+}
+
+int momc_b200_filter_pool(momc_ctx* ctx, const uint64_t* words, size_t M, int64_t* out_F, double* filtering_s,
+                          char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (M == 0) usage("non-dominated filter needs a non-empty pool");
+        const auto t0 = std::chrono::steady_clock::now();
+        upload_words(*ctx, words, M);
+        DevArchive& a = resident_archive(*ctx);
+        filter_pool_device(*ctx, ctx->d_upload.p, static_cast<long long>(M), a, nullptr);
+        if (out_F) *out_F = a.F;
+        if (filtering_s) *filtering_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+int momc_b200_filter_values(momc_ctx* ctx, const double* vals, size_t M, int k, int sense, int64_t* out_F,
+                            char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (M == 0) usage("non-dominated filter needs a non-empty pool");
+        if (k < 1) usage("objective vector must be non-empty");
+        std::vector<double> v(vals, vals + M * static_cast<size_t>(k));
+        if (sense) for (double& x : v) x = -x;  // filter in maximisation space (pareto.hpp:267-271)
+        DevBuf<double> dv;
+        dv.reserve(v.size());
+        ck(cudaMemcpyAsync(dv.p, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        DevArchive& a = resident_archive(*ctx);
+        filter_values_device(*ctx, dv.p, nullptr, 0, 0, static_cast<long long>(M), k, a, nullptr);
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        dv.release();
+        if (sense) {  // back to Hamiltonian values, archive ordered by them (pareto.hpp:283-289)
+            std::vector<double> f(static_cast<size_t>(a.F) * k);
+            ck(cudaMemcpy(f.data(), a.vals.p, sizeof(double) * f.size(), cudaMemcpyDeviceToHost), "D2H");
+            std::vector<std::vector<double>> rows(static_cast<size_t>(a.F));
+            for (long long i = 0; i < a.F; ++i) {
+                rows[static_cast<size_t>(i)].assign(f.begin() + i * k, f.begin() + (i + 1) * k);
+                for (double& x : rows[static_cast<size_t>(i)]) x = -x;
+            }
+            std::sort(rows.begin(), rows.end(), std::greater<>());
+            for (long long i = 0; i < a.F; ++i)
+                std::copy(rows[static_cast<size_t>(i)].begin(), rows[static_cast<size_t>(i)].end(), f.begin() + i * k);
+            ck(cudaMemcpy(a.vals.p, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice), "H2D");
+        }
+        if (out_F) *out_F = a.F;
+    });
+}
+
+int momc_b200_filter_values_dev(momc_ctx* ctx, const double* d_vals, const uint64_t* d_words, int wpc, size_t M,
+                                int k, int64_t* out_F, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DevArchive& a = resident_archive(*ctx);
+        filter_values_device(*ctx, d_vals, d_words, wpc, ctx->n, static_cast<long long>(M), k, a, nullptr);
+        if (out_F) *out_F = a.F;
+    });
+}
+
+int64_t momc_b200_archive_size(momc_ctx* ctx) { return ctx->archive ? resident_archive(*ctx).F : 0; }
+
+int momc_b200_archive_get(momc_ctx* ctx, double* vals, uint64_t* words, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        DevArchive& a = resident_archive(*ctx);
+        if (vals && a.F)
+            ck(cudaMemcpyAsync(vals, a.vals.p, sizeof(double) * a.F * a.K, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        if (words && a.F && a.wpc)
+            ck(cudaMemcpyAsync(words, a.words.p, sizeof(uint64_t) * a.F * a.wpc, cudaMemcpyDeviceToHost, ctx->stream),
+               "D2H");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int momc_b200_archive_copy_device(momc_ctx* ctx, double* d_vals, uint64_t* d_words, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        DevArchive& a = resident_archive(*ctx);
+        if (d_vals && a.F)
+            ck(cudaMemcpyAsync(d_vals, a.vals.p, sizeof(double) * a.F * a.K, cudaMemcpyDeviceToDevice, ctx->stream),
+               "D2D");
+        if (d_words && a.F && a.wpc)
+            ck(cudaMemcpyAsync(d_words, a.words.p, sizeof(uint64_t) * a.F * a.wpc, cudaMemcpyDeviceToDevice,
+                               ctx->stream),
+               "D2D");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int momc_b200_hypervolume(momc_ctx* ctx, const double* vals, int64_t F, int k, const double* r, double* out,
+                          char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (F <= 0) usage("hypervolume of an empty archive");
+        DevBuf<double> dv;
+        dv.reserve(static_cast<size_t>(F) * k);
+        ck(cudaMemcpyAsync(dv.p, vals, sizeof(double) * F * k, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        *out = hypervolume_device(*ctx, dv.p, F, k, std::vector<double>(r, r + k));
+        dv.release();
+    });
+}
+
+int momc_b200_archive_hypervolume(momc_ctx* ctx, const double* r, double* out, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DevArchive& a = resident_archive(*ctx);
+        *out = hypervolume_device(*ctx, a.vals.p, a.F, a.K, std::vector<double>(r, r + a.K));
+    });
+}
+
+int momc_b200_evaluate_cuts(momc_ctx* ctx, const uint64_t* words, size_t U, double* out, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (ctx->n == 0) usage("no instance set");
+        if (U == 0) return;
+        upload_words(*ctx, words, U);
+        DevBuf<double> d;
+        d.reserve(U * ctx->k);
+        evaluate_cuts_device(*ctx, ctx->d_upload.p, static_cast<long long>(U), d.p);
+        ck(cudaMemcpyAsync(out, d.p, sizeof(double) * U * ctx->k, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        d.release();
+    });
+}
+
+int momc_b200_reference_point_sampled(momc_ctx* ctx, int count, uint64_t seed, double* r, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (ctx->n == 0) usage("no instance set");
+        const auto v = reference_point_sampled_device(*ctx, count, seed);
+        std::copy(v.begin(), v.end(), r);
+    });
+}
+
+int momc_b200_clamp_reference(momc_ctx* ctx, double* r, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        DevArchive& a = resident_archive(*ctx);
+        std::vector<double> f(static_cast<size_t>(a.F) * a.K);
+        if (a.F)
+            ck(cudaMemcpyAsync(f.data(), a.vals.p, sizeof(double) * f.size(), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        for (long long i = 0; i < a.F; ++i)  // clamp_reference (pareto.hpp:647-655)
+            for (int l = 0; l < a.K; ++l) r[l] = std::min(r[l], f[static_cast<size_t>(i * a.K + l)]);
+    });
+}
+
+int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t* nums, int L, int H,
+                    const momc_solver_cfg* cfg, int runs, int ref_count, const double* fixed_ref, uint64_t* out_pool,
+                    momc_bench_report* rep, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (runs < 1) usage("runs must be >= 1");
+        validate_cfg(cfg);
+        std::memset(rep, 0, sizeof *rep);
+        using clk = std::chrono::steady_clock;
+        const auto t0 = clk::now();
+        set_instance(*ctx, inst);
+        set_weights(*ctx, nums, L, H);
+        rep->model_construction_s = std::chrono::duration<double>(clk::now() - t0).count();
+        double ss = 0;
+        sample(*ctx, cfg, runs, 0, -1, &ss);
+        rep->sampling_s = ss;
+        rep->pool_size = ctx->pool_size;
+        const auto tf = clk::now();
+        ParetoTimings tm;
+        DevArchive& a = resident_archive(*ctx);
+        filter_pool_device(*ctx, ctx->d_words.p, ctx->pool_size, a, &tm);
+        rep->unique_configs = tm.unique_configs;
+        rep->unique_vectors = tm.unique_vectors;
+        rep->archive_size = a.F;
+        rep->dedup_s = tm.dedup_s;
+        rep->eval_s = tm.eval_s;
+        rep->collapse_s = tm.collapse_s;
+        rep->front_s = tm.front_s;
+        rep->order_s = tm.order_s;
+        rep->front_method = tm.front_method;
+        const auto tr = clk::now();
+        std::vector<double> r(static_cast<size_t>(ctx->k));
+        if (fixed_ref) {
+            r.assign(fixed_ref, fixed_ref + ctx->k);
+        } else {
+            r = reference_point_sampled_device(*ctx, ref_count, cfg->seed);
+            std::vector<double> f(static_cast<size_t>(a.F) * a.K);
+            ck(cudaMemcpyAsync(f.data(), a.vals.p, sizeof(double) * f.size(), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+            ck(cudaStreamSynchronize(ctx->stream), "sync");
+            for (long long i = 0; i < a.F; ++i)
+                for (int l = 0; l < a.K; ++l) r[static_cast<size_t>(l)] = std::min(r[static_cast<size_t>(l)], f[static_cast<size_t>(i * a.K + l)]);
+        }
+        const auto th = clk::now();
+        rep->reference_s = std::chrono::duration<double>(th - tr).count();
+        rep->hv = hypervolume_device(*ctx, a.vals.p, a.F, a.K, r);
+        const auto te = clk::now();
+        rep->hv_s = std::chrono::duration<double>(te - th).count();
+        for (int l = 0; l < ctx->k && l < 16; ++l) rep->reference[l] = r[static_cast<size_t>(l)];
+        rep->pareto_filtering_s = std::chrono::duration<double>(te - tf).count();
+        if (out_pool) pool_get(*ctx, out_pool, nullptr);
+        rep->end_to_end_s = std::chrono::duration<double>(clk::now() - t0).count();
     });
 }
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -79,6 +80,9 @@ struct Ctx {
     DevBuf<int> d_nan, d_badstep;
     DevBuf<unsigned long long> d_block_end, d_t0;
     DevBuf<double> d_gx, d_gy, d_gxn, d_gnoise;  // generic-n scratch
+    DevBuf<uint64_t> d_upload;                   // host pools uploaded for filtering
+    std::shared_ptr<void> pareto_scratch;         // pareto.cu working buffers
+    std::shared_ptr<void> archive;                // resident DevArchive (pareto.cuh)
 
     ~Ctx();
 };

@@ -1,0 +1,997 @@
+// Pareto stage kernels (pareto.cuh). Design:
+//   K5 dedup      open-addressing hash set over packed configs (warp-aggregated compaction)
+//   K4 eval       exact int32 edge loop when all weights are integral (every partial sum is
+//                 an integer < 2^31, so it equals evaluate_cuts' FP64 GEMM result exactly);
+//                 otherwise the shim's FP64 order of evaluate_cuts (pareto.hpp:346-359)
+//   K6 collapse   hash map keyed by the objective vector; the owner is the lexicographically
+//                 smallest spin configuration (instance.hpp:63-67), kept by a CAS loop
+//   K7 front      "grid" method: coordinates compressed to ranks; a (K-1)-d table holds,
+//                 per cell, the max last-coordinate rank; a suffix max along every axis then
+//                 decides weak dominance of every vector in O(1) (exact, order-free);
+//                 all-pairs fallback when the compressed grid would not fit
+//   archive       rank sort, lexicographically descending (pareto.hpp:405-406)
+//   K8 HV         the same compressed grid over the front: HV = sum over cells of
+//                 (cell volume) x (max covering gain), accumulated exactly in __int128 when
+//                 the values are integers (bit-equal to the reference's exact double result)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "pareto.cuh"
+#include "rng.cuh"
+
+namespace momc_b200 {
+
+namespace {
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+constexpr int kMaxK = 16;
+constexpr long long kGridCap = 1ll << 27;  // max cells of a compressed grid table
+constexpr int kDistinctCap = 1 << 15;      // max distinct values per axis for the grid method
+
+__device__ __forceinline__ uint64_t hash_words(const uint64_t* w, int wpc)
+{  // WordSpanHash-like mixing (pareto.hpp:297-306), any good mixer works here
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+    for (int i = 0; i < wpc; ++i) h ^= mix64(w[i] + h);
+    return h;
+}
+
+// order-preserving key of a double (-0.0 canonicalised to +0.0); 0 is below every value
+__host__ __device__ __forceinline__ uint64_t dkey(double v)
+{
+    v = v + 0.0;
+    uint64_t b;
+#ifdef __CUDA_ARCH__
+    b = static_cast<uint64_t>(__double_as_longlong(v));
+#else
+    std::memcpy(&b, &v, 8);
+#endif
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ uint64_t hash_vals(const double* v, int K)
+{
+    uint64_t h = 0x243F6A8885A308D3ull;
+    for (int k = 0; k < K; ++k) h ^= mix64(dkey(v[k]) + h);
+    return h;
+}
+
+__device__ __forceinline__ bool vals_equal(const double* a, const double* b, int K)
+{
+    for (int k = 0; k < K; ++k)
+        if (!(a[k] == b[k])) return false;
+    return true;
+}
+
+// SpinConfiguration operator< (instance.hpp:63-67): spins compared from index 0 with
+// -1 < +1; for packed words that is numeric order of the bit-reversed words, word 0 first.
+__device__ __forceinline__ bool config_less(const uint64_t* a, const uint64_t* b, int wpc)
+{
+    for (int i = 0; i < wpc; ++i) {
+        const uint64_t x = __brevll(a[i]), y = __brevll(b[i]);
+        if (x != y) return x < y;
+    }
+    return false;
+}
+
+__device__ __forceinline__ void warp_append(bool flag, uint32_t value, uint32_t* out, unsigned long long* count)
+{
+    const unsigned mask = __activemask();
+    const unsigned b = __ballot_sync(mask, flag);
+    if (!b) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(b) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(count, static_cast<unsigned long long>(__popc(b)));
+    base = __shfl_sync(mask, base, leader);
+    if (flag) out[base + __popc(b & ((1u << lane) - 1))] = value;
+}
+
+// ---- K5: dedup of packed configs (pareto.hpp:309-326)
+__global__ void k_dedup(const uint64_t* __restrict__ words, long long M, int wpc, uint32_t* table, uint64_t tmask,
+                        uint32_t* uniq, unsigned long long* ucount)
+{
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x); i0 < M;
+         i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        bool fresh = false;
+        if (i < M) {
+            const uint64_t* w = words + i * wpc;
+            uint64_t h = hash_words(w, wpc) & tmask;
+            for (;;) {
+                uint32_t s = atomicAdd(&table[h], 0u);
+                if (s == kEmpty) {
+                    s = atomicCAS(&table[h], kEmpty, static_cast<uint32_t>(i));
+                    if (s == kEmpty) {
+                        fresh = true;
+                        break;
+                    }
+                }
+                bool eq = true;
+                for (int q = 0; q < wpc; ++q) eq &= words[static_cast<long long>(s) * wpc + q] == w[q];
+                if (eq) break;
+                h = (h + 1) & tmask;
+            }
+        }
+        warp_append(fresh, static_cast<uint32_t>(i), uniq, ucount);
+    }
+}
+
+// ---- K4: exact integer cut values, instance.hpp:183-194 (== evaluate_cuts for integer weights)
+__global__ void k_eval_int(const uint64_t* __restrict__ words, const uint32_t* __restrict__ idx, long long U, int wpc,
+                           int m, int K, const int* __restrict__ ei, const int* __restrict__ ej,
+                           const int* __restrict__ wi, double* out)
+{
+    extern __shared__ int sm[];
+    const bool staged = m * (2 + K) <= 12000;
+    if (staged) {
+        for (int e = threadIdx.x; e < m; e += blockDim.x) {
+            sm[e] = ei[e];
+            sm[m + e] = ej[e];
+        }
+        for (int q = threadIdx.x; q < m * K; q += blockDim.x) sm[2 * m + q] = wi[q];
+        __syncthreads();
+    }
+    const int* sei = staged ? sm : ei;
+    const int* sej = staged ? sm + m : ej;
+    const int* swi = staged ? sm + 2 * m : wi;
+    for (long long u = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; u < U;
+         u += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const uint64_t* w = words + static_cast<long long>(idx ? idx[u] : u) * wpc;
+        int acc[kMaxK];
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k) acc[k] = 0;
+        if (wpc == 1) {
+            const uint64_t w0 = w[0];
+            for (int e = 0; e < m; ++e) {
+                const uint64_t d = (w0 >> sei[e]) ^ (w0 >> sej[e]);
+                const int cut = -static_cast<int>(d & 1ull);  // all-ones when the edge is cut
+#pragma unroll
+                for (int k = 0; k < kMaxK; ++k)
+                    if (k < K) acc[k] += swi[e * K + k] & cut;
+            }
+        } else {
+            for (int e = 0; e < m; ++e) {
+                const int a = sei[e], b = sej[e];
+                const uint64_t d = (w[a >> 6] >> (a & 63)) ^ (w[b >> 6] >> (b & 63));
+                const int cut = -static_cast<int>(d & 1ull);
+#pragma unroll
+                for (int k = 0; k < kMaxK; ++k)
+                    if (k < K) acc[k] += swi[e * K + k] & cut;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k)
+            if (k < K) out[u * K + k] = static_cast<double>(acc[k]);
+    }
+}
+
+// ---- K4 general: evaluate_cuts' FP64 order in the shim (pareto.hpp:346-359):
+//      JS_i = sum_j J_k(i,j) s_j (j ascending, from +0.0); h = 0.5 * sum_i s_i JS_i; C = 0.5 (W - h)
+__global__ void k_eval_dbl(const uint64_t* __restrict__ words, const uint32_t* __restrict__ idx, long long U, int wpc,
+                           int n, int K, const int* __restrict__ rowptr, const int* __restrict__ col,
+                           const int* __restrict__ eidx, const double* __restrict__ w, const double* __restrict__ W,
+                           double* out)
+{
+    for (long long u = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; u < U;
+         u += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const uint64_t* cw = words + static_cast<long long>(idx ? idx[u] : u) * wpc;
+        for (int k = 0; k < K; ++k) {
+            double dot = 0.0;
+            for (int i = 0; i < n; ++i) {
+                double js = 0.0;
+                for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+                    const int j = col[e];
+                    const double sj = (cw[j >> 6] >> (j & 63)) & 1ull ? 1.0 : -1.0;
+                    js = __dadd_rn(js, __dmul_rn(w[static_cast<long long>(eidx[e]) * K + k], sj));
+                }
+                const double si = (cw[i >> 6] >> (i & 63)) & 1ull ? 1.0 : -1.0;
+                dot = __dadd_rn(dot, __dmul_rn(si, js));
+            }
+            out[u * K + k] = __dmul_rn(0.5, __dsub_rn(W[k], __dmul_rn(0.5, dot)));
+        }
+    }
+}
+
+// ---- K6: collapse equal vectors onto the lex-smallest config (pareto.hpp:383-387)
+// vals: U x K; cfg: per-row config pointer index (into words); table slots hold a row index.
+__global__ void k_collapse(const double* __restrict__ vals, long long U, int K, const uint64_t* __restrict__ words,
+                           const uint32_t* __restrict__ cfg_of_row, int wpc, uint32_t* table, uint32_t* owner,
+                           uint64_t tmask, uint32_t* reps, unsigned long long* vcount)
+{
+    for (long long u0 = blockIdx.x * static_cast<long long>(blockDim.x); u0 < U;
+         u0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long u = u0 + threadIdx.x;
+        bool fresh = false;
+        uint32_t slot_of = 0;
+        if (u < U) {
+            const double* v = vals + u * K;
+            uint64_t h = hash_vals(v, K) & tmask;
+            for (;;) {
+                uint32_t s = atomicAdd(&table[h], 0u);
+                if (s == kEmpty) {
+                    s = atomicCAS(&table[h], kEmpty, static_cast<uint32_t>(u));
+                    if (s == kEmpty) {
+                        fresh = true;
+                        break;
+                    }
+                }
+                if (vals_equal(vals + static_cast<long long>(s) * K, v, K)) break;
+                h = (h + 1) & tmask;
+            }
+            slot_of = static_cast<uint32_t>(h);
+            if (words) {  // keep the lexicographically smallest configuration per vector
+                const uint32_t me = static_cast<uint32_t>(u);
+                uint32_t cur = atomicAdd(&owner[h], 0u);
+                for (;;) {
+                    if (cur != kEmpty) {
+                        const uint64_t* a = words + static_cast<long long>(cfg_of_row ? cfg_of_row[me] : me) * wpc;
+                        const uint64_t* b = words + static_cast<long long>(cfg_of_row ? cfg_of_row[cur] : cur) * wpc;
+                        if (!config_less(a, b, wpc)) break;
+                    }
+                    const uint32_t prev = atomicCAS(&owner[h], cur, me);
+                    if (prev == cur) break;
+                    cur = prev;
+                }
+            }
+        }
+        warp_append(fresh, slot_of, reps, vcount);
+    }
+}
+
+// ---- distinct values of one axis (hash set of keys), then ascending order by rank count
+__global__ void k_distinct(const double* __restrict__ vals, long long V, int K, int axis, unsigned long long* table,
+                           uint64_t tmask, double* out, unsigned long long* count, long long cap)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double v = vals[i * K + axis];
+        const unsigned long long key = dkey(v);
+        uint64_t h = mix64(key) & tmask;
+        for (;;) {
+            unsigned long long s = atomicCAS(&table[h], 0ull, key);
+            if (s == 0ull) {
+                const unsigned long long at = atomicAdd(count, 1ull);
+                if (static_cast<long long>(at) < cap) out[at] = v + 0.0;
+                break;
+            }
+            if (s == key) break;
+            h = (h + 1) & tmask;
+        }
+    }
+}
+
+__global__ void k_rank_sort_asc(const double* __restrict__ in, int D, double* out)
+{  // distinct values: rank = #smaller
+    extern __shared__ double tile[];
+    for (int base = blockIdx.x * blockDim.x; base < D; base += gridDim.x * blockDim.x) {
+        const int i = base + threadIdx.x;
+        const double v = i < D ? in[i] : 0.0;
+        int rank = 0;
+        for (int t0 = 0; t0 < D; t0 += blockDim.x) {
+            __syncthreads();
+            if (t0 + threadIdx.x < D) tile[threadIdx.x] = in[t0 + threadIdx.x];
+            __syncthreads();
+            const int lim = min(static_cast<int>(blockDim.x), D - t0);
+            if (i < D)
+                for (int q = 0; q < lim; ++q) rank += tile[q] < v;
+        }
+        if (i < D) out[rank] = v;
+    }
+}
+
+__device__ __forceinline__ int lower_rank(const double* sorted, int D, double v)
+{
+    int lo = 0, hi = D;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sorted[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+struct GridGeo {
+    int dims;                 // K - 1
+    long long stride[kMaxK];  // row-major strides over the first K-1 axes
+    int D[kMaxK];             // distinct values per axis (all K axes)
+    const double* axis[kMaxK];  // sorted distinct values per axis
+};
+
+// cell index and last-axis rank+1 of vector i
+__device__ __forceinline__ long long cell_of(const GridGeo& g, const double* v, int* r)
+{
+    long long c = 0;
+    for (int a = 0; a < g.dims; ++a) {
+        r[a] = lower_rank(g.axis[a], g.D[a], v[a]);
+        c += r[a] * g.stride[a];
+    }
+    return c;
+}
+
+__global__ void k_grid_scatter(const double* __restrict__ vals, long long V, int K, GridGeo g, uint32_t* T)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double* v = vals + i * K;
+        int r[kMaxK];
+        const long long c = cell_of(g, v, r);
+        const uint32_t last = static_cast<uint32_t>(lower_rank(g.axis[g.dims], g.D[g.dims], v[g.dims])) + 1;
+        atomicMax(&T[c], last);
+    }
+}
+
+// suffix max along one axis: S[.., a, ..] = max(S[.., a, ..], S[.., a+1, ..])
+__global__ void k_suffix_max(uint32_t* S, long long cells, long long stride, int D)
+{
+    const long long lines = cells / D;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < lines;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long inner = t % stride, outer = t / stride;
+        long long p = outer * stride * D + inner + static_cast<long long>(D - 1) * stride;
+        uint32_t run = S[p];
+        for (int a = D - 2; a >= 0; --a) {
+            p -= stride;
+            run = max(run, S[p]);
+            S[p] = run;
+        }
+    }
+}
+
+// weak dominance test of every vector (pareto.hpp:49-57): dominated iff a vector in the
+// same cell has a larger last coordinate, or a vector at least as large in all axes and
+// strictly larger in one of the first K-1 has a last coordinate >= this one
+__global__ void k_grid_test(const double* __restrict__ vals, long long V, int K, GridGeo g, const uint32_t* T,
+                            const uint32_t* S, unsigned char* keep)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double* v = vals + i * K;
+        int r[kMaxK];
+        const long long c = cell_of(g, v, r);
+        const uint32_t last = static_cast<uint32_t>(lower_rank(g.axis[g.dims], g.D[g.dims], v[g.dims])) + 1;
+        bool dom = T[c] > last;
+        for (int a = 0; a < g.dims && !dom; ++a)
+            if (r[a] + 1 < g.D[a]) dom = S[c + g.stride[a]] >= last;
+        keep[i] = !dom;
+    }
+}
+
+// all-pairs fallback: dominates_max over every other vector (distinct vectors)
+__global__ void k_pairwise(const double* __restrict__ vals, long long V, int K, unsigned char* keep)
+{
+    extern __shared__ double tile[];  // blockDim.x x K
+    for (long long base = blockIdx.x * static_cast<long long>(blockDim.x); base < V;
+         base += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = base + threadIdx.x;
+        double mine[kMaxK];
+        for (int k = 0; k < K; ++k) mine[k] = i < V ? vals[i * K + k] : 0.0;
+        bool dom = i >= V;
+        for (long long t0 = 0; t0 < V; t0 += blockDim.x) {
+            if (__syncthreads_and(dom)) break;
+            for (int q = threadIdx.x; q < static_cast<int>(blockDim.x) * K; q += blockDim.x) {
+                const long long row = t0 + q / K;
+                tile[q] = row < V ? vals[row * K + q % K] : -INFINITY;
+            }
+            __syncthreads();
+            const int lim = static_cast<int>(min(static_cast<long long>(blockDim.x), V - t0));
+            for (int q = 0; q < lim && !dom; ++q) {
+                bool ge = true, gt = false;
+                for (int k = 0; k < K; ++k) {
+                    const double a = tile[q * K + k];
+                    ge &= a >= mine[k];
+                    gt |= a > mine[k];
+                }
+                dom = ge && gt;
+            }
+        }
+        if (i < V) keep[i] = !dom;
+    }
+}
+
+// archive order: rank = #vectors lexicographically greater (pareto.hpp:405-406)
+__global__ void k_lex_desc_rank(const double* __restrict__ vals, long long F, int K, long long* rank)
+{
+    extern __shared__ double tile[];
+    for (long long base = blockIdx.x * static_cast<long long>(blockDim.x); base < F;
+         base += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = base + threadIdx.x;
+        double mine[kMaxK];
+        for (int k = 0; k < K; ++k) mine[k] = i < F ? vals[i * K + k] : 0.0;
+        long long rk = 0;
+        for (long long t0 = 0; t0 < F; t0 += blockDim.x) {
+            __syncthreads();
+            for (int q = threadIdx.x; q < static_cast<int>(blockDim.x) * K; q += blockDim.x) {
+                const long long row = t0 + q / K;
+                tile[q] = row < F ? vals[row * K + q % K] : 0.0;
+            }
+            __syncthreads();
+            const int lim = static_cast<int>(min(static_cast<long long>(blockDim.x), F - t0));
+            if (i < F)
+                for (int q = 0; q < lim; ++q) {
+                    int cmp = 0;
+                    for (int k = 0; k < K && cmp == 0; ++k) {
+                        const double a = tile[q * K + k];
+                        cmp = a > mine[k] ? 1 : (a < mine[k] ? -1 : 0);
+                    }
+                    rk += cmp > 0;
+                }
+        }
+        if (i < F) rank[i] = rk;
+    }
+}
+
+__global__ void k_gather_rows(const double* __restrict__ src_vals, const uint32_t* __restrict__ rows, long long F, int K,
+                              const uint64_t* __restrict__ src_words, const uint32_t* __restrict__ cfg_rows, int wpc,
+                              const long long* __restrict__ rank, double* dst_vals, uint64_t* dst_words)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long dst = rank ? rank[i] : i;
+        const long long sr = rows ? rows[i] : i;
+        for (int k = 0; k < K; ++k) dst_vals[dst * K + k] = src_vals[sr * K + k];
+        if (dst_words) {
+            const long long cr = cfg_rows ? cfg_rows[i] : sr;
+            for (int q = 0; q < wpc; ++q) dst_words[dst * wpc + q] = src_words[cr * wpc + q];
+        }
+    }
+}
+
+// ---- reference_point_sampled (pareto.hpp:620-642): cut_values (instance.hpp:183-194, edge
+// order) of `count` configs drawn 64 spins per next_u64 from
+// Stream(derive_key(seed, 0x70617265), c, 0, tag_word(reference_sample)); per-objective min.
+__global__ void k_ref_sample(int count, uint64_t key, int n, int m, int K, const int* __restrict__ ei,
+                             const int* __restrict__ ej, const double* __restrict__ w, unsigned long long* rmin)
+{
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < count; c += gridDim.x * blockDim.x) {
+        DevStream s;
+        s.init(key, static_cast<uint32_t>(c), 0u, tag_word(kTagReferenceSample, 0));
+        uint64_t wd[16];
+        const int wpc = (n + 63) / 64;
+        for (int q = 0; q < wpc && q < 16; ++q) wd[q] = s.next_u64();
+        for (int k = 0; k < K; ++k) {
+            double acc = 0.0;
+            for (int e = 0; e < m; ++e) {
+                const int a = ei[e], b = ej[e];
+                if (((wd[a >> 6] >> (a & 63)) ^ (wd[b >> 6] >> (b & 63))) & 1ull)
+                    acc = __dadd_rn(acc, w[static_cast<long long>(e) * K + k]);
+            }
+            atomicMin(&rmin[k], dkey(acc));
+        }
+    }
+}
+
+// ---- K8: hypervolume over the compressed grid of the front (gains g = v - r)
+__global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, GridGeo g, const double* __restrict__ r,
+                           bool integral, __int128* ipart, double* dpart, double* dcomp)
+{
+    __int128 iacc = 0;
+    double dacc = 0.0, dc = 0.0;
+    for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < cells;
+         c += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const uint32_t top = S[c];
+        if (!top) continue;
+        const double hgain = g.axis[g.dims][top - 1] - r[g.dims];
+        if (!(hgain > 0.0)) continue;
+        long long rem = c;
+        if (integral) {
+            __int128 vol = static_cast<long long>(hgain);
+            for (int a = 0; a < g.dims; ++a) {
+                const int ra = static_cast<int>(rem / g.stride[a]);
+                rem -= ra * g.stride[a];
+                const double lo = ra ? g.axis[a][ra - 1] : r[a];
+                vol *= static_cast<long long>(g.axis[a][ra] - lo);
+            }
+            iacc += vol;
+        } else {
+            double vol = hgain;
+            for (int a = 0; a < g.dims; ++a) {
+                const int ra = static_cast<int>(rem / g.stride[a]);
+                rem -= ra * g.stride[a];
+                const double lo = ra ? g.axis[a][ra - 1] : r[a];
+                vol *= g.axis[a][ra] - lo;
+            }
+            const double y = vol - dc;  // Kahan
+            const double t = dacc + y;
+            dc = (t - dacc) - y;
+            dacc = t;
+        }
+    }
+    __shared__ __int128 si[256];
+    __shared__ double sd[256];
+    si[threadIdx.x] = iacc;
+    sd[threadIdx.x] = dacc - dc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __int128 a = 0;
+        double b = 0.0;
+        for (int q = 0; q < static_cast<int>(blockDim.x); ++q) {
+            a += si[q];
+            b += sd[q];
+        }
+        ipart[blockIdx.x] = a;
+        dpart[blockIdx.x] = b;
+        (void)dcomp;
+    }
+}
+
+__global__ void k_ref_check(const double* __restrict__ vals, long long F, int K, const double* __restrict__ r,
+                            unsigned long long* first)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        for (int k = 0; k < K; ++k)
+            if (r[k] > vals[i * K + k]) atomicMin(first, static_cast<unsigned long long>(i * K + k));
+}
+
+uint64_t pow2_at_least(uint64_t x)
+{
+    uint64_t p = 1024;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+int grid_blocks(long long n, int threads = 256)
+{
+    long long b = (n + threads - 1) / threads;
+    if (b > 148 * 32) b = 148 * 32;
+    if (b < 1) b = 1;
+    return static_cast<int>(b);
+}
+
+double seconds_between(cudaEvent_t a, cudaEvent_t b)
+{
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms * 1e-3;
+}
+
+// scratch reused across calls
+struct Scratch {
+    DevBuf<uint32_t> table, uniq, table2, owner, reps, rows, cfgrows;
+    DevBuf<unsigned long long> counters, dtable;
+    DevBuf<double> vals, axisbuf, axis_sorted, rdev;
+    DevBuf<uint32_t> T, S;
+    DevBuf<unsigned char> keep;
+    DevBuf<long long> rank;
+    DevBuf<__int128> ipart;
+    DevBuf<double> dpart;
+};
+Scratch& scratch(Ctx& c)
+{
+    if (!c.pareto_scratch) c.pareto_scratch = std::shared_ptr<void>(new Scratch(), [](void* p) {
+        auto* s = static_cast<Scratch*>(p);
+        s->table.release(); s->uniq.release(); s->table2.release(); s->owner.release(); s->reps.release();
+        s->rows.release(); s->cfgrows.release(); s->counters.release(); s->dtable.release(); s->vals.release();
+        s->axisbuf.release(); s->axis_sorted.release(); s->rdev.release(); s->T.release(); s->S.release();
+        s->keep.release(); s->rank.release(); s->ipart.release(); s->dpart.release();
+        delete s;
+    });
+    return *static_cast<Scratch*>(c.pareto_scratch.get());
+}
+
+unsigned long long read_counter(Ctx& c, unsigned long long* d)
+{
+    unsigned long long h = 0;
+    ck(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    return h;
+}
+
+// Builds the compressed grid over V vectors (K >= 2). Returns false when it would not fit.
+bool build_grid(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, GridGeo& g, long long& cells,
+                std::vector<std::vector<double>>* host_axes = nullptr)
+{
+    g.dims = K - 1;
+    const uint64_t tsize = pow2_at_least(2ull * static_cast<uint64_t>(V) + 16);
+    s.dtable.reserve(tsize);
+    s.axisbuf.reserve(static_cast<size_t>(kDistinctCap));
+    s.axis_sorted.reserve(static_cast<size_t>(kDistinctCap) * K);
+    s.counters.reserve(8);
+    long long prod = 1;
+    for (int a = 0; a < K; ++a) {
+        ck(cudaMemsetAsync(s.dtable.p, 0, sizeof(unsigned long long) * tsize, c.stream), "memset");
+        ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long), c.stream), "memset");
+        k_distinct<<<grid_blocks(V), 256, 0, c.stream>>>(d_vals, V, K, a, s.dtable.p, tsize - 1, s.axisbuf.p,
+                                                           s.counters.p, kDistinctCap);
+        c.launches++;
+        const long long D = static_cast<long long>(read_counter(c, s.counters.p));
+        if (D > kDistinctCap) return false;
+        g.D[a] = static_cast<int>(D);
+        double* sorted = s.axis_sorted.p + static_cast<size_t>(a) * kDistinctCap;
+        k_rank_sort_asc<<<grid_blocks(D, 256), 256, 256 * sizeof(double), c.stream>>>(s.axisbuf.p, static_cast<int>(D),
+                                                                                       sorted);
+        c.launches++;
+        g.axis[a] = sorted;
+        if (a < K - 1) {
+            prod *= D;
+            if (prod > kGridCap) return false;
+        }
+        if (host_axes) {
+            std::vector<double> hv(static_cast<size_t>(D));
+            ck(cudaMemcpyAsync(hv.data(), sorted, sizeof(double) * D, cudaMemcpyDeviceToHost, c.stream), "D2H");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            host_axes->push_back(std::move(hv));
+        }
+    }
+    cells = prod;
+    long long st = 1;
+    for (int a = K - 2; a >= 0; --a) {
+        g.stride[a] = st;
+        st *= g.D[a];
+    }
+    s.T.reserve(static_cast<size_t>(cells));
+    s.S.reserve(static_cast<size_t>(cells));
+    ck(cudaMemsetAsync(s.T.p, 0, sizeof(uint32_t) * cells, c.stream), "memset");
+    k_grid_scatter<<<grid_blocks(V), 256, 0, c.stream>>>(d_vals, V, K, g, s.T.p);
+    c.launches++;
+    ck(cudaMemcpyAsync(s.S.p, s.T.p, sizeof(uint32_t) * cells, cudaMemcpyDeviceToDevice, c.stream), "D2D");
+    for (int a = 0; a < K - 1; ++a) {
+        if (g.D[a] < 2) continue;
+        k_suffix_max<<<grid_blocks(cells / g.D[a]), 256, 0, c.stream>>>(s.S.p, cells, g.stride[a], g.D[a]);
+        c.launches++;
+    }
+    return true;
+}
+
+// front of V distinct vectors (device rows); keep[i] set for non-dominated rows
+int front_keep(Ctx& c, Scratch& s, const double* d_vals, long long V, int K)
+{
+    s.keep.reserve(static_cast<size_t>(V) + 1);
+    if (K >= 2) {
+        GridGeo g{};
+        long long cells = 0;
+        if (build_grid(c, s, d_vals, V, K, g, cells)) {
+            k_grid_test<<<grid_blocks(V), 256, 0, c.stream>>>(d_vals, V, K, g, s.T.p, s.S.p, s.keep.p);
+            c.launches++;
+            return 1;
+        }
+    }
+    k_pairwise<<<grid_blocks(V), 256, 256 * K * sizeof(double), c.stream>>>(d_vals, V, K, s.keep.p);
+    c.launches++;
+    return 2;
+}
+
+__global__ void k_compact_keep(const unsigned char* __restrict__ keep, long long V, const uint32_t* __restrict__ map,
+                               uint32_t* out, unsigned long long* count)
+{
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x); i0 < V;
+         i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        const bool f = i < V && keep[i];
+        warp_append(f, f ? (map ? map[i] : static_cast<uint32_t>(i)) : 0u, out, count);
+    }
+}
+
+__global__ void k_slots_to_rows(const uint32_t* __restrict__ slots, long long V, const uint32_t* __restrict__ table,
+                                const uint32_t* __restrict__ owner, uint32_t* rows, uint32_t* own_rows)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        rows[i] = table[slots[i]];
+        if (own_rows) own_rows[i] = owner[slots[i]];
+    }
+}
+
+__global__ void k_gather_vals(const double* __restrict__ src, const uint32_t* __restrict__ rows, long long V, int K,
+                              double* dst)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V * K;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        dst[i] = src[static_cast<long long>(rows[i / K]) * K + i % K];
+}
+
+__global__ void k_map_u32(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ map, long long n, uint32_t* out)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = map[idx[i]];
+}
+
+// Shared tail of both filters: V distinct vectors (d_vv, V x K) with owner configs
+// (row index into `words` via d_own, or none) -> front -> archive (lex-descending).
+void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, const uint64_t* words,
+                    const uint32_t* d_own, int wpc, DevArchive& out, ParetoTimings* tm)
+{
+    cudaEvent_t e0, e1, e2;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventCreate(&e2);
+    cudaEventRecord(e0, c.stream);
+    const int method = front_keep(c, s, d_vv, V, K);
+    s.rows.reserve(static_cast<size_t>(V) + 1);
+    ck(cudaMemsetAsync(s.counters.p + 1, 0, sizeof(unsigned long long), c.stream), "memset");
+    k_compact_keep<<<grid_blocks(V), 256, 0, c.stream>>>(s.keep.p, V, nullptr, s.rows.p, s.counters.p + 1);
+    c.launches++;
+    const long long F = static_cast<long long>(read_counter(c, s.counters.p + 1));
+    cudaEventRecord(e1, c.stream);
+    // gather front rows, then order them lexicographically descending
+    DevBuf<double> fv;
+    fv.reserve(static_cast<size_t>(F) * K + 1);
+    DevBuf<uint32_t> fown;
+    if (d_own) {
+        fown.reserve(static_cast<size_t>(F) + 1);
+        k_map_u32<<<grid_blocks(F), 256, 0, c.stream>>>(s.rows.p, d_own, F, fown.p);
+        c.launches++;
+    }
+    k_gather_rows<<<grid_blocks(F), 256, 0, c.stream>>>(d_vv, s.rows.p, F, K, nullptr, nullptr, 0, nullptr, fv.p,
+                                                         nullptr);
+    c.launches++;
+    s.rank.reserve(static_cast<size_t>(F) + 1);
+    k_lex_desc_rank<<<grid_blocks(F), 256, 256 * K * sizeof(double), c.stream>>>(fv.p, F, K, s.rank.p);
+    c.launches++;
+    out.F = F;
+    out.K = K;
+    out.wpc = d_own ? wpc : 0;
+    out.vals.reserve(static_cast<size_t>(F) * K + 1);
+    if (d_own) out.words.reserve(static_cast<size_t>(F) * wpc + 1);
+    k_gather_rows<<<grid_blocks(F), 256, 0, c.stream>>>(fv.p, nullptr, F, K, words, d_own ? fown.p : nullptr, wpc,
+                                                         s.rank.p, out.vals.p, d_own ? out.words.p : nullptr);
+    c.launches++;
+    cudaEventRecord(e2, c.stream);
+    ck(cudaStreamSynchronize(c.stream), "archive");
+    if (tm) {
+        tm->front_s = seconds_between(e0, e1);
+        tm->order_s = seconds_between(e1, e2);
+        tm->front_method = method;
+        tm->unique_vectors = V;
+    }
+    fv.release();
+    fown.release();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+}
+
+}  // namespace
+
+void evaluate_cuts_device(Ctx& c, const uint64_t* d_words, long long U, double* d_out)
+{
+    const int wpc = (c.n + 63) / 64;
+    if (c.k > kMaxK) usage("the GPU path supports at most 16 objectives");
+    if (U == 0) return;
+    if (c.integer_weights) {
+        const int sm = c.m * (2 + c.k) <= 12000 ? c.m * (2 + c.k) * 4 : 0;
+        k_eval_int<<<grid_blocks(U), 256, sm, c.stream>>>(d_words, nullptr, U, wpc, c.m, c.k, c.d_ei.p, c.d_ej.p,
+                                                           c.d_wi.p, d_out);
+    } else {
+        std::vector<double> W(static_cast<size_t>(c.k), 0.0);
+        for (int e = 0; e < c.m; ++e)
+            for (int q = 0; q < c.k; ++q) W[static_cast<size_t>(q)] += c.h_w[static_cast<size_t>(e) * c.k + q];
+        DevBuf<double> dW;
+        dW.reserve(static_cast<size_t>(c.k));
+        ck(cudaMemcpyAsync(dW.p, W.data(), sizeof(double) * c.k, cudaMemcpyHostToDevice, c.stream), "H2D");
+        k_eval_dbl<<<grid_blocks(U, 128), 128, 0, c.stream>>>(d_words, nullptr, U, wpc, c.n, c.k, c.d_rowptr.p,
+                                                               c.d_col.p, c.d_eidx.p, c.d_w.p, dW.p, d_out);
+        ck(cudaStreamSynchronize(c.stream), "eval");
+        dW.release();
+    }
+    c.launches++;
+    ck(cudaGetLastError(), "evaluate_cuts");
+}
+
+void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive& out, ParetoTimings* tm)
+{
+    if (M <= 0) usage("non-dominated filter needs a non-empty pool");
+    if (c.n == 0) usage("pool does not match instance");
+    if (c.k > kMaxK) usage("the GPU path supports at most 16 objectives");
+    if (M >= 0xFFFFFFFFll) usage("pool too large for one device pass (shard it)");
+    Scratch& s = scratch(c);
+    const int wpc = (c.n + 63) / 64;
+    const int K = c.k;
+    cudaEvent_t e0, e1, e2, e3;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventCreate(&e2);
+    cudaEventCreate(&e3);
+    cudaEventRecord(e0, c.stream);
+    // K5 dedup
+    const uint64_t tsize = pow2_at_least(2ull * static_cast<uint64_t>(M));
+    s.table.reserve(tsize);
+    s.uniq.reserve(static_cast<size_t>(M));
+    s.counters.reserve(8);
+    ck(cudaMemsetAsync(s.table.p, 0xFF, sizeof(uint32_t) * tsize, c.stream), "memset");
+    ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long) * 8, c.stream), "memset");
+    k_dedup<<<grid_blocks(M), 256, 0, c.stream>>>(d_words, M, wpc, s.table.p, tsize - 1, s.uniq.p, s.counters.p);
+    c.launches++;
+    const long long U = static_cast<long long>(read_counter(c, s.counters.p));
+    cudaEventRecord(e1, c.stream);
+    // K4 eval of the unique configs
+    s.vals.reserve(static_cast<size_t>(U) * K + 1);
+    if (c.integer_weights) {
+        const int sm = c.m * (2 + K) <= 12000 ? c.m * (2 + K) * 4 : 0;
+        k_eval_int<<<grid_blocks(U), 256, sm, c.stream>>>(d_words, s.uniq.p, U, wpc, c.m, K, c.d_ei.p, c.d_ej.p,
+                                                           c.d_wi.p, s.vals.p);
+        c.launches++;
+    } else {
+        std::vector<double> W(static_cast<size_t>(K), 0.0);
+        for (int e = 0; e < c.m; ++e)
+            for (int q = 0; q < K; ++q) W[static_cast<size_t>(q)] += c.h_w[static_cast<size_t>(e) * K + q];
+        s.rdev.reserve(static_cast<size_t>(K));
+        ck(cudaMemcpyAsync(s.rdev.p, W.data(), sizeof(double) * K, cudaMemcpyHostToDevice, c.stream), "H2D");
+        k_eval_dbl<<<grid_blocks(U, 128), 128, 0, c.stream>>>(d_words, s.uniq.p, U, wpc, c.n, K, c.d_rowptr.p,
+                                                               c.d_col.p, c.d_eidx.p, c.d_w.p, s.rdev.p, s.vals.p);
+        c.launches++;
+    }
+    ck(cudaGetLastError(), "eval");
+    cudaEventRecord(e2, c.stream);
+    // K6 collapse onto the lex-smallest config
+    const uint64_t t2 = pow2_at_least(2ull * static_cast<uint64_t>(U) + 16);
+    s.table2.reserve(t2);
+    s.owner.reserve(t2);
+    s.reps.reserve(static_cast<size_t>(U) + 1);
+    ck(cudaMemsetAsync(s.table2.p, 0xFF, sizeof(uint32_t) * t2, c.stream), "memset");
+    ck(cudaMemsetAsync(s.owner.p, 0xFF, sizeof(uint32_t) * t2, c.stream), "memset");
+    k_collapse<<<grid_blocks(U), 256, 0, c.stream>>>(s.vals.p, U, K, d_words, s.uniq.p, wpc, s.table2.p, s.owner.p,
+                                                      t2 - 1, s.reps.p, s.counters.p + 2);
+    c.launches++;
+    const long long V = static_cast<long long>(read_counter(c, s.counters.p + 2));
+    // distinct vectors (row of the first inserter) + owner rows -> dense arrays
+    DevBuf<uint32_t> vrow, vown;
+    vrow.reserve(static_cast<size_t>(V) + 1);
+    vown.reserve(static_cast<size_t>(V) + 1);
+    k_slots_to_rows<<<grid_blocks(V), 256, 0, c.stream>>>(s.reps.p, V, s.table2.p, s.owner.p, vrow.p, vown.p);
+    c.launches++;
+    DevBuf<double> vv;
+    vv.reserve(static_cast<size_t>(V) * K + 1);
+    k_gather_vals<<<grid_blocks(V * K), 256, 0, c.stream>>>(s.vals.p, vrow.p, V, K, vv.p);
+    c.launches++;
+    // owner rows index the unique list; map them to pool rows
+    DevBuf<uint32_t> vcfg;
+    vcfg.reserve(static_cast<size_t>(V) + 1);
+    k_map_u32<<<grid_blocks(V), 256, 0, c.stream>>>(vown.p, s.uniq.p, V, vcfg.p);
+    c.launches++;
+    cudaEventRecord(e3, c.stream);
+    ck(cudaStreamSynchronize(c.stream), "collapse");
+    if (tm) {
+        tm->dedup_s = seconds_between(e0, e1);
+        tm->eval_s = seconds_between(e1, e2);
+        tm->collapse_s = seconds_between(e2, e3);
+        tm->unique_configs = U;
+    }
+    finish_archive(c, s, vv.p, V, K, d_words, vcfg.p, wpc, out, tm);
+    vrow.release();
+    vown.release();
+    vv.release();
+    vcfg.release();
+    for (auto ev : {e0, e1, e2, e3}) cudaEventDestroy(ev);
+}
+
+void filter_values_device(Ctx& c, const double* d_vals, const uint64_t* d_words, int wpc, int n_spins, long long M,
+                          int K, DevArchive& out, ParetoTimings* tm)
+{
+    (void)n_spins;
+    if (M <= 0) usage("non-dominated filter needs a non-empty pool");
+    if (K > kMaxK) usage("the GPU path supports at most 16 objectives");
+    Scratch& s = scratch(c);
+    s.counters.reserve(8);
+    ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long) * 8, c.stream), "memset");
+    const uint64_t t2 = pow2_at_least(2ull * static_cast<uint64_t>(M) + 16);
+    s.table2.reserve(t2);
+    s.owner.reserve(t2);
+    s.reps.reserve(static_cast<size_t>(M) + 1);
+    ck(cudaMemsetAsync(s.table2.p, 0xFF, sizeof(uint32_t) * t2, c.stream), "memset");
+    ck(cudaMemsetAsync(s.owner.p, 0xFF, sizeof(uint32_t) * t2, c.stream), "memset");
+    k_collapse<<<grid_blocks(M), 256, 0, c.stream>>>(d_vals, M, K, d_words, nullptr, wpc, s.table2.p, s.owner.p,
+                                                      t2 - 1, s.reps.p, s.counters.p + 2);
+    c.launches++;
+    const long long V = static_cast<long long>(read_counter(c, s.counters.p + 2));
+    DevBuf<uint32_t> vrow, vown;
+    vrow.reserve(static_cast<size_t>(V) + 1);
+    vown.reserve(static_cast<size_t>(V) + 1);
+    k_slots_to_rows<<<grid_blocks(V), 256, 0, c.stream>>>(s.reps.p, V, s.table2.p, s.owner.p, vrow.p,
+                                                           d_words ? vown.p : nullptr);
+    c.launches++;
+    DevBuf<double> vv;
+    vv.reserve(static_cast<size_t>(V) * K + 1);
+    k_gather_vals<<<grid_blocks(V * K), 256, 0, c.stream>>>(d_vals, vrow.p, V, K, vv.p);
+    c.launches++;
+    if (tm) {
+        tm->unique_configs = M;
+    }
+    finish_archive(c, s, vv.p, V, K, d_words, d_words ? vown.p : nullptr, wpc, out, tm);
+    vrow.release();
+    vown.release();
+    vv.release();
+}
+
+std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed)
+{
+    if (count < 1) usage("sampled reference needs count >= 1");
+    if (c.n > 1024) usage("reference sampling on the GPU path supports n <= 1024");
+    Scratch& s = scratch(c);
+    s.counters.reserve(8 + kMaxK);
+    DevBuf<unsigned long long> rmin;
+    rmin.reserve(static_cast<size_t>(c.k));
+    std::vector<unsigned long long> init(static_cast<size_t>(c.k), ~0ull);
+    ck(cudaMemcpyAsync(rmin.p, init.data(), sizeof(unsigned long long) * c.k, cudaMemcpyHostToDevice, c.stream), "H2D");
+    k_ref_sample<<<grid_blocks(count, 128), 128, 0, c.stream>>>(count, derive_key(seed, 0x70617265u), c.n, c.m, c.k,
+                                                                 c.d_ei.p, c.d_ej.p, c.d_w.p, rmin.p);
+    c.launches++;
+    std::vector<unsigned long long> h(static_cast<size_t>(c.k));
+    ck(cudaMemcpyAsync(h.data(), rmin.p, sizeof(unsigned long long) * c.k, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "reference point");
+    rmin.release();
+    std::vector<double> r(static_cast<size_t>(c.k));
+    for (int k = 0; k < c.k; ++k) {
+        const uint64_t key = h[static_cast<size_t>(k)];
+        const uint64_t b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
+        std::memcpy(&r[static_cast<size_t>(k)], &b, 8);
+    }
+    return r;
+}
+
+double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, const std::vector<double>& r)
+{
+    if (F <= 0) usage("hypervolume of an empty archive");
+    if (static_cast<int>(r.size()) != K) usage("reference point length does not match archive");
+    if (K > kMaxK) usage("the GPU path supports at most 16 objectives");
+    Scratch& s = scratch(c);
+    s.rdev.reserve(static_cast<size_t>(K));
+    s.counters.reserve(8);
+    ck(cudaMemcpyAsync(s.rdev.p, r.data(), sizeof(double) * K, cudaMemcpyHostToDevice, c.stream), "H2D");
+    const unsigned long long none = ~0ull;
+    ck(cudaMemcpyAsync(s.counters.p + 3, &none, sizeof none, cudaMemcpyHostToDevice, c.stream), "H2D");
+    k_ref_check<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, F, K, s.rdev.p, s.counters.p + 3);
+    c.launches++;
+    const unsigned long long bad = read_counter(c, s.counters.p + 3);
+    if (bad != none)
+        usage("reference point not dominated by archive entry " + std::to_string(bad / K) + " (objective " +
+              std::to_string(bad % K) + ")");
+    // gains are exact integers when every value and r is integral (n=42 configs): then the
+    // __int128 cell sum is the exact hypervolume, i.e. the reference's exact double result
+    std::vector<double> hv(static_cast<size_t>(F) * K);
+    ck(cudaMemcpyAsync(hv.data(), d_vals, sizeof(double) * F * K, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    bool integral = true;
+    double maxg = 0;
+    for (long long i = 0; i < F; ++i)
+        for (int k = 0; k < K; ++k) {
+            const double g = hv[static_cast<size_t>(i * K + k)] - r[static_cast<size_t>(k)];
+            integral &= std::floor(hv[static_cast<size_t>(i * K + k)]) == hv[static_cast<size_t>(i * K + k)] &&
+                        std::fabs(hv[static_cast<size_t>(i * K + k)]) < 9.0e15;
+            maxg = std::max(maxg, g);
+        }
+    for (int k = 0; k < K; ++k) integral &= std::floor(r[static_cast<size_t>(k)]) == r[static_cast<size_t>(k)];
+    if (integral && K * std::log2(std::max(maxg, 1.0)) > 120.0) integral = false;  // keep __int128 exact
+    if (K == 1) {
+        double best = 0;  // pareto.hpp:544-548
+        for (long long i = 0; i < F; ++i) best = std::max(best, hv[static_cast<size_t>(i)] - r[0]);
+        return best;
+    }
+    GridGeo g{};
+    long long cells = 0;
+    if (!build_grid(c, s, d_vals, F, K, g, cells))
+        runtime("hypervolume: front too large for the compressed-grid method (" + std::to_string(F) + " points)");
+    const int blocks = grid_blocks(cells);
+    s.ipart.reserve(static_cast<size_t>(blocks));
+    s.dpart.reserve(static_cast<size_t>(blocks));
+    k_hv_cells<<<blocks, 256, 0, c.stream>>>(s.S.p, cells, g, s.rdev.p, integral, s.ipart.p, s.dpart.p, nullptr);
+    c.launches++;
+    ck(cudaGetLastError(), "hv");
+    std::vector<__int128> ip(static_cast<size_t>(blocks));
+    std::vector<double> dp(static_cast<size_t>(blocks));
+    ck(cudaMemcpyAsync(ip.data(), s.ipart.p, sizeof(__int128) * blocks, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaMemcpyAsync(dp.data(), s.dpart.p, sizeof(double) * blocks, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "hv");
+    if (integral) {
+        __int128 tot = 0;
+        for (auto v : ip) tot += v;
+        return static_cast<double>(tot);
+    }
+    double tot = 0, comp = 0;
+    for (double v : dp) {
+        const double y = v - comp;
+        const double t = tot + y;
+        comp = (t - tot) - y;
+        tot = t;
+    }
+    return tot;
+}
+
+}  // namespace momc_b200

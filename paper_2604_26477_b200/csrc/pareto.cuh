@@ -1,0 +1,48 @@
+// Pareto stage on the device: dedup -> cut evaluation -> collapse -> non-dominated front
+// -> archive order -> reference point -> hypervolume. Restates pareto.hpp:253-410, 540-655.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace momc_b200 {
+
+// Device-resident archive / value set produced by the Pareto stage.
+struct DevArchive {
+    long long F = 0;  // entries
+    int K = 0;
+    int wpc = 0;      // 0 for objective-only archives
+    DevBuf<double> vals;     // F x K, lexicographically descending
+    DevBuf<uint64_t> words;  // F x wpc
+};
+
+struct ParetoTimings {
+    double dedup_s = 0, eval_s = 0, collapse_s = 0, front_s = 0, order_s = 0;
+    long long unique_configs = 0, unique_vectors = 0;
+    int front_method = 0;  // 1 grid, 2 pairwise
+};
+
+// non_dominated_filter(pool, inst) (pareto.hpp:370-410) over M configs resident on the
+// device (d_words, M x wpc). The result replaces `out`. Synchronous.
+void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive& out, ParetoTimings* tm);
+
+// non_dominated_filter(vector<ObjectiveVector>) (pareto.hpp:253-293), cut sense; d_vals M x K.
+// With d_words != nullptr (wpc words per vector), equal vectors keep the lex-smallest
+// config (the cross-shard merge of pool archives, pareto.hpp:383-387).
+void filter_values_device(Ctx& c, const double* d_vals, const uint64_t* d_words, int wpc, int n_spins,
+                          long long M, int K, DevArchive& out, ParetoTimings* tm);
+
+// detail::evaluate_cuts (pareto.hpp:330-363) for U configs: d_out U x K.
+void evaluate_cuts_device(Ctx& c, const uint64_t* d_words, long long U, double* d_out);
+
+// reference_point_sampled (pareto.hpp:620-642)
+std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed);
+
+// hypervolume (pareto.hpp:540-552) of F x K values (device) against r (host); validates r
+// (pareto.hpp:103-118) and throws the reference's messages.
+double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, const std::vector<double>& r);
+
+}  // namespace momc_b200
