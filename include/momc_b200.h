@@ -62,6 +62,8 @@ int momc_b200_ctx_sync(momc_ctx* ctx, char* err, size_t errlen);
 void* momc_b200_ctx_stream(momc_ctx* ctx);
 /* number of kernel launches issued by this context since creation */
 long long momc_b200_ctx_launches(momc_ctx* ctx);
+/* sampler blocks re-run on the exact sequential path (noise-event buffer overflow) */
+long long momc_b200_ctx_fallback_blocks(momc_ctx* ctx);
 
 /* Upload / validate the instance (MultiObjectiveInstance ctor checks, instance.hpp:104-123)
  * and build the CSR graph on the device. */
@@ -145,6 +147,15 @@ typedef struct {
 int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t* nums, int L, int H,
                     const momc_solver_cfg* cfg, int runs, int ref_count, const double* fixed_ref, uint64_t* out_pool,
                     momc_bench_report* report, char* err, size_t errlen);
+
+/* The same pipeline on the resident instance + weights (no host copies besides scalars):
+ * scalarise -> sample blocks [block_begin, block_end) -> filter -> (if do_hv) reference
+ * point + hypervolume. Used for device-resident throughput and per-rank shards. */
+int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long long block_begin,
+                       long long block_end, int do_hv, int ref_count, const double* fixed_ref,
+                       momc_bench_report* report, char* err, size_t errlen);
+/* flattened (run, weight, chunk) block count of a run configuration on this context */
+long long momc_b200_num_blocks(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs);
 
 #ifdef __cplusplus
 }

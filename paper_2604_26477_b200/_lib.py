@@ -80,6 +80,7 @@ SIGNATURES = [
     ("momc_b200_ctx_sync", C.c_int, [vp, C.c_char_p, C.c_size_t]),
     ("momc_b200_ctx_stream", vp, [vp]),
     ("momc_b200_ctx_launches", C.c_longlong, [vp]),
+    ("momc_b200_ctx_fallback_blocks", C.c_longlong, [vp]),
     ("momc_b200_set_instance", C.c_int, [vp, C.POINTER(InstanceViewC), C.c_char_p, C.c_size_t]),
     ("momc_b200_set_weights", C.c_int, [vp, i32p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     ("momc_b200_get_coupling", C.c_int, [vp, C.c_int, dp, dp, C.c_char_p, C.c_size_t]),
@@ -105,6 +106,9 @@ SIGNATURES = [
     ("momc_b200_clamp_reference", C.c_int, [vp, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_bench", C.c_int, [vp, C.POINTER(InstanceViewC), i32p, C.c_int, C.c_int, C.POINTER(SolverCfgC),
                                   C.c_int, C.c_int, dp, u64p, C.POINTER(BenchReportC), C.c_char_p, C.c_size_t]),
+    ("momc_b200_pipeline", C.c_int, [vp, C.POINTER(SolverCfgC), C.c_int, C.c_longlong, C.c_longlong, C.c_int,
+                                     C.c_int, dp, C.POINTER(BenchReportC), C.c_char_p, C.c_size_t]),
+    ("momc_b200_num_blocks", C.c_longlong, [vp, C.POINTER(SolverCfgC), C.c_int]),
 ]
 
 _lib = None

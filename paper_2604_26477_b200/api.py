@@ -464,6 +464,9 @@ class Session:
     def launches(self) -> int:
         return int(self.lib.momc_b200_ctx_launches(self.h))
 
+    def fallback_blocks(self) -> int:
+        return int(self.lib.momc_b200_ctx_fallback_blocks(self.h))
+
     def stream(self) -> int:
         return int(self.lib.momc_b200_ctx_stream(self.h) or 0)
 
@@ -516,6 +519,52 @@ class Session:
 
     def pool_device_ptr(self) -> int:
         return int(self.lib.momc_b200_pool_device(self.h) or 0)
+
+    def num_blocks(self, config: SolverConfig, runs: int = 1) -> int:
+        cfg = config.c()
+        return int(self.lib.momc_b200_num_blocks(self.h, C.byref(cfg), runs))
+
+    def pipeline(self, config: SolverConfig, runs: int = 1, block_begin: int = 0, block_end: int = -1,
+                 do_hv: bool = True, ref_count: int = 4096, fixed_reference=None) -> dict:
+        """Resident-instance pipeline (momc_b200_pipeline): scalarise, sample, filter, [r, HV]."""
+        config.validate()
+        cfg = config.c()
+        rep = _lib.BenchReportC()
+        fr = np.ascontiguousarray(fixed_reference, np.float64) if fixed_reference is not None else None
+        err = _errbuf()
+        _raise(self.lib.momc_b200_pipeline(self.h, C.byref(cfg), runs, block_begin, block_end, int(do_hv), ref_count,
+                                           fr.ctypes.data_as(_lib.dp) if fr is not None else None, C.byref(rep),
+                                           err, 2048), err)
+        self._pool_geom = (runs, self.L, config.batch_size)
+        out = {name: getattr(rep, name) for name, _ in _lib.BenchReportC._fields_}
+        out["reference"] = list(rep.reference)[: self.inst.k()]
+        return out
+
+    def archive(self, with_configs: bool = True) -> "ParetoArchive":
+        return _fetch_archive(self, self.inst.k(), self.inst.n(), with_configs)
+
+    def archive_hypervolume(self, r) -> float:
+        r = np.ascontiguousarray(r, np.float64)
+        out = C.c_double()
+        err = _errbuf()
+        _raise(self.lib.momc_b200_archive_hypervolume(self.h, r.ctypes.data_as(_lib.dp), C.byref(out), err, 2048), err)
+        return out.value
+
+    def merge_device(self, d_vals: int, d_words: int, wpc: int, M: int, k: int) -> int:
+        """Filter M device vectors (+ configs) into the resident archive (multi-GPU merge)."""
+        F = C.c_int64()
+        err = _errbuf()
+        _raise(self.lib.momc_b200_filter_values_dev(self.h, C.c_void_p(d_vals), C.c_void_p(d_words), wpc, M, k,
+                                                    C.byref(F), err, 2048), err)
+        return F.value
+
+    def archive_copy_device(self, d_vals: int, d_words: int):
+        err = _errbuf()
+        _raise(self.lib.momc_b200_archive_copy_device(self.h, C.c_void_p(d_vals), C.c_void_p(d_words), err, 2048),
+               err)
+
+    def archive_size(self) -> int:
+        return int(self.lib.momc_b200_archive_size(self.h))
 
 
 _default_session = None

@@ -395,6 +395,8 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         ck(cudaMemsetAsync(q.nan_block, 0, sizeof(int), c.stream), "memset");
         ck(static_cast<cudaError_t>(launch_sampler_generic(q, 1, g, c.stream)), "sampler fallback");
         c.launches += 3 + 2ll * p.T;
+        ++c.fallback_blocks;
+        c.fallback_reasons |= flags[static_cast<size_t>(b)];
         ck(cudaMemcpyAsync(&flags[static_cast<size_t>(b)], q.nan_block, sizeof(int), cudaMemcpyDeviceToHost, c.stream),
            "D2H");
     }
@@ -525,6 +527,7 @@ int momc_b200_ctx_sync(momc_ctx* ctx, char* err, size_t errlen)
 
 void* momc_b200_ctx_stream(momc_ctx* ctx) { return ctx->stream; }
 long long momc_b200_ctx_launches(momc_ctx* ctx) { return ctx->launches; }
+long long momc_b200_ctx_fallback_blocks(momc_ctx* ctx) { return ctx->fallback_blocks | (static_cast<long long>(ctx->fallback_reasons) << 40); }
 
 int momc_b200_set_instance(momc_ctx* ctx, const momc_instance_view* inst, char* err, size_t errlen)
 {
@@ -827,6 +830,88 @@ int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t
         if (out_pool) pool_get(*ctx, out_pool, nullptr);
         rep->end_to_end_s = std::chrono::duration<double>(clk::now() - t0).count();
     });
+}
+
+
+int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long long block_begin, long long block_end,
+                       int do_hv, int ref_count, const double* fixed_ref, momc_bench_report* rep, char* err,
+                       size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        validate_cfg(cfg);
+        if (ctx->n == 0) usage("no instance set");
+        if (ctx->L < 1) usage("run_sampler needs at least one weight vector");
+        std::memset(rep, 0, sizeof *rep);
+        using clk = std::chrono::steady_clock;
+        const auto t0 = clk::now();
+        // model construction: re-scalarise the resident lattice (build_block_system)
+        std::vector<int32_t> nums(static_cast<size_t>(ctx->L) * ctx->k);
+        ck(cudaMemcpyAsync(nums.data(), ctx->d_nums.p, sizeof(int32_t) * nums.size(), cudaMemcpyDeviceToHost,
+                           ctx->stream), "D2H");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        set_weights(*ctx, nums.data(), ctx->L, ctx->H);
+        rep->model_construction_s = std::chrono::duration<double>(clk::now() - t0).count();
+        double ss = 0;
+        sample(*ctx, cfg, runs, block_begin, block_end, &ss);
+        rep->sampling_s = ss;
+        rep->pool_size = ctx->pool_size;
+        const auto tf = clk::now();
+        ParetoTimings tm;
+        DevArchive& a = resident_archive(*ctx);
+        // only the sampled blocks hold fresh configs: filter their contiguous pool rows
+        const int bt = ctx->pool_block_traj;
+        const int chunks = (cfg->batch_size + bt - 1) / bt;
+        long long r0 = 0, r1 = ctx->pool_size;
+        if (ctx->pool_blocks > 0) {
+            const long long b0 = ctx->pool_block_begin, b1 = b0 + ctx->pool_blocks - 1;
+            r0 = (b0 / chunks) * cfg->batch_size + (b0 % chunks) * static_cast<long long>(bt);
+            r1 = std::min<long long>((b1 / chunks) * cfg->batch_size + std::min<long long>((b1 % chunks + 1) * static_cast<long long>(bt), cfg->batch_size),
+                                     ctx->pool_size);
+        }
+        const int wpc = (ctx->n + 63) / 64;
+        filter_pool_device(*ctx, ctx->d_words.p + r0 * wpc, r1 - r0, a, &tm);
+        rep->pool_size = r1 - r0;
+        rep->unique_configs = tm.unique_configs;
+        rep->unique_vectors = tm.unique_vectors;
+        rep->archive_size = a.F;
+        rep->dedup_s = tm.dedup_s;
+        rep->eval_s = tm.eval_s;
+        rep->collapse_s = tm.collapse_s;
+        rep->front_s = tm.front_s;
+        rep->order_s = tm.order_s;
+        rep->front_method = tm.front_method;
+        if (do_hv) {
+            const auto tr = clk::now();
+            std::vector<double> r(static_cast<size_t>(ctx->k));
+            if (fixed_ref) {
+                r.assign(fixed_ref, fixed_ref + ctx->k);
+            } else {
+                r = reference_point_sampled_device(*ctx, ref_count, cfg->seed);
+                std::vector<double> f(static_cast<size_t>(a.F) * a.K);
+                ck(cudaMemcpyAsync(f.data(), a.vals.p, sizeof(double) * f.size(), cudaMemcpyDeviceToHost, ctx->stream),
+                   "D2H");
+                ck(cudaStreamSynchronize(ctx->stream), "sync");
+                for (long long i = 0; i < a.F; ++i)
+                    for (int l = 0; l < a.K; ++l)
+                        r[static_cast<size_t>(l)] = std::min(r[static_cast<size_t>(l)], f[static_cast<size_t>(i * a.K + l)]);
+            }
+            const auto th = clk::now();
+            rep->reference_s = std::chrono::duration<double>(th - tr).count();
+            rep->hv = hypervolume_device(*ctx, a.vals.p, a.F, a.K, r);
+            rep->hv_s = std::chrono::duration<double>(clk::now() - th).count();
+            for (int l = 0; l < ctx->k && l < 16; ++l) rep->reference[l] = r[static_cast<size_t>(l)];
+        }
+        rep->pareto_filtering_s = std::chrono::duration<double>(clk::now() - tf).count();
+        rep->end_to_end_s = std::chrono::duration<double>(clk::now() - t0).count();
+    });
+}
+
+long long momc_b200_num_blocks(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs)
+{
+    if (!ctx || !cfg || cfg->batch_size < 1 || runs < 1 || ctx->L < 1) return 0;
+    const int bt = sampler_block_traj(ctx->n, cfg->alpha);
+    return static_cast<long long>(runs) * ctx->L * ((cfg->batch_size + bt - 1) / bt);
 }
 
 }  // extern "C"

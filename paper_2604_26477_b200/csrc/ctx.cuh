@@ -53,6 +53,8 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
+    long long fallback_blocks = 0;  // sampler blocks re-run on the sequential path
+    int fallback_reasons = 0;
 
     // instance
     int n = 0, k = 0, m = 0, nnz = 0;

@@ -65,9 +65,9 @@ struct Geo {
     static constexpr int kNP = kNQ * LANES;                 // integrated spins (>= n)
     static constexpr int kNB = ((kNP + 3) / 4 + 2 + LANES - 1) / LANES * LANES;  // Philox blocks per step
     static constexpr int kNU = 4 * kNB;                     // words covered by the fast mask
-    static constexpr int kNA = kNU + 16;                    // allocated words (A2 extends on demand)
+    static constexpr int kNA = kNU + 40;                    // allocated words (A2 extends on demand; P(overflow) ~ 1e-15)
     static constexpr int kUS = kTPC + 1;                    // word-row stride (odd: lanes of a trajectory hit distinct banks)
-    static constexpr int kECAP = 8;                         // event entries per trajectory-step
+    static constexpr int kECAP = 16;                        // event entries per trajectory-step (P(>16) ~ 1e-14)
     static constexpr int zig = 0;                                           // ZigTables (2560 B)
     static constexpr int ubuf = 2560;                                       // kNA x kUS u32
     static constexpr int ent = ubuf + (kNA * kUS * 4 + 15) / 16 * 16;       // kECAP x kTPC u32
@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     const int* pcs = pc + s0 * DMAX;
     const double* pvs = pv + s0 * DMAX;
     bool overflow = false;
+    int ovf_code = 0;  // which buffer overflowed (diagnostics)
     __syncwarp(wmask);
 
     for (int t = 0; t < p.T; ++t) {
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                 if (q > last) break;  // every remaining normal is a fast attempt
                 if (q + 9 >= G::kNA) {
                     overflow = true;
+                    ovf_code |= 4;
                     break;
                 }
                 while (gen <= q + 8) {  // words a wedge attempt may consume
@@ -284,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                     for (;;) {
                         if (qq + 4 > G::kNA) {
                             overflow = true;
+                    ovf_code |= 8;
                             break;
                         }
                         while (gen < qq + 4) {
@@ -327,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                 if (ne > 0 && static_cast<int>(en[(ne - 1) * TPC] & 0xFFu) == idx) --ne;
                 if (ne >= G::kECAP) {
                     overflow = true;
+                    ovf_code |= 16;
                     break;
                 }
                 en[ne * TPC] = static_cast<uint32_t>(idx) | (static_cast<uint32_t>(new_pos - new_i) << 8) |
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     // NaN (numerical failure) -> bit 1; noise-event buffer overflow (re-run on the exact
     // sequential path) -> bit 2
     if (bad) atomicOr(&p.nan_block[blockIdx.x], 1);
-    if (overflow) atomicOr(&p.nan_block[blockIdx.x], 2);
+    if (overflow) atomicOr(&p.nan_block[blockIdx.x], 2 | ovf_code);
     if (p.block_end_ns && (tid & 31) == 0) atomicMax(&p.block_end_ns[blockIdx.x], globaltimer());
 }
 
