@@ -166,7 +166,7 @@ def load_instance(path) -> MultiObjectiveInstance:
 
     with fh:
         text = fh.read()
-    lines = text.split("\n")
+    lines = text.split("\n") if text else []
     if text.endswith("\n"):
         lines = lines[:-1]  # std::getline reports EOF after a trailing newline
     if not lines:
