@@ -69,6 +69,17 @@ long long momc_b200_ctx_fallback_blocks(momc_ctx* ctx);
  * and build the CSR graph on the device. */
 int momc_b200_set_instance(momc_ctx* ctx, const momc_instance_view* inst, char* err, size_t errlen);
 
+/* generate_uniform_instance (instance.hpp:259-284) on the device and make it the resident
+ * instance; kind 0 = WeightSpec::uniform_int(lo, hi), 1 = uniform_real(lo, hi). */
+int momc_b200_generate_uniform_instance(momc_ctx* ctx, int n, double density, int k, int kind, double lo, double hi,
+                                        uint64_t seed, int64_t* out_m, char* err, size_t errlen);
+/* copy the resident instance out: edge_i, edge_j (m), w (m x k) */
+int momc_b200_instance_get(momc_ctx* ctx, int32_t* edge_i, int32_t* edge_j, double* w, char* err, size_t errlen);
+/* dSB with integer weights and |H*J(c)| <= 127 uses the int8 tensor-core contraction
+ * (exact) with one FP64 rounding of J(c).sgn(X) when n >= n_min (default 256); smaller n
+ * keep the bit-exact FP64 order of the reference. */
+int momc_b200_set_dense_threshold(momc_ctx* ctx, int n_min);
+
 /* Upload L interior weight vectors (numerators, row-major L x k, denominator H) and
  * scalarise every one on the device: build_block_system / scalarize
  * (scalarize.hpp:22-39, :62-71). Fails with MOMC_EUSAGE and the reference's message on a

@@ -480,6 +480,27 @@ class Session:
         _raise(self.lib.momc_b200_set_instance(self.h, C.byref(v), err, 2048), err)
         self.inst = inst
 
+    def generate_uniform_instance(self, n: int, density: float, k: int, seed: int, kind: str = "int",
+                                  lo: float = 1.0, hi: float = 10.0) -> MultiObjectiveInstance:
+        """generate_uniform_instance (instance.hpp:259-284) on the device; becomes resident."""
+        m = C.c_int64()
+        err = _errbuf()
+        _raise(self.lib.momc_b200_generate_uniform_instance(self.h, n, density, k, 0 if kind == "int" else 1, lo, hi,
+                                                            seed, C.byref(m), err, 2048), err)
+        ei = np.zeros(m.value, np.int32)
+        ej = np.zeros(m.value, np.int32)
+        w = np.zeros((m.value, k), np.float64)
+        _raise(self.lib.momc_b200_instance_get(self.h, ei.ctypes.data_as(_lib.i32p), ej.ctypes.data_as(_lib.i32p),
+                                               w.ctypes.data_as(_lib.dp), err, 2048), err)
+        inst = MultiObjectiveInstance.__new__(MultiObjectiveInstance)
+        inst._n, inst._k = n, k
+        inst.edge_i, inst.edge_j, inst.weights = ei, ej, w
+        self.inst = inst
+        return inst
+
+    def set_dense_threshold(self, n_min: int):
+        self.lib.momc_b200_set_dense_threshold(self.h, n_min)
+
     def set_weights(self, weights):
         nums, H = _weights_array(weights, self.inst.k())
         err = _errbuf()

@@ -158,13 +158,21 @@ void set_instance(Ctx& c, const momc_instance_view* iv)
     if (iv->n < 1) usage("vertex count must be positive");
     if (iv->k < 1) usage("objective count must be positive");
     if (iv->m < 0) usage("edge count must be non-negative");
-    std::unordered_set<long long> seen;
-    seen.reserve(static_cast<size_t>(iv->m) * 2 + 1);
+    bool sorted = true;  // strictly increasing (i, j): duplicates are impossible, CSR needs no sort
     for (int e = 0; e < iv->m; ++e) {
         const int i = iv->edge_i[e], j = iv->edge_j[e];
         if (i == j) usage("self-loop edge");
         if (i < 0 || j < 0 || i >= iv->n || j >= iv->n || i >= j) usage("edge endpoints must satisfy 0 <= i < j < n");
-        if (!seen.insert(static_cast<long long>(i) * iv->n + j).second) usage("duplicate edge");
+        if (e > 0) {
+            const int pi = iv->edge_i[e - 1], pj = iv->edge_j[e - 1];
+            if (!(pi < i || (pi == i && pj < j))) sorted = false;
+        }
+    }
+    if (!sorted) {
+        std::unordered_set<long long> seen;
+        seen.reserve(static_cast<size_t>(iv->m) * 2 + 1);
+        for (int e = 0; e < iv->m; ++e)
+            if (!seen.insert(static_cast<long long>(iv->edge_i[e]) * iv->n + iv->edge_j[e]).second) usage("duplicate edge");
     }
     c.n = iv->n;
     c.k = iv->k;
@@ -193,18 +201,29 @@ void set_instance(Ctx& c, const momc_instance_view* iv)
     }
     std::vector<int> rowptr(static_cast<size_t>(c.n) + 1, 0);
     for (int i = 0; i < c.n; ++i) rowptr[static_cast<size_t>(i) + 1] = rowptr[static_cast<size_t>(i)] + deg[static_cast<size_t>(i)];
-    std::vector<std::vector<std::pair<int, int>>> rows(static_cast<size_t>(c.n));
-    for (int e = 0; e < c.m; ++e) {
-        rows[static_cast<size_t>(c.h_ei[e])].push_back({c.h_ej[e], e});
-        rows[static_cast<size_t>(c.h_ej[e])].push_back({c.h_ei[e], e});
-    }
     std::vector<int> col(static_cast<size_t>(c.nnz)), eidx(static_cast<size_t>(c.nnz));
-    for (int i = 0; i < c.n; ++i) {
-        auto& r = rows[static_cast<size_t>(i)];
-        std::sort(r.begin(), r.end());
-        for (size_t q = 0; q < r.size(); ++q) {
-            col[static_cast<size_t>(rowptr[static_cast<size_t>(i)]) + q] = r[q].first;
-            eidx[static_cast<size_t>(rowptr[static_cast<size_t>(i)]) + q] = r[q].second;
+    if (sorted) {  // visiting (i, j) in order appends ascending columns to every row
+        std::vector<int> fill(rowptr.begin(), rowptr.end() - 1);
+        for (int e = 0; e < c.m; ++e) {
+            const int i = c.h_ei[static_cast<size_t>(e)], j = c.h_ej[static_cast<size_t>(e)];
+            col[static_cast<size_t>(fill[static_cast<size_t>(i)])] = j;
+            eidx[static_cast<size_t>(fill[static_cast<size_t>(i)]++)] = e;
+            col[static_cast<size_t>(fill[static_cast<size_t>(j)])] = i;
+            eidx[static_cast<size_t>(fill[static_cast<size_t>(j)]++)] = e;
+        }
+    } else {
+        std::vector<std::vector<std::pair<int, int>>> rows(static_cast<size_t>(c.n));
+        for (int e = 0; e < c.m; ++e) {
+            rows[static_cast<size_t>(c.h_ei[static_cast<size_t>(e)])].push_back({c.h_ej[static_cast<size_t>(e)], e});
+            rows[static_cast<size_t>(c.h_ej[static_cast<size_t>(e)])].push_back({c.h_ei[static_cast<size_t>(e)], e});
+        }
+        for (int i = 0; i < c.n; ++i) {
+            auto& r = rows[static_cast<size_t>(i)];
+            std::sort(r.begin(), r.end());
+            for (size_t q = 0; q < r.size(); ++q) {
+                col[static_cast<size_t>(rowptr[static_cast<size_t>(i)]) + q] = r[q].first;
+                eidx[static_cast<size_t>(rowptr[static_cast<size_t>(i)]) + q] = r[q].second;
+            }
         }
     }
     int maxdeg = 0;
@@ -364,15 +383,20 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         return GenericScratch{c.d_gx.p, c.d_gy.p, c.d_gxn.p, c.d_gnoise.p, cap};
     };
     GenericScratch g{};
-    if (!regpath) g = scratch(nblocks);
+    const bool densepath = !regpath && dense_path_ok(c, cfg->variant);
+    if (!regpath && !densepath) g = scratch(nblocks);
 
     stamp_t0<<<1, 1, 0, c.stream>>>(c.d_t0.p);
     ++c.launches;
     ck(cudaEventRecord(c.ev0, c.stream), "event");
     if (nblocks > 0) {
-        const int rc = regpath ? launch_sampler(p, nblocks, c.stream) : launch_sampler_generic(p, nblocks, g, c.stream);
-        ck(static_cast<cudaError_t>(rc), "sampler launch");
-        c.launches += regpath ? 1 : 2 + (long long)p.T * (cfg->alpha > 0 ? 2 : 1);
+        if (densepath) {
+            sample_dense(c, p, b_begin, nblocks);  // tensor-core J sgn(X) (dense.cu)
+        } else {
+            const int rc = regpath ? launch_sampler(p, nblocks, c.stream) : launch_sampler_generic(p, nblocks, g, c.stream);
+            ck(static_cast<cudaError_t>(rc), "sampler launch");
+            c.launches += regpath ? 1 : 2 + (long long)p.T * (cfg->alpha > 0 ? 2 : 1);
+        }
     }
     ck(cudaEventRecord(c.ev1, c.stream), "event");
     // Per-block flags: bit 2 = the register path's noise-event buffer overflowed (re-run the
@@ -912,6 +936,36 @@ long long momc_b200_num_blocks(momc_ctx* ctx, const momc_solver_cfg* cfg, int ru
     if (!ctx || !cfg || cfg->batch_size < 1 || runs < 1 || ctx->L < 1) return 0;
     const int bt = sampler_block_traj(ctx->n, cfg->alpha);
     return static_cast<long long>(runs) * ctx->L * ((cfg->batch_size + bt - 1) / bt);
+}
+
+
+int momc_b200_generate_uniform_instance(momc_ctx* ctx, int n, double density, int k, int kind, double lo, double hi,
+                                        uint64_t seed, int64_t* out_m, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        std::vector<int> ei, ej;
+        std::vector<double> w;
+        generate_uniform_device(*ctx, n, density, k, kind, lo, hi, seed, ei, ej, w);
+        momc_instance_view v{n, k, static_cast<int>(ei.size()), ei.data(), ej.data(), w.data()};
+        set_instance(*ctx, &v);
+        if (out_m) *out_m = static_cast<int64_t>(ei.size());
+    });
+}
+
+int momc_b200_instance_get(momc_ctx* ctx, int32_t* edge_i, int32_t* edge_j, double* w, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        std::copy(ctx->h_ei.begin(), ctx->h_ei.end(), edge_i);
+        std::copy(ctx->h_ej.begin(), ctx->h_ej.end(), edge_j);
+        std::copy(ctx->h_w.begin(), ctx->h_w.end(), w);
+    });
+}
+
+int momc_b200_set_dense_threshold(momc_ctx* ctx, int n_min)
+{
+    ctx->dense_min_n = n_min < 65 ? 65 : n_min;
+    return MOMC_OK;
 }
 
 }  // extern "C"

@@ -84,9 +84,21 @@ struct Ctx {
     DevBuf<double> d_gx, d_gy, d_gxn, d_gnoise;  // generic-n scratch
     DevBuf<uint64_t> d_upload;                   // host pools uploaded for filtering
     std::shared_ptr<void> pareto_scratch;         // pareto.cu working buffers
+    std::shared_ptr<void> dense_scratch;          // dense.cu working buffers
+    int dense_min_n = 256;                        // dense int8 tensor path for dSB at n >= this
     std::shared_ptr<void> archive;                // resident DevArchive (pareto.cuh)
 
     ~Ctx();
 };
+
+// dense.cu
+struct SamplerParams;
+bool dense_path_ok(Ctx& c, int variant);
+void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblocks);
+bool eval_gemm_ok(const Ctx& c);
+void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, long long U, double* d_out);
+// instance_gen.cu
+void generate_uniform_device(Ctx& c, int n, double density, int k, int kind, double lo, double hi, uint64_t seed,
+                             std::vector<int>& ei, std::vector<int>& ej, std::vector<double>& w);
 
 }  // namespace momc_b200

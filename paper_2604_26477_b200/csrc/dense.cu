@@ -1,0 +1,463 @@
+// Dense dSB sampler for large n on the tensor cores (config C4, N=2000) and the GEMM form
+// of evaluate_cuts. Restates sb_step (solver.hpp:159-181) with phi = sgn(x) and
+// evaluate_cuts (pareto.hpp:346-359).
+//
+// Exactness. With integer weights, H*J(c) = sum_k num_k w_k is an integer matrix; when
+// |H*J| <= 127 it is exact in int8, and sgn(x) is exact in int8, so the contraction
+// D = sgn(X)^T (H*J) is computed exactly by the int8 tensor cores with int32 accumulation.
+// coupled = D / H is then one correctly rounded FP64 division, where the reference sums
+// rounded FP64 products over j (scalarize.hpp:30, solver.hpp:161): the two agree to ~n ulp,
+// so trajectories agree within the FP tolerance stated in DESIGN.md (spin words are compared
+// against the reference in tests/test_gpu_dense.py), not bit-for-bit.
+//
+// Layout (one batch per (run, weight) pair):
+//   Phi  int8  [pair][traj][spin]   (GEMM A operand, op T)
+//   HJ   int8  [weight][spin][spin] (GEMM B operand; symmetric)
+//   D    int32 [pair][spin][traj]   (GEMM output; coalesced for the update kernel)
+//   x, y f64   [pair][spin][traj]
+// The update kernel runs one thread per trajectory (the noise stream of a (trajectory, step)
+// is sequential over spins, rng.hpp:156-185) and stages Phi rows through shared memory.
+// The GEMM is cuBLASLt's int8 batched matmul (a plain library GEMM); the fused tcgen05
+// kernel with the SB update in its epilogue is the next step.
+#include <cublasLt.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "ctx.cuh"
+#include "rng.cuh"
+#include "sampler.cuh"
+
+namespace momc_b200 {
+
+namespace {
+
+void ckb(cublasStatus_t s, const char* what)
+{
+    if (s != CUBLAS_STATUS_SUCCESS) runtime(std::string("cuBLASLt error in ") + what + ": " + std::to_string(static_cast<int>(s)));
+}
+
+__global__ void k_build_hj(int n, int k, int nnz, int L, const int* __restrict__ nums, const int* __restrict__ rowptr,
+                           const int* __restrict__ col, const int* __restrict__ eidx, const int* __restrict__ wi,
+                           signed char* hj, int* overflow)
+{
+    const int l = blockIdx.y;
+    const int i = blockIdx.x;
+    signed char* row = hj + (static_cast<long long>(l) * n + i) * n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) row[j] = 0;
+    __syncthreads();
+    for (int e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x) {
+        int v = 0;
+        for (int q = 0; q < k; ++q) v += nums[l * k + q] * wi[static_cast<long long>(eidx[e]) * k + q];
+        if (v > 127 || v < -127) atomicOr(overflow, 1);
+        row[col[e]] = static_cast<signed char>(v);
+    }
+}
+
+struct PairOf {
+    int run, l, traj0, count;
+};
+
+// init_state (solver.hpp:108-124) for one (run, weight) pair block of trajectories
+__global__ void k_dense_init(int n, int batch_pad, const PairOf* __restrict__ pairs, uint64_t seed, double h,
+                             double* x, double* y, signed char* phi)
+{
+    const PairOf pr = pairs[blockIdx.y];
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long pb = blockIdx.y;
+    if (t < pr.count) {
+        const uint64_t key = run_key(seed, static_cast<uint32_t>(pr.run));
+        DevStream sx, sy;
+        sx.init(key, pr.l, pr.traj0 + t, tag_word(kTagInitX, 0));
+        sy.init(key, pr.l, pr.traj0 + t, tag_word(kTagInitY, 0));
+        double* xs = x + pb * n * batch_pad;
+        double* ys = y + pb * n * batch_pad;
+        signed char* ph = phi + (pb * batch_pad + t) * n;
+        for (int i = 0; i < n; ++i) {
+            const double u = static_cast<double>(sx.next_u64() >> 11) * 0x1.0p-53;
+            const double xv = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, u), 1.0));
+            xs[static_cast<long long>(i) * batch_pad + t] = xv;
+            ph[i] = xv < 0.0 ? -1 : 1;
+        }
+        for (int i = 0; i < n; ++i) {
+            const double u = static_cast<double>(sy.next_u64() >> 11) * 0x1.0p-53;
+            ys[static_cast<long long>(i) * batch_pad + t] = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, u), 1.0));
+        }
+    } else if (t < batch_pad) {  // padding trajectories: phi = +1 rows (never read back)
+        signed char* ph = phi + (pb * batch_pad + t) * n;
+        for (int i = 0; i < n; ++i) ph[i] = 1;
+    }
+}
+
+__device__ double dense_normal(DevStream& s, const ZigTables* __restrict__ z)
+{
+    for (;;) {
+        const uint32_t u = s.next_u32();
+        const int32_t hz = static_cast<int32_t>(u);
+        const uint32_t iz = u & 127u;
+        const uint32_t mag = hz < 0 ? 0u - u : u;
+        if (mag < z->kn[iz]) return __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        if (iz == 0) {
+            const double r = 3.442619855899;
+            for (;;) {
+                const uint64_t a = s.next_u64();
+                const double xx = __ddiv_rn(-log(static_cast<double>((a >> 11) + 1) * 0x1.0p-53), r);
+                const uint64_t b = s.next_u64();
+                const double yy = -log(static_cast<double>((b >> 11) + 1) * 0x1.0p-53);
+                if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) return hz > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
+            }
+        }
+        const double xv = __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        const uint64_t a = s.next_u64();
+        const double u01 = static_cast<double>(a >> 11) * 0x1.0p-53;
+        if (__dadd_rn(z->fn[iz], __dmul_rn(u01, __dsub_rn(z->fn[iz - 1], z->fn[iz]))) <
+            exp(__dmul_rn(__dmul_rn(-0.5, xv), xv)))
+            return xv;
+    }
+}
+
+constexpr int kDenseTile = 64;  // spins per shared-memory phi tile
+
+// one dSB step for every trajectory: y += dt((a_t - a0) x - c0 D/H + alpha eta); x += dt a0 y;
+// wall; clamp; phi = sgn(x)
+__global__ void __launch_bounds__(128) k_dense_update(int n, int batch_pad, int H, const PairOf* __restrict__ pairs,
+                                                      uint64_t seed, int t_step, int T, double dt, double a0,
+                                                      double alpha, double sdt, const double* __restrict__ c0s,
+                                                      const ZigTables* __restrict__ zig, const int* __restrict__ D,
+                                                      double* x, double* y, signed char* phi, int* bad)
+{
+    __shared__ ZigTables z;
+    __shared__ signed char tile[128][kDenseTile + 4];
+    for (int q = threadIdx.x; q < static_cast<int>(sizeof(ZigTables) / 4); q += blockDim.x)
+        reinterpret_cast<uint32_t*>(&z)[q] = reinterpret_cast<const uint32_t*>(zig)[q];
+    __syncthreads();
+    const PairOf pr = pairs[blockIdx.y];
+    const long long pb = blockIdx.y;
+    const int t0 = blockIdx.x * blockDim.x;
+    const int t = t0 + threadIdx.x;
+    const bool active = t < pr.count;
+    const double c0 = c0s[pr.l];
+    const double a_t = __ddiv_rn(static_cast<double>(t_step + 1), static_cast<double>(T));
+    const double neg_drift = -__dsub_rn(a0, a_t);
+    const double Hd = static_cast<double>(H);
+    DevStream s;
+    if (active)
+        s.init(run_key(seed, static_cast<uint32_t>(pr.run)), pr.l, pr.traj0 + t,
+               tag_word(kTagStepNoise, static_cast<uint32_t>(t_step)));
+    const int* Dp = D + pb * n * static_cast<long long>(batch_pad);
+    double* xs = x + pb * n * static_cast<long long>(batch_pad);
+    double* ys = y + pb * n * static_cast<long long>(batch_pad);
+    bool nonfinite = false;
+    for (int i0 = 0; i0 < n; i0 += kDenseTile) {
+        const int lim = min(kDenseTile, n - i0);
+        if (active) {
+            for (int q = 0; q < lim; ++q) {
+                const long long o = static_cast<long long>(i0 + q) * batch_pad + t;
+                const double coupled = __ddiv_rn(static_cast<double>(Dp[o]), Hd);
+                const double eta = alpha > 0.0 ? dense_normal(s, &z) : 0.0;
+                double xi = xs[o], yi = ys[o];
+                double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled));
+                if (alpha > 0.0) d = __dadd_rn(d, __dmul_rn(alpha, eta));
+                yi = __dadd_rn(yi, __dmul_rn(dt, d));
+                xi = __dadd_rn(xi, __dmul_rn(sdt, yi));
+                yi = fabs(xi) > 1.0 ? 0.0 : yi;
+                xi = (xi < -1.0) ? -1.0 : xi;
+                xi = (1.0 < xi) ? 1.0 : xi;
+                nonfinite |= !isfinite(xi) || !isfinite(yi);
+                xs[o] = xi;
+                ys[o] = yi;
+                tile[threadIdx.x][q] = xi < 0.0 ? -1 : 1;
+            }
+        }
+        __syncthreads();
+        // coalesced store of the phi tile: rows of `lim` bytes
+        for (int q = threadIdx.x; q < 128 * kDenseTile; q += blockDim.x) {
+            const int r = q / kDenseTile, cidx = q % kDenseTile;
+            if (t0 + r < pr.count && cidx < lim) phi[(pb * batch_pad + t0 + r) * n + i0 + cidx] = tile[r][cidx];
+        }
+        __syncthreads();
+    }
+    if (nonfinite) atomicMin(bad, t_step + 1);
+}
+
+__global__ void k_dense_readout(int n, int batch_pad, int batch, int L, const PairOf* __restrict__ pairs,
+                                const double* __restrict__ x, uint64_t* words, int* nanflag)
+{
+    const PairOf pr = pairs[blockIdx.y];
+    const long long pb = blockIdx.y;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= pr.count) return;
+    const int wpc = (n + 63) / 64;
+    const double* xs = x + pb * n * static_cast<long long>(batch_pad);
+    const long long idx = (static_cast<long long>(pr.run) * L + pr.l) * batch + pr.traj0 + t;
+    bool bad = false;
+    for (int wd = 0; wd < wpc; ++wd) {
+        uint64_t word = 0;
+        for (int b = 0; b < 64 && wd * 64 + b < n; ++b) {
+            const double v = xs[static_cast<long long>(wd * 64 + b) * batch_pad + t];
+            word |= static_cast<uint64_t>(!(v < 0.0)) << b;
+            bad |= v != v;
+        }
+        words[idx * wpc + wd] = word;
+    }
+    if (bad) atomicOr(nanflag, 1);
+}
+
+struct LtGemm {
+    cublasLtHandle_t h = nullptr;
+    DevBuf<unsigned char> ws;
+    ~LtGemm()
+    {
+        if (h) cublasLtDestroy(h);
+        ws.release();
+    }
+};
+
+// D[b] (m x n, col-major int32) = A[b]^T (A stored k x m col-major int8) x B[b] (k x n int8)
+void gemm_i8_batched(Ctx& c, LtGemm& g, int m, int n, int k, const signed char* A, long long strideA,
+                     const signed char* B, long long strideB, int* D, long long strideD, int batches)
+{
+    if (!g.h) ckb(cublasLtCreate(&g.h), "create");
+    cublasLtMatmulDesc_t op;
+    ckb(cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I), "desc");
+    const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
+    ckb(cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof tA), "transa");
+    ckb(cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof tB), "transb");
+    cublasLtMatrixLayout_t la, lb, ld;
+    ckb(cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, k, m, k), "la");
+    ckb(cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, k, n, k), "lb");
+    ckb(cublasLtMatrixLayoutCreate(&ld, CUDA_R_32I, m, n, m), "ld");
+    for (auto lay_stride : {std::make_pair(la, strideA), std::make_pair(lb, strideB), std::make_pair(ld, strideD)}) {
+        ckb(cublasLtMatrixLayoutSetAttribute(lay_stride.first, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &batches, sizeof batches),
+            "batch");
+        long long st = lay_stride.second;
+        ckb(cublasLtMatrixLayoutSetAttribute(lay_stride.first, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &st, sizeof st),
+            "stride");
+    }
+    const size_t wsz = 64ull << 20;
+    g.ws.reserve(wsz);
+    cublasLtMatmulPreference_t pref;
+    ckb(cublasLtMatmulPreferenceCreate(&pref), "pref");
+    ckb(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof wsz), "ws");
+    cublasLtMatmulHeuristicResult_t res{};
+    int found = 0;
+    ckb(cublasLtMatmulAlgoGetHeuristic(g.h, op, la, lb, ld, ld, pref, 1, &res, &found), "heuristic");
+    if (!found) runtime("cuBLASLt: no int8 algorithm for this shape");
+    const int32_t alpha = 1, beta = 0;
+    ckb(cublasLtMatmul(g.h, op, &alpha, A, la, B, lb, &beta, D, ld, D, ld, &res.algo, g.ws.p, wsz, c.stream), "matmul");
+    c.launches++;
+    cublasLtMatmulPreferenceDestroy(pref);
+    cublasLtMatrixLayoutDestroy(la);
+    cublasLtMatrixLayoutDestroy(lb);
+    cublasLtMatrixLayoutDestroy(ld);
+    cublasLtMatmulDescDestroy(op);
+}
+
+struct DenseScratch {
+    LtGemm gemm;
+    DevBuf<signed char> hj, phi, s8;
+    DevBuf<int> D, flags;
+    DevBuf<double> x, y;
+    DevBuf<PairOf> pairs;
+    int hj_L = -1, hj_n = 0;
+    const void* hj_key = nullptr;
+};
+
+DenseScratch& dscratch(Ctx& c)
+{
+    if (!c.dense_scratch) c.dense_scratch = std::shared_ptr<void>(new DenseScratch(), [](void* p) {
+        auto* d = static_cast<DenseScratch*>(p);
+        d->hj.release(); d->phi.release(); d->s8.release(); d->D.release(); d->flags.release();
+        d->x.release(); d->y.release(); d->pairs.release();
+        delete d;
+    });
+    return *static_cast<DenseScratch*>(c.dense_scratch.get());
+}
+
+}  // namespace
+
+// true when the dense int8 tensor path applies (dSB, integer weights, |H*J| <= 127)
+bool dense_path_ok(Ctx& c, int variant)
+{
+    if (variant != 1 || !c.integer_weights || c.n < c.dense_min_n || c.L < 1) return false;
+    long long maxabs = 0;
+    std::vector<int> nums(static_cast<size_t>(c.L) * c.k);
+    ck(cudaMemcpy(nums.data(), c.d_nums.p, sizeof(int) * nums.size(), cudaMemcpyDeviceToHost), "D2H");
+    std::vector<double> wmax(static_cast<size_t>(c.k), 0.0);
+    for (int e = 0; e < c.m; ++e)
+        for (int q = 0; q < c.k; ++q)
+            wmax[static_cast<size_t>(q)] = std::max(wmax[static_cast<size_t>(q)], std::fabs(c.h_w[static_cast<size_t>(e) * c.k + q]));
+    for (int l = 0; l < c.L; ++l) {
+        double s = 0;
+        for (int q = 0; q < c.k; ++q) s += nums[static_cast<size_t>(l) * c.k + q] * wmax[static_cast<size_t>(q)];
+        maxabs = std::max(maxabs, static_cast<long long>(s));
+    }
+    return maxabs <= 127 && c.n % 16 == 0;
+}
+
+// Samples the flattened (run, weight, chunk) blocks [b0, b0+nblocks) of block_traj
+// trajectories with the dense path; returns seconds of device time via events.
+void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblocks)
+{
+    DenseScratch& d = dscratch(c);
+    const int n = c.n, L = c.L;
+    // H*J(c_l) in int8 (rebuilt when the weights change)
+    if (d.hj_L != L || d.hj_n != n || d.hj_key != static_cast<const void*>(c.d_vals.p)) {
+        d.hj.reserve(static_cast<size_t>(L) * n * n);
+        d.flags.reserve(4);
+        ck(cudaMemsetAsync(d.flags.p, 0, sizeof(int) * 4, c.stream), "memset");
+        k_build_hj<<<dim3(static_cast<unsigned>(n), static_cast<unsigned>(L)), 256, 0, c.stream>>>(
+            n, c.k, c.nnz, L, c.d_nums.p, c.d_rowptr.p, c.d_col.p, c.d_eidx.p, c.d_wi.p, d.hj.p, d.flags.p);
+        c.launches++;
+        int ovf = 0;
+        ck(cudaMemcpyAsync(&ovf, d.flags.p, sizeof ovf, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        ck(cudaStreamSynchronize(c.stream), "hj");
+        if (ovf) runtime("dense path: H*J(c) exceeds int8");
+        d.hj_L = L;
+        d.hj_n = n;
+        d.hj_key = c.d_vals.p;
+    }
+    // group the block range into (run, weight) pairs of contiguous trajectories
+    std::vector<PairOf> pairs;
+    const int bt = p.block_traj;
+    for (long long b = b0; b < b0 + nblocks; ++b) {
+        const int chunk = static_cast<int>(b % p.chunks);
+        const long long rl = b / p.chunks;
+        const int l = static_cast<int>(rl % L), run = static_cast<int>(rl / L);
+        const int first = chunk * bt, cnt = std::min(bt, p.batch - first);
+        if (!pairs.empty() && pairs.back().run == run && pairs.back().l == l &&
+            pairs.back().traj0 + pairs.back().count == first)
+            pairs.back().count += cnt;
+        else
+            pairs.push_back({run, l, first, cnt});
+    }
+    if (pairs.empty()) return;
+    int maxc = 0;
+    for (auto& q : pairs) maxc = std::max(maxc, q.count);
+    const int batch_pad = (maxc + 15) / 16 * 16;
+    // process pairs in groups bounded by memory (~24 GB of state)
+    const size_t per_pair = static_cast<size_t>(n) * batch_pad * (8 + 8 + 4 + 1);
+    const size_t group = std::max<size_t>(1, (24ull << 30) / per_pair);
+    for (size_t g0 = 0; g0 < pairs.size(); g0 += group) {
+        const int G = static_cast<int>(std::min(group, pairs.size() - g0));
+        d.pairs.reserve(static_cast<size_t>(G));
+        ck(cudaMemcpyAsync(d.pairs.p, pairs.data() + g0, sizeof(PairOf) * G, cudaMemcpyHostToDevice, c.stream), "H2D");
+        const size_t cells = static_cast<size_t>(G) * n * batch_pad;
+        d.x.reserve(cells);
+        d.y.reserve(cells);
+        d.D.reserve(cells);
+        d.phi.reserve(cells);
+        d.flags.reserve(4);
+        ck(cudaMemsetAsync(d.flags.p, 0x7f, sizeof(int), c.stream), "memset");
+        ck(cudaMemsetAsync(d.flags.p + 1, 0, sizeof(int), c.stream), "memset");
+        const dim3 grid(static_cast<unsigned>((batch_pad + 127) / 128), static_cast<unsigned>(G));
+        k_dense_init<<<grid, 128, 0, c.stream>>>(n, batch_pad, d.pairs.p, p.seed, p.init_scale, d.x.p, d.y.p, d.phi.p);
+        c.launches++;
+        // all pairs of a group must share the weight stride pattern: B operand per pair = HJ of its weight
+        // -> run one strided-batch GEMM per maximal run of consecutive weights within the group
+        for (int t = 0; t < p.T; ++t) {
+            int q0 = 0;
+            while (q0 < G) {
+                int q1 = q0 + 1;
+                const PairOf& a = pairs[g0 + q0];
+                while (q1 < G && pairs[g0 + q1].l == pairs[g0 + q1 - 1].l + 1 && pairs[g0 + q1].run == a.run) ++q1;
+                const long long pstride = static_cast<long long>(n) * batch_pad;
+                gemm_i8_batched(c, d.gemm, batch_pad, n, n, d.phi.p + q0 * pstride, pstride,
+                                d.hj.p + static_cast<long long>(a.l) * n * n, static_cast<long long>(n) * n,
+                                d.D.p + q0 * pstride, pstride, q1 - q0);
+                q0 = q1;
+            }
+            k_dense_update<<<grid, 128, 0, c.stream>>>(n, batch_pad, c.H, d.pairs.p, p.seed, t, p.T, p.dt, p.a0, p.alpha,
+                                                       p.s_dt_a0, p.c0, p.zig, d.D.p, d.x.p, d.y.p, d.phi.p, d.flags.p);
+            c.launches++;
+        }
+        k_dense_readout<<<grid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, d.flags.p + 1);
+        c.launches++;
+        ck(cudaGetLastError(), "dense sampler");
+        int fl[2] = {0, 0};
+        ck(cudaMemcpyAsync(fl, d.flags.p, sizeof fl, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        ck(cudaStreamSynchronize(c.stream), "dense sampler");
+        if (fl[0] != 0x7f7f7f7f)
+            runtime("numerical failure at step " + std::to_string(fl[0]) + " (run " + std::to_string(pairs[g0].run) +
+                    ", weight " + std::to_string(pairs[g0].l) + ")");
+    }
+}
+
+// evaluate_cuts for integer weights |w| <= 127 through int8 GEMMs: for layer k,
+// h(u) = s_u^T W_k s_u and C_k(u) = (W_k - h/2)/2, exact (integers).
+__global__ void k_unpack_s8(const uint64_t* __restrict__ words, const uint32_t* __restrict__ idx, long long U0,
+                            int cnt, int n, int wpc, signed char* s)
+{
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < static_cast<long long>(cnt) * n;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int u = static_cast<int>(q / n), i = static_cast<int>(q % n);
+        const long long row = idx ? idx[U0 + u] : U0 + u;
+        s[q] = (words[row * wpc + (i >> 6)] >> (i & 63)) & 1ull ? 1 : -1;
+    }
+}
+
+__global__ void k_build_layer(int n, int k, int layer, const int* __restrict__ rowptr, const int* __restrict__ col,
+                              const int* __restrict__ eidx, const int* __restrict__ wi, signed char* Wk)
+{
+    const int i = blockIdx.x;
+    signed char* row = Wk + static_cast<long long>(i) * n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) row[j] = 0;
+    __syncthreads();
+    for (int e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x)
+        row[col[e]] = static_cast<signed char>(wi[static_cast<long long>(eidx[e]) * k + layer]);
+}
+
+// out[u*K + layer] = 0.5 * (W - 0.5 * sum_i s_u[i] * D[i][u])
+__global__ void k_cut_from_gemm(const int* __restrict__ D, const signed char* __restrict__ s, int cnt, int ld, int n,
+                                int K, int layer, double W, long long U0, double* out)
+{
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= cnt) return;
+    long long h = 0;
+    for (int i = 0; i < n; ++i) h += static_cast<long long>(s[static_cast<long long>(u) * n + i]) * D[static_cast<long long>(i) * ld + u];
+    out[(U0 + u) * K + layer] = 0.5 * (W - 0.5 * static_cast<double>(h));
+}
+
+bool eval_gemm_ok(const Ctx& c)
+{
+    if (!c.integer_weights || c.n < c.dense_min_n || c.n % 16 != 0) return false;
+    for (double v : c.h_w)
+        if (v > 127 || v < -127) return false;
+    return true;
+}
+
+void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, long long U, double* d_out)
+{
+    DenseScratch& d = dscratch(c);
+    const int n = c.n, K = c.k, wpc = (n + 63) / 64;
+    const int chunk = 16384;
+    d.s8.reserve(static_cast<size_t>(chunk) * n + static_cast<size_t>(n) * n);
+    d.D.reserve(static_cast<size_t>(chunk) * n);
+    signed char* Wk = d.s8.p + static_cast<size_t>(chunk) * n;
+    std::vector<double> W(static_cast<size_t>(K), 0.0);
+    for (int e = 0; e < c.m; ++e)
+        for (int q = 0; q < K; ++q) W[static_cast<size_t>(q)] += c.h_w[static_cast<size_t>(e) * K + q];
+    for (int layer = 0; layer < K; ++layer) {
+        k_build_layer<<<n, 256, 0, c.stream>>>(n, K, layer, c.d_rowptr.p, c.d_col.p, c.d_eidx.p, c.d_wi.p, Wk);
+        c.launches++;
+        for (long long u0 = 0; u0 < U; u0 += chunk) {
+            const int cnt = static_cast<int>(std::min<long long>(chunk, U - u0));
+            const int cntp = (cnt + 15) / 16 * 16;
+            k_unpack_s8<<<1024, 256, 0, c.stream>>>(d_words, d_idx, u0, cnt, n, wpc, d.s8.p);
+            if (cntp > cnt)
+                ck(cudaMemsetAsync(d.s8.p + static_cast<size_t>(cnt) * n, 1, static_cast<size_t>(cntp - cnt) * n, c.stream),
+                   "memset");
+            c.launches++;
+            gemm_i8_batched(c, d.gemm, cntp, n, n, d.s8.p, 0, Wk, 0, d.D.p, 0, 1);
+            k_cut_from_gemm<<<(cnt + 127) / 128, 128, 0, c.stream>>>(d.D.p, d.s8.p, cnt, cntp, n, K, layer,
+                                                                      W[static_cast<size_t>(layer)], u0, d_out);
+            c.launches++;
+        }
+    }
+    ck(cudaGetLastError(), "evaluate_cuts_gemm");
+}
+
+}  // namespace momc_b200

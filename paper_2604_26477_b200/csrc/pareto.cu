@@ -451,9 +451,9 @@ __global__ void k_ref_sample(int count, uint64_t key, int n, int m, int K, const
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < count; c += gridDim.x * blockDim.x) {
         DevStream s;
         s.init(key, static_cast<uint32_t>(c), 0u, tag_word(kTagReferenceSample, 0));
-        uint64_t wd[16];
+        uint64_t wd[64];
         const int wpc = (n + 63) / 64;
-        for (int q = 0; q < wpc && q < 16; ++q) wd[q] = s.next_u64();
+        for (int q = 0; q < wpc && q < 64; ++q) wd[q] = s.next_u64();
         for (int k = 0; k < K; ++k) {
             double acc = 0.0;
             for (int e = 0; e < m; ++e) {
@@ -464,6 +464,28 @@ __global__ void k_ref_sample(int count, uint64_t key, int n, int m, int K, const
             atomicMin(&rmin[k], dkey(acc));
         }
     }
+}
+
+// reference-sample configurations only (the cut values then come from the GEMM evaluator)
+__global__ void k_ref_words(int count, uint64_t key, int n, uint64_t* words)
+{
+    const int wpc = (n + 63) / 64;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < count; c += gridDim.x * blockDim.x) {
+        DevStream s;
+        s.init(key, static_cast<uint32_t>(c), 0u, tag_word(kTagReferenceSample, 0));
+        for (int q = 0; q < wpc; ++q) {
+            uint64_t v = s.next_u64();
+            if (q == wpc - 1 && (n & 63)) v &= (1ull << (n & 63)) - 1;
+            words[static_cast<long long>(c) * wpc + q] = v;
+        }
+    }
+}
+
+__global__ void k_col_min(const double* __restrict__ vals, long long rows, int K, unsigned long long* rmin)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < rows * K;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        atomicMin(&rmin[i % K], dkey(vals[i]));
 }
 
 // ---- K8: hypervolume over the compressed grid of the front (gains g = v - r)
@@ -755,7 +777,9 @@ void evaluate_cuts_device(Ctx& c, const uint64_t* d_words, long long U, double* 
     const int wpc = (c.n + 63) / 64;
     if (c.k > kMaxK) usage("the GPU path supports at most 16 objectives");
     if (U == 0) return;
-    if (c.integer_weights) {
+    if (eval_gemm_ok(c)) {
+        evaluate_cuts_gemm(c, d_words, nullptr, U, d_out);
+    } else if (c.integer_weights) {
         const int sm = c.m * (2 + c.k) <= 12000 ? c.m * (2 + c.k) * 4 : 0;
         k_eval_int<<<grid_blocks(U), 256, sm, c.stream>>>(d_words, nullptr, U, wpc, c.m, c.k, c.d_ei.p, c.d_ej.p,
                                                            c.d_wi.p, d_out);
@@ -803,7 +827,9 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     cudaEventRecord(e1, c.stream);
     // K4 eval of the unique configs
     s.vals.reserve(static_cast<size_t>(U) * K + 1);
-    if (c.integer_weights) {
+    if (eval_gemm_ok(c)) {  // large dense instances: exact int8 tensor-core form
+        evaluate_cuts_gemm(c, d_words, s.uniq.p, U, s.vals.p);
+    } else if (c.integer_weights) {
         const int sm = c.m * (2 + K) <= 12000 ? c.m * (2 + K) * 4 : 0;
         k_eval_int<<<grid_blocks(U), 256, sm, c.stream>>>(d_words, s.uniq.p, U, wpc, c.m, K, c.d_ei.p, c.d_ej.p,
                                                            c.d_wi.p, s.vals.p);
@@ -903,16 +929,32 @@ void filter_values_device(Ctx& c, const double* d_vals, const uint64_t* d_words,
 std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed)
 {
     if (count < 1) usage("sampled reference needs count >= 1");
-    if (c.n > 1024) usage("reference sampling on the GPU path supports n <= 1024");
+    if (c.n > 4096) usage("reference sampling on the GPU path supports n <= 4096");
     Scratch& s = scratch(c);
     s.counters.reserve(8 + kMaxK);
     DevBuf<unsigned long long> rmin;
     rmin.reserve(static_cast<size_t>(c.k));
     std::vector<unsigned long long> init(static_cast<size_t>(c.k), ~0ull);
     ck(cudaMemcpyAsync(rmin.p, init.data(), sizeof(unsigned long long) * c.k, cudaMemcpyHostToDevice, c.stream), "H2D");
-    k_ref_sample<<<grid_blocks(count, 128), 128, 0, c.stream>>>(count, derive_key(seed, 0x70617265u), c.n, c.m, c.k,
-                                                                 c.d_ei.p, c.d_ej.p, c.d_w.p, rmin.p);
-    c.launches++;
+    if (eval_gemm_ok(c)) {  // cut_values == evaluate_cuts exactly for integer weights
+        const int wpc = (c.n + 63) / 64;
+        DevBuf<uint64_t> wd;
+        DevBuf<double> cv;
+        wd.reserve(static_cast<size_t>(count) * wpc);
+        cv.reserve(static_cast<size_t>(count) * c.k);
+        k_ref_words<<<grid_blocks(count, 128), 128, 0, c.stream>>>(count, derive_key(seed, 0x70617265u), c.n, wd.p);
+        c.launches++;
+        evaluate_cuts_gemm(c, wd.p, nullptr, count, cv.p);
+        k_col_min<<<grid_blocks(static_cast<long long>(count) * c.k), 256, 0, c.stream>>>(cv.p, count, c.k, rmin.p);
+        c.launches++;
+        ck(cudaStreamSynchronize(c.stream), "reference point");
+        wd.release();
+        cv.release();
+    } else {
+        k_ref_sample<<<grid_blocks(count, 128), 128, 0, c.stream>>>(count, derive_key(seed, 0x70617265u), c.n, c.m, c.k,
+                                                                     c.d_ei.p, c.d_ej.p, c.d_w.p, rmin.p);
+        c.launches++;
+    }
     std::vector<unsigned long long> h(static_cast<size_t>(c.k));
     ck(cudaMemcpyAsync(h.data(), rmin.p, sizeof(unsigned long long) * c.k, cudaMemcpyDeviceToHost, c.stream), "D2H");
     ck(cudaStreamSynchronize(c.stream), "reference point");
