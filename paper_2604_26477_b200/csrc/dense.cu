@@ -113,9 +113,16 @@ __device__ double dense_normal(DevStream& s, const ZigTables* __restrict__ z)
         const double xv = __dmul_rn(static_cast<double>(hz), z->wn[iz]);
         const uint64_t a = s.next_u64();
         const double u01 = static_cast<double>(a >> 11) * 0x1.0p-53;
-        if (__dadd_rn(z->fn[iz], __dmul_rn(u01, __dsub_rn(z->fn[iz - 1], z->fn[iz]))) <
-            exp(__dmul_rn(__dmul_rn(-0.5, xv), xv)))
-            return xv;
+        const double lhs = __dadd_rn(z->fn[iz], __dmul_rn(u01, __dsub_rn(z->fn[iz - 1], z->fn[iz])));
+        const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
+        // FP32 exp brackets the FP64 one within 1e-6 relative on [-6, 0]; the FP64 exp is
+        // only evaluated inside the +-1e-5 band (same decision as rng.hpp:180-183)
+        const float ef = __expf(static_cast<float>(targ));
+        bool accept;
+        if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) accept = true;
+        else if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) accept = false;
+        else accept = lhs < exp(targ);
+        if (accept) return xv;
     }
 }
 
@@ -154,11 +161,22 @@ __global__ void __launch_bounds__(128) k_dense_update(int n, int batch_pad, int 
     for (int i0 = 0; i0 < n; i0 += kDenseTile) {
         const int lim = min(kDenseTile, n - i0);
         if (active) {
+            // software pipeline: the next spin's loads are in flight during this spin's draw
+            long long o = static_cast<long long>(i0) * batch_pad + t;
+            int dn = Dp[o];
+            double xn = xs[o], yn = ys[o];
             for (int q = 0; q < lim; ++q) {
-                const long long o = static_cast<long long>(i0 + q) * batch_pad + t;
-                const double coupled = __ddiv_rn(static_cast<double>(Dp[o]), Hd);
+                const int dq = dn;
+                double xi = xn, yi = yn;
+                const long long oq = o;
+                if (q + 1 < lim) {
+                    o += batch_pad;
+                    dn = Dp[o];
+                    xn = xs[o];
+                    yn = ys[o];
+                }
+                const double coupled = __ddiv_rn(static_cast<double>(dq), Hd);
                 const double eta = alpha > 0.0 ? dense_normal(s, &z) : 0.0;
-                double xi = xs[o], yi = ys[o];
                 double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled));
                 if (alpha > 0.0) d = __dadd_rn(d, __dmul_rn(alpha, eta));
                 yi = __dadd_rn(yi, __dmul_rn(dt, d));
@@ -167,8 +185,8 @@ __global__ void __launch_bounds__(128) k_dense_update(int n, int batch_pad, int 
                 xi = (xi < -1.0) ? -1.0 : xi;
                 xi = (1.0 < xi) ? 1.0 : xi;
                 nonfinite |= !isfinite(xi) || !isfinite(yi);
-                xs[o] = xi;
-                ys[o] = yi;
+                xs[oq] = xi;
+                ys[oq] = yi;
                 tile[threadIdx.x][q] = xi < 0.0 ? -1 : 1;
             }
         }
@@ -206,54 +224,80 @@ __global__ void k_dense_readout(int n, int batch_pad, int batch, int L, const Pa
     if (bad) atomicOr(nanflag, 1);
 }
 
+// cuBLASLt int8 GEMM with the plan (descriptors + heuristic algorithm) cached per shape:
+// the heuristic query costs far more than a 2000x2000x3000 int8 GEMM.
+struct LtPlan {
+    int m, n, k, batches;
+    long long sa, sb, sd;
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, ld = nullptr;
+    cublasLtMatmulAlgo_t algo{};
+};
+
 struct LtGemm {
     cublasLtHandle_t h = nullptr;
     DevBuf<unsigned char> ws;
+    std::vector<LtPlan> plans;
     ~LtGemm()
     {
+        for (auto& p : plans) {
+            cublasLtMatrixLayoutDestroy(p.la);
+            cublasLtMatrixLayoutDestroy(p.lb);
+            cublasLtMatrixLayoutDestroy(p.ld);
+            cublasLtMatmulDescDestroy(p.op);
+        }
         if (h) cublasLtDestroy(h);
         ws.release();
     }
 };
 
-// D[b] (m x n, col-major int32) = A[b]^T (A stored k x m col-major int8) x B[b] (k x n int8)
-void gemm_i8_batched(Ctx& c, LtGemm& g, int m, int n, int k, const signed char* A, long long strideA,
-                     const signed char* B, long long strideB, int* D, long long strideD, int batches)
+constexpr size_t kLtWorkspace = 64ull << 20;
+
+const LtPlan& lt_plan(LtGemm& g, int m, int n, int k, long long sa, long long sb, long long sd, int batches)
 {
+    for (const auto& p : g.plans)
+        if (p.m == m && p.n == n && p.k == k && p.sa == sa && p.sb == sb && p.sd == sd && p.batches == batches) return p;
     if (!g.h) ckb(cublasLtCreate(&g.h), "create");
-    cublasLtMatmulDesc_t op;
-    ckb(cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I), "desc");
+    g.ws.reserve(kLtWorkspace);
+    LtPlan p{m, n, k, batches, sa, sb, sd};
+    ckb(cublasLtMatmulDescCreate(&p.op, CUBLAS_COMPUTE_32I, CUDA_R_32I), "desc");
     const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
-    ckb(cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof tA), "transa");
-    ckb(cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof tB), "transb");
-    cublasLtMatrixLayout_t la, lb, ld;
-    ckb(cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, k, m, k), "la");
-    ckb(cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, k, n, k), "lb");
-    ckb(cublasLtMatrixLayoutCreate(&ld, CUDA_R_32I, m, n, m), "ld");
-    for (auto lay_stride : {std::make_pair(la, strideA), std::make_pair(lb, strideB), std::make_pair(ld, strideD)}) {
+    ckb(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof tA), "transa");
+    ckb(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof tB), "transb");
+    ckb(cublasLtMatrixLayoutCreate(&p.la, CUDA_R_8I, k, m, k), "la");
+    ckb(cublasLtMatrixLayoutCreate(&p.lb, CUDA_R_8I, k, n, k), "lb");
+    ckb(cublasLtMatrixLayoutCreate(&p.ld, CUDA_R_32I, m, n, m), "ld");
+    for (auto lay_stride : {std::make_pair(p.la, sa), std::make_pair(p.lb, sb), std::make_pair(p.ld, sd)}) {
         ckb(cublasLtMatrixLayoutSetAttribute(lay_stride.first, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &batches, sizeof batches),
             "batch");
         long long st = lay_stride.second;
         ckb(cublasLtMatrixLayoutSetAttribute(lay_stride.first, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &st, sizeof st),
             "stride");
     }
-    const size_t wsz = 64ull << 20;
-    g.ws.reserve(wsz);
     cublasLtMatmulPreference_t pref;
     ckb(cublasLtMatmulPreferenceCreate(&pref), "pref");
+    const size_t wsz = kLtWorkspace;
     ckb(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof wsz), "ws");
     cublasLtMatmulHeuristicResult_t res{};
     int found = 0;
-    ckb(cublasLtMatmulAlgoGetHeuristic(g.h, op, la, lb, ld, ld, pref, 1, &res, &found), "heuristic");
-    if (!found) runtime("cuBLASLt: no int8 algorithm for this shape");
-    const int32_t alpha = 1, beta = 0;
-    ckb(cublasLtMatmul(g.h, op, &alpha, A, la, B, lb, &beta, D, ld, D, ld, &res.algo, g.ws.p, wsz, c.stream), "matmul");
-    c.launches++;
+    ckb(cublasLtMatmulAlgoGetHeuristic(g.h, p.op, p.la, p.lb, p.ld, p.ld, pref, 1, &res, &found), "heuristic");
     cublasLtMatmulPreferenceDestroy(pref);
-    cublasLtMatrixLayoutDestroy(la);
-    cublasLtMatrixLayoutDestroy(lb);
-    cublasLtMatrixLayoutDestroy(ld);
-    cublasLtMatmulDescDestroy(op);
+    if (!found) runtime("cuBLASLt: no int8 algorithm for this shape");
+    p.algo = res.algo;
+    g.plans.push_back(p);
+    return g.plans.back();
+}
+
+// D[b] (m x n, col-major int32) = A[b]^T (A stored k x m col-major int8) x B[b] (k x n int8)
+void gemm_i8_batched(Ctx& c, LtGemm& g, int m, int n, int k, const signed char* A, long long strideA,
+                     const signed char* B, long long strideB, int* D, long long strideD, int batches)
+{
+    const LtPlan& p = lt_plan(g, m, n, k, strideA, strideB, strideD, batches);
+    const int32_t alpha = 1, beta = 0;
+    ckb(cublasLtMatmul(g.h, p.op, &alpha, A, p.la, B, p.lb, &beta, D, p.ld, D, p.ld, &p.algo, g.ws.p, kLtWorkspace,
+                       c.stream),
+        "matmul");
+    c.launches++;
 }
 
 struct DenseScratch {

@@ -16,7 +16,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -551,6 +554,15 @@ __global__ void k_ref_check(const double* __restrict__ vals, long long F, int K,
             if (r[k] > vals[i * K + k]) atomicMin(first, static_cast<unsigned long long>(i * K + k));
 }
 
+// MOMC_TRACE=1: host timestamps of the Pareto stage on stderr (diagnostics)
+void trace(const char* what)
+{
+    static const bool on = std::getenv("MOMC_TRACE") != nullptr;
+    if (!on) return;
+    static auto t0 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[momc %9.3f ms] %s\n", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what);
+}
+
 uint64_t pow2_at_least(uint64_t x)
 {
     uint64_t p = 1024;
@@ -726,6 +738,7 @@ void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, 
     cudaEventCreate(&e2);
     cudaEventRecord(e0, c.stream);
     const int method = front_keep(c, s, d_vv, V, K);
+    trace("finish_archive: front launched");
     s.rows.reserve(static_cast<size_t>(V) + 1);
     ck(cudaMemsetAsync(s.counters.p + 1, 0, sizeof(unsigned long long), c.stream), "memset");
     k_compact_keep<<<grid_blocks(V), 256, 0, c.stream>>>(s.keep.p, V, nullptr, s.rows.p, s.counters.p + 1);
@@ -805,6 +818,7 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     if (c.n == 0) usage("pool does not match instance");
     if (c.k > kMaxK) usage("the GPU path supports at most 16 objectives");
     if (M >= 0xFFFFFFFFll) usage("pool too large for one device pass (shard it)");
+    trace("filter_pool: enter");
     Scratch& s = scratch(c);
     const int wpc = (c.n + 63) / 64;
     const int K = c.k;
@@ -824,6 +838,7 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     k_dedup<<<grid_blocks(M), 256, 0, c.stream>>>(d_words, M, wpc, s.table.p, tsize - 1, s.uniq.p, s.counters.p);
     c.launches++;
     const long long U = static_cast<long long>(read_counter(c, s.counters.p));
+    trace("filter_pool: dedup done");
     cudaEventRecord(e1, c.stream);
     // K4 eval of the unique configs
     s.vals.reserve(static_cast<size_t>(U) * K + 1);
@@ -857,6 +872,7 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
                                                       t2 - 1, s.reps.p, s.counters.p + 2);
     c.launches++;
     const long long V = static_cast<long long>(read_counter(c, s.counters.p + 2));
+    trace("filter_pool: eval+collapse done");
     // distinct vectors (row of the first inserter) + owner rows -> dense arrays
     DevBuf<uint32_t> vrow, vown;
     vrow.reserve(static_cast<size_t>(V) + 1);
@@ -880,7 +896,9 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
         tm->collapse_s = seconds_between(e2, e3);
         tm->unique_configs = U;
     }
+    trace("filter_pool: finish_archive");
     finish_archive(c, s, vv.p, V, K, d_words, vcfg.p, wpc, out, tm);
+    trace("filter_pool: archive done");
     vrow.release();
     vown.release();
     vv.release();
