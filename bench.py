@@ -55,28 +55,54 @@ def env_int(name, default):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in-process through NVML
+    (a forked nvidia-smi per sample stalls the timed host thread); nvidia-smi if NVML is
+    unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, pci_bus_id: str | None = None):
         self.index = index
+        self.pci = pci_bus_id
         self.rows = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
+    def _nvml_handle(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            if self.pci:
+                try:
+                    return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(self.pci)
+                except Exception:
+                    pass
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return None, None
+
     def _run(self):
+        nv, hd = self._nvml_handle()
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                f = [x.strip() for x in out.stdout.strip().split(",")]
-                if len(f) >= 6:
-                    self.rows.append(f)
+                if hd is not None:
+                    sm = nv.nvmlDeviceGetClockInfo(hd, nv.NVML_CLOCK_SM)
+                    mx = nv.nvmlDeviceGetMaxClockInfo(hd, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(hd)
+                    bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                            nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+                    self.rows.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5)
+                    f = [x.strip() for x in out.stdout.strip().split(",")]
+                    if len(f) >= 6:
+                        self.rows.append(f)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05 if hd is not None else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -236,7 +262,9 @@ def main():
     launches0 = s.launches()
     sync_all()
     step_ms, reps = [], []
-    with ClockSampler(local) as clocks:
+    pr = torch.cuda.get_device_properties(local)
+    pci = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+    with ClockSampler(local, pci) as clocks:
         for _ in range(args.steps):
             flush.zero_()
             sync_all()
@@ -317,13 +345,13 @@ def main():
               "reference_s", "hv_s", "pareto_filtering_s")}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "step_ms": [round(float(x), 3) for x in step_ms], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "runs": runs, "samples_per_step": samples_total,
                    "parallelism": f"{world} GPU(s): run r on rank r, NCCL all-gather front merge",
                    "l2": "256 MB buffer written between timed steps"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": float(np.mean(e2e_ms)), "api": "momc_b200_bench (C-ABI, host buffers)"},
+                "ms_per_step": float(np.mean(e2e_ms)), "step_ms": [round(float(x), 3) for x in e2e_ms], "api": "momc_b200_bench (C-ABI, host buffers)"},
         "time_to_optimal_hv_s": float(np.mean(e2e_ms)) * 1e-3 if e2e_hv_ok else None,
         "hv": last["hv"], "hv_star": hv_star, "hv_equals_reference": bool(hv_ok and e2e_hv_ok),
         "archive_size": int(last["archive_size"]),

@@ -23,6 +23,9 @@ namespace momc_b200 {
 
 Ctx::~Ctx()
 {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    g_alloc_stream = nullptr;  // synchronous frees from here on (the stream goes away below)
     for (auto* b : {&d_ei, &d_ej, &d_rowptr, &d_col, &d_eidx, &d_wi, &d_nums, &d_nan, &d_badstep}) b->release();
     for (auto* b : {&d_w, &d_vals, &d_c0, &d_padv, &d_gx, &d_gy, &d_gxn, &d_gnoise}) b->release();
     d_zig.release();
@@ -536,6 +539,10 @@ int momc_b200_ctx_create(int device, momc_ctx** out, char* err, size_t errlen)
         auto* c = new momc_ctx();
         c->device = device;
         ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        cudaMemPool_t pool;
+        ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+        uint64_t keep = ~0ull;  // keep freed blocks cached in the pool
+        ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
         ck(cudaEventCreate(&c->ev0), "event");
         ck(cudaEventCreate(&c->ev1), "event");
         *out = c;
@@ -556,7 +563,7 @@ long long momc_b200_ctx_fallback_blocks(momc_ctx* ctx) { return ctx->fallback_bl
 int momc_b200_set_instance(momc_ctx* ctx, const momc_instance_view* inst, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         set_instance(*ctx, inst);
     });
 }
@@ -564,7 +571,7 @@ int momc_b200_set_instance(momc_ctx* ctx, const momc_instance_view* inst, char* 
 int momc_b200_set_weights(momc_ctx* ctx, const int32_t* nums, int L, int H, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         set_weights(*ctx, nums, L, H);
     });
 }
@@ -593,7 +600,7 @@ int momc_b200_sample(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long l
                      double* seconds, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         sample(*ctx, cfg, runs, block_begin, block_end, seconds);
     });
 }
@@ -612,7 +619,7 @@ int momc_b200_run_sampler(momc_ctx* ctx, const momc_instance_view* inst, const i
                           double* out_seconds, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         validate_cfg(cfg);
         if (L < 1) usage("run_sampler needs at least one weight vector");
         if (runs < 1) usage("runs must be >= 1");
@@ -634,7 +641,7 @@ int momc_b200_run_sampler(momc_ctx* ctx, const momc_instance_view* inst, const i
 int momc_b200_filter(momc_ctx* ctx, int64_t* out_F, double* seconds, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         if (ctx->pool_size <= 0) usage("non-dominated filter needs a non-empty pool");
         ParetoTimings tm;
         DevArchive& a = resident_archive(*ctx);
@@ -654,7 +661,7 @@ int momc_b200_filter_pool(momc_ctx* ctx, const uint64_t* words, size_t M, int64_
                           char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         if (M == 0) usage("non-dominated filter needs a non-empty pool");
         const auto t0 = std::chrono::steady_clock::now();
         upload_words(*ctx, words, M);
@@ -669,7 +676,7 @@ int momc_b200_filter_values(momc_ctx* ctx, const double* vals, size_t M, int k, 
                             char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         if (M == 0) usage("non-dominated filter needs a non-empty pool");
         if (k < 1) usage("objective vector must be non-empty");
         std::vector<double> v(vals, vals + M * static_cast<size_t>(k));
@@ -702,7 +709,7 @@ int momc_b200_filter_values_dev(momc_ctx* ctx, const double* d_vals, const uint6
                                 int k, int64_t* out_F, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         DevArchive& a = resident_archive(*ctx);
         filter_values_device(*ctx, d_vals, d_words, wpc, ctx->n, static_cast<long long>(M), k, a, nullptr);
         if (out_F) *out_F = a.F;
@@ -743,7 +750,7 @@ int momc_b200_hypervolume(momc_ctx* ctx, const double* vals, int64_t F, int k, c
                           char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         if (F <= 0) usage("hypervolume of an empty archive");
         DevBuf<double> dv;
         dv.reserve(static_cast<size_t>(F) * k);
@@ -756,7 +763,7 @@ int momc_b200_hypervolume(momc_ctx* ctx, const double* vals, int64_t F, int k, c
 int momc_b200_archive_hypervolume(momc_ctx* ctx, const double* r, double* out, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         DevArchive& a = resident_archive(*ctx);
         *out = hypervolume_device(*ctx, a.vals.p, a.F, a.K, std::vector<double>(r, r + a.K));
     });
@@ -765,7 +772,7 @@ int momc_b200_archive_hypervolume(momc_ctx* ctx, const double* r, double* out, c
 int momc_b200_evaluate_cuts(momc_ctx* ctx, const uint64_t* words, size_t U, double* out, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         if (ctx->n == 0) usage("no instance set");
         if (U == 0) return;
         upload_words(*ctx, words, U);
@@ -781,7 +788,7 @@ int momc_b200_evaluate_cuts(momc_ctx* ctx, const uint64_t* words, size_t U, doub
 int momc_b200_reference_point_sampled(momc_ctx* ctx, int count, uint64_t seed, double* r, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         if (ctx->n == 0) usage("no instance set");
         const auto v = reference_point_sampled_device(*ctx, count, seed);
         std::copy(v.begin(), v.end(), r);
@@ -806,7 +813,7 @@ int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t
                     momc_bench_report* rep, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         if (runs < 1) usage("runs must be >= 1");
         validate_cfg(cfg);
         std::memset(rep, 0, sizeof *rep);
@@ -862,7 +869,7 @@ int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long
                        size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         validate_cfg(cfg);
         if (ctx->n == 0) usage("no instance set");
         if (ctx->L < 1) usage("run_sampler needs at least one weight vector");
@@ -943,7 +950,7 @@ int momc_b200_generate_uniform_instance(momc_ctx* ctx, int n, double density, in
                                         uint64_t seed, int64_t* out_m, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        bind(*ctx);
         std::vector<int> ei, ej;
         std::vector<double> w;
         generate_uniform_device(*ctx, n, density, k, kind, lo, hi, seed, ei, ej, w);

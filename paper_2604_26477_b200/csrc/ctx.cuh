@@ -26,6 +26,12 @@ inline void ck(cudaError_t e, const char* what)
     if (e != cudaSuccess) runtime(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
+// Stream of the context the calling thread is working for (set by bind()). Device
+// buffers are stream-ordered allocations on it from the device's default memory pool
+// (release threshold raised at context creation), so per-call scratch costs neither a
+// cudaMalloc nor the implicit device synchronisation of cudaFree.
+inline thread_local cudaStream_t g_alloc_stream = nullptr;
+
 // Growable device buffer.
 template <class T>
 struct DevBuf {
@@ -34,15 +40,18 @@ struct DevBuf {
     void reserve(size_t n)
     {
         if (n <= cap) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        ck(cudaMalloc(&p, sizeof(T) * (n ? n : 1)), "cudaMalloc");
+        release();
+        const size_t bytes = sizeof(T) * (n ? n : 1);
+        if (g_alloc_stream) ck(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, g_alloc_stream), "cudaMallocAsync");
+        else ck(cudaMalloc(&p, bytes), "cudaMalloc");
         cap = n;
     }
     void release()
     {
-        if (p) cudaFree(p);
+        if (p) {
+            if (g_alloc_stream) cudaFreeAsync(p, g_alloc_stream);
+            else cudaFree(p);
+        }
         p = nullptr;
         cap = 0;
     }
@@ -90,6 +99,13 @@ struct Ctx {
 
     ~Ctx();
 };
+
+// Makes ctx's device current and its stream the allocation stream of this thread.
+inline void bind(Ctx& c)
+{
+    ck(cudaSetDevice(c.device), "cudaSetDevice");
+    g_alloc_stream = c.stream;
+}
 
 // dense.cu
 struct SamplerParams;
