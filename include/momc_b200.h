@@ -138,6 +138,18 @@ int momc_b200_evaluate_cuts(momc_ctx* ctx, const uint64_t* words, size_t U, doub
 int momc_b200_reference_point_sampled(momc_ctx* ctx, int count, uint64_t seed, double* r, char* err, size_t errlen);
 int momc_b200_clamp_reference(momc_ctx* ctx, double* r, char* err, size_t errlen);
 
+/* brute_force_pareto (oracle.hpp:25-77) of the resident instance into the resident archive:
+ * exact front over all configurations with s_0 = +1, equal vectors on the lex-smallest
+ * configuration, entries lex-descending. Replaces the reference's 2^(n-1) Gray walk
+ * (enumerate.hpp:38-83) by a vertex-separator decomposition, so the n <= 22 cap
+ * (enumerate.hpp:17) becomes n <= 64 for graphs with a small separator (heavy-hex 42: under a
+ * second). Integer weights only (usage error otherwise). r_exact (K, may be NULL) receives
+ * reference_point_exact. */
+int momc_b200_brute_force_pareto(momc_ctx* ctx, int64_t* out_F, double* r_exact, char* err, size_t errlen);
+/* reference_point_exact (pareto.hpp:603-617): componentwise minimum of the cut values over
+ * every configuration, by the same decomposition (no front). */
+int momc_b200_reference_point_exact(momc_ctx* ctx, double* r, char* err, size_t errlen);
+
 /* ---------------------------------------------------------------- pipeline (pipeline.hpp:309-393) */
 typedef struct {
     double model_construction_s; /* instance + lattice scalarisation (build_block_system) */
@@ -161,7 +173,10 @@ int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t
 
 /* The same pipeline on the resident instance + weights (no host copies besides scalars):
  * scalarise -> sample blocks [block_begin, block_end) -> filter -> (if do_hv) reference
- * point + hypervolume. Used for device-resident throughput and per-rank shards. */
+ * point + hypervolume. Used for device-resident throughput and per-rank shards. The pool
+ * holds only the rows of the sampled blocks afterwards (momc_b200_pool_size / pool_get /
+ * pool_device see that contiguous canonical slice), so a streaming caller can sample run r
+ * of a long job without a pool sized for all r runs. */
 int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long long block_begin,
                        long long block_end, int do_hv, int ref_count, const double* fixed_ref,
                        momc_bench_report* report, char* err, size_t errlen);

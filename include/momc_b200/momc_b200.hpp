@@ -14,6 +14,8 @@
 //   hypervolume                       pareto.hpp:540-552
 //   reference_point_sampled           pareto.hpp:620-642
 //   scalarize                         scalarize.hpp:22-39   (as coupling(): J(c) and c0)
+//   brute_force_pareto                oracle.hpp:25-77      (n <= 64 with a small separator)
+//   reference_point_exact             pareto.hpp:603-617
 #ifndef MOMC_B200_HPP
 #define MOMC_B200_HPP
 
@@ -259,6 +261,29 @@ inline std::vector<double> reference_point_sampled(const MultiObjectiveInstance&
     detail::raise(momc_b200_set_instance(ctx.get(), &ia.view, err, sizeof err), err);
     std::vector<double> r(static_cast<size_t>(inst.k()));
     detail::raise(momc_b200_reference_point_sampled(ctx.get(), count, seed, r.data(), err, sizeof err), err);
+    return r;
+}
+
+// oracle.hpp:25-77. The reference caps n at 22 (enumerate.hpp:17); the device enumeration
+// splits the graph at a small vertex separator and needs integer weights instead (n <= 64).
+inline ParetoArchive brute_force_pareto(const MultiObjectiveInstance& inst, Context& ctx = default_context())
+{
+    detail::InstanceArrays ia(inst);
+    char err[1024] = {0};
+    detail::raise(momc_b200_set_instance(ctx.get(), &ia.view, err, sizeof err), err);
+    int64_t F = 0;
+    detail::raise(momc_b200_brute_force_pareto(ctx.get(), &F, nullptr, err, sizeof err), err);
+    return fetch_archive(ctx, inst.k(), inst.n());
+}
+
+// pareto.hpp:603-617
+inline std::vector<double> reference_point_exact(const MultiObjectiveInstance& inst, Context& ctx = default_context())
+{
+    detail::InstanceArrays ia(inst);
+    char err[1024] = {0};
+    detail::raise(momc_b200_set_instance(ctx.get(), &ia.view, err, sizeof err), err);
+    std::vector<double> r(static_cast<size_t>(inst.k()));
+    detail::raise(momc_b200_reference_point_exact(ctx.get(), r.data(), err, sizeof err), err);
     return r;
 }
 

@@ -795,6 +795,32 @@ def reference_point_sampled(inst: MultiObjectiveInstance, count: int, seed: int,
     return r.tolist()
 
 
+def brute_force_pareto(inst: MultiObjectiveInstance, session: Session | None = None,
+                       with_reference: bool = False):
+    """oracle.hpp:25-77 on the device: the exact front over every configuration with s_0 = +1
+    (equal vectors keep the lex-smallest configuration; entries lex-descending). No n <= 22
+    cap for integer-weight graphs with a small vertex separator (n <= 64). With
+    ``with_reference`` also returns reference_point_exact (pareto.hpp:603-617)."""
+    if inst.n() < 1:
+        raise InvalidArgument("enumeration needs n >= 1")
+    s = _session_for(inst, session)
+    F = C.c_int64()
+    r = np.zeros(inst.k(), np.float64)
+    err = _errbuf()
+    _raise(s.lib.momc_b200_brute_force_pareto(s.h, C.byref(F), r.ctypes.data_as(_lib.dp), err, 2048), err)
+    arc = _fetch_archive(s, inst.k(), inst.n(), True)
+    return (arc, r.tolist()) if with_reference else arc
+
+
+def reference_point_exact(inst: MultiObjectiveInstance, session: Session | None = None) -> list:
+    """pareto.hpp:603-617 (componentwise minimum over every configuration), on the device."""
+    s = _session_for(inst, session)
+    r = np.zeros(inst.k(), np.float64)
+    err = _errbuf()
+    _raise(s.lib.momc_b200_reference_point_exact(s.h, r.ctypes.data_as(_lib.dp), err, 2048), err)
+    return r.tolist()
+
+
 def clamp_reference(r, archive: ParetoArchive):
     """pareto.hpp:647-655 (host; the archive is small)."""
     out = list(r)

@@ -37,6 +37,17 @@ Ctx::~Ctx()
     if (stream) cudaStreamDestroy(stream);
 }
 
+DevArchive& resident_archive(Ctx& c)
+{
+    if (!c.archive) c.archive = std::shared_ptr<void>(new DevArchive(), [](void* p) {
+        auto* a = static_cast<DevArchive*>(p);
+        a->vals.release();
+        a->words.release();
+        delete a;
+    });
+    return *static_cast<DevArchive*>(c.archive.get());
+}
+
 namespace {
 
 void put_err(char* err, size_t errlen, const char* msg)
@@ -310,7 +321,20 @@ void set_weights(Ctx& c, const int32_t* nums, int L, int H)
     }
 }
 
-void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, long long b_end, double* seconds)
+// canonical pool rows [r0, r1) covered by sampler blocks [b0, b1)
+std::pair<long long, long long> rows_of_blocks(int batch, int bt, long long b0, long long b1)
+{
+    if (b1 <= b0) return {0, 0};
+    const int chunks = (batch + bt - 1) / bt;
+    const long long r0 = (b0 / chunks) * batch + (b0 % chunks) * static_cast<long long>(bt);
+    const long long last = b1 - 1;
+    const long long r1 = (last / chunks) * batch + std::min<long long>((last % chunks + 1) * static_cast<long long>(bt), batch);
+    return {r0, r1};
+}
+
+// compact: d_words holds only the rows of the sampled blocks (pool_row0 = first row)
+void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, long long b_end, double* seconds,
+            bool compact = false)
 {
     validate_cfg(cfg);
     if (c.n == 0) usage("no instance set");
@@ -326,6 +350,12 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     const long long nblocks = b_end - b_begin;
     const int wpc = (c.n + 63) / 64;
     c.pool_size = static_cast<long long>(runs) * c.L * batch;
+    c.pool_row0 = 0;
+    if (compact) {
+        const auto rr = rows_of_blocks(batch, bt, b_begin, b_end);
+        c.pool_row0 = rr.first;
+        c.pool_size = rr.second - rr.first;
+    }
     c.pool_runs = runs;
     c.pool_batch = batch;
     c.pool_block_begin = b_begin;
@@ -371,6 +401,7 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     std::copy(c.h_pad_col.begin(), c.h_pad_col.end(), p.pad_col);
     p.zig = c.d_zig.p;
     p.words = c.d_words.p;
+    p.row0 = c.pool_row0;
     p.block_end_ns = c.d_block_end.p;
     p.nan_block = c.d_nan.p;
     p.first_bad_step_task = -1;
@@ -454,7 +485,9 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         ck(cudaMemsetAsync(c.d_badstep.p, 0x7f, sizeof(int) * (re - rb), c.stream), "memset");
         // scratch outputs so the pool / flags of the real run are untouched
         DevBuf<uint64_t> wtmp;
-        wtmp.reserve(static_cast<size_t>(c.pool_size) * wpc);
+        const auto tr = rows_of_blocks(batch, bt, rb, re);
+        q.row0 = tr.first;
+        wtmp.reserve(static_cast<size_t>(tr.second - tr.first) * wpc + 1);
         DevBuf<int> ntmp;
         ntmp.reserve(static_cast<size_t>(re - rb));
         q.words = wtmp.p;
@@ -494,21 +527,10 @@ void pool_get(Ctx& c, uint64_t* words, int64_t* stamps)
             const long long rl = gb / chunks;
             const long long base = rl * c.pool_batch + static_cast<long long>(chunk) * bt;
             const long long stamp = be[static_cast<size_t>(b)] > t0 ? static_cast<long long>(be[static_cast<size_t>(b)] - t0) : 0;
-            for (int t = 0; t < bt && chunk * bt + t < c.pool_batch; ++t) stamps[base + t] = stamp;
+            for (int t = 0; t < bt && chunk * bt + t < c.pool_batch; ++t) stamps[base + t - c.pool_row0] = stamp;
         }
     }
     ck(cudaStreamSynchronize(c.stream), "sync");
-}
-
-DevArchive& resident_archive(Ctx& c)
-{
-    if (!c.archive) c.archive = std::shared_ptr<void>(new DevArchive(), [](void* p) {
-        auto* a = static_cast<DevArchive*>(p);
-        a->vals.release();
-        a->words.release();
-        delete a;
-    });
-    return *static_cast<DevArchive*>(c.archive.get());
 }
 
 void upload_words(Ctx& c, const uint64_t* words, size_t M)
@@ -795,6 +817,29 @@ int momc_b200_reference_point_sampled(momc_ctx* ctx, int count, uint64_t seed, d
     });
 }
 
+int momc_b200_brute_force_pareto(momc_ctx* ctx, int64_t* out_F, double* r_exact, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        if (ctx->n == 0) usage("no instance set");
+        std::vector<double> r;
+        brute_force_device(*ctx, &r, true);
+        if (r_exact) std::copy(r.begin(), r.end(), r_exact);
+        if (out_F) *out_F = resident_archive(*ctx).F;
+    });
+}
+
+int momc_b200_reference_point_exact(momc_ctx* ctx, double* r, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        if (ctx->n == 0) usage("no instance set");
+        std::vector<double> v;
+        brute_force_device(*ctx, &v, false);
+        std::copy(v.begin(), v.end(), r);
+    });
+}
+
 int momc_b200_clamp_reference(momc_ctx* ctx, double* r, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
@@ -884,25 +929,14 @@ int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long
         set_weights(*ctx, nums.data(), ctx->L, ctx->H);
         rep->model_construction_s = std::chrono::duration<double>(clk::now() - t0).count();
         double ss = 0;
-        sample(*ctx, cfg, runs, block_begin, block_end, &ss);
+        // compact pool: only the rows of the sampled blocks, which are all fresh
+        sample(*ctx, cfg, runs, block_begin, block_end, &ss, true);
         rep->sampling_s = ss;
-        rep->pool_size = ctx->pool_size;
         const auto tf = clk::now();
         ParetoTimings tm;
         DevArchive& a = resident_archive(*ctx);
-        // only the sampled blocks hold fresh configs: filter their contiguous pool rows
-        const int bt = ctx->pool_block_traj;
-        const int chunks = (cfg->batch_size + bt - 1) / bt;
-        long long r0 = 0, r1 = ctx->pool_size;
-        if (ctx->pool_blocks > 0) {
-            const long long b0 = ctx->pool_block_begin, b1 = b0 + ctx->pool_blocks - 1;
-            r0 = (b0 / chunks) * cfg->batch_size + (b0 % chunks) * static_cast<long long>(bt);
-            r1 = std::min<long long>((b1 / chunks) * cfg->batch_size + std::min<long long>((b1 % chunks + 1) * static_cast<long long>(bt), cfg->batch_size),
-                                     ctx->pool_size);
-        }
-        const int wpc = (ctx->n + 63) / 64;
-        filter_pool_device(*ctx, ctx->d_words.p + r0 * wpc, r1 - r0, a, &tm);
-        rep->pool_size = r1 - r0;
+        filter_pool_device(*ctx, ctx->d_words.p, ctx->pool_size, a, &tm);
+        rep->pool_size = ctx->pool_size;
         rep->unique_configs = tm.unique_configs;
         rep->unique_vectors = tm.unique_vectors;
         rep->archive_size = a.F;

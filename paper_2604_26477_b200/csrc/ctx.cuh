@@ -87,6 +87,7 @@ struct Ctx {
     int pool_runs = 0, pool_batch = 0;
     long long pool_block_begin = 0, pool_blocks = 0;
     int pool_block_traj = 128;
+    long long pool_row0 = 0;  // first canonical row held in d_words (compact pipeline pools)
     DevBuf<uint64_t> d_words;
     DevBuf<int> d_nan, d_badstep;
     DevBuf<unsigned long long> d_block_end, d_t0;
@@ -113,6 +114,8 @@ bool dense_path_ok(Ctx& c, int variant);
 void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblocks);
 bool eval_gemm_ok(const Ctx& c);
 void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, long long U, double* d_out);
+// enumerate.cu: exact front (resident archive) and/or exact reference point
+void brute_force_device(Ctx& c, std::vector<double>* r_exact, bool front);
 // instance_gen.cu
 void generate_uniform_device(Ctx& c, int n, double density, int k, int kind, double lo, double hi, uint64_t seed,
                              std::vector<int>& ei, std::vector<int>& ej, std::vector<double>& w);

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(128) k_dense_update(int n, int batch_pad, int 
 }
 
 __global__ void k_dense_readout(int n, int batch_pad, int batch, int L, const PairOf* __restrict__ pairs,
-                                const double* __restrict__ x, uint64_t* words, int* nanflag)
+                                const double* __restrict__ x, uint64_t* words, long long row0, int* nanflag)
 {
     const PairOf pr = pairs[blockIdx.y];
     const long long pb = blockIdx.y;
@@ -219,7 +219,7 @@ __global__ void k_dense_readout(int n, int batch_pad, int batch, int L, const Pa
             word |= static_cast<uint64_t>(!(v < 0.0)) << b;
             bad |= v != v;
         }
-        words[idx * wpc + wd] = word;
+        words[(idx - row0) * wpc + wd] = word;
     }
     if (bad) atomicOr(nanflag, 1);
 }
@@ -418,7 +418,7 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
                                                        p.s_dt_a0, p.c0, p.zig, d.D.p, d.x.p, d.y.p, d.phi.p, d.flags.p);
             c.launches++;
         }
-        k_dense_readout<<<grid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, d.flags.p + 1);
+        k_dense_readout<<<grid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, p.row0, d.flags.p + 1);
         c.launches++;
         ck(cudaGetLastError(), "dense sampler");
         int fl[2] = {0, 0};

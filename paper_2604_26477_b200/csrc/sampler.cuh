@@ -32,7 +32,8 @@ struct SamplerParams {
     int pad_dmax;             // 0: runtime CSR rows; else the padded row length
     int pad_col[64 * kMaxPadDeg];  // padded column indices (pad = the row's own index)
     const ZigTables* zig;
-    uint64_t* words;          // (runs * L * batch) * wpc, canonical order
+    uint64_t* words;          // (runs * L * batch) * wpc, canonical order, from row row0
+    long long row0;           // first pool row held by `words` (compact pipeline pools)
     unsigned long long* block_end_ns;  // per launched block (optional)
     int* nan_block;           // per launched block: 1 if any trajectory went non-finite
     int first_bad_step_task;  // debug rerun: -1, else records first bad step per block

@@ -169,7 +169,7 @@ __global__ void gen_readout(WaveCtx w, const double* __restrict__ x)
             word |= static_cast<uint64_t>(!(v < 0.0)) << b;
             bad |= v != v;
         }
-        w.p.words[idx * wpc + wd] = word;
+        w.p.words[(idx - w.p.row0) * wpc + wd] = word;
     }
     const long long blk = w.wave_block0 + wt / w.p.block_traj;
     if (bad) w.p.nan_block[blk] = 1;

@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     word = lane_or<LANES>(wmask, word);
     if (h == 0) {
         const long long idx = (static_cast<long long>(run) * p.L + l) * p.batch + traj;
-        p.words[idx] = word;
+        p.words[idx - p.row0] = word;
     }
     // NaN (numerical failure) -> bit 1; noise-event buffer overflow (re-run on the exact
     // sequential path) -> bit 2

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "momc/oracle.hpp"
 #include "momc/pipeline.hpp"
 #include "momc_b200/momc_b200.hpp"
 
@@ -64,6 +65,16 @@ int main(int argc, char** argv)
         std::vector<SpinConfiguration> cfgs;
         for (size_t i = 0; i < 2000; ++i) cfgs.push_back(gpu.config(i));
         CHECK(b200::evaluate_cuts(inst, cfgs) == momc::detail::evaluate_cuts(inst, cfgs));
+    }
+    {  // exact front by enumeration (oracle.hpp:25-77), reference_point_exact (pareto.hpp:603-617)
+        const auto inst = generate_uniform_instance(18, 0.3, 3, WeightSpec::uniform_int(-10, 10), 3);
+        const auto a = brute_force_pareto(inst);
+        const auto b = b200::brute_force_pareto(inst);
+        bool same = a.size() == b.size() && a.size() > 0;
+        for (size_t i = 0; same && i < a.size(); ++i)
+            same = a.entries[i].value == b.entries[i].value && a.entries[i].config == b.entries[i].config;
+        CHECK(same);
+        CHECK(reference_point_exact(inst) == b200::reference_point_exact(inst));
     }
     {  // exceptions keep the reference's types and messages
         const auto inst = generate_uniform_instance(4, 1.0, 2, WeightSpec{}, 1);
