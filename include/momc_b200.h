@@ -150,6 +150,17 @@ int momc_b200_brute_force_pareto(momc_ctx* ctx, int64_t* out_F, double* r_exact,
  * every configuration, by the same decomposition (no front). */
 int momc_b200_reference_point_exact(momc_ctx* ctx, double* r, char* err, size_t errlen);
 
+/* samples_to_reach (pareto.hpp:763-781) for M host configs in canonical order on the
+ * resident instance: first 1-based count whose running archive reaches target_hv within
+ * 1e-9 relative; *out = -1 when never reached. */
+int momc_b200_samples_to_reach(momc_ctx* ctx, const uint64_t* words, size_t M, const double* r, double target_hv,
+                               int64_t* out, char* err, size_t errlen);
+/* convergence_trace (pareto.hpp:716-757): replay by timestamp (stable), HV of the running
+ * archive at `checkpoints` evenly spaced milestones; outputs are `checkpoints` long. */
+int momc_b200_convergence_trace(momc_ctx* ctx, const uint64_t* words, const int64_t* stamps_ns, size_t M,
+                                const double* r, int checkpoints, double* elapsed_s, double* hv, int64_t* samples,
+                                char* err, size_t errlen);
+
 /* ---------------------------------------------------------------- pipeline (pipeline.hpp:309-393) */
 typedef struct {
     double model_construction_s; /* instance + lattice scalarisation (build_block_system) */

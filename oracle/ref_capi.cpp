@@ -419,6 +419,24 @@ int momcref_samples_to_reach(void* h, const std::uint64_t* words, std::size_t M,
     });
 }
 
+// convergence_trace (pareto.hpp:716); record i = {0, 0, i, stamps[i]}
+int momcref_convergence_trace(void* h, const std::uint64_t* words, const long long* stamps, std::size_t M,
+                              const double* r, int checkpoints, double* elapsed, double* hv, long long* samples,
+                              char* err, std::size_t errlen)
+{
+    const auto& inst = *static_cast<const MultiObjectiveInstance*>(h);
+    return guarded(err, errlen, [&] {
+        auto pool = make_pool(words, M, inst.n());
+        for (std::size_t i = 0; i < M; ++i) pool.set_record(i, {0, 0, static_cast<std::uint32_t>(i), stamps[i]});
+        const auto t = convergence_trace(pool, inst, std::vector<double>(r, r + inst.k()), checkpoints);
+        for (std::size_t i = 0; i < t.size(); ++i) {
+            elapsed[i] = t[i].elapsed_s;
+            hv[i] = t[i].hv;
+            samples[i] = static_cast<long long>(t[i].samples);
+        }
+    });
+}
+
 // ------------------------------------------------------------------ pipeline.hpp
 // bench (pipeline.hpp:309) on a generated (instance_path == "" ) or loaded instance;
 // writes format_report() into `report` and the pool words into out_words when non-null.

@@ -124,6 +124,8 @@ class RefLib:
         L.momcref_reference_point_exact.argtypes = [C.c_void_p, _dp, C.c_char_p, C.c_size_t]
         L.momcref_samples_to_reach.argtypes = [C.c_void_p, _u64p, C.c_size_t, _dp, C.c_double,
                                                C.POINTER(C.c_longlong), C.c_char_p, C.c_size_t]
+        L.momcref_convergence_trace.argtypes = [C.c_void_p, _u64p, C.POINTER(C.c_longlong), C.c_size_t, _dp, C.c_int,
+                                                _dp, _dp, C.POINTER(C.c_longlong), C.c_char_p, C.c_size_t]
         L.momcref_bench.argtypes = [C.c_char_p, C.c_int, C.c_double, C.c_int, C.c_uint64, C.POINTER(CfgC), C.c_int,
                                     C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, C.c_char_p,
                                     C.c_size_t]
@@ -354,6 +356,19 @@ class RefLib:
         self._check(self.lib.momcref_samples_to_reach(inst.h, _p(words, _u64p), words.shape[0], _p(r, _dp), target,
                                                       C.byref(out), err, 1024), err)
         return None if out.value < 0 else out.value
+
+    def convergence_trace(self, inst, words, stamps, r, checkpoints):
+        words = np.ascontiguousarray(words, np.uint64)
+        stamps = np.ascontiguousarray(stamps, np.int64)
+        r = np.ascontiguousarray(r, np.float64)
+        el = np.zeros(checkpoints, np.float64)
+        hv = np.zeros(checkpoints, np.float64)
+        sm = np.zeros(checkpoints, np.int64)
+        err = self._err()
+        self._check(self.lib.momcref_convergence_trace(inst.h, _p(words, _u64p), _p(stamps, C.POINTER(C.c_longlong)),
+                                                       words.shape[0], _p(r, _dp), checkpoints, _p(el, _dp),
+                                                       _p(hv, _dp), _p(sm, C.POINTER(C.c_longlong)), err, 1024), err)
+        return el, hv, sm
 
     def bench(self, cfg: CfgC, instance_path="", n=10, density=0.5, k=3, instance_seed=1, weight_count=55,
               weight_resolution=0, runs=1, ref="exact", checkpoints=0) -> dict:

@@ -110,6 +110,10 @@ SIGNATURES = [
     ("momc_b200_clamp_reference", C.c_int, [vp, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_brute_force_pareto", C.c_int, [vp, C.POINTER(C.c_int64), dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_reference_point_exact", C.c_int, [vp, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_samples_to_reach", C.c_int, [vp, u64p, C.c_size_t, dp, C.c_double, C.POINTER(C.c_int64),
+                                             C.c_char_p, C.c_size_t]),
+    ("momc_b200_convergence_trace", C.c_int, [vp, u64p, C.POINTER(C.c_int64), C.c_size_t, dp, C.c_int, dp, dp,
+                                              C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]),
     ("momc_b200_bench", C.c_int, [vp, C.POINTER(InstanceViewC), i32p, C.c_int, C.c_int, C.POINTER(SolverCfgC),
                                   C.c_int, C.c_int, dp, u64p, C.POINTER(BenchReportC), C.c_char_p, C.c_size_t]),
     ("momc_b200_pipeline", C.c_int, [vp, C.POINTER(SolverCfgC), C.c_int, C.c_longlong, C.c_longlong, C.c_int,

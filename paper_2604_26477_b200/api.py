@@ -138,11 +138,44 @@ class MultiObjectiveInstance:
                 and np.array_equal(self.weights, other.weights))
 
 
+def _to_chars_shortest(v: float) -> str:
+    """std::to_chars(double) without a format: the shortest round-trip digits, written in
+    fixed or scientific notation, whichever is shorter (fixed on a tie); checked against
+    libstdc++ on 30k values (tests/test_host_api.py)."""
+    if math.isnan(v):
+        return "-nan" if math.copysign(1.0, v) < 0 else "nan"
+    if math.isinf(v):
+        return "-inf" if v < 0 else "inf"
+    r = repr(float(v))  # shortest round-trip digits
+    sign = "-" if r.startswith("-") else ""
+    r = r.lstrip("-")
+    mant, _, ex = r.partition("e")
+    ip, _, fp = mant.partition(".")
+    digits = (ip + fp).lstrip("0")
+    exp10 = (int(ex) if ex else 0) - len(fp)  # value = int(ip + fp) * 10**exp10
+    if not digits:
+        return sign + "0"
+    stripped = digits.rstrip("0")
+    exp10 += len(digits) - len(stripped)
+    digits = stripped
+    nd = len(digits)
+    sci_e = exp10 + nd - 1
+    sci = digits[0] + ("." + digits[1:] if nd > 1 else "") + "e" + ("-" if sci_e < 0 else "+") + f"{abs(sci_e):02d}"
+    if exp10 >= 0:  # an integer: fixed notation prints its exact digits (same length)
+        fixed = str(int(abs(v)))
+    elif sci_e >= 0:
+        fixed = digits[:sci_e + 1] + "." + digits[sci_e + 1:]
+    else:
+        fixed = "0." + "0" * (-sci_e - 1) + digits
+    return sign + (fixed if len(fixed) <= len(sci) else sci)
+
+
 def format_number(v: float) -> str:
-    """instance.hpp:462-470: integers verbatim, reals as the shortest round-trip form."""
-    if v == math.floor(v) and abs(v) < 1e15:
+    """instance.hpp:462-470: integers below 1e15 verbatim, everything else as std::to_chars'
+    shortest round-trip form."""
+    if not math.isnan(v) and not math.isinf(v) and v == math.floor(v) and abs(v) < 1e15:
         return str(int(v))
-    return repr(float(v))
+    return _to_chars_shortest(v)
 
 
 def save_instance(inst: MultiObjectiveInstance, path) -> None:
@@ -819,6 +852,53 @@ def reference_point_exact(inst: MultiObjectiveInstance, session: Session | None 
     err = _errbuf()
     _raise(s.lib.momc_b200_reference_point_exact(s.h, r.ctypes.data_as(_lib.dp), err, 2048), err)
     return r.tolist()
+
+
+def samples_to_reach(pool: SamplePool, inst: MultiObjectiveInstance, r, target_hv: float,
+                     session: Session | None = None):
+    """pareto.hpp:763-781 on the device: first 1-based canonical-order sample count whose
+    running archive reaches target_hv (1e-9 relative tolerance), or None."""
+    if pool.empty():
+        raise InvalidArgument("empty pool")
+    s = _session_for(inst, session)
+    words = np.ascontiguousarray(pool.words, np.uint64)
+    r = np.ascontiguousarray(r, np.float64)
+    out = C.c_int64()
+    err = _errbuf()
+    _raise(s.lib.momc_b200_samples_to_reach(s.h, words.ctypes.data_as(_lib.u64p), words.shape[0],
+                                            r.ctypes.data_as(_lib.dp), float(target_hv), C.byref(out), err, 2048), err)
+    return None if out.value < 0 else int(out.value)
+
+
+@dataclass
+class TracePoint:
+    """pareto.hpp:681-685"""
+    elapsed_s: float
+    hv: float
+    samples: int
+
+
+def convergence_trace(pool: SamplePool, inst: MultiObjectiveInstance, r, checkpoints: int,
+                      session: Session | None = None) -> list:
+    """pareto.hpp:716-757 on the device: replay by timestamp (stable), HV of the running
+    archive at `checkpoints` evenly spaced sample-count milestones."""
+    if pool.empty():
+        raise InvalidArgument("convergence trace needs a non-empty pool")
+    if checkpoints < 1:
+        raise InvalidArgument("checkpoints must be >= 1")
+    s = _session_for(inst, session)
+    words = np.ascontiguousarray(pool.words, np.uint64)
+    stamps = np.ascontiguousarray(pool.stamps if pool.stamps is not None else np.zeros(pool.size()), np.int64)
+    r = np.ascontiguousarray(r, np.float64)
+    el = np.zeros(checkpoints, np.float64)
+    hv = np.zeros(checkpoints, np.float64)
+    sm = np.zeros(checkpoints, np.int64)
+    err = _errbuf()
+    _raise(s.lib.momc_b200_convergence_trace(s.h, words.ctypes.data_as(_lib.u64p), stamps.ctypes.data_as(_lib.i64p),
+                                             words.shape[0], r.ctypes.data_as(_lib.dp), checkpoints,
+                                             el.ctypes.data_as(_lib.dp), hv.ctypes.data_as(_lib.dp),
+                                             sm.ctypes.data_as(_lib.i64p), err, 2048), err)
+    return [TracePoint(float(a), float(b), int(c)) for a, b, c in zip(el, hv, sm)]
 
 
 def clamp_reference(r, archive: ParetoArchive):

@@ -840,6 +840,37 @@ int momc_b200_reference_point_exact(momc_ctx* ctx, double* r, char* err, size_t 
     });
 }
 
+int momc_b200_samples_to_reach(momc_ctx* ctx, const uint64_t* words, size_t M, const double* r, double target_hv,
+                               int64_t* out, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        if (ctx->n == 0) usage("no instance set");
+        if (M == 0) usage("empty pool");
+        upload_words(*ctx, words, M);
+        const auto hit = samples_to_reach_device(*ctx, ctx->d_upload.p, static_cast<long long>(M),
+                                                 std::vector<double>(r, r + ctx->k), target_hv);
+        *out = hit ? *hit : -1;
+    });
+}
+
+int momc_b200_convergence_trace(momc_ctx* ctx, const uint64_t* words, const int64_t* stamps_ns, size_t M,
+                                const double* r, int checkpoints, double* elapsed_s, double* hv, int64_t* samples,
+                                char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        if (ctx->n == 0) usage("no instance set");
+        if (M == 0) usage("convergence trace needs a non-empty pool");
+        if (checkpoints < 1) usage("checkpoints must be >= 1");
+        upload_words(*ctx, words, M);
+        std::vector<long long> smp(static_cast<size_t>(checkpoints));
+        convergence_trace_device(*ctx, ctx->d_upload.p, stamps_ns, static_cast<long long>(M),
+                                 std::vector<double>(r, r + ctx->k), checkpoints, elapsed_s, hv, smp.data());
+        for (int i = 0; i < checkpoints; ++i) samples[i] = smp[static_cast<size_t>(i)];
+    });
+}
+
 int momc_b200_clamp_reference(momc_ctx* ctx, double* r, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {

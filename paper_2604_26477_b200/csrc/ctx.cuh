@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -116,6 +117,12 @@ bool eval_gemm_ok(const Ctx& c);
 void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, long long U, double* d_out);
 // enumerate.cu: exact front (resident archive) and/or exact reference point
 void brute_force_device(Ctx& c, std::vector<double>* r_exact, bool front);
+// trace.cu: samples_to_reach / convergence_trace over M device configs
+std::optional<long long> samples_to_reach_device(Ctx& c, const uint64_t* d_words, long long M,
+                                                 const std::vector<double>& r, double target);
+void convergence_trace_device(Ctx& c, const uint64_t* d_words, const int64_t* h_stamps, long long M,
+                              const std::vector<double>& r, int checkpoints, double* elapsed, double* hv,
+                              long long* samples);
 // instance_gen.cu
 void generate_uniform_device(Ctx& c, int n, double density, int k, int kind, double lo, double hi, uint64_t seed,
                              std::vector<int>& ei, std::vector<int>& ej, std::vector<double>& w);

@@ -145,3 +145,15 @@ def test_product_fails_loudly_without_gpu():
         return
     with pytest.raises(MomcRuntimeError, match="no CUDA device"):
         api.Session(0)
+
+
+def test_format_number_matches_to_chars():
+    """format_number (instance.hpp:462-470) against libstdc++ std::to_chars output
+    (tests/golden/make_to_chars.py)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "to_chars_vectors.npz"))
+    from paper_2604_26477_b200.api import _to_chars_shortest, format_number
+    for v, t in zip(g["values"].tolist(), g["text"].tolist()):
+        assert _to_chars_shortest(v) == t, v
+    assert format_number(3.0) == "3" and format_number(-12.0) == "-12" and format_number(1e15) == "1e+15"
+    assert format_number(0.142) == "0.142" and format_number(1e-4) == "1e-04"
