@@ -161,6 +161,23 @@ int momc_b200_convergence_trace(momc_ctx* ctx, const uint64_t* words, const int6
                                 const double* r, int checkpoints, double* elapsed_s, double* hv, int64_t* samples,
                                 char* err, size_t errlen);
 
+/* ---------------------------------------------------------------- pool CSV (solver.hpp:357-432) */
+/* The record rows of save_pool_csv, formatted on the device: for each of M records
+ * "run,weight,trajectory,timestamp_ns,<16 hex nibbles per word>\n". With out == NULL only
+ * *out_len (bytes) is computed; otherwise cap must be >= that. The two header lines are the
+ * caller's (they carry the pool's timings). */
+int momc_b200_format_pool_rows(momc_ctx* ctx, const uint32_t* run, const uint32_t* weight, const uint32_t* trajectory,
+                               const int64_t* stamps_ns, const uint64_t* words, size_t M, int n, char* out, size_t cap,
+                               size_t* out_len, char* err, size_t errlen);
+/* load_pool_csv's record loop on the device: `text` = the file bytes after the two header
+ * lines (the first of them is line first_lineno); empty lines are skipped; the first bad
+ * line raises the reference's "<path>:<line>: malformed pool record" / "bad spin field
+ * width" (code 1). The records stay on the context: *out_M, then momc_b200_parsed_pool_get. */
+int momc_b200_parse_pool_rows(momc_ctx* ctx, const char* text, size_t len, int n, int first_lineno, const char* path,
+                              size_t* out_M, char* err, size_t errlen);
+int momc_b200_parsed_pool_get(momc_ctx* ctx, uint32_t* run, uint32_t* weight, uint32_t* trajectory, int64_t* stamps_ns,
+                              uint64_t* words, char* err, size_t errlen);
+
 /* ---------------------------------------------------------------- pipeline (pipeline.hpp:309-393) */
 typedef struct {
     double model_construction_s; /* instance + lattice scalarisation (build_block_system) */

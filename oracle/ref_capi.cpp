@@ -437,6 +437,92 @@ int momcref_convergence_trace(void* h, const std::uint64_t* words, const long lo
     });
 }
 
+// ------------------------------------------------------------------ CSV formats
+// save_pool_csv (solver.hpp:357) of a pool built from words + records (rec3 = run, weight,
+// trajectory per record) + stamps + timings
+int momcref_save_pool_csv(const std::uint64_t* words, const std::uint32_t* rec3, const long long* stamps,
+                          std::size_t M, int n, double mc, double ss, const char* path, char* err, std::size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        SamplePool pool(n);
+        pool.resize(M);
+        const int wpc = (n + 63) / 64;
+        for (std::size_t i = 0; i < M; ++i) {
+            pool.set_record(i, {rec3[3 * i], rec3[3 * i + 1], rec3[3 * i + 2], stamps[i]});
+            pool.set_config(i, unpack(words + i * static_cast<std::size_t>(wpc), n));
+        }
+        pool.model_construction_seconds = mc;
+        pool.sampling_seconds = ss;
+        save_pool_csv(pool, path);
+    });
+}
+// load_pool_csv (solver.hpp:377): with cap < M only *M / *n / timings are returned
+int momcref_load_pool_csv(const char* path, std::size_t* M, int* n, double* mc, double* ss, std::uint64_t* words,
+                          std::uint32_t* rec3, long long* stamps, std::size_t cap, char* err, std::size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        const auto pool = load_pool_csv(path);
+        *M = pool.size();
+        *n = pool.n();
+        *mc = pool.model_construction_seconds;
+        *ss = pool.sampling_seconds;
+        if (cap < pool.size()) return;
+        const int wpc = pool.words_per_config();
+        for (std::size_t i = 0; i < pool.size(); ++i) {
+            const auto& r = pool.record(i);
+            rec3[3 * i] = r.run;
+            rec3[3 * i + 1] = r.weight;
+            rec3[3 * i + 2] = r.trajectory;
+            stamps[i] = r.timestamp_ns;
+            for (int w = 0; w < wpc; ++w) words[i * wpc + w] = pool.packed_words()[i * wpc + w];
+        }
+    });
+}
+// save_archive_csv (pareto.hpp:787): words == nullptr -> objective-only entries
+int momcref_save_archive_csv(const double* vals, const std::uint64_t* words, std::size_t F, int k, int n, double fs,
+                             const double* r, int nr, const char* path, char* err, std::size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        ParetoArchive a;
+        const int wpc = (n + 63) / 64;
+        for (std::size_t i = 0; i < F; ++i) {
+            ParetoArchive::Entry e;
+            e.value.assign(vals + i * k, vals + (i + 1) * k);
+            if (words) e.config = unpack(words + i * static_cast<std::size_t>(wpc), n);
+            a.entries.push_back(std::move(e));
+        }
+        a.filtering_seconds = fs;
+        a.reference.assign(r, r + nr);
+        save_archive_csv(a, path);
+    });
+}
+// load_archive_csv (pareto.hpp:823): with cap < F only the sizes are returned; has_cfg[i]
+// marks entries with a configuration
+int momcref_load_archive_csv(const char* path, std::size_t* F, int* k, int* n, double* fs, int* nr, double* r,
+                             double* vals, std::uint64_t* words, unsigned char* has_cfg, std::size_t cap, char* err,
+                             std::size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        const auto a = load_archive_csv(path);
+        *F = a.entries.size();
+        *k = a.k();
+        int nn = 0;
+        for (const auto& e : a.entries) nn = std::max(nn, e.config.size());
+        *n = nn;
+        *fs = a.filtering_seconds;
+        *nr = static_cast<int>(a.reference.size());
+        for (std::size_t i = 0; i < a.reference.size() && i < 16; ++i) r[i] = a.reference[i];
+        if (cap < a.entries.size()) return;
+        const int wpc = (nn + 63) / 64;
+        for (std::size_t i = 0; i < a.entries.size(); ++i) {
+            const auto& e = a.entries[i];
+            for (int l = 0; l < *k; ++l) vals[i * *k + l] = e.value[static_cast<std::size_t>(l)];
+            has_cfg[i] = e.config.size() > 0;
+            if (wpc && e.config.size() > 0) pack(e.config, words + i * wpc);
+        }
+    });
+}
+
 // ------------------------------------------------------------------ pipeline.hpp
 // bench (pipeline.hpp:309) on a generated (instance_path == "" ) or loaded instance;
 // writes format_report() into `report` and the pool words into out_words when non-null.

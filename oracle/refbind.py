@@ -126,6 +126,16 @@ class RefLib:
                                                C.POINTER(C.c_longlong), C.c_char_p, C.c_size_t]
         L.momcref_convergence_trace.argtypes = [C.c_void_p, _u64p, C.POINTER(C.c_longlong), C.c_size_t, _dp, C.c_int,
                                                 _dp, _dp, C.POINTER(C.c_longlong), C.c_char_p, C.c_size_t]
+        L.momcref_save_pool_csv.argtypes = [_u64p, C.POINTER(C.c_uint32), C.POINTER(C.c_longlong), C.c_size_t, C.c_int,
+                                            C.c_double, C.c_double, C.c_char_p, C.c_char_p, C.c_size_t]
+        L.momcref_load_pool_csv.argtypes = [C.c_char_p, C.POINTER(C.c_size_t), C.POINTER(C.c_int), _dp, _dp, _u64p,
+                                            C.POINTER(C.c_uint32), C.POINTER(C.c_longlong), C.c_size_t, C.c_char_p,
+                                            C.c_size_t]
+        L.momcref_save_archive_csv.argtypes = [_dp, _u64p, C.c_size_t, C.c_int, C.c_int, C.c_double, _dp, C.c_int,
+                                               C.c_char_p, C.c_char_p, C.c_size_t]
+        L.momcref_load_archive_csv.argtypes = [C.c_char_p, C.POINTER(C.c_size_t), C.POINTER(C.c_int),
+                                               C.POINTER(C.c_int), _dp, C.POINTER(C.c_int), _dp, _dp, _u64p,
+                                               C.POINTER(C.c_ubyte), C.c_size_t, C.c_char_p, C.c_size_t]
         L.momcref_bench.argtypes = [C.c_char_p, C.c_int, C.c_double, C.c_int, C.c_uint64, C.POINTER(CfgC), C.c_int,
                                     C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, C.c_char_p,
                                     C.c_size_t]
@@ -356,6 +366,54 @@ class RefLib:
         self._check(self.lib.momcref_samples_to_reach(inst.h, _p(words, _u64p), words.shape[0], _p(r, _dp), target,
                                                       C.byref(out), err, 1024), err)
         return None if out.value < 0 else out.value
+
+    def save_pool_csv(self, path, words, rec3, stamps, n, mc, ss):
+        words = np.ascontiguousarray(words, np.uint64)
+        rec3 = np.ascontiguousarray(rec3, np.uint32)
+        stamps = np.ascontiguousarray(stamps, np.int64)
+        err = self._err()
+        self._check(self.lib.momcref_save_pool_csv(_p(words, _u64p), _p(rec3, C.POINTER(C.c_uint32)),
+                                                   _p(stamps, C.POINTER(C.c_longlong)), stamps.shape[0], n, mc, ss,
+                                                   str(path).encode(), err, 1024), err)
+
+    def load_pool_csv(self, path):
+        M, n, mc, ss = C.c_size_t(), C.c_int(), C.c_double(), C.c_double()
+        err = self._err()
+        self._check(self.lib.momcref_load_pool_csv(str(path).encode(), C.byref(M), C.byref(n), C.byref(mc),
+                                                   C.byref(ss), None, None, None, 0, err, 1024), err)
+        wpc = (n.value + 63) // 64
+        words = np.zeros((M.value, wpc), np.uint64)
+        rec3 = np.zeros((M.value, 3), np.uint32)
+        stamps = np.zeros(M.value, np.int64)
+        self._check(self.lib.momcref_load_pool_csv(str(path).encode(), C.byref(M), C.byref(n), C.byref(mc),
+                                                   C.byref(ss), _p(words, _u64p), _p(rec3, C.POINTER(C.c_uint32)),
+                                                   _p(stamps, C.POINTER(C.c_longlong)), M.value, err, 1024), err)
+        return {"n": n.value, "mc": mc.value, "ss": ss.value, "words": words, "rec3": rec3, "stamps": stamps}
+
+    def save_archive_csv(self, path, vals, words, n, fs, r):
+        vals = np.ascontiguousarray(vals, np.float64)
+        F, k = vals.shape
+        r = np.ascontiguousarray(r, np.float64)
+        err = self._err()
+        wp = _p(np.ascontiguousarray(words, np.uint64), _u64p) if words is not None else None
+        self._check(self.lib.momcref_save_archive_csv(_p(vals, _dp), wp, F, k, n, fs, _p(r, _dp), r.shape[0],
+                                                      str(path).encode(), err, 1024), err)
+
+    def load_archive_csv(self, path):
+        F, k, n, nr = C.c_size_t(), C.c_int(), C.c_int(), C.c_int()
+        fs = C.c_double()
+        r = np.zeros(16, np.float64)
+        err = self._err()
+        args = (str(path).encode(), C.byref(F), C.byref(k), C.byref(n), C.byref(fs), C.byref(nr), _p(r, _dp))
+        self._check(self.lib.momcref_load_archive_csv(*args, None, None, None, 0, err, 1024), err)
+        wpc = (n.value + 63) // 64
+        vals = np.zeros((F.value, k.value), np.float64)
+        words = np.zeros((F.value, max(wpc, 1)), np.uint64)
+        has = np.zeros(F.value, np.uint8)
+        self._check(self.lib.momcref_load_archive_csv(*args, _p(vals, _dp), _p(words, _u64p),
+                                                      _p(has, C.POINTER(C.c_ubyte)), F.value, err, 1024), err)
+        return {"values": vals, "words": words[:, :wpc], "has_cfg": has.astype(bool), "n": n.value,
+                "fs": fs.value, "reference": r[: nr.value].tolist()}
 
     def convergence_trace(self, inst, words, stamps, r, checkpoints):
         words = np.ascontiguousarray(words, np.uint64)

@@ -422,7 +422,8 @@ class SampleRecord:
 class SamplePool:
     """solver.hpp:258-338: packed spins in canonical (run, weight, trajectory) order."""
 
-    def __init__(self, n: int, words=None, runs: int = 0, weights: int = 0, batch: int = 0, stamps=None):
+    def __init__(self, n: int, words=None, runs: int = 0, weights: int = 0, batch: int = 0, stamps=None,
+                 records=None):
         if n < 1:
             raise InvalidArgument("pool spin count must be positive")
         self._n = n
@@ -431,6 +432,9 @@ class SamplePool:
                       else np.ascontiguousarray(words, np.uint64).reshape(-1, wpc))
         self.runs, self.L, self.batch = runs, weights, batch
         self.stamps = stamps
+        # explicit (run, weight, trajectory) keys, M x 3 uint32 (a loaded pool); otherwise the
+        # keys follow from the canonical index and (runs, L, batch)
+        self.records = None if records is None else np.ascontiguousarray(records, np.uint32).reshape(-1, 3)
         self.model_construction_seconds = 0.0
         self.sampling_seconds = 0.0
 
@@ -450,11 +454,33 @@ class SamplePool:
         return (self._n + 63) // 64
 
     def record(self, i: int) -> SampleRecord:
+        ts = int(self.stamps[i]) if self.stamps is not None else 0
+        if self.records is not None:
+            r = self.records[i]
+            return SampleRecord(int(r[0]), int(r[1]), int(r[2]), ts)
         per_run = self.L * self.batch
         run, rem = divmod(i, per_run)
         l, t = divmod(rem, self.batch)
-        ts = int(self.stamps[i]) if self.stamps is not None else 0
         return SampleRecord(run, l, t, ts)
+
+    def record_keys(self) -> np.ndarray:
+        """M x 3 uint32 (run, weight, trajectory) of every record."""
+        if self.records is not None:
+            return self.records
+        i = np.arange(self.size(), dtype=np.int64)
+        per_run = max(self.L * self.batch, 1)
+        b = max(self.batch, 1)
+        return np.stack([i // per_run, (i % per_run) // b, i % b], axis=1).astype(np.uint32)
+
+    def timestamps(self) -> np.ndarray:
+        return (np.zeros(self.size(), np.int64) if self.stamps is None
+                else np.ascontiguousarray(self.stamps, np.int64))
+
+    def __eq__(self, other):
+        """solver.hpp:329-332: n, records (timestamps included) and spins"""
+        return (isinstance(other, SamplePool) and self._n == other._n and self.size() == other.size()
+                and np.array_equal(self.record_keys(), other.record_keys())
+                and np.array_equal(self.timestamps(), other.timestamps()) and np.array_equal(self.words, other.words))
 
     def config(self, i: int) -> np.ndarray:
         w = self.words[i]
@@ -466,7 +492,7 @@ class SamplePool:
 
 def same_samples(a: SamplePool, b: SamplePool) -> bool:
     """solver.hpp:316-327"""
-    return (a.n() == b.n() and a.size() == b.size() and (a.runs, a.L, a.batch) == (b.runs, b.L, b.batch)
+    return (a.n() == b.n() and a.size() == b.size() and np.array_equal(a.record_keys(), b.record_keys())
             and np.array_equal(a.words, b.words))
 
 

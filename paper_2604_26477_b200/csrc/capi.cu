@@ -871,6 +871,34 @@ int momc_b200_convergence_trace(momc_ctx* ctx, const uint64_t* words, const int6
     });
 }
 
+int momc_b200_format_pool_rows(momc_ctx* ctx, const uint32_t* run, const uint32_t* weight, const uint32_t* trajectory,
+                               const int64_t* stamps_ns, const uint64_t* words, size_t M, int n, char* out, size_t cap,
+                               size_t* out_len, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        *out_len = format_pool_rows(*ctx, run, weight, trajectory, stamps_ns, words, static_cast<long long>(M), n, out, cap);
+    });
+}
+
+int momc_b200_parse_pool_rows(momc_ctx* ctx, const char* text, size_t len, int n, int first_lineno, const char* path,
+                              size_t* out_M, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        *out_M = static_cast<size_t>(parse_pool_rows(*ctx, text, len, n, first_lineno, path ? path : ""));
+    });
+}
+
+int momc_b200_parsed_pool_get(momc_ctx* ctx, uint32_t* run, uint32_t* weight, uint32_t* trajectory, int64_t* stamps_ns,
+                              uint64_t* words, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        parsed_pool_get(*ctx, run, weight, trajectory, stamps_ns, words);
+    });
+}
+
 int momc_b200_clamp_reference(momc_ctx* ctx, double* r, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {

@@ -97,6 +97,7 @@ struct Ctx {
     std::shared_ptr<void> pareto_scratch;         // pareto.cu working buffers
     std::shared_ptr<void> dense_scratch;          // dense.cu working buffers
     int dense_min_n = 256;                        // dense int8 tensor path for dSB at n >= this
+    std::shared_ptr<void> csv_scratch;            // csv.cu parsed pool
     std::shared_ptr<void> archive;                // resident DevArchive (pareto.cuh)
 
     ~Ctx();
@@ -123,6 +124,11 @@ std::optional<long long> samples_to_reach_device(Ctx& c, const uint64_t* d_words
 void convergence_trace_device(Ctx& c, const uint64_t* d_words, const int64_t* h_stamps, long long M,
                               const std::vector<double>& r, int checkpoints, double* elapsed, double* hv,
                               long long* samples);
+// csv.cu: pool CSV record rows (save_pool_csv / load_pool_csv bodies)
+size_t format_pool_rows(Ctx& c, const uint32_t* run, const uint32_t* wt, const uint32_t* tr, const int64_t* ts,
+                        const uint64_t* words, long long M, int n, char* out, size_t cap);
+long long parse_pool_rows(Ctx& c, const char* text, size_t len, int n, int first_lineno, const std::string& path);
+void parsed_pool_get(Ctx& c, uint32_t* run, uint32_t* wt, uint32_t* tr, int64_t* ts, uint64_t* words);
 // instance_gen.cu
 void generate_uniform_device(Ctx& c, int n, double density, int k, int kind, double lo, double hi, uint64_t seed,
                              std::vector<int>& ei, std::vector<int>& ej, std::vector<double>& w);
