@@ -73,6 +73,13 @@ int momc_b200_set_instance(momc_ctx* ctx, const momc_instance_view* inst, char* 
  * instance; kind 0 = WeightSpec::uniform_int(lo, hi), 1 = uniform_real(lo, hi). */
 int momc_b200_generate_uniform_instance(momc_ctx* ctx, int n, double density, int k, int kind, double lo, double hi,
                                         uint64_t seed, int64_t* out_m, char* err, size_t errlen);
+/* generate_correlated_instance (instance.hpp:364-458) on the device (K = 3: U{1..10} base
+ * layers, third layer -lambda (w1 + w2) + sigma g with sigma bisected to target_rho over the
+ * 2048-config probe pool); becomes the resident instance. */
+int momc_b200_generate_correlated_instance(momc_ctx* ctx, int n, double density, double target_rho, uint64_t seed,
+                                           int64_t* out_m, char* err, size_t errlen);
+/* measured_correlation (instance.hpp:338-357) of the resident K = 3 instance */
+int momc_b200_measured_correlation(momc_ctx* ctx, int pool_size, uint64_t seed, double* out, char* err, size_t errlen);
 /* copy the resident instance out: edge_i, edge_j (m), w (m x k) */
 int momc_b200_instance_get(momc_ctx* ctx, int32_t* edge_i, int32_t* edge_j, double* w, char* err, size_t errlen);
 /* dSB with integer weights and |H*J(c)| <= 127 uses the int8 tensor-core contraction

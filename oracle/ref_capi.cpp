@@ -209,6 +209,19 @@ void* momcref_instance_generate_uniform(int n, double density, int k, int kind, 
     });
     return p;
 }
+void* momcref_instance_generate_correlated(int n, double density, double rho, std::uint64_t seed, char* err,
+                                           std::size_t errlen)
+{  // instance.hpp:364 generate_correlated_instance
+    MultiObjectiveInstance* p = nullptr;
+    guarded(err, errlen, [&] { p = new MultiObjectiveInstance(generate_correlated_instance(n, density, rho, seed)); });
+    return p;
+}
+int momcref_measured_correlation(void* h, int pool_size, std::uint64_t seed, double* out, char* err, std::size_t errlen)
+{  // instance.hpp:338
+    return guarded(err, errlen, [&] {
+        *out = measured_correlation(*static_cast<const MultiObjectiveInstance*>(h), pool_size, seed);
+    });
+}
 void momcref_instance_dims(void* h, int* n, int* k, int* m)
 {
     const auto* p = static_cast<const MultiObjectiveInstance*>(h);

@@ -96,6 +96,10 @@ class RefLib:
         L.momcref_instance_generate_uniform.restype = C.c_void_p
         L.momcref_instance_generate_uniform.argtypes = [C.c_int, C.c_double, C.c_int, C.c_int, C.c_double,
                                                         C.c_double, C.c_uint64, C.c_char_p, C.c_size_t]
+        L.momcref_instance_generate_correlated.restype = C.c_void_p
+        L.momcref_instance_generate_correlated.argtypes = [C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_char_p,
+                                                           C.c_size_t]
+        L.momcref_measured_correlation.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _dp, C.c_char_p, C.c_size_t]
         L.momcref_instance_dims.argtypes = [C.c_void_p, _ip, _ip, _ip]
         L.momcref_instance_edges.argtypes = [C.c_void_p, _ip, _ip, _dp]
         L.momcref_instance_save.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_size_t]
@@ -230,6 +234,19 @@ class RefLib:
         if not h:
             raise RefError(2, err.value.decode())
         return RefInstance(self, h)
+
+    def generate_correlated(self, n, density, rho, seed) -> "RefInstance":
+        err = self._err()
+        h = self.lib.momcref_instance_generate_correlated(n, density, rho, seed, err, 1024)
+        if not h:
+            raise RefError(2, err.value.decode())
+        return RefInstance(self, h)
+
+    def measured_correlation(self, inst, pool_size=2048, seed=0) -> float:
+        out = C.c_double()
+        err = self._err()
+        self._check(self.lib.momcref_measured_correlation(inst.h, pool_size, seed, C.byref(out), err, 1024), err)
+        return out.value
 
     # --------------------------------------------------------------- solver
     def scalarize(self, inst, nums, H):

@@ -110,6 +110,9 @@ SIGNATURES = [
     ("momc_b200_clamp_reference", C.c_int, [vp, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_brute_force_pareto", C.c_int, [vp, C.POINTER(C.c_int64), dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_reference_point_exact", C.c_int, [vp, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_generate_correlated_instance", C.c_int, [vp, C.c_int, C.c_double, C.c_double, C.c_uint64, i64p,
+                                                         C.c_char_p, C.c_size_t]),
+    ("momc_b200_measured_correlation", C.c_int, [vp, C.c_int, C.c_uint64, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_format_pool_rows", C.c_int, [vp, u32p, u32p, u32p, i64p, u64p, C.c_size_t, C.c_int, C.c_char_p,
                                              C.c_size_t, C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t]),
     ("momc_b200_parse_pool_rows", C.c_int, [vp, C.c_char_p, C.c_size_t, C.c_int, C.c_int, C.c_char_p,

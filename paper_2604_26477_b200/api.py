@@ -546,9 +546,29 @@ class Session:
         err = _errbuf()
         _raise(self.lib.momc_b200_generate_uniform_instance(self.h, n, density, k, 0 if kind == "int" else 1, lo, hi,
                                                             seed, C.byref(m), err, 2048), err)
-        ei = np.zeros(m.value, np.int32)
-        ej = np.zeros(m.value, np.int32)
-        w = np.zeros((m.value, k), np.float64)
+        return self._fetch_instance(n, k, m.value)
+
+    def generate_correlated_instance(self, n: int, density: float, target_rho: float,
+                                     seed: int) -> MultiObjectiveInstance:
+        """generate_correlated_instance (instance.hpp:364-458) on the device; becomes resident."""
+        m = C.c_int64()
+        err = _errbuf()
+        _raise(self.lib.momc_b200_generate_correlated_instance(self.h, n, density, target_rho, seed, C.byref(m), err,
+                                                               2048), err)
+        return self._fetch_instance(n, 3, m.value)
+
+    def measured_correlation(self, pool_size: int = 2048, seed: int = 0) -> float:
+        """measured_correlation (instance.hpp:338-357) of the resident K=3 instance."""
+        out = C.c_double()
+        err = _errbuf()
+        _raise(self.lib.momc_b200_measured_correlation(self.h, pool_size, seed, C.byref(out), err, 2048), err)
+        return out.value
+
+    def _fetch_instance(self, n, k, m):
+        err = _errbuf()
+        ei = np.zeros(m, np.int32)
+        ej = np.zeros(m, np.int32)
+        w = np.zeros((m, k), np.float64)
         _raise(self.lib.momc_b200_instance_get(self.h, ei.ctypes.data_as(_lib.i32p), ej.ctypes.data_as(_lib.i32p),
                                                w.ctypes.data_as(_lib.dp), err, 2048), err)
         inst = MultiObjectiveInstance.__new__(MultiObjectiveInstance)
@@ -925,6 +945,22 @@ def convergence_trace(pool: SamplePool, inst: MultiObjectiveInstance, r, checkpo
                                              el.ctypes.data_as(_lib.dp), hv.ctypes.data_as(_lib.dp),
                                              sm.ctypes.data_as(_lib.i64p), err, 2048), err)
     return [TracePoint(float(a), float(b), int(c)) for a, b, c in zip(el, hv, sm)]
+
+
+def generate_correlated_instance(n: int, density: float, target_rho: float, seed: int,
+                                 session: Session | None = None) -> MultiObjectiveInstance:
+    """instance.hpp:364-458 (device generation; the instance is returned on the host)."""
+    s = session or default_session()
+    return s.generate_correlated_instance(n, density, target_rho, seed)
+
+
+def measured_correlation(inst: MultiObjectiveInstance, pool_size: int = 2048, seed: int = 0,
+                         session: Session | None = None) -> float:
+    """instance.hpp:338-357"""
+    if inst.k() != 3:
+        raise InvalidArgument("correlation measure requires K=3")
+    s = _session_for(inst, session)
+    return s.measured_correlation(pool_size, seed)
 
 
 def clamp_reference(r, archive: ParetoArchive):

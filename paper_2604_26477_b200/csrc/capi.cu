@@ -366,12 +366,7 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     c.d_badstep.reserve(static_cast<size_t>(nblocks) + 1);
     c.d_block_end.reserve(static_cast<size_t>(nblocks) + 1);
     c.d_t0.reserve(2);
-    if (!c.d_zig.p) {
-        c.d_zig.reserve(1);
-        const ZigTables z = host_ziggurat();
-        ck(cudaMemcpyAsync(c.d_zig.p, &z, sizeof z, cudaMemcpyHostToDevice, c.stream), "H2D");
-        ck(cudaStreamSynchronize(c.stream), "sync");
-    }
+    device_zig(c);
     ck(cudaMemsetAsync(c.d_nan.p, 0, sizeof(int) * (nblocks + 1), c.stream), "memset");
     ck(cudaMemsetAsync(c.d_block_end.p, 0, sizeof(unsigned long long) * (nblocks + 1), c.stream), "memset");
 
@@ -541,6 +536,18 @@ void upload_words(Ctx& c, const uint64_t* words, size_t M)
 }
 
 }  // namespace
+
+const ZigTables* device_zig(Ctx& c)
+{
+    if (!c.d_zig.p) {
+        c.d_zig.reserve(1);
+        const ZigTables z = host_ziggurat();
+        ck(cudaMemcpyAsync(c.d_zig.p, &z, sizeof z, cudaMemcpyHostToDevice, c.stream), "H2D");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    }
+    return c.d_zig.p;
+}
+
 }  // namespace momc_b200
 
 extern "C" {
@@ -1050,6 +1057,29 @@ int momc_b200_generate_uniform_instance(momc_ctx* ctx, int n, double density, in
         momc_instance_view v{n, k, static_cast<int>(ei.size()), ei.data(), ej.data(), w.data()};
         set_instance(*ctx, &v);
         if (out_m) *out_m = static_cast<int64_t>(ei.size());
+    });
+}
+
+int momc_b200_generate_correlated_instance(momc_ctx* ctx, int n, double density, double target_rho, uint64_t seed,
+                                           int64_t* out_m, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        std::vector<int> ei, ej;
+        std::vector<double> w;
+        generate_correlated_device(*ctx, n, density, target_rho, seed, ei, ej, w);
+        momc_instance_view v{n, 3, static_cast<int>(ei.size()), ei.data(), ej.data(), w.data()};
+        set_instance(*ctx, &v);
+        if (out_m) *out_m = static_cast<int64_t>(ei.size());
+    });
+}
+
+int momc_b200_measured_correlation(momc_ctx* ctx, int pool_size, uint64_t seed, double* out, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        if (ctx->n == 0) usage("no instance set");
+        *out = measured_correlation_device(*ctx, pool_size, seed);
     });
 }
 

@@ -129,7 +129,12 @@ size_t format_pool_rows(Ctx& c, const uint32_t* run, const uint32_t* wt, const u
                         const uint64_t* words, long long M, int n, char* out, size_t cap);
 long long parse_pool_rows(Ctx& c, const char* text, size_t len, int n, int first_lineno, const std::string& path);
 void parsed_pool_get(Ctx& c, uint32_t* run, uint32_t* wt, uint32_t* tr, int64_t* ts, uint64_t* words);
+// capi.cu: the ziggurat tables on the device (uploaded once)
+const ZigTables* device_zig(Ctx& c);
 // instance_gen.cu
+void generate_correlated_device(Ctx& c, int n, double density, double target_rho, uint64_t seed, std::vector<int>& ei,
+                                std::vector<int>& ej, std::vector<double>& w);
+double measured_correlation_device(Ctx& c, int pool_size, uint64_t seed);
 void generate_uniform_device(Ctx& c, int n, double density, int k, int kind, double lo, double hi, uint64_t seed,
                              std::vector<int>& ei, std::vector<int>& ej, std::vector<double>& w);
 

@@ -18,7 +18,7 @@ constexpr uint32_t kWeyl0 = 0x9E3779B9u;
 constexpr uint32_t kWeyl1 = 0xBB67AE85u;
 
 constexpr uint32_t kTagInitX = 1, kTagInitY = 2, kTagStepNoise = 3, kTagEdgePresence = 4,
-                   kTagEdgeWeight = 5, kTagReferenceSample = 8;
+                   kTagEdgeWeight = 5, kTagCorrelationNoise = 6, kTagProbePool = 7, kTagReferenceSample = 8;
 
 __host__ __device__ __forceinline__ uint32_t tag_word(uint32_t tag, uint32_t step)
 {
@@ -118,5 +118,33 @@ struct ZigTables {
     double wn[128];
     double fn[128];
 };
+
+// rng.hpp:156-185 over a DevStream (sequential; this path is not throughput-critical)
+__device__ inline double normal_seq(DevStream& s, const ZigTables* __restrict__ z)
+{
+    for (;;) {
+        const uint32_t u = s.next_u32();
+        const int32_t hz = static_cast<int32_t>(u);
+        const uint32_t iz = u & 127u;
+        const uint32_t mag = hz < 0 ? static_cast<uint32_t>(-static_cast<int64_t>(hz)) : static_cast<uint32_t>(hz);
+        if (mag < z->kn[iz]) return __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        if (iz == 0) {
+            const double r = 3.442619855899;
+            for (;;) {
+                const uint64_t a = s.next_u64();
+                const double x = __ddiv_rn(-log(static_cast<double>((a >> 11) + 1) * 0x1.0p-53), r);
+                const uint64_t b = s.next_u64();
+                const double y = -log(static_cast<double>((b >> 11) + 1) * 0x1.0p-53);
+                if (__dadd_rn(y, y) >= __dmul_rn(x, x)) return hz > 0 ? __dadd_rn(r, x) : -__dadd_rn(r, x);
+            }
+        }
+        const double x = __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        const uint64_t a = s.next_u64();
+        const double u01 = static_cast<double>(a >> 11) * 0x1.0p-53;
+        if (__dadd_rn(z->fn[iz], __dmul_rn(u01, __dsub_rn(z->fn[iz - 1], z->fn[iz]))) <
+            exp(__dmul_rn(__dmul_rn(-0.5, x), x)))
+            return x;
+    }
+}
 
 }  // namespace momc_b200
