@@ -60,6 +60,7 @@ __device__ __forceinline__ uint32_t zmag(uint32_t u)
 
 template <int NMAX, int LANES>
 struct Geo {
+    static constexpr int kPackWords = ((NMAX + LANES - 1) / LANES + 4) / 5;  // u32 words of 5 packed offsets
     static constexpr int kTPC = kThreads / LANES;           // trajectories per CTA
     static constexpr int kNQ = (NMAX + LANES - 1) / LANES;  // spins per lane
     static constexpr int kNP = kNQ * LANES;                 // integrated spins (>= n)
@@ -75,6 +76,7 @@ struct Geo {
     static constexpr int phi = entv + kECAP * kTPC * 8;                     // kNP x kTPC f64
     static constexpr int csr = phi + kNP * kTPC * 8;
     static_assert(kNU <= 128, "mask covers at most 128 words");
+    static_assert(kNA <= 255, "word positions are stored in 8 bits");
 };
 
 // first p in [from, kNU) whose mask bit is clear, else kNU
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     constexpr int NQ = G::kNQ;
     constexpr int NP = G::kNP;
     constexpr int US = G::kUS;
+    constexpr int kPK = G::kPackWords;
     extern __shared__ __align__(16) unsigned char smem[];
     ZigTables* zig = reinterpret_cast<ZigTables*>(smem + G::zig);
     uint32_t* ubuf = reinterpret_cast<uint32_t*>(smem + G::ubuf);
@@ -235,17 +238,22 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         F1 = lane_or<LANES>(wmask, F1);
         __syncwarp(wmask);  // the other lanes' words are visible
 
-        // ---- A2: resolve the slow attempts (rng.hpp:164-184), identically on every lane
-        int ne = 0;
+        // ---- A2w: the slow attempts' positions (rng.hpp:164-184), identically on every lane.
+        //      A wedge attempt takes 3 words whatever its outcome and a tail 1 + 4k, so the
+        //      positions follow from the fast mask alone; candidates are listed until even
+        //      all-rejected wedges would have produced NP normals before them. Tails (rare)
+        //      are resolved here; entry = q | tail length << 8 | tail flag << 16.
+        int m = 0;
         {
             int gen = G::kNU;  // words present in ub
-            int pos = 0, i = 0;
+            int pos = 0;       // next attempt position
+            int slow = 0;      // words taken by the listed slow attempts
             for (;;) {
-                const int last = pos + (NP - 1 - i);  // position of normal NP-1 if the rest is fast
+                const int lastq = NP - 1 + slow;  // fast normals before q = q - slow must stay < NP
                 int q = next_slow<G::kNU>(F0, F1, pos);
                 if (q >= G::kNU) {  // beyond the mask: extend the word buffer, test on demand
                     q = pos > G::kNU ? pos : G::kNU;
-                    for (; q <= last; ++q) {
+                    for (; q <= lastq; ++q) {
                         if (q >= G::kNA) break;
                         while (gen <= q) {  // every lane writes the same words
                             const uint4 r = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
@@ -259,13 +267,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                         if (!(zmag(w) < kn[w & 127u])) break;
                     }
                 }
-                if (q > last) break;  // every remaining normal is a fast attempt
-                if (q + 9 >= G::kNA) {
+                if (q > lastq) break;
+                if (m >= G::kECAP || q + 9 >= G::kNA) {
                     overflow = true;
                     ovf_code |= 4;
                     break;
                 }
-                while (gen <= q + 8) {  // words a wedge attempt may consume
+                while (gen <= q + 8) {  // words a wedge attempt may read
                     const uint4 r = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
                     ub[(gen + 0) * US] = r.x;
                     ub[(gen + 1) * US] = r.y;
@@ -273,20 +281,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                     ub[(gen + 3) * US] = r.w;
                     gen += 4;
                 }
-                const int iq = i + (q - pos);  // normal index of the attempt at q
                 const uint32_t u = ub[q * US];
-                const int32_t hz = static_cast<int32_t>(u);
-                const uint32_t iz = u & 127u;
-                int new_i, new_pos;
-                bool special = false;
-                double sval = 0.0;
-                if (iz == 0) {  // tail: 4 words per (x, y) trial
+                if ((u & 127u) == 0) {  // tail: 4 words per (x, y) trial
                     const double r = 3.442619855899;
                     int qq = q + 1;
+                    double sval = 0.0;
                     for (;;) {
                         if (qq + 4 > G::kNA) {
                             overflow = true;
-                    ovf_code |= 8;
+                            ovf_code |= 8;
                             break;
                         }
                         while (gen < qq + 4) {
@@ -301,76 +304,108 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                         const double yy = -log(u01_open_from(ub[(qq + 2) * US], ub[(qq + 3) * US]));
                         qq += 4;
                         if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) {
-                            sval = hz > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
+                            sval = static_cast<int32_t>(u) > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
                             break;
                         }
                     }
                     if (overflow) break;
-                    special = true;
-                    new_i = iq + 1;
-                    new_pos = qq;
-                } else {  // wedge: accept iff fn[iz] + u01 (fn[iz-1] - fn[iz]) < exp(-x^2 / 2)
-                    const double xv = __dmul_rn(i32_to_f64(hz), wn[iz]);
-                    const double lhs = __dadd_rn(
-                        fn[iz], __dmul_rn(u01_from(ub[(q + 1) * US], ub[(q + 2) * US]), __dsub_rn(fn[iz - 1], fn[iz])));
-                    const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
-                    // FP32 exp brackets the FP64 one within 1e-6 relative on [-6, 0]; decide
-                    // from it unless lhs falls in the +-1e-5 band, then use the FP64 exp
-                    const float ef = __expf(static_cast<float>(targ));
-                    bool accept;
-                    if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) accept = true;
-                    else if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) accept = false;
-                    else accept = lhs < exp(targ);
-                    new_pos = q + 3;
-                    new_i = accept ? iq + 1 : iq;
+                    en[m * TPC] = static_cast<uint32_t>(q) | (static_cast<uint32_t>(qq - q) << 8) | (1u << 16);
+                    ev[m * TPC] = sval;
+                    slow += qq - q;
+                    pos = qq;
+                } else {
+                    en[m * TPC] = static_cast<uint32_t>(q);
+                    slow += 3;
+                    pos = q + 3;
                 }
-                // event: from normal new_i on, words continue at offset new_pos - new_i; a tail
-                // also pins normal iq to sval (one event per normal index: later ones replace)
-                const int idx = special ? iq : new_i;
-                if (ne > 0 && static_cast<int>(en[(ne - 1) * TPC] & 0xFFu) == idx) --ne;
-                if (ne >= G::kECAP) {
-                    overflow = true;
-                    ovf_code |= 16;
-                    break;
+                ++m;
+            }
+        }
+        __syncwarp(wmask);  // candidate list and extension words visible
+
+        // ---- A2t: the wedge tests, candidate j on lane j % LANES; accept iff
+        //      fn[iz] + u01 (fn[iz-1] - fn[iz]) < exp(-x^2 / 2) (tails always give a normal)
+        uint32_t acc = 0;
+        for (int j = h; j < m; j += LANES) {
+            const uint32_t e = en[j * TPC];
+            if (e >> 16) {
+                acc |= 1u << j;
+                continue;
+            }
+            const int q = static_cast<int>(e & 0xFFu);
+            const uint32_t u = ub[q * US];
+            const uint32_t iz = u & 127u;
+            const double xv = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), wn[iz]);
+            const double lhs = __dadd_rn(
+                fn[iz], __dmul_rn(u01_from(ub[(q + 1) * US], ub[(q + 2) * US]), __dsub_rn(fn[iz - 1], fn[iz])));
+            const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
+            // FP32 exp brackets the FP64 one within 1e-6 relative on [-6, 0]; decide from it
+            // unless lhs falls in the +-1e-5 band, then use the FP64 exp
+            const float ef = __expf(static_cast<float>(targ));
+            bool accept;
+            if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) accept = true;
+            else if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) accept = false;
+            else accept = lhs < exp(targ);
+            acc |= static_cast<uint32_t>(accept) << j;
+        }
+        acc = static_cast<uint32_t>(lane_or<LANES>(wmask, acc));
+
+        // ---- A2e: walk the candidates with their outcomes; every lane keeps the word offset
+        //      of each of its spins packed 6 bits per field (5 fields per u32) and a mask of its
+        //      tail normals, whose value goes into the tail's last two words
+        uint32_t P[kPK];
+#pragma unroll
+        for (int k = 0; k < kPK; ++k) P[k] = 0;
+        uint32_t specm = 0;
+        {
+            int pos = 0, i = 0;
+            for (int j = 0; j < m; ++j) {
+                const uint32_t e = en[j * TPC];
+                const int q = static_cast<int>(e & 0xFFu);
+                i += q - pos;  // fast normals before the attempt
+                if (i >= NP) break;
+                const bool tail = e >> 16;
+                const int new_pos = tail ? q + static_cast<int>((e >> 8) & 0xFFu) : q + 3;
+                const int new_i = tail ? i + 1 : i + static_cast<int>((acc >> j) & 1u);
+                const int idx = tail ? i : new_i;  // from this normal on, words sit at +off
+                const int off = new_pos - new_i;
+                const int jl = idx - s0;
+                if (jl < NQ) {
+                    if (off > 63) {
+                        overflow = true;
+                        ovf_code |= 16;
+                    }
+                    const uint32_t val = static_cast<uint32_t>(off & 63) * 0x01041041u;
+#pragma unroll
+                    for (int k = 0; k < kPK; ++k) {
+                        const int f = jl - 5 * k;  // first field of P[k] that changes
+                        if (f < 5) {
+                            const uint32_t mask = f <= 0 ? 0x3FFFFFFFu : (0x3FFFFFFFu << (6 * f)) & 0x3FFFFFFFu;
+                            P[k] = (P[k] & ~mask) | (val & mask);
+                        }
+                    }
+                    if (tail && jl >= 0) {
+                        specm |= 1u << jl;
+                        const double sv = ev[j * TPC];
+                        ub[(new_pos - 1) * US] = static_cast<uint32_t>(__double2loint(sv));
+                        ub[(new_pos - 2) * US] = static_cast<uint32_t>(__double2hiint(sv));
+                    }
                 }
-                en[ne * TPC] = static_cast<uint32_t>(idx) | (static_cast<uint32_t>(new_pos - new_i) << 8) |
-                               (special ? 1u << 16 : 0u);
-                if (special) ev[ne * TPC] = sval;
-                ++ne;
                 pos = new_pos;
                 i = new_i;
                 if (i >= NP) break;
             }
         }
-        // lanes h > 0 start at normal s0: apply the events of earlier normals
-        int e = 0, off = 0;
-        while (e < ne) {
-            const uint32_t w = en[e * TPC];
-            if (static_cast<int>(w & 0xFFu) >= s0) break;
-            off = static_cast<int>((w >> 8) & 0xFFu);
-            ++e;
-        }
-        int nxt = e < ne ? static_cast<int>(en[e * TPC] & 0xFFu) - s0 : 255;  // lane-local spin index
 
         // ---- B: spin updates (sb_step solver.hpp:159-181 / simcim_step :196-210)
         const uint32_t* ubs = ub + s0 * US;
 #pragma unroll
         for (int s = 0; s < NQ; ++s) {
-            bool sp = false;
-            double spv = 0.0;
-            if (s == nxt) {  // rare: an event changes the word offset at this normal
-                const uint32_t w = en[e * TPC];
-                off = static_cast<int>((w >> 8) & 0xFFu);
-                if (w >> 16) {
-                    sp = true;
-                    spv = ev[e * TPC];
-                }
-                ++e;
-                nxt = e < ne ? static_cast<int>(en[e * TPC] & 0xFFu) - s0 : 255;
-            }
-            const uint32_t u = ubs[(s + off) * US];
-            double eta = __dmul_rn(i32_to_f64(static_cast<int32_t>(u)), wn[u & 127u]);
-            eta = sp ? spv : eta;
+            const int off = static_cast<int>((P[s / 5] >> (6 * (s % 5))) & 63u);
+            const uint32_t* wp = ubs + (s + off) * US;
+            const uint32_t u = wp[0];
+            double eta = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), wn[u & 127u]);
+            if (specm & (1u << s)) eta = __hiloint2double(static_cast<int>(wp[-US]), static_cast<int>(u));
             // coupled_i = sum_j J_ij phi(x_j), j ascending, from +0.0 (shim GEMM order)
             double coupled = 0.0;
             if constexpr (DMAX > 0) {

@@ -65,3 +65,71 @@ def time_to_target(session, cfg, reference, hv_target: float, max_runs: int, wor
     torch.cuda.synchronize(device)
     return {"reached": hv == hv_target, "runs": runs_done, "samples": runs_done * samples_per_run,
             "seconds": time.perf_counter() - t0, "hv": hv, "archive": int(running.shape[0]) if running is not None else 0}
+
+
+def time_to_target_overlapped(sessions: list, cfg, reference, hv_target: float, max_runs: int, device=None,
+                              trace: list | None = None) -> dict:
+    """One GPU, several sessions (contexts: own stream + buffers) in host threads: run r is
+    sampled by session r % S while the previous run's front is filtered / merged on another
+    session's stream, so the Pareto stage hides under the next run's sampler. Merges happen
+    strictly in run order, so the result (runs, samples, archive, HV) equals the sequential
+    stream's; only the wall time differs."""
+    import threading
+
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    S = len(sessions)
+    per_run = sessions[0].num_blocks(cfg, 1)
+    samples_per_run = sessions[0].L * cfg.batch_size
+    st = {"next": 0, "running": None, "hv": 0.0, "done": False, "runs": 0, "error": None}
+    cv = threading.Condition()
+    t0 = time.perf_counter()
+
+    def worker(w):
+        s = sessions[w]
+        try:
+            torch.cuda.set_device(device)
+            for run in range(w, max_runs, S):
+                with cv:
+                    if st["done"]:
+                        return
+                s.pipeline(cfg, run + 1, run * per_run, (run + 1) * per_run, do_hv=False)
+                mine = _packed_front(s, device)
+                with cv:
+                    while st["next"] != run and not st["done"]:
+                        cv.wait()
+                    if st["done"]:
+                        return
+                    if st["running"] is not None:
+                        rows = torch.cat([st["running"], mine], dim=0)
+                        k = s.inst.k()
+                        mdist.merge_on_device(s, rows[:, :k].contiguous().view(torch.float64), rows[:, k:].contiguous())
+                        st["running"] = _packed_front(s, device)
+                    else:
+                        st["running"] = mine
+                    st["hv"] = s.archive_hypervolume(reference)
+                    st["runs"] = run + 1
+                    if trace is not None:
+                        trace.append({"runs": run + 1, "samples": (run + 1) * samples_per_run,
+                                      "archive": int(st["running"].shape[0]), "hv": st["hv"],
+                                      "wall_s": time.perf_counter() - t0})
+                    st["next"] = run + 1
+                    if st["hv"] == hv_target:
+                        st["done"] = True
+                    cv.notify_all()
+        except BaseException as ex:  # surface worker errors in the caller
+            with cv:
+                st["error"] = ex
+                st["done"] = True
+                cv.notify_all()
+
+    threads = [threading.Thread(target=worker, args=(w,)) for w in range(S)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if st["error"] is not None:
+        raise st["error"]
+    torch.cuda.synchronize(device)
+    return {"reached": st["hv"] == hv_target, "runs": st["runs"], "samples": st["runs"] * samples_per_run,
+            "seconds": time.perf_counter() - t0, "hv": st["hv"],
+            "archive": int(st["running"].shape[0]) if st["running"] is not None else 0}
