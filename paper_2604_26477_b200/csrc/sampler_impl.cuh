@@ -58,7 +58,7 @@ __device__ __forceinline__ uint32_t zmag(uint32_t u)
     return static_cast<int32_t>(u) < 0 ? 0u - u : u;
 }
 
-template <int NMAX, int LANES>
+template <int NMAX, int LANES, int VAR>
 struct Geo {
     static constexpr int kPackWords = ((NMAX + LANES - 1) / LANES + 4) / 5;  // u32 words of 5 packed offsets
     static constexpr int kTPC = kThreads / LANES;           // trajectories per CTA
@@ -73,8 +73,15 @@ struct Geo {
     static constexpr int ubuf = 2560;                                       // kNA x kUS u32
     static constexpr int ent = ubuf + (kNA * kUS * 4 + 15) / 16 * 16;       // kECAP x kTPC u32
     static constexpr int entv = ent + kECAP * kTPC * 4;                     // kECAP x kTPC f64
-    static constexpr int phi = entv + kECAP * kTPC * 8;                     // kNP x kTPC f64
-    static constexpr int csr = phi + kNP * kTPC * 8;
+    // phi(x_j) rows, trajectory-major: dSB keeps the sign as a u32 mask (J_ij phi_j is J_ij
+    // with its sign flipped), bSB / SimCIM keep x as f64. Row strides put the 4 lanes x 8
+    // trajectories of a warp on distinct banks for both the writes (spin s0 + s of lane h) and
+    // the neighbour gathers (j ~ i +- 1 on a heavy-hex chain): u32 rows == 4 mod 32, f64 rows
+    // == 2 mod 16 elements.
+    static constexpr int kPhiW = VAR == 1 ? 4 : 8;
+    static constexpr int kPStr = VAR == 1 ? (kNP + 27) / 32 * 32 + 4 : (kNP + 13) / 16 * 16 + 2;
+    static constexpr int phi = entv + kECAP * kTPC * 8;                     // kTPC x kPStr phi entries
+    static constexpr int csr = (phi + kTPC * kPStr * kPhiW + 15) / 16 * 16;
     static_assert(kNU <= 128, "mask covers at most 128 words");
     static_assert(kNA <= 255, "word positions are stored in 8 bits");
 };
@@ -117,7 +124,7 @@ __device__ __forceinline__ uint64_t lane_or(unsigned mask, uint64_t v)
 template <int NMAX, int LANES, int VAR, int DMAX>
 __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel(const SamplerParams p)
 {
-    using G = Geo<NMAX, LANES>;
+    using G = Geo<NMAX, LANES, VAR>;
     constexpr int TPC = G::kTPC;
     constexpr int NQ = G::kNQ;
     constexpr int NP = G::kNP;
@@ -128,14 +135,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     uint32_t* ubuf = reinterpret_cast<uint32_t*>(smem + G::ubuf);
     uint32_t* ent = reinterpret_cast<uint32_t*>(smem + G::ent);
     double* entv = reinterpret_cast<double*>(smem + G::entv);
-    double* phis = reinterpret_cast<double*>(smem + G::phi);
+    unsigned char* phis = smem + G::phi;
     unsigned char* csr = smem + G::csr;
-    // DMAX == 0: rp[NP+1] | cv[nnz] | cc[nnz];  DMAX > 0: pc[NP*DMAX] int | pv[NP*DMAX] f64
+    // DMAX == 0: rp[NP+1] | cv[nnz] | cc[nnz];  DMAX == 3: one 48-byte record per spin,
+    // {J_i,j0, J_i,j1 | J_i,j2, off_j0, off_j1 | off_j2, -, -, -} (off = byte offset of phi_j
+    // in a trajectory's row), three LDS.128 per spin
     int* rp = reinterpret_cast<int*>(csr);
     double* cv = reinterpret_cast<double*>(csr + ((NP + 1) * 4 + 15) / 16 * 16);
     int* cc = reinterpret_cast<int*>(cv + p.nnz);
-    int* pc = reinterpret_cast<int*>(csr);
-    double* pv = reinterpret_cast<double*>(csr + (NP * DMAX * 4 + 15) / 16 * 16);
+    static_assert(DMAX == 0 || DMAX == 3, "padded rows are 3 wide");
 
     const int n = p.n;
     const long long gblock = p.block_begin + blockIdx.x;
@@ -160,10 +168,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
             }
         } else {
             const double* v = p.pad_vals + static_cast<long long>(l) * n * DMAX;
-            for (int q = tid; q < NP * DMAX; q += kThreads) {
-                const int i = q / DMAX;
-                pc[q] = (i < n ? p.pad_col[q] : i) * TPC * 8;  // byte offset of phi row j
-                pv[q] = i < n ? v[q] : 0.0;
+            for (int i = tid; i < NP; i += kThreads) {  // phantom rows: zero couplings to themselves
+                double* rv = reinterpret_cast<double*>(csr + i * 48);
+                int* ro = reinterpret_cast<int*>(csr + i * 48 + 24);
+                for (int d = 0; d < 3; ++d) {
+                    rv[d] = i < n ? v[i * 3 + d] : 0.0;
+                    ro[d] = (i < n ? p.pad_col[i * 3 + d] : i) * G::kPhiW;
+                }
+                ro[3] = 0;
             }
         }
     }
@@ -194,10 +206,20 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         y[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(ry.z, ry.w) : u01_from(ry.x, ry.y)), 1.0));
     }
 
-    double* ph = phis + t_loc;  // phi_j of this trajectory at ph[j * TPC]
-    const unsigned char* phb = reinterpret_cast<const unsigned char*>(ph);
+    unsigned char* phb = phis + t_loc * G::kPStr * G::kPhiW;  // this trajectory's phi row
+    // dSB: phi = (x < 0 ? -1 : +1) (solver.hpp:161-165) kept as the sign mask of the product
+    auto put_phi = [&](int j, double xv) {
+        if constexpr (VAR == 1) reinterpret_cast<uint32_t*>(phb)[j] = xv < 0.0 ? 0x80000000u : 0u;
+        else reinterpret_cast<double*>(phb)[j] = xv;
+    };
+    // J_ij * phi_j for the phi entry at byte offset o: exact (a sign flip for dSB)
+    auto term = [&](double jv, int o) -> double {
+        if constexpr (VAR == 1)
+            return __hiloint2double(__double2hiint(jv) ^ *reinterpret_cast<const int*>(phb + o), __double2loint(jv));
+        else return __dmul_rn(jv, *reinterpret_cast<const double*>(phb + o));
+    };
 #pragma unroll
-    for (int s = 0; s < NQ; ++s) ph[(s0 + s) * TPC] = VAR == 1 ? (x[s] < 0.0 ? -1.0 : 1.0) : x[s];
+    for (int s = 0; s < NQ; ++s) put_phi(s0 + s, x[s]);
 
     const uint32_t* kn = zig->kn;
     const double* wn = zig->wn;
@@ -205,8 +227,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     uint32_t* ub = ubuf + t_loc;  // this trajectory's word column, stride US
     uint32_t* en = ent + t_loc;   // this trajectory's event column, stride TPC
     double* ev = entv + t_loc;
-    const int* pcs = pc + s0 * DMAX;
-    const double* pvs = pv + s0 * DMAX;
+    const uint4* recs = reinterpret_cast<const uint4*>(csr) + s0 * 3;  // this lane's coupling records
     bool overflow = false;
     int ovf_code = 0;  // which buffer overflowed (diagnostics)
     __syncwarp(wmask);
@@ -409,15 +430,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
             // coupled_i = sum_j J_ij phi(x_j), j ascending, from +0.0 (shim GEMM order)
             double coupled = 0.0;
             if constexpr (DMAX > 0) {
-#pragma unroll
-                for (int d = 0; d < DMAX; ++d) {
-                    const double phj = *reinterpret_cast<const double*>(phb + pcs[s * DMAX + d]);
-                    coupled = __dadd_rn(coupled, __dmul_rn(pvs[s * DMAX + d], phj));
-                }
+                const uint4 r0 = recs[3 * s], r1 = recs[3 * s + 1], r2 = recs[3 * s + 2];
+                coupled = __dadd_rn(coupled, term(__hiloint2double(r0.y, r0.x), static_cast<int>(r1.z)));
+                coupled = __dadd_rn(coupled, term(__hiloint2double(r0.w, r0.z), static_cast<int>(r1.w)));
+                coupled = __dadd_rn(coupled, term(__hiloint2double(r1.y, r1.x), static_cast<int>(r2.x)));
             } else {
                 const int i = s0 + s;
                 const int e1 = rp[i + 1];
-                for (int q = rp[i]; q < e1; ++q) coupled = __dadd_rn(coupled, __dmul_rn(cv[q], ph[cc[q] * TPC]));
+                for (int q = rp[i]; q < e1; ++q) coupled = __dadd_rn(coupled, term(cv[q], cc[q] * G::kPhiW));
             }
             double xi = x[s], yi = y[s];
             if constexpr (VAR == 2) {
@@ -439,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         }
         __syncwarp(wmask);  // every lane has finished reading phi(t) and this step's words
 #pragma unroll
-        for (int s = 0; s < NQ; ++s) ph[(s0 + s) * TPC] = VAR == 1 ? (x[s] < 0.0 ? -1.0 : 1.0) : x[s];
+        for (int s = 0; s < NQ; ++s) put_phi(s0 + s, x[s]);
         __syncwarp(wmask);  // phi(t+1) complete
     }
 
@@ -469,9 +489,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
 template <int NMAX, int LANES, int VAR, int DMAX>
 int launch_small(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
-    using G = Geo<NMAX, LANES>;
-    const int csr_bytes = DMAX == 0 ? ((G::kNP + 1) * 4 + 15) / 16 * 16 + p.nnz * 12
-                                    : (G::kNP * DMAX * 4 + 15) / 16 * 16 + G::kNP * DMAX * 8;
+    using G = Geo<NMAX, LANES, VAR>;
+    const int csr_bytes = DMAX == 0 ? ((G::kNP + 1) * 4 + 15) / 16 * 16 + p.nnz * 12 : G::kNP * 48;
     const int smem = G::csr + csr_bytes + 16;
     auto kern = sb_small_kernel<NMAX, LANES, VAR, DMAX>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
