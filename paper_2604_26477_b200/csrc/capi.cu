@@ -27,7 +27,7 @@ Ctx::~Ctx()
     if (stream) cudaStreamSynchronize(stream);
     g_alloc_stream = nullptr;  // synchronous frees from here on (the stream goes away below)
     for (auto* b : {&d_ei, &d_ej, &d_rowptr, &d_col, &d_eidx, &d_wi, &d_nums, &d_nan, &d_badstep}) b->release();
-    for (auto* b : {&d_w, &d_vals, &d_c0, &d_padv, &d_gx, &d_gy, &d_gxn, &d_gnoise}) b->release();
+    for (auto* b : {&d_w, &d_vals, &d_c0, &d_padv, &d_gx, &d_gy, &d_gxn, &d_gnoise, &d_sched}) b->release();
     d_zig.release();
     d_words.release();
     d_block_end.release();
@@ -397,6 +397,18 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     p.zig = c.d_zig.p;
     p.words = c.d_words.p;
     p.row0 = c.pool_row0;
+    {  // pump schedule per step (solver.hpp:70-76), same IEEE operations as the device formula
+        std::vector<double> sched(2 * static_cast<size_t>(cfg->n_iterations));
+        for (int t = 0; t < cfg->n_iterations; ++t) {
+            const double a_t = static_cast<double>(t + 1) / static_cast<double>(cfg->n_iterations);
+            sched[2 * static_cast<size_t>(t)] = -(cfg->a0 - a_t);
+            sched[2 * static_cast<size_t>(t) + 1] = -0.5 * (1.0 - a_t);
+        }
+        c.d_sched.reserve(sched.size());
+        ck(cudaMemcpyAsync(c.d_sched.p, sched.data(), sizeof(double) * sched.size(), cudaMemcpyHostToDevice, c.stream),
+           "H2D");
+        p.sched = c.d_sched.p;
+    }
     p.block_end_ns = c.d_block_end.p;
     p.nan_block = c.d_nan.p;
     p.first_bad_step_task = -1;

@@ -93,6 +93,7 @@ struct Ctx {
     DevBuf<int> d_nan, d_badstep;
     DevBuf<unsigned long long> d_block_end, d_t0;
     DevBuf<double> d_gx, d_gy, d_gxn, d_gnoise;  // generic-n scratch
+    DevBuf<double> d_sched;                      // pump schedule table (register sampler)
     DevBuf<uint64_t> d_upload;                   // host pools uploaded for filtering
     std::shared_ptr<void> pareto_scratch;         // pareto.cu working buffers
     std::shared_ptr<void> dense_scratch;          // dense.cu working buffers

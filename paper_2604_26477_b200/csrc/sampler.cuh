@@ -34,6 +34,7 @@ struct SamplerParams {
     const ZigTables* zig;
     uint64_t* words;          // (runs * L * batch) * wpc, canonical order, from row row0
     long long row0;           // first pool row held by `words` (compact pipeline pools)
+    const double* sched;      // 2 x T: {-(a0 - a_t), -0.5 (1 - a_t)} per step (register path)
     unsigned long long* block_end_ns;  // per launched block (optional)
     int* nan_block;           // per launched block: 1 if any trajectory went non-finite
     int first_bad_step_task;  // debug rerun: -1, else records first bad step per block

@@ -60,7 +60,6 @@ __device__ __forceinline__ uint32_t zmag(uint32_t u)
 
 template <int NMAX, int LANES, int VAR>
 struct Geo {
-    static constexpr int kPackWords = ((NMAX + LANES - 1) / LANES + 4) / 5;  // u32 words of 5 packed offsets
     static constexpr int kTPC = kThreads / LANES;           // trajectories per CTA
     static constexpr int kNQ = (NMAX + LANES - 1) / LANES;  // spins per lane
     static constexpr int kNP = kNQ * LANES;                 // integrated spins (>= n)
@@ -84,6 +83,7 @@ struct Geo {
     static constexpr int csr = (phi + kTPC * kPStr * kPhiW + 15) / 16 * 16;
     static_assert(kNU <= 128, "mask covers at most 128 words");
     static_assert(kNA <= 255, "word positions are stored in 8 bits");
+    static_assert(kNQ <= 16, "word offsets are packed in 16 fields");
 };
 
 // first p in [from, kNU) whose mask bit is clear, else kNU
@@ -129,7 +129,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     constexpr int NQ = G::kNQ;
     constexpr int NP = G::kNP;
     constexpr int US = G::kUS;
-    constexpr int kPK = G::kPackWords;
     extern __shared__ __align__(16) unsigned char smem[];
     ZigTables* zig = reinterpret_cast<ZigTables*>(smem + G::zig);
     uint32_t* ubuf = reinterpret_cast<uint32_t*>(smem + G::ubuf);
@@ -215,7 +214,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     // J_ij * phi_j for the phi entry at byte offset o: exact (a sign flip for dSB)
     auto term = [&](double jv, int o) -> double {
         if constexpr (VAR == 1)
-            return __hiloint2double(__double2hiint(jv) ^ *reinterpret_cast<const int*>(phb + o), __double2loint(jv));
+            return __longlong_as_double(__double_as_longlong(jv) ^
+                                        (static_cast<long long>(*reinterpret_cast<const uint32_t*>(phb + o)) << 32));
         else return __dmul_rn(jv, *reinterpret_cast<const double*>(phb + o));
     };
 #pragma unroll
@@ -233,9 +233,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     __syncwarp(wmask);
 
     for (int t = 0; t < p.T; ++t) {
-        const double a_t = __ddiv_rn(static_cast<double>(t + 1), static_cast<double>(p.T));
-        const double neg_drift = -__dsub_rn(p.a0, a_t);            // -(a0 - a_t)
-        const double pump = __dmul_rn(-0.5, __dsub_rn(1.0, a_t));  // simcim_schedule
+        // -(a0 - a_t) and simcim's -0.5 (1 - a_t), a_t = (t + 1) / T (solver.hpp:70-76),
+        // tabulated on the host with the same IEEE operations
+        const double neg_drift = p.sched[2 * t];
+        const double pump = p.sched[2 * t + 1];
         const uint32_t lo = tag_word(kTagStepNoise, static_cast<uint32_t>(t));
 
         // ---- A1: Philox blocks (lane h: blocks h, h+LANES, ...) + fast-attempt mask
@@ -372,13 +373,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         acc = static_cast<uint32_t>(lane_or<LANES>(wmask, acc));
 
         // ---- A2e: walk the candidates with their outcomes; every lane keeps the word offset
-        //      of each of its spins packed 6 bits per field (5 fields per u32) and a mask of its
+        //      of each of its spins packed 6 bits per field (10 fields per u64) and a mask of its
         //      tail normals, whose value goes into the tail's last two words
-        uint32_t P[kPK];
-#pragma unroll
-        for (int k = 0; k < kPK; ++k) P[k] = 0;
+        uint64_t P0 = 0, P1 = 0;  // fields 0..9 and 10..15
         uint32_t specm = 0;
         {
+            constexpr uint64_t kRep = 0x041041041041041ull;  // one in each of 10 fields
+            constexpr uint64_t kF60 = (1ull << 60) - 1, kF36 = (1ull << 36) - 1;
             int pos = 0, i = 0;
             for (int j = 0; j < m; ++j) {
                 const uint32_t e = en[j * TPC];
@@ -396,14 +397,17 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                         overflow = true;
                         ovf_code |= 16;
                     }
-                    const uint32_t val = static_cast<uint32_t>(off & 63) * 0x01041041u;
-#pragma unroll
-                    for (int k = 0; k < kPK; ++k) {
-                        const int f = jl - 5 * k;  // first field of P[k] that changes
-                        if (f < 5) {
-                            const uint32_t mask = f <= 0 ? 0x3FFFFFFFu : (0x3FFFFFFFu << (6 * f)) & 0x3FFFFFFFu;
-                            P[k] = (P[k] & ~mask) | (val & mask);
-                        }
+                    const uint64_t val = static_cast<uint64_t>(off & 63) * kRep;
+                    if (jl <= 0) {
+                        P0 = val;
+                        P1 = val & kF36;
+                    } else if (jl < 10) {
+                        const uint64_t msk = (kF60 << (6 * jl)) & kF60;
+                        P0 = (P0 & ~msk) | (val & msk);
+                        P1 = val & kF36;
+                    } else {
+                        const uint64_t msk = (kF36 << (6 * (jl - 10))) & kF36;
+                        P1 = (P1 & ~msk) | (val & msk);
                     }
                     if (tail && jl >= 0) {
                         specm |= 1u << jl;
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         const uint32_t* ubs = ub + s0 * US;
 #pragma unroll
         for (int s = 0; s < NQ; ++s) {
-            const int off = static_cast<int>((P[s / 5] >> (6 * (s % 5))) & 63u);
+            const int off = static_cast<int>(((s < 10 ? P0 >> (6 * s) : P1 >> (6 * (s - 10)))) & 63u);
             const uint32_t* wp = ubs + (s + off) * US;
             const uint32_t u = wp[0];
             double eta = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), wn[u & 127u]);
@@ -449,11 +453,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                     __dadd_rn(__dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled)), __dmul_rn(alpha, eta));
                 yi = __dadd_rn(yi, __dmul_rn(dt, d));
                 xi = __dadd_rn(xi, __dmul_rn(sdt, yi));
-                yi = fabs(xi) > 1.0 ? 0.0 : yi;
             }
-            // cwiseMax(-1).cwiseMin(1) == std::max/std::min (NaN propagates)
-            xi = (xi < -1.0) ? -1.0 : xi;
-            xi = (1.0 < xi) ? 1.0 : xi;
+            // y <- 0 where |x| > 1 (strict, SB only), then cwiseMax(-1).cwiseMin(1): both fire
+            // exactly when |x| > 1 (never for NaN, which propagates), and the clamp is +-1
+            // with x's sign
+            if (fabs(xi) > 1.0) {
+                if constexpr (VAR != 2) yi = 0.0;
+                xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
+            }
             x[s] = xi;
             y[s] = yi;
         }
