@@ -15,6 +15,8 @@
 //                 the values are integers (bit-equal to the reference's exact double result)
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -397,36 +399,35 @@ __global__ void k_pairwise(const double* __restrict__ vals, long long V, int K, 
     }
 }
 
-// archive order: rank = #vectors lexicographically greater (pareto.hpp:405-406)
-__global__ void k_lex_desc_rank(const double* __restrict__ vals, long long F, int K, long long* rank)
+// ---- archive order (pareto.hpp:405-406, lexicographically descending) by LSD radix passes:
+// the last objective first, each pass a stable
+// descending sort of the rows' current order by one objective (orderable u64 keys; -0 == +0)
+__device__ __forceinline__ unsigned long long ord_key(double v)
 {
-    extern __shared__ double tile[];
-    for (long long base = blockIdx.x * static_cast<long long>(blockDim.x); base < F;
-         base += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long i = base + threadIdx.x;
-        double mine[kMaxK];
-        for (int k = 0; k < K; ++k) mine[k] = i < F ? vals[i * K + k] : 0.0;
-        long long rk = 0;
-        for (long long t0 = 0; t0 < F; t0 += blockDim.x) {
-            __syncthreads();
-            for (int q = threadIdx.x; q < static_cast<int>(blockDim.x) * K; q += blockDim.x) {
-                const long long row = t0 + q / K;
-                tile[q] = row < F ? vals[row * K + q % K] : 0.0;
-            }
-            __syncthreads();
-            const int lim = static_cast<int>(min(static_cast<long long>(blockDim.x), F - t0));
-            if (i < F)
-                for (int q = 0; q < lim; ++q) {
-                    int cmp = 0;
-                    for (int k = 0; k < K && cmp == 0; ++k) {
-                        const double a = tile[q * K + k];
-                        cmp = a > mine[k] ? 1 : (a < mine[k] ? -1 : 0);
-                    }
-                    rk += cmp > 0;
-                }
-        }
-        if (i < F) rank[i] = rk;
-    }
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v == 0.0 ? 0.0 : v));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_column_keys(const double* __restrict__ vals, const uint32_t* __restrict__ idx, long long F, int K,
+                              int k, unsigned long long* keys)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        keys[i] = ord_key(vals[static_cast<long long>(idx[i]) * K + k]);
+}
+
+__global__ void k_iota_u32(uint32_t* a, long long n)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        a[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void k_rank_of(const uint32_t* __restrict__ order, long long F, long long* rank)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        rank[order[i]] = i;
 }
 
 __global__ void k_gather_rows(const double* __restrict__ src_vals, const uint32_t* __restrict__ rows, long long F, int K,
@@ -727,6 +728,41 @@ __global__ void k_map_u32(const uint32_t* __restrict__ idx, const uint32_t* __re
         out[i] = map[idx[i]];
 }
 
+// rank[i] = position of row i in the lexicographically descending order (rows distinct)
+void lex_desc_rank(Ctx& c, const double* d_vals, long long F, int K, long long* rank)
+{
+    if (F <= 0) return;
+    DevBuf<uint32_t> ia, ib;
+    DevBuf<unsigned long long> ka, kb;
+    ia.reserve(static_cast<size_t>(F));
+    ib.reserve(static_cast<size_t>(F));
+    ka.reserve(static_cast<size_t>(F));
+    kb.reserve(static_cast<size_t>(F));
+    k_iota_u32<<<grid_blocks(F), 256, 0, c.stream>>>(ia.p, F);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, ka.p, kb.p, ia.p, ib.p, static_cast<int>(F), 0, 64,
+                                              c.stream);
+    DevBuf<unsigned char> tmp;
+    tmp.reserve(tb + 1);
+    uint32_t* cur = ia.p;
+    uint32_t* nxt = ib.p;
+    for (int k = K - 1; k >= 0; --k) {
+        k_column_keys<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, cur, F, K, k, ka.p);
+        ck(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, ka.p, kb.p, cur, nxt, static_cast<int>(F), 0, 64,
+                                                     c.stream),
+           "sort");
+        std::swap(cur, nxt);
+        c.launches += 2;
+    }
+    k_rank_of<<<grid_blocks(F), 256, 0, c.stream>>>(cur, F, rank);
+    c.launches += 2;
+    ia.release();
+    ib.release();
+    ka.release();
+    kb.release();
+    tmp.release();
+}
+
 // Shared tail of both filters: V distinct vectors (d_vv, V x K) with owner configs
 // (row index into `words` via d_own, or none) -> front -> archive (lex-descending).
 void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, const uint64_t* words,
@@ -758,8 +794,7 @@ void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, 
                                                          nullptr);
     c.launches++;
     s.rank.reserve(static_cast<size_t>(F) + 1);
-    k_lex_desc_rank<<<grid_blocks(F), 256, 256 * K * sizeof(double), c.stream>>>(fv.p, F, K, s.rank.p);
-    c.launches++;
+    lex_desc_rank(c, fv.p, F, K, s.rank.p);
     out.F = F;
     out.K = K;
     out.wpc = d_own ? wpc : 0;
