@@ -66,11 +66,13 @@ struct Geo {
     static constexpr int kNB = ((kNP + 3) / 4 + 2 + LANES - 1) / LANES * LANES;  // Philox blocks per step
     static constexpr int kNU = 4 * kNB;                     // words covered by the fast mask
     static constexpr int kNA = kNU + 40;                    // allocated words (A2 extends on demand; P(overflow) ~ 1e-15)
-    static constexpr int kUS = kTPC + 1;                    // word-row stride (odd: lanes of a trajectory hit distinct banks)
+    // word rows, trajectory-major, stride == 4 mod 32 words: a block's 4 words are one
+    // STS.128, and the 4 lanes x 8 trajectories of a warp reading spin s0 + s hit 32 banks
+    static constexpr int kUS = (kNA + 27) / 32 * 32 + 4;
     static constexpr int kECAP = 16;                        // event entries per trajectory-step (P(>16) ~ 1e-14)
     static constexpr int zig = 0;                                           // ZigTables (2560 B)
-    static constexpr int ubuf = 2560;                                       // kNA x kUS u32
-    static constexpr int ent = ubuf + (kNA * kUS * 4 + 15) / 16 * 16;       // kECAP x kTPC u32
+    static constexpr int ubuf = 2560;                                       // kTPC x kUS u32
+    static constexpr int ent = ubuf + kTPC * kUS * 4;                       // kECAP x kTPC u32
     static constexpr int entv = ent + kECAP * kTPC * 4;                     // kECAP x kTPC f64
     // phi(x_j) rows, trajectory-major: dSB keeps the sign as a u32 mask (J_ij phi_j is J_ij
     // with its sign flipped), bSB / SimCIM keep x as f64. Row strides put the 4 lanes x 8
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     const uint32_t* kn = zig->kn;
     const double* wn = zig->wn;
     const double* fn = zig->fn;
-    uint32_t* ub = ubuf + t_loc;  // this trajectory's word column, stride US
+    uint32_t* ub = ubuf + t_loc * US;  // this trajectory's word row
     uint32_t* en = ent + t_loc;   // this trajectory's event column, stride TPC
     double* ev = entv + t_loc;
     const uint4* recs = reinterpret_cast<const uint4*>(csr) + s0 * 3;  // this lane's coupling records
@@ -244,10 +246,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
 #pragma unroll 1
         for (int b = h; b < G::kNB; b += LANES) {
             const uint4 r = philox(k0, k1, static_cast<uint32_t>(b), lo, tr, wl);
-            ub[(4 * b + 0) * US] = r.x;
-            ub[(4 * b + 1) * US] = r.y;
-            ub[(4 * b + 2) * US] = r.z;
-            ub[(4 * b + 3) * US] = r.w;
+            *reinterpret_cast<uint4*>(ub + 4 * b) = r;
             const uint64_t f = static_cast<uint64_t>(zmag(r.x) < kn[r.x & 127u]) |
                                static_cast<uint64_t>(zmag(r.y) < kn[r.y & 127u]) << 1 |
                                static_cast<uint64_t>(zmag(r.z) < kn[r.z & 127u]) << 2 |
@@ -263,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         // ---- A2w: the slow attempts' positions (rng.hpp:164-184), identically on every lane.
         //      A wedge attempt takes 3 words whatever its outcome and a tail 1 + 4k, so the
         //      positions follow from the fast mask alone; candidates are listed until even
-        //      all-rejected wedges would have produced NP normals before them. Tails (rare)
+        //      all-rejected wedges would have produced n normals before them. Tails (rare)
         //      are resolved here; entry = q | tail length << 8 | tail flag << 16.
         int m = 0;
         {
@@ -271,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
             int pos = 0;       // next attempt position
             int slow = 0;      // words taken by the listed slow attempts
             for (;;) {
-                const int lastq = NP - 1 + slow;  // fast normals before q = q - slow must stay < NP
+                const int lastq = n - 1 + slow;  // fast normals before q = q - slow must stay < n
                 int q = next_slow<G::kNU>(F0, F1, pos);
                 if (q >= G::kNU) {  // beyond the mask: extend the word buffer, test on demand
                     q = pos > G::kNU ? pos : G::kNU;
@@ -279,13 +278,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                         if (q >= G::kNA) break;
                         while (gen <= q) {  // every lane writes the same words
                             const uint4 r = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
-                            ub[(gen + 0) * US] = r.x;
-                            ub[(gen + 1) * US] = r.y;
-                            ub[(gen + 2) * US] = r.z;
-                            ub[(gen + 3) * US] = r.w;
+                            *reinterpret_cast<uint4*>(ub + gen) = r;
                             gen += 4;
                         }
-                        const uint32_t w = ub[q * US];
+                        const uint32_t w = ub[q];
                         if (!(zmag(w) < kn[w & 127u])) break;
                     }
                 }
@@ -297,13 +293,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                 }
                 while (gen <= q + 8) {  // words a wedge attempt may read
                     const uint4 r = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
-                    ub[(gen + 0) * US] = r.x;
-                    ub[(gen + 1) * US] = r.y;
-                    ub[(gen + 2) * US] = r.z;
-                    ub[(gen + 3) * US] = r.w;
+                    *reinterpret_cast<uint4*>(ub + gen) = r;
                     gen += 4;
                 }
-                const uint32_t u = ub[q * US];
+                const uint32_t u = ub[q];
                 if ((u & 127u) == 0) {  // tail: 4 words per (x, y) trial
                     const double r = 3.442619855899;
                     int qq = q + 1;
@@ -316,14 +309,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                         }
                         while (gen < qq + 4) {
                             const uint4 rr = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
-                            ub[(gen + 0) * US] = rr.x;
-                            ub[(gen + 1) * US] = rr.y;
-                            ub[(gen + 2) * US] = rr.z;
-                            ub[(gen + 3) * US] = rr.w;
+                            *reinterpret_cast<uint4*>(ub + gen) = rr;
                             gen += 4;
                         }
-                        const double xx = __ddiv_rn(-log(u01_open_from(ub[qq * US], ub[(qq + 1) * US])), r);
-                        const double yy = -log(u01_open_from(ub[(qq + 2) * US], ub[(qq + 3) * US]));
+                        const double xx = __ddiv_rn(-log(u01_open_from(ub[qq], ub[qq + 1])), r);
+                        const double yy = -log(u01_open_from(ub[qq + 2], ub[qq + 3]));
                         qq += 4;
                         if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) {
                             sval = static_cast<int32_t>(u) > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
@@ -355,11 +345,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                 continue;
             }
             const int q = static_cast<int>(e & 0xFFu);
-            const uint32_t u = ub[q * US];
+            const uint32_t u = ub[q];
             const uint32_t iz = u & 127u;
             const double xv = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), wn[iz]);
             const double lhs = __dadd_rn(
-                fn[iz], __dmul_rn(u01_from(ub[(q + 1) * US], ub[(q + 2) * US]), __dsub_rn(fn[iz - 1], fn[iz])));
+                fn[iz], __dmul_rn(u01_from(ub[q + 1], ub[q + 2]), __dsub_rn(fn[iz - 1], fn[iz])));
             const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
             // FP32 exp brackets the FP64 one within 1e-6 relative on [-6, 0]; decide from it
             // unless lhs falls in the +-1e-5 band, then use the FP64 exp
@@ -385,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                 const uint32_t e = en[j * TPC];
                 const int q = static_cast<int>(e & 0xFFu);
                 i += q - pos;  // fast normals before the attempt
-                if (i >= NP) break;
+                if (i >= n) break;  // phantom spins (>= n) read any word: no couplings
                 const bool tail = e >> 16;
                 const int new_pos = tail ? q + static_cast<int>((e >> 8) & 0xFFu) : q + 3;
                 const int new_i = tail ? i + 1 : i + static_cast<int>((acc >> j) & 1u);
@@ -412,25 +402,25 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                     if (tail && jl >= 0) {
                         specm |= 1u << jl;
                         const double sv = ev[j * TPC];
-                        ub[(new_pos - 1) * US] = static_cast<uint32_t>(__double2loint(sv));
-                        ub[(new_pos - 2) * US] = static_cast<uint32_t>(__double2hiint(sv));
+                        ub[new_pos - 1] = static_cast<uint32_t>(__double2loint(sv));
+                        ub[new_pos - 2] = static_cast<uint32_t>(__double2hiint(sv));
                     }
                 }
                 pos = new_pos;
                 i = new_i;
-                if (i >= NP) break;
+                if (i >= n) break;
             }
         }
 
         // ---- B: spin updates (sb_step solver.hpp:159-181 / simcim_step :196-210)
-        const uint32_t* ubs = ub + s0 * US;
+        const uint32_t* ubs = ub + s0;
 #pragma unroll
         for (int s = 0; s < NQ; ++s) {
             const int off = static_cast<int>(((s < 10 ? P0 >> (6 * s) : P1 >> (6 * (s - 10)))) & 63u);
-            const uint32_t* wp = ubs + (s + off) * US;
+            const uint32_t* wp = ubs + s + off;
             const uint32_t u = wp[0];
             double eta = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), wn[u & 127u]);
-            if (specm & (1u << s)) eta = __hiloint2double(static_cast<int>(wp[-US]), static_cast<int>(u));
+            if (specm & (1u << s)) eta = __hiloint2double(static_cast<int>(wp[-1]), static_cast<int>(u));
             // coupled_i = sum_j J_ij phi(x_j), j ascending, from +0.0 (shim GEMM order)
             double coupled = 0.0;
             if constexpr (DMAX > 0) {
