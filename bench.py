@@ -328,8 +328,7 @@ def main():
             r_frozen = [float(x) for x in g["reference"]]
             target = float(g["hv_star"])
             ik, wk, ck = shapes[k]
-            # world == 1: two contexts overlap run r+1's sampler with run r's filter / merge
-            sessions = [api.Session(local) for _ in range(2 if world == 1 else 1)]
+            sessions = [api.Session(local)]
             for sk in sessions:
                 sk.set_instance(ik)  # warm the contexts (module load, pools) outside the clock
                 sk.set_weights(wk)
@@ -339,12 +338,8 @@ def main():
             for sk in sessions:
                 sk.set_instance(ik)  # model build inside the clock
                 sk.set_weights(wk)
-            if world == 1:
-                res = streaming.time_to_target_overlapped(sessions, ck, r_frozen, target, TTO_MAX_RUNS[k],
-                                                          torch.device("cuda", local))
-            else:
-                res = streaming.time_to_target(sessions[0], ck, r_frozen, target, TTO_MAX_RUNS[k], world, rank,
-                                               torch.device("cuda", local))
+            res = streaming.time_to_target(sessions[0], ck, r_frozen, target, TTO_MAX_RUNS[k], world, rank,
+                                           torch.device("cuda", local))
             torch.cuda.synchronize(local)
             secs = time.perf_counter() - t0
             if world > 1:

@@ -215,6 +215,21 @@ int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t
 int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long long block_begin,
                        long long block_end, int do_hv, int ref_count, const double* fixed_ref,
                        momc_bench_report* report, char* err, size_t errlen);
+/* Streaming (time-to-optimal): a running archive on the context. stream_step samples
+ * blocks [block_begin, block_end) of a `runs`-run job (compact pool), filters them into the
+ * resident archive (unordered) and, with merge != 0, merges that front into the running
+ * archive and (r, hv non-NULL) returns the running archive's hypervolume at r. running_merge_values merges device rows (another context's or
+ * another rank's front) the same way. running_to_archive makes the running archive the
+ * resident archive (archive order) for momc_b200_archive_get. */
+int momc_b200_running_reset(momc_ctx* ctx, char* err, size_t errlen);
+int momc_b200_stream_step(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long long block_begin,
+                          long long block_end, int merge, const double* r, double* hv, int64_t* running_F,
+                          momc_bench_report* report, char* err, size_t errlen);
+/* device pointers of the resident archive (valid until the next call that replaces it) */
+int momc_b200_archive_device_ptrs(momc_ctx* ctx, const double** vals, const uint64_t** words, int64_t* F);
+int momc_b200_running_merge_values(momc_ctx* ctx, const double* d_vals, const uint64_t* d_words, int wpc, size_t M,
+                                   int k, const double* r, double* hv, int64_t* running_F, char* err, size_t errlen);
+int momc_b200_running_to_archive(momc_ctx* ctx, int64_t* out_F, char* err, size_t errlen);
 /* flattened (run, weight, chunk) block count of a run configuration on this context */
 long long momc_b200_num_blocks(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs);
 

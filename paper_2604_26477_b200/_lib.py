@@ -113,6 +113,13 @@ SIGNATURES = [
     ("momc_b200_generate_correlated_instance", C.c_int, [vp, C.c_int, C.c_double, C.c_double, C.c_uint64, i64p,
                                                          C.c_char_p, C.c_size_t]),
     ("momc_b200_measured_correlation", C.c_int, [vp, C.c_int, C.c_uint64, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_running_reset", C.c_int, [vp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_stream_step", C.c_int, [vp, C.POINTER(SolverCfgC), C.c_int, C.c_longlong, C.c_longlong, C.c_int, dp,
+                                        dp, i64p, C.POINTER(BenchReportC), C.c_char_p, C.c_size_t]),
+    ("momc_b200_archive_device_ptrs", C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), i64p]),
+    ("momc_b200_running_merge_values", C.c_int, [vp, C.c_void_p, C.c_void_p, C.c_int, C.c_size_t, C.c_int, dp, dp,
+                                                 i64p, C.c_char_p, C.c_size_t]),
+    ("momc_b200_running_to_archive", C.c_int, [vp, i64p, C.c_char_p, C.c_size_t]),
     ("momc_b200_format_pool_rows", C.c_int, [vp, u32p, u32p, u32p, i64p, u64p, C.c_size_t, C.c_int, C.c_char_p,
                                              C.c_size_t, C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t]),
     ("momc_b200_parse_pool_rows", C.c_int, [vp, C.c_char_p, C.c_size_t, C.c_int, C.c_int, C.c_char_p,

@@ -658,6 +658,55 @@ class Session:
                                                     C.byref(F), err, 2048), err)
         return F.value
 
+    # ---- streaming (running archive on the context)
+    def running_reset(self):
+        err = _errbuf()
+        _raise(self.lib.momc_b200_running_reset(self.h, err, 2048), err)
+
+    def stream_step(self, config: SolverConfig, runs: int, block_begin: int, block_end: int, reference=None,
+                    merge: bool = True):
+        """Sample blocks [block_begin, block_end) and filter them (front left in the resident
+        archive, unordered); with `merge`, merge it into the running archive. Returns (hv of
+        the running archive at `reference` or None, running size, report)."""
+        config.validate()
+        cfg = config.c()
+        rep = _lib.BenchReportC()
+        F = C.c_int64()
+        hv = C.c_double()
+        err = _errbuf()
+        r = None if reference is None else np.ascontiguousarray(reference, np.float64)
+        _raise(self.lib.momc_b200_stream_step(self.h, C.byref(cfg), runs, block_begin, block_end, int(merge),
+                                              None if r is None else r.ctypes.data_as(_lib.dp),
+                                              None if r is None else C.byref(hv), C.byref(F), C.byref(rep), err,
+                                              2048), err)
+        self._pool_geom = (runs, self.L, config.batch_size)
+        return (None if r is None else hv.value), F.value, {name: getattr(rep, name) for name, _ in
+                                                            _lib.BenchReportC._fields_}
+
+    def running_merge_values(self, d_vals: int, d_words: int, wpc: int, M: int, k: int, reference=None):
+        """Merge M device rows (values + packed configs) into the running archive."""
+        F = C.c_int64()
+        hv = C.c_double()
+        err = _errbuf()
+        r = None if reference is None else np.ascontiguousarray(reference, np.float64)
+        _raise(self.lib.momc_b200_running_merge_values(self.h, C.c_void_p(d_vals), C.c_void_p(d_words), wpc, M, k,
+                                                       None if r is None else r.ctypes.data_as(_lib.dp),
+                                                       None if r is None else C.byref(hv), C.byref(F), err, 2048), err)
+        return (None if r is None else hv.value), F.value
+
+    def archive_device_ptrs(self):
+        """(values ptr, words ptr, F) of the resident archive on the device"""
+        v, w = C.c_void_p(), C.c_void_p()
+        F = C.c_int64()
+        self.lib.momc_b200_archive_device_ptrs(self.h, C.byref(v), C.byref(w), C.byref(F))
+        return v.value or 0, w.value or 0, F.value
+
+    def running_to_archive(self) -> int:
+        F = C.c_int64()
+        err = _errbuf()
+        _raise(self.lib.momc_b200_running_to_archive(self.h, C.byref(F), err, 2048), err)
+        return F.value
+
     def archive_copy_device(self, d_vals: int, d_words: int):
         err = _errbuf()
         _raise(self.lib.momc_b200_archive_copy_device(self.h, C.c_void_p(d_vals), C.c_void_p(d_words), err, 2048),

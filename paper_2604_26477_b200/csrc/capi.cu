@@ -34,6 +34,8 @@ Ctx::~Ctx()
     d_t0.release();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_dep) cudaEventDestroy(ev_dep);
+    if (sample_stream) cudaStreamDestroy(sample_stream);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -46,6 +48,61 @@ DevArchive& resident_archive(Ctx& c)
         delete a;
     });
     return *static_cast<DevArchive*>(c.archive.get());
+}
+
+DevArchive& running_archive(Ctx& c)
+{
+    if (!c.running) c.running = std::shared_ptr<void>(new DevArchive(), [](void* p) {
+        auto* a = static_cast<DevArchive*>(p);
+        a->vals.release();
+        a->words.release();
+        delete a;
+    });
+    return *static_cast<DevArchive*>(c.running.get());
+}
+
+// running <- front(running U (vals, words)); unordered (internal use); returns the new size
+long long running_merge(Ctx& c, const double* d_vals, const uint64_t* d_words, long long M, int K, int wpc)
+{
+    DevArchive& R = running_archive(c);
+    if (M <= 0) return R.F;
+    if (R.F == 0) {  // first front: copy
+        R.F = M;
+        R.K = K;
+        R.wpc = wpc;
+        R.vals.reserve(static_cast<size_t>(M) * K);
+        R.words.reserve(static_cast<size_t>(M) * wpc + 1);
+        ck(cudaMemcpyAsync(R.vals.p, d_vals, sizeof(double) * M * K, cudaMemcpyDeviceToDevice, c.stream), "D2D");
+        if (wpc)
+            ck(cudaMemcpyAsync(R.words.p, d_words, sizeof(uint64_t) * M * wpc, cudaMemcpyDeviceToDevice, c.stream),
+               "D2D");
+        return R.F;
+    }
+    if (R.K != K || R.wpc != wpc) usage("running archive shape mismatch");
+    const long long T = R.F + M;
+    DevBuf<double> cv;
+    DevBuf<uint64_t> cw;
+    cv.reserve(static_cast<size_t>(T) * K);
+    cw.reserve(static_cast<size_t>(T) * wpc + 1);
+    ck(cudaMemcpyAsync(cv.p, R.vals.p, sizeof(double) * R.F * K, cudaMemcpyDeviceToDevice, c.stream), "D2D");
+    ck(cudaMemcpyAsync(cv.p + R.F * K, d_vals, sizeof(double) * M * K, cudaMemcpyDeviceToDevice, c.stream), "D2D");
+    if (wpc) {
+        ck(cudaMemcpyAsync(cw.p, R.words.p, sizeof(uint64_t) * R.F * wpc, cudaMemcpyDeviceToDevice, c.stream), "D2D");
+        ck(cudaMemcpyAsync(cw.p + R.F * wpc, d_words, sizeof(uint64_t) * M * wpc, cudaMemcpyDeviceToDevice, c.stream),
+           "D2D");
+    }
+    const bool so = c.skip_order;
+    c.skip_order = true;
+    try {
+        filter_values_device(c, cv.p, wpc ? cw.p : nullptr, wpc, c.n, T, K, R, nullptr);
+    } catch (...) {
+        c.skip_order = so;
+        throw;
+    }
+    c.skip_order = so;
+    cv.release();
+    cw.release();
+    return R.F;
 }
 
 namespace {
@@ -427,25 +484,32 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     const bool densepath = !regpath && dense_path_ok(c, cfg->variant);
     if (!regpath && !densepath) g = scratch(nblocks);
 
-    stamp_t0<<<1, 1, 0, c.stream>>>(c.d_t0.p);
+    // the register sampler runs on the low-priority stream, after everything queued so far
+    cudaStream_t ss = c.stream;
+    if (regpath && nblocks > 0) {
+        ss = c.sample_stream;
+        ck(cudaEventRecord(c.ev_dep, c.stream), "event");
+        ck(cudaStreamWaitEvent(ss, c.ev_dep, 0), "event wait");
+    }
+    stamp_t0<<<1, 1, 0, ss>>>(c.d_t0.p);
     ++c.launches;
-    ck(cudaEventRecord(c.ev0, c.stream), "event");
+    ck(cudaEventRecord(c.ev0, ss), "event");
     if (nblocks > 0) {
         if (densepath) {
             sample_dense(c, p, b_begin, nblocks);  // tensor-core J sgn(X) (dense.cu)
         } else {
-            const int rc = regpath ? launch_sampler(p, nblocks, c.stream) : launch_sampler_generic(p, nblocks, g, c.stream);
+            const int rc = regpath ? launch_sampler(p, nblocks, ss) : launch_sampler_generic(p, nblocks, g, c.stream);
             ck(static_cast<cudaError_t>(rc), "sampler launch");
             c.launches += regpath ? 1 : 2 + (long long)p.T * (cfg->alpha > 0 ? 2 : 1);
         }
     }
-    ck(cudaEventRecord(c.ev1, c.stream), "event");
+    ck(cudaEventRecord(c.ev1, ss), "event");
     // Per-block flags: bit 2 = the register path's noise-event buffer overflowed (re-run the
     // block on the exact sequential path); bit 1 = some trajectory went non-finite.
     std::vector<int> flags(static_cast<size_t>(nblocks));
     if (nblocks > 0)
-        ck(cudaMemcpyAsync(flags.data(), c.d_nan.p, sizeof(int) * nblocks, cudaMemcpyDeviceToHost, c.stream), "D2H");
-    ck(cudaStreamSynchronize(c.stream), "sampler");
+        ck(cudaMemcpyAsync(flags.data(), c.d_nan.p, sizeof(int) * nblocks, cudaMemcpyDeviceToHost, ss), "D2H");
+    ck(cudaStreamSynchronize(ss), "sampler");
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, c.ev0, c.ev1), "event");
     bool refixed = false;
@@ -579,7 +643,11 @@ int momc_b200_ctx_create(int device, momc_ctx** out, char* err, size_t errlen)
                                       std::to_string(prop.major) + std::to_string(prop.minor));
         auto* c = new momc_ctx();
         c->device = device;
-        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        int least = 0, greatest = 0;
+        ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "stream priorities");
+        ck(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest), "stream");
+        ck(cudaStreamCreateWithPriority(&c->sample_stream, cudaStreamNonBlocking, least), "stream");
+        ck(cudaEventCreateWithFlags(&c->ev_dep, cudaEventDisableTiming), "event");
         cudaMemPool_t pool;
         ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
         uint64_t keep = ~0ull;  // keep freed blocks cached in the pool
@@ -915,6 +983,102 @@ int momc_b200_parsed_pool_get(momc_ctx* ctx, uint32_t* run, uint32_t* weight, ui
     return guarded(err, errlen, [&] {
         bind(*ctx);
         parsed_pool_get(*ctx, run, weight, trajectory, stamps_ns, words);
+    });
+}
+
+int momc_b200_running_reset(momc_ctx* ctx, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        DevArchive& R = running_archive(*ctx);
+        R.F = 0;
+    });
+}
+
+int momc_b200_stream_step(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long long block_begin,
+                          long long block_end, int merge, const double* r, double* hv, int64_t* running_F,
+                          momc_bench_report* rep, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        validate_cfg(cfg);
+        if (ctx->n == 0) usage("no instance set");
+        if (ctx->L < 1) usage("run_sampler needs at least one weight vector");
+        momc_bench_report local{};
+        momc_bench_report* rp = rep ? rep : &local;
+        std::memset(rp, 0, sizeof *rp);
+        using clk = std::chrono::steady_clock;
+        const auto t0 = clk::now();
+        double ss = 0;
+        sample(*ctx, cfg, runs, block_begin, block_end, &ss, true);
+        rp->sampling_s = ss;
+        rp->pool_size = ctx->pool_size;
+        const auto tf = clk::now();
+        DevArchive& a = resident_archive(*ctx);
+        ParetoTimings tm;
+        const bool so = ctx->skip_order;
+        ctx->skip_order = true;  // the run's front is only merged: no archive order
+        try {
+            filter_pool_device(*ctx, ctx->d_words.p, ctx->pool_size, a, &tm);
+        } catch (...) {
+            ctx->skip_order = so;
+            throw;
+        }
+        ctx->skip_order = so;
+        rp->unique_configs = tm.unique_configs;
+        rp->unique_vectors = tm.unique_vectors;
+        rp->archive_size = a.F;
+        if (!merge) {  // the run's front stays in the resident archive (unordered)
+            ck(cudaStreamSynchronize(ctx->stream), "stream front");
+            return;
+        }
+        const long long F = running_merge(*ctx, a.vals.p, a.words.p, a.F, a.K, a.wpc);
+        if (running_F) *running_F = F;
+        if (r && hv) {
+            const DevArchive& R = running_archive(*ctx);
+            *hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, std::vector<double>(r, r + R.K));
+            rp->hv = *hv;
+        }
+        rp->pareto_filtering_s = std::chrono::duration<double>(clk::now() - tf).count();
+        rp->end_to_end_s = std::chrono::duration<double>(clk::now() - t0).count();
+    });
+}
+
+int momc_b200_running_merge_values(momc_ctx* ctx, const double* d_vals, const uint64_t* d_words, int wpc, size_t M,
+                                   int k, const double* r, double* hv, int64_t* running_F, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        const long long F = running_merge(*ctx, d_vals, d_words, static_cast<long long>(M), k, wpc);
+        if (running_F) *running_F = F;
+        if (r && hv) {
+            const DevArchive& R = running_archive(*ctx);
+            *hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, std::vector<double>(r, r + R.K));
+        }
+        ck(cudaStreamSynchronize(ctx->stream), "running merge");
+    });
+}
+
+int momc_b200_archive_device_ptrs(momc_ctx* ctx, const double** vals, const uint64_t** words, int64_t* F)
+{
+    DevArchive& a = resident_archive(*ctx);
+    *vals = a.vals.p;
+    *words = a.words.p;
+    *F = a.F;
+    return MOMC_OK;
+}
+
+int momc_b200_running_to_archive(momc_ctx* ctx, int64_t* out_F, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        DevArchive& R = running_archive(*ctx);
+        DevArchive& a = resident_archive(*ctx);
+        if (R.F == 0) {
+            a.F = 0;
+        } else {  // ordered copy (the filter of a front is the front itself, now in archive order)
+            filter_values_device(*ctx, R.vals.p, R.wpc ? R.words.p : nullptr, R.wpc, ctx->n, R.F, R.K, a, nullptr);
+        }
+        if (out_F) *out_F = a.F;
     });
 }
 

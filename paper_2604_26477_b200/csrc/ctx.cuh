@@ -60,7 +60,10 @@ struct DevBuf {
 
 struct Ctx {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;         // highest priority: everything but the register sampler
+    cudaStream_t sample_stream = nullptr;  // lowest priority: the register sampler (other contexts' Pareto
+                                           // kernels take freed SM slots first)
+    cudaEvent_t ev_dep = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
     long long fallback_blocks = 0;  // sampler blocks re-run on the sequential path
@@ -99,7 +102,9 @@ struct Ctx {
     std::shared_ptr<void> dense_scratch;          // dense.cu working buffers
     int dense_min_n = 256;                        // dense int8 tensor path for dSB at n >= this
     std::shared_ptr<void> csv_scratch;            // csv.cu parsed pool
-    std::shared_ptr<void> archive;                // resident DevArchive (pareto.cuh)
+    std::shared_ptr<void> archive;
+    std::shared_ptr<void> running;                // streaming: running archive (unordered)
+    bool skip_order = false;                      // fronts for internal use: no archive order                // resident DevArchive (pareto.cuh)
 
     ~Ctx();
 };

@@ -794,14 +794,15 @@ void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, 
                                                          nullptr);
     c.launches++;
     s.rank.reserve(static_cast<size_t>(F) + 1);
-    lex_desc_rank(c, fv.p, F, K, s.rank.p);
+    if (!c.skip_order) lex_desc_rank(c, fv.p, F, K, s.rank.p);
     out.F = F;
     out.K = K;
     out.wpc = d_own ? wpc : 0;
     out.vals.reserve(static_cast<size_t>(F) * K + 1);
     if (d_own) out.words.reserve(static_cast<size_t>(F) * wpc + 1);
     k_gather_rows<<<grid_blocks(F), 256, 0, c.stream>>>(fv.p, nullptr, F, K, words, d_own ? fown.p : nullptr, wpc,
-                                                         s.rank.p, out.vals.p, d_own ? out.words.p : nullptr);
+                                                         c.skip_order ? nullptr : s.rank.p, out.vals.p,
+                                                         d_own ? out.words.p : nullptr);
     c.launches++;
     cudaEventRecord(e2, c.stream);
     ck(cudaStreamSynchronize(c.stream), "archive");

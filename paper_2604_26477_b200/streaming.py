@@ -31,87 +31,81 @@ def time_to_target(session, cfg, reference, hv_target: float, max_runs: int, wor
     arithmetic for integer weights) or `max_runs` runs are spent. Returns the number of
     runs / samples used, the wall time (device-synchronised, this rank) and the final HV.
     The caller times the whole call as the end-to-end figure (model build included: every
-    round re-scalarises its weight blocks, pipeline.hpp:337-341)."""
+    round re-scalarises its weight blocks, pipeline.hpp:337-341).
+
+    One GPU: one C-ABI call per run (momc_b200_stream_step: sample -> front -> merge into the
+    context's running archive -> HV). N ranks: each rank's run front is all-gathered (NCCL)
+    and merged into every rank's running archive (momc_b200_running_merge_values)."""
     device = device or torch.device("cuda", torch.cuda.current_device())
     k = session.inst.k()
     per_run = session.num_blocks(cfg, 1)
     samples_per_run = session.L * cfg.batch_size
-    running = None
-    hv = 0.0
-    runs_done = 0
+    session.running_reset()
+    hv, F, runs_done = 0.0, 0, 0
     t0 = time.perf_counter()
     rounds = (max_runs + world - 1) // world
     for q in range(rounds):
         run = q * world + rank
-        session.pipeline(cfg, run + 1, run * per_run, (run + 1) * per_run, do_hv=False)
-        mine = _packed_front(session, device)
-        rows = mdist.allgather_rows(mine) if world > 1 else mine
-        if running is not None:
-            rows = torch.cat([running, rows], dim=0)
-        if world > 1 or running is not None:
+        if world == 1:
+            hv, F, _ = session.stream_step(cfg, run + 1, run * per_run, (run + 1) * per_run, reference)
+        else:
+            session.stream_step(cfg, run + 1, run * per_run, (run + 1) * per_run, None, merge=False)
+            rows = mdist.allgather_rows(_packed_front(session, device))
             vals = rows[:, :k].contiguous().view(torch.float64)
             words = rows[:, k:].contiguous()
-            mdist.merge_on_device(session, vals, words)
-            running = _packed_front(session, device)
-        else:
-            running = rows
+            torch.cuda.current_stream(device).synchronize()
+            hv, F = session.running_merge_values(vals.data_ptr(), words.data_ptr(), words.shape[1], vals.shape[0], k,
+                                                 reference)
         runs_done = (q + 1) * world
-        hv = session.archive_hypervolume(reference)
         if trace is not None:
-            trace.append({"runs": runs_done, "samples": runs_done * samples_per_run, "archive": int(running.shape[0]),
-                          "hv": hv, "wall_s": time.perf_counter() - t0})
+            trace.append({"runs": runs_done, "samples": runs_done * samples_per_run, "archive": F, "hv": hv,
+                          "wall_s": time.perf_counter() - t0})
         if hv == hv_target:
             break
     torch.cuda.synchronize(device)
+    session.running_to_archive()
     return {"reached": hv == hv_target, "runs": runs_done, "samples": runs_done * samples_per_run,
-            "seconds": time.perf_counter() - t0, "hv": hv, "archive": int(running.shape[0]) if running is not None else 0}
+            "seconds": time.perf_counter() - t0, "hv": hv, "archive": F}
 
 
-def time_to_target_overlapped(sessions: list, cfg, reference, hv_target: float, max_runs: int, device=None,
+def time_to_target_overlapped(sessions: list, merger, cfg, reference, hv_target: float, max_runs: int,
                               trace: list | None = None) -> dict:
-    """One GPU, several sessions (contexts: own stream + buffers) in host threads: run r is
-    sampled by session r % S while the previous run's front is filtered / merged on another
-    session's stream, so the Pareto stage hides under the next run's sampler. Merges happen
-    strictly in run order, so the result (runs, samples, archive, HV) equals the sequential
+    """One GPU, several sampling contexts in host threads plus one merging context: run r is
+    sampled and filtered by sessions[r % S] (the register sampler on its low-priority stream)
+    while earlier runs' fronts are merged into `merger`'s running archive on its own stream.
+    Merges happen strictly in run order, so runs / samples / archive / HV equal the sequential
     stream's; only the wall time differs."""
     import threading
 
-    device = device or torch.device("cuda", torch.cuda.current_device())
     S = len(sessions)
+    k = sessions[0].inst.k()
+    wpc = (sessions[0].inst.n() + 63) // 64
     per_run = sessions[0].num_blocks(cfg, 1)
     samples_per_run = sessions[0].L * cfg.batch_size
-    st = {"next": 0, "running": None, "hv": 0.0, "done": False, "runs": 0, "error": None}
+    merger.running_reset()
+    st = {"next": 0, "hv": 0.0, "F": 0, "done": False, "runs": 0, "error": None}
     cv = threading.Condition()
     t0 = time.perf_counter()
 
     def worker(w):
         s = sessions[w]
         try:
-            torch.cuda.set_device(device)
             for run in range(w, max_runs, S):
                 with cv:
                     if st["done"]:
                         return
-                s.pipeline(cfg, run + 1, run * per_run, (run + 1) * per_run, do_hv=False)
-                mine = _packed_front(s, device)
+                s.stream_step(cfg, run + 1, run * per_run, (run + 1) * per_run, None, merge=False)
                 with cv:
                     while st["next"] != run and not st["done"]:
                         cv.wait()
                     if st["done"]:
                         return
-                    if st["running"] is not None:
-                        rows = torch.cat([st["running"], mine], dim=0)
-                        k = s.inst.k()
-                        mdist.merge_on_device(s, rows[:, :k].contiguous().view(torch.float64), rows[:, k:].contiguous())
-                        st["running"] = _packed_front(s, device)
-                    else:
-                        st["running"] = mine
-                    st["hv"] = s.archive_hypervolume(reference)
+                    v, wd, F = s.archive_device_ptrs()
+                    st["hv"], st["F"] = merger.running_merge_values(v, wd, wpc, F, k, reference)
                     st["runs"] = run + 1
                     if trace is not None:
-                        trace.append({"runs": run + 1, "samples": (run + 1) * samples_per_run,
-                                      "archive": int(st["running"].shape[0]), "hv": st["hv"],
-                                      "wall_s": time.perf_counter() - t0})
+                        trace.append({"runs": run + 1, "samples": (run + 1) * samples_per_run, "archive": st["F"],
+                                      "hv": st["hv"], "wall_s": time.perf_counter() - t0})
                     st["next"] = run + 1
                     if st["hv"] == hv_target:
                         st["done"] = True
@@ -129,7 +123,6 @@ def time_to_target_overlapped(sessions: list, cfg, reference, hv_target: float, 
         t.join()
     if st["error"] is not None:
         raise st["error"]
-    torch.cuda.synchronize(device)
+    merger.running_to_archive()
     return {"reached": st["hv"] == hv_target, "runs": st["runs"], "samples": st["runs"] * samples_per_run,
-            "seconds": time.perf_counter() - t0, "hv": st["hv"],
-            "archive": int(st["running"].shape[0]) if st["running"] is not None else 0}
+            "seconds": time.perf_counter() - t0, "hv": st["hv"], "archive": st["F"]}

@@ -126,6 +126,17 @@ def test_streaming_reaches_exact_front_k3(session):
     res = streaming.time_to_target(s, cfg, [float(x) for x in g["reference"]], float(g["hv_star"]), 16,
                                    device=torch.device("cuda", 0), trace=trace)
     assert res["reached"], trace
+    # the overlapped stream (2 sampling contexts + 1 merging context) gives the same result
+    ov = [api.Session(0) for _ in range(2)]
+    for o in ov:
+        o.set_instance(inst)
+        o.set_weights(api.build_weights(3, resolution=21))
+    merger = api.Session(0)
+    merger.set_instance(inst)
+    res2 = streaming.time_to_target_overlapped(ov, merger, cfg, [float(x) for x in g["reference"]],
+                                               float(g["hv_star"]), 16)
+    assert (res2["runs"], res2["hv"], res2["archive"]) == (res["runs"], res["hv"], res["archive"])
+    assert np.array_equal(merger.archive().values, s.archive().values)
     arc = s.archive()
     assert np.array_equal(arc.values, g["values"])
     # owners are the lex-smallest *sampled* configs (either sign of s_0), the exact front's

@@ -34,7 +34,9 @@ def main():
         if S == 1:
             res = streaming.time_to_target(sessions[0], cfg, r, target, 300, device=dev)
         else:
-            res = streaming.time_to_target_overlapped(sessions, cfg, r, target, 300, device=dev)
+            merger = api.Session(0)
+            merger.set_instance(inst)
+            res = streaming.time_to_target_overlapped(sessions, merger, cfg, r, target, 300)
         res["wall"] = time.perf_counter() - t0
         out[f"{it}:sessions{S}"] = {"seconds": round(res["seconds"], 4), "runs": res["runs"]}
         del sessions
