@@ -348,6 +348,32 @@ __global__ void k_suffix_max(uint32_t* S, long long cells, long long stride, int
     }
 }
 
+// the same along the contiguous axis (stride 1): one warp per row, 32 cells per step
+// from the end, an in-warp suffix max (shuffles) carried into the next chunk, so every load
+// is coalesced
+__global__ void k_suffix_max_rows(uint32_t* S, long long rows, int D)
+{
+    const int lane = threadIdx.x & 31;
+    const long long warps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long row = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; row < rows;
+         row += warps) {
+        uint32_t* r = S + row * D;
+        uint32_t carry = 0;
+        for (int base = D - 32; base > -32; base -= 32) {
+            const int a = base + lane;
+            uint32_t v = a >= 0 ? r[a] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_down_sync(0xffffffffu, v, o);
+                if (lane + o < 32) v = max(v, u);
+            }
+            v = max(v, carry);
+            if (a >= 0) r[a] = v;
+            carry = __shfl_sync(0xffffffffu, v, 0);
+        }
+    }
+}
+
 // weak dominance test of every vector (pareto.hpp:49-57): dominated iff a vector in the
 // same cell has a larger last coordinate, or a vector at least as large in all axes and
 // strictly larger in one of the first K-1 has a last coordinate >= this one
@@ -668,7 +694,10 @@ bool build_grid(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, Gr
     ck(cudaMemcpyAsync(s.S.p, s.T.p, sizeof(uint32_t) * cells, cudaMemcpyDeviceToDevice, c.stream), "D2D");
     for (int a = 0; a < K - 1; ++a) {
         if (g.D[a] < 2) continue;
-        k_suffix_max<<<grid_blocks(cells / g.D[a]), 256, 0, c.stream>>>(s.S.p, cells, g.stride[a], g.D[a]);
+        if (g.stride[a] == 1)
+            k_suffix_max_rows<<<grid_blocks(cells / g.D[a] * 32), 256, 0, c.stream>>>(s.S.p, cells / g.D[a], g.D[a]);
+        else
+            k_suffix_max<<<grid_blocks(cells / g.D[a]), 256, 0, c.stream>>>(s.S.p, cells, g.stride[a], g.D[a]);
         c.launches++;
     }
     return true;
