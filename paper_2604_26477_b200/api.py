@@ -1032,8 +1032,12 @@ class BenchResult:
 
 
 def bench(inst: MultiObjectiveInstance, weights, config: SolverConfig, runs: int = 1, ref_count: int = 1000,
-          fixed_reference=None, keep_pool: bool = True, session: Session | None = None) -> BenchResult:
-    """pipeline.hpp:309-393 on the GPU: scalarise -> sample -> filter -> reference -> HV."""
+          fixed_reference=None, keep_pool: bool = True, session: Session | None = None,
+          pool_out=None) -> BenchResult:
+    """pipeline.hpp:309-393 on the GPU: scalarise -> sample -> filter -> reference -> HV.
+
+    ``pool_out``: optional preallocated (ideally page-locked) uint64 array of M x wpc words
+    that receives the pool; the returned SamplePool then views it."""
     config.validate()
     if runs < 1:
         raise InvalidArgument("runs must be >= 1")
@@ -1042,7 +1046,12 @@ def bench(inst: MultiObjectiveInstance, weights, config: SolverConfig, runs: int
     L = nums.shape[0]
     M = runs * L * config.batch_size
     wpc = (inst.n() + 63) // 64
-    words = np.zeros((M, wpc), np.uint64) if keep_pool else None
+    if keep_pool and pool_out is not None:
+        words = np.asarray(pool_out).view(np.uint64).reshape(M, wpc)
+        if not words.flags["C_CONTIGUOUS"]:
+            raise InvalidArgument("pool_out must be contiguous")
+    else:
+        words = np.empty((M, wpc), np.uint64) if keep_pool else None
     rep = _lib.BenchReportC()
     cfg = config.c()
     v = inst.view()
