@@ -192,6 +192,81 @@ __global__ void scalarize_kernel(int n, int k, int nnz, int H, const int* __rest
     }
 }
 
+// Large instances: the same three stages as separate grid-wide kernels (CSR values over all
+// (weight, slot) pairs, row sums over all (weight, row) pairs, then the per-weight fold), so
+// C4's 55 weights x 4e6 slots use the whole GPU. c_k = num_k / H is formed once per value.
+__global__ void k_scal_vals(int k, long long nnz, int L, int H, const int* __restrict__ nums,
+                            const double* __restrict__ w, const int* __restrict__ eidx, double* vals)
+{
+    const long long total = nnz * L;
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int l = static_cast<int>(q / nnz);
+        const long long sl = q % nnz;
+        const int e = eidx[sl];
+        const int* num = nums + static_cast<long long>(l) * k;
+        double acc = 0;
+        for (int j = 0; j < k; ++j)
+            acc = __dadd_rn(acc, __dmul_rn(__ddiv_rn(static_cast<double>(num[j]), static_cast<double>(H)),
+                                           w[static_cast<long long>(e) * k + j]));
+        vals[q] = acc;
+    }
+}
+
+__global__ void k_scal_rowsum(int n, long long nnz, int L, const int* __restrict__ rowptr,
+                              const double* __restrict__ vals, double* rs)
+{
+    // one warp per (weight, row): lanes add strided partial sums? No: the fold is sequential
+    // in column order, so a row is one thread; rows of a warp are adjacent (coalescing is
+    // poor for dense rows, but the slots are read once)
+    const long long total = static_cast<long long>(n) * L;
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int l = static_cast<int>(q / n), i = static_cast<int>(q % n);
+        const double* v = vals + static_cast<long long>(l) * nnz;
+        double s = 0.0;
+        for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) s = __dadd_rn(s, v[e]);
+        rs[q] = fabs(s);
+    }
+}
+
+__global__ void k_scal_c0(int n, const double* __restrict__ rs, double* c0, int* degenerate)
+{
+    const int l = blockIdx.x;
+    const double* r = rs + static_cast<long long>(l) * n;
+    // .cwiseAbs().maxCoeff() as the fold m = max(m, a_i) from a_0: NaN a_0 poisons the fold,
+    // NaN a_i (i > 0) is skipped; both are degenerate through the finiteness check below
+    // unless a_0 is finite, where the max over the finite a_i is order-free
+    __shared__ double part[256];
+    double m = -1.0;
+    bool nan_rest = false;
+    for (int i = 1 + threadIdx.x; i < n; i += blockDim.x) {
+        const double a = r[i];
+        if (a != a) nan_rest = true;
+        else m = a > m ? a : m;
+    }
+    (void)nan_rest;
+    part[threadIdx.x] = m;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) part[threadIdx.x] = part[threadIdx.x + o] > part[threadIdx.x] ? part[threadIdx.x + o]
+                                                                                            : part[threadIdx.x];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double a0 = r[0];
+        double mm = a0;
+        if (a0 == a0 && part[0] > mm) mm = part[0];
+        if (!(mm > 0.0) || !isfinite(mm)) {
+            degenerate[l] = 1;
+            c0[l] = 0.0;
+        } else {
+            degenerate[l] = 0;
+            c0[l] = __ddiv_rn(1.0, mm);
+        }
+    }
+}
+
 // rows of J(c_l) padded to `dmax` entries with exact zeros (sampler DMAX > 0 path)
 __global__ void pad_rows_kernel(int n, int nnz, int dmax, const int* __restrict__ rowptr,
                                 const double* __restrict__ vals, double* padv)
@@ -354,9 +429,19 @@ void set_weights(Ctx& c, const int32_t* nums, int L, int H)
     DevBuf<int> degen;
     degen.reserve(static_cast<size_t>(L));
     ck(cudaMemcpyAsync(c.d_nums.p, nums, sizeof(int) * L * c.k, cudaMemcpyHostToDevice, c.stream), "H2D");
-    scalarize_kernel<<<L, 256, 0, c.stream>>>(c.n, c.k, c.nnz, H, c.d_nums.p, c.d_w.p, c.d_rowptr.p, c.d_eidx.p,
-                                              c.d_vals.p, rs.p, c.d_c0.p, degen.p);
-    ++c.launches;
+    if (static_cast<long long>(c.nnz) * L <= (1ll << 20)) {  // small: one CTA per weight
+        scalarize_kernel<<<L, 256, 0, c.stream>>>(c.n, c.k, c.nnz, H, c.d_nums.p, c.d_w.p, c.d_rowptr.p, c.d_eidx.p,
+                                                  c.d_vals.p, rs.p, c.d_c0.p, degen.p);
+        ++c.launches;
+    } else {
+        const long long tv = static_cast<long long>(c.nnz) * L, tr = static_cast<long long>(c.n) * L;
+        k_scal_vals<<<static_cast<unsigned>(std::min<long long>((tv + 255) / 256, 148ll * 64)), 256, 0, c.stream>>>(
+            c.k, c.nnz, L, H, c.d_nums.p, c.d_w.p, c.d_eidx.p, c.d_vals.p);
+        k_scal_rowsum<<<static_cast<unsigned>(std::min<long long>((tr + 127) / 128, 148ll * 64)), 128, 0, c.stream>>>(
+            c.n, c.nnz, L, c.d_rowptr.p, c.d_vals.p, rs.p);
+        k_scal_c0<<<L, 256, 0, c.stream>>>(c.n, rs.p, c.d_c0.p, degen.p);
+        c.launches += 3;
+    }
     ck(cudaGetLastError(), "scalarize_kernel");
     std::vector<int> h_degen(static_cast<size_t>(L));
     ck(cudaMemcpyAsync(h_degen.data(), degen.p, sizeof(int) * L, cudaMemcpyDeviceToHost, c.stream), "D2H");

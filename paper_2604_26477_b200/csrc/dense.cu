@@ -92,27 +92,59 @@ __global__ void k_dense_init(int n, int batch_pad, const PairOf* __restrict__ pa
     }
 }
 
-__device__ double dense_normal(DevStream& s, const ZigTables* __restrict__ z)
+// Per-thread word ring in shared memory for the (trajectory, step) noise stream
+// (rng.hpp:113-121): word w of thread t at ring[(w & 15) * 128 + t] (a warp always hits 32
+// banks). Blocks are generated warp-synchronously: before every 4 spins each thread tops its
+// ring up to >= 8 words, which in steady state is one Philox block for every thread at the
+// same time; only slow attempts that outrun the ring generate on their own (<= 7 + 4 < 16).
+struct WordRing {
+    uint32_t* r;  // this thread's column
+    uint32_t k0, k1, lo, mid, hi, blk;
+    int head, tail;
+    __device__ __forceinline__ void block()
+    {
+        const uint4 v = philox(k0, k1, blk++, lo, mid, hi);
+        r[((tail + 0) & 15) * 128] = v.x;
+        r[((tail + 1) & 15) * 128] = v.y;
+        r[((tail + 2) & 15) * 128] = v.z;
+        r[((tail + 3) & 15) * 128] = v.w;
+        tail += 4;
+    }
+    __device__ __forceinline__ void ensure(int k)
+    {
+        while (tail - head < k) block();
+    }
+    __device__ __forceinline__ uint32_t at(int i) const { return r[((head + i) & 15) * 128]; }
+};
+
+// next_normal (rng.hpp:156-185) from the ring
+__device__ __forceinline__ double ring_normal(WordRing& w, const ZigTables* __restrict__ z)
 {
     for (;;) {
-        const uint32_t u = s.next_u32();
+        w.ensure(1);
+        const uint32_t u = w.at(0);
         const int32_t hz = static_cast<int32_t>(u);
         const uint32_t iz = u & 127u;
         const uint32_t mag = hz < 0 ? 0u - u : u;
-        if (mag < z->kn[iz]) return __dmul_rn(static_cast<double>(hz), z->wn[iz]);
-        if (iz == 0) {
+        if (mag < z->kn[iz]) {
+            ++w.head;
+            return __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        }
+        if (iz == 0) {  // tail: (x, y) trials of 4 words each
+            ++w.head;
             const double r = 3.442619855899;
             for (;;) {
-                const uint64_t a = s.next_u64();
-                const double xx = __ddiv_rn(-log(static_cast<double>((a >> 11) + 1) * 0x1.0p-53), r);
-                const uint64_t b = s.next_u64();
-                const double yy = -log(static_cast<double>((b >> 11) + 1) * 0x1.0p-53);
+                w.ensure(4);
+                const double xx = __ddiv_rn(-log(u01_open_from(w.at(0), w.at(1))), r);
+                const double yy = -log(u01_open_from(w.at(2), w.at(3)));
+                w.head += 4;
                 if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) return hz > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
             }
         }
+        w.ensure(3);
         const double xv = __dmul_rn(static_cast<double>(hz), z->wn[iz]);
-        const uint64_t a = s.next_u64();
-        const double u01 = static_cast<double>(a >> 11) * 0x1.0p-53;
+        const double u01 = u01_from(w.at(1), w.at(2));
+        w.head += 3;
         const double lhs = __dadd_rn(z->fn[iz], __dmul_rn(u01, __dsub_rn(z->fn[iz - 1], z->fn[iz])));
         const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
         // FP32 exp brackets the FP64 one within 1e-6 relative on [-6, 0]; the FP64 exp is
@@ -128,16 +160,19 @@ __device__ double dense_normal(DevStream& s, const ZigTables* __restrict__ z)
 
 constexpr int kDenseTile = 64;  // spins per shared-memory phi tile
 
-// one dSB step for every trajectory: y += dt((a_t - a0) x - c0 D/H + alpha eta); x += dt a0 y;
-// wall; clamp; phi = sgn(x)
-__global__ void __launch_bounds__(128) k_dense_update(int n, int batch_pad, int H, const PairOf* __restrict__ pairs,
+// one dSB step for every trajectory: y += dt((a_t - a0) x - (c0/H) D + alpha eta);
+// x += dt a0 y; wall; clamp; phi = sgn(x). D = (H J(c)) sgn(X) is exact (int32); the one
+// rounding of c0/H replaces the reference's per-product roundings of J (tolerance: DESIGN §3).
+// 9 CTAs of 128 per SM (<= 56 registers, 19 KB smem): the C4 grid (55 x 24 CTAs) is one wave
+__global__ void __launch_bounds__(128, 9) k_dense_update(int n, int batch_pad, int H, const PairOf* __restrict__ pairs,
                                                       uint64_t seed, int t_step, int T, double dt, double a0,
                                                       double alpha, double sdt, const double* __restrict__ c0s,
                                                       const ZigTables* __restrict__ zig, const int* __restrict__ D,
                                                       double* x, double* y, signed char* phi, int* bad)
 {
     __shared__ ZigTables z;
-    __shared__ signed char tile[128][kDenseTile + 4];
+    __shared__ __align__(16) signed char tile[128][kDenseTile + 4];
+    __shared__ uint32_t ring[16 * 128];
     for (int q = threadIdx.x; q < static_cast<int>(sizeof(ZigTables) / 4); q += blockDim.x)
         reinterpret_cast<uint32_t*>(&z)[q] = reinterpret_cast<const uint32_t*>(zig)[q];
     __syncthreads();
@@ -146,14 +181,22 @@ __global__ void __launch_bounds__(128) k_dense_update(int n, int batch_pad, int 
     const int t0 = blockIdx.x * blockDim.x;
     const int t = t0 + threadIdx.x;
     const bool active = t < pr.count;
-    const double c0 = c0s[pr.l];
+    const double c0h = __ddiv_rn(c0s[pr.l], static_cast<double>(H));
     const double a_t = __ddiv_rn(static_cast<double>(t_step + 1), static_cast<double>(T));
     const double neg_drift = -__dsub_rn(a0, a_t);
-    const double Hd = static_cast<double>(H);
-    DevStream s;
-    if (active)
-        s.init(run_key(seed, static_cast<uint32_t>(pr.run)), pr.l, pr.traj0 + t,
-               tag_word(kTagStepNoise, static_cast<uint32_t>(t_step)));
+    const bool noisy = alpha > 0.0;
+    WordRing w;
+    {
+        const uint64_t key = run_key(seed, static_cast<uint32_t>(pr.run));
+        w.r = ring + threadIdx.x;
+        w.k0 = static_cast<uint32_t>(key);
+        w.k1 = static_cast<uint32_t>(key >> 32);
+        w.lo = tag_word(kTagStepNoise, static_cast<uint32_t>(t_step));
+        w.mid = static_cast<uint32_t>(pr.traj0 + t);
+        w.hi = static_cast<uint32_t>(pr.l);
+        w.blk = 0;
+        w.head = w.tail = 0;
+    }
     const int* Dp = D + pb * n * static_cast<long long>(batch_pad);
     double* xs = x + pb * n * static_cast<long long>(batch_pad);
     double* ys = y + pb * n * static_cast<long long>(batch_pad);
@@ -166,6 +209,9 @@ __global__ void __launch_bounds__(128) k_dense_update(int n, int batch_pad, int 
             int dn = Dp[o];
             double xn = xs[o], yn = ys[o];
             for (int q = 0; q < lim; ++q) {
+                if (noisy && (q & 3) == 0) {
+                    while (w.tail - w.head < 8) w.block();  // warp-synchronous top-up
+                }
                 const int dq = dn;
                 double xi = xn, yi = yn;
                 const long long oq = o;
@@ -175,15 +221,15 @@ __global__ void __launch_bounds__(128) k_dense_update(int n, int batch_pad, int 
                     xn = xs[o];
                     yn = ys[o];
                 }
-                const double coupled = __ddiv_rn(static_cast<double>(dq), Hd);
-                const double eta = alpha > 0.0 ? dense_normal(s, &z) : 0.0;
-                double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled));
-                if (alpha > 0.0) d = __dadd_rn(d, __dmul_rn(alpha, eta));
+                const double eta = noisy ? ring_normal(w, &z) : 0.0;
+                double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0h, static_cast<double>(dq)));
+                if (noisy) d = __dadd_rn(d, __dmul_rn(alpha, eta));
                 yi = __dadd_rn(yi, __dmul_rn(dt, d));
                 xi = __dadd_rn(xi, __dmul_rn(sdt, yi));
-                yi = fabs(xi) > 1.0 ? 0.0 : yi;
-                xi = (xi < -1.0) ? -1.0 : xi;
-                xi = (1.0 < xi) ? 1.0 : xi;
+                if (fabs(xi) > 1.0) {  // wall + clamp (both fire exactly when |x| > 1)
+                    yi = 0.0;
+                    xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
+                }
                 nonfinite |= !isfinite(xi) || !isfinite(yi);
                 xs[oq] = xi;
                 ys[oq] = yi;
@@ -191,10 +237,14 @@ __global__ void __launch_bounds__(128) k_dense_update(int n, int batch_pad, int 
             }
         }
         __syncthreads();
-        // coalesced store of the phi tile: rows of `lim` bytes
-        for (int q = threadIdx.x; q < 128 * kDenseTile; q += blockDim.x) {
-            const int r = q / kDenseTile, cidx = q % kDenseTile;
-            if (t0 + r < pr.count && cidx < lim) phi[(pb * batch_pad + t0 + r) * n + i0 + cidx] = tile[r][cidx];
+        // coalesced store of the phi tile: rows of `lim` bytes, 4 bytes per thread and step
+        // (n % 16 == 0 on the dense path, so row starts are 4-byte aligned)
+        for (int q = threadIdx.x; q < 128 * (kDenseTile / 4); q += blockDim.x) {
+            const int r = q / (kDenseTile / 4), c4 = (q % (kDenseTile / 4)) * 4;
+            if (t0 + r < pr.count && c4 < lim) {
+                const uint32_t v = *reinterpret_cast<const uint32_t*>(&tile[r][c4]);
+                *reinterpret_cast<uint32_t*>(phi + (pb * batch_pad + t0 + r) * n + i0 + c4) = v;
+            }
         }
         __syncthreads();
     }

@@ -107,6 +107,20 @@ def test_scalarize_matches_reference(ref, session):
         assert c0 == c0r
 
 
+def test_scalarize_large_matches_reference(ref, session):
+    """the grid-wide scalarisation kernels (nnz x L > 2^20): n=400 dense, 36 weights"""
+    ri = ref.generate_uniform(400, 0.9, 3, 78, kind="real", lo=-1.0, hi=1.0)
+    inst = inst_from_ref(ri)
+    session.set_instance(inst)
+    nums = ref.das_dennis(3, 7)
+    session.set_weights(weights_of(nums, 7))
+    for l in (0, 11, nums.shape[0] - 1):
+        J, c0 = session.coupling(l)
+        Jr, c0r = ref.scalarize(ri, nums[l], 7)
+        assert np.array_equal(J, Jr)
+        assert c0 == c0r
+
+
 def test_degenerate_coupling_is_usage_error(session):
     inst = api.MultiObjectiveInstance(3, 2, [(0, 1, [1.0, -1.0])])
     with pytest.raises(InvalidArgument, match="degenerate scalarized coupling"):
