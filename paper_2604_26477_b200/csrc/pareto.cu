@@ -703,6 +703,155 @@ bool build_grid(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, Gr
     return true;
 }
 
+// ---- sieve front for large value sets the compressed grid cannot hold: a front F0 of a
+// good sample (the rows with the largest objective sums) kills most rows; the front of the
+// survivors is the front. Exact whatever the sample: a dominated row is dominated by a
+// front row, which either lies in F0 (the row is killed) or survives (pairwise removes it).
+__global__ void k_sum_keys(const double* __restrict__ vals, long long V, int K, unsigned long long* keys, uint32_t* idx)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        double sum = 0.0;
+        for (int k = 0; k < K; ++k) sum += vals[i * K + k];
+        const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(sum == 0.0 ? 0.0 : sum));
+        keys[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+        idx[i] = static_cast<uint32_t>(i);
+    }
+}
+
+__global__ void k_gather_vals_idx(const double* __restrict__ vals, const uint32_t* __restrict__ idx, long long n, int K,
+                                  double* out)
+{
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n * K;
+         q += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[q] = vals[static_cast<long long>(idx[q / K]) * K + q % K];
+}
+
+// alive[i] = no row of F (nF x K, staged in shared memory) dominates row i
+__global__ void k_kill(const double* __restrict__ vals, long long V, int K, const double* __restrict__ F, int nF,
+                       unsigned char* alive)
+{
+    extern __shared__ double fs[];
+    for (int q = threadIdx.x; q < nF * K; q += blockDim.x) fs[q] = F[q];
+    __syncthreads();
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        double mine[kMaxK];
+        for (int k = 0; k < K; ++k) mine[k] = vals[i * K + k];
+        bool dom = false;
+        for (int f = 0; f < nF && !dom; ++f) {
+            bool ge = true, gt = false;
+            for (int k = 0; k < K; ++k) {
+                ge &= fs[f * K + k] >= mine[k];
+                gt |= fs[f * K + k] > mine[k];
+            }
+            dom = ge && gt;
+        }
+        alive[i] = !dom;
+    }
+}
+
+__global__ void k_scatter_keep(const uint32_t* __restrict__ idx, const unsigned char* __restrict__ sub_keep, long long n,
+                               unsigned char* keep)
+{
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<long long>(gridDim.x) * blockDim.x)
+        keep[idx[q]] = sub_keep[q];
+}
+
+__global__ void k_map_u32(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ map, long long n, uint32_t* out);
+
+__global__ void k_compact_flags(const unsigned char* __restrict__ f, long long V, uint32_t* out, unsigned long long* count)
+{
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x); i0 < V;
+         i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        const bool on = i < V && f[i];
+        const unsigned b = __ballot_sync(0xffffffffu, on);
+        unsigned long long base = 0;
+        if ((threadIdx.x & 31) == 0 && b) base = atomicAdd(count, static_cast<unsigned long long>(__popc(b)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (on) out[base + __popc(b & ((1u << (threadIdx.x & 31)) - 1))] = static_cast<uint32_t>(i);
+    }
+}
+
+// rows `idx` (n of them) -> keep flags of their pairwise front (sub_keep, n)
+void pairwise_subset(Ctx& c, const double* d_vals, const uint32_t* idx, long long n, int K, unsigned char* sub_keep)
+{
+    DevBuf<double> sub;
+    sub.reserve(static_cast<size_t>(n) * K + 1);
+    k_gather_vals_idx<<<grid_blocks(n * K), 256, 0, c.stream>>>(d_vals, idx, n, K, sub.p);
+    k_pairwise<<<grid_blocks(n), 256, 256 * K * sizeof(double), c.stream>>>(sub.p, n, K, sub_keep);
+    c.launches += 2;
+    ck(cudaStreamSynchronize(c.stream), "pairwise subset");
+    sub.release();
+}
+
+void sieve_front(Ctx& c, Scratch& s, const double* d_vals, long long V, int K)
+{
+    const long long B = std::min<long long>(V, 8192);
+    DevBuf<unsigned long long> ka, kb;
+    DevBuf<uint32_t> ia, ib, fidx, sidx;
+    DevBuf<unsigned char> fkeep, alive, skeep, tmp;
+    ka.reserve(static_cast<size_t>(V));
+    kb.reserve(static_cast<size_t>(V));
+    ia.reserve(static_cast<size_t>(V));
+    ib.reserve(static_cast<size_t>(V));
+    k_sum_keys<<<grid_blocks(V), 256, 0, c.stream>>>(d_vals, V, K, ka.p, ia.p);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, ka.p, kb.p, ia.p, ib.p, static_cast<int>(V), 0, 64, c.stream);
+    tmp.reserve(tb + 1);
+    ck(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, ka.p, kb.p, ia.p, ib.p, static_cast<int>(V), 0, 64,
+                                                 c.stream),
+       "sort");
+    c.launches += 2;
+    // F0 = front of the B rows with the largest sums
+    fkeep.reserve(static_cast<size_t>(B));
+    pairwise_subset(c, d_vals, ib.p, B, K, fkeep.p);
+    s.counters.reserve(8);
+    ck(cudaMemsetAsync(s.counters.p + 3, 0, sizeof(unsigned long long), c.stream), "memset");
+    fidx.reserve(static_cast<size_t>(B));
+    k_compact_flags<<<grid_blocks(B), 256, 0, c.stream>>>(fkeep.p, B, fidx.p, s.counters.p + 3);
+    c.launches++;
+    const long long nF0 = static_cast<long long>(read_counter(c, s.counters.p + 3));
+    // positions in the sorted order -> row ids, then the F0 rows themselves
+    DevBuf<uint32_t> f0rows;
+    f0rows.reserve(static_cast<size_t>(nF0) + 1);
+    k_map_u32<<<grid_blocks(nF0), 256, 0, c.stream>>>(fidx.p, ib.p, nF0, f0rows.p);
+    DevBuf<double> f0;
+    f0.reserve(static_cast<size_t>(nF0) * K + 1);
+    k_gather_vals_idx<<<grid_blocks(nF0 * K), 256, 0, c.stream>>>(d_vals, f0rows.p, nF0, K, f0.p);
+    c.launches += 2;
+    // kill every row dominated by F0 (F0 staged in shared memory when it fits)
+    alive.reserve(static_cast<size_t>(V));
+    const size_t fbytes = static_cast<size_t>(nF0) * K * sizeof(double);
+    if (fbytes <= 160 * 1024) {
+        if (fbytes > 48 * 1024)
+            ck(cudaFuncSetAttribute(k_kill, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fbytes)),
+               "smem");
+        k_kill<<<grid_blocks(V), 256, fbytes, c.stream>>>(d_vals, V, K, f0.p, static_cast<int>(nF0), alive.p);
+    } else {  // F0 too large to stage: plain pairwise over everything
+        k_pairwise<<<grid_blocks(V), 256, 256 * K * sizeof(double), c.stream>>>(d_vals, V, K, s.keep.p);
+        c.launches++;
+        return;
+    }
+    c.launches++;
+    ck(cudaMemsetAsync(s.counters.p + 3, 0, sizeof(unsigned long long), c.stream), "memset");
+    sidx.reserve(static_cast<size_t>(V));
+    k_compact_flags<<<grid_blocks(V), 256, 0, c.stream>>>(alive.p, V, sidx.p, s.counters.p + 3);
+    c.launches++;
+    const long long nS = static_cast<long long>(read_counter(c, s.counters.p + 3));
+    skeep.reserve(static_cast<size_t>(nS) + 1);
+    pairwise_subset(c, d_vals, sidx.p, nS, K, skeep.p);
+    ck(cudaMemsetAsync(s.keep.p, 0, static_cast<size_t>(V), c.stream), "memset");
+    k_scatter_keep<<<grid_blocks(nS), 256, 0, c.stream>>>(sidx.p, skeep.p, nS, s.keep.p);
+    c.launches++;
+    for (auto* b : {&ka, &kb}) b->release();
+    for (auto* b : {&ia, &ib, &fidx, &sidx, &f0rows}) b->release();
+    for (auto* b : {&fkeep, &alive, &skeep, &tmp}) b->release();
+    f0.release();
+}
+
 // front of V distinct vectors (device rows); keep[i] set for non-dominated rows
 int front_keep(Ctx& c, Scratch& s, const double* d_vals, long long V, int K)
 {
@@ -715,6 +864,10 @@ int front_keep(Ctx& c, Scratch& s, const double* d_vals, long long V, int K)
             c.launches++;
             return 1;
         }
+    }
+    if (V > 16384) {  // the sieve: a good sample's front kills most rows first
+        sieve_front(c, s, d_vals, V, K);
+        return 3;
     }
     k_pairwise<<<grid_blocks(V), 256, 256 * K * sizeof(double), c.stream>>>(d_vals, V, K, s.keep.p);
     c.launches++;

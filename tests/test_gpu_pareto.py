@@ -104,6 +104,17 @@ def test_filter_values_matches_reference(ref, session, k):
     assert np.array_equal(got.values, want.values)
 
 
+@pytest.mark.parametrize("k,V", [(3, 60000), (4, 40000)])
+def test_filter_values_sieve_matches_reference(ref, session, k, V):
+    """continuous values: the compressed grid does not fit (> 32768 distinct per axis), so
+    the sieve (front of the largest-sum sample kills, pairwise on the survivors) runs"""
+    rng = np.random.default_rng(V + k)
+    vals = rng.normal(size=(V, k)) + rng.normal(size=(V, 1))  # correlated: a non-trivial front
+    got = api.non_dominated_filter([ObjectiveVector(list(v), Sense.cut) for v in vals], session=session)
+    want = ref.filter_values(vals)
+    assert np.array_equal(got.values, want.values)
+
+
 def test_filter_values_hamiltonian_sense(ref, session):
     vals = grid_vectors(3000, 3, 77)
     got = api.non_dominated_filter([ObjectiveVector(v, Sense.hamiltonian) for v in vals], session=session)
