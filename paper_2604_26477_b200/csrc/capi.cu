@@ -300,6 +300,7 @@ void validate_cfg(const momc_solver_cfg* c)
 
 void set_instance(Ctx& c, const momc_instance_view* iv)
 {
+    ++c.inst_gen;
     // MultiObjectiveInstance ctor (instance.hpp:104-123)
     if (iv->n < 1) usage("vertex count must be positive");
     if (iv->k < 1) usage("objective count must be positive");

@@ -71,6 +71,7 @@ struct Ctx {
 
     // instance
     int n = 0, k = 0, m = 0, nnz = 0;
+    long long inst_gen = 0;  // bumped by every set_instance (caches keyed on the instance)
     bool integer_weights = false;  // every weight integral and sum |w| < 2^31 (exact int32 cut path)
     std::vector<int> h_ei, h_ej;
     std::vector<double> h_w;

@@ -358,13 +358,15 @@ struct DenseScratch {
     DevBuf<PairOf> pairs;
     int hj_L = -1, hj_n = 0;
     const void* hj_key = nullptr;
+    DevBuf<signed char> wk;  // the K weight layers as dense int8 (evaluate_cuts), per instance
+    long long wk_gen = -1;
 };
 
 DenseScratch& dscratch(Ctx& c)
 {
     if (!c.dense_scratch) c.dense_scratch = std::shared_ptr<void>(new DenseScratch(), [](void* p) {
         auto* d = static_cast<DenseScratch*>(p);
-        d->hj.release(); d->phi.release(); d->s8.release(); d->D.release(); d->flags.release();
+        d->hj.release(); d->phi.release(); d->s8.release(); d->D.release(); d->flags.release(); d->wk.release();
         d->x.release(); d->y.release(); d->pairs.release();
         delete d;
     });
@@ -505,14 +507,38 @@ __global__ void k_build_layer(int n, int k, int layer, const int* __restrict__ r
 }
 
 // out[u*K + layer] = 0.5 * (W - 0.5 * sum_i s_u[i] * D[i][u])
-__global__ void k_cut_from_gemm(const int* __restrict__ D, const signed char* __restrict__ s, int cnt, int ld, int n,
-                                int K, int layer, double W, long long U0, double* out)
+// h_u = s_u . (W_k s_u): D[i][u] = (W_k s_u)_i from the GEMM; s_u from the packed words
+// (bit i set = +1). A CTA of 256 threads takes 32 configs x 8 slices of the spin range (the
+// slices' partial sums meet in shared memory): coalesced D loads, 8x the memory parallelism
+// of one thread per config.
+__global__ void __launch_bounds__(256) k_cut_from_gemm(const int* __restrict__ D, const uint64_t* __restrict__ words,
+                                                       const uint32_t* __restrict__ idx, int cnt, int ld, int n,
+                                                       int wpc, int K, int layer, double W, long long U0, double* out)
 {
-    const int u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= cnt) return;
+    __shared__ long long part[8][32];
+    const int ul = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const int u = blockIdx.x * 32 + ul;
     long long h = 0;
-    for (int i = 0; i < n; ++i) h += static_cast<long long>(s[static_cast<long long>(u) * n + i]) * D[static_cast<long long>(i) * ld + u];
-    out[(U0 + u) * K + layer] = 0.5 * (W - 0.5 * static_cast<double>(h));
+    if (u < cnt) {
+        const long long row = idx ? idx[U0 + u] : U0 + u;
+        const uint64_t* wr = words + row * wpc;
+        const int len = (n + 7) / 8;
+        const int i0 = sl * len, i1 = min(n, i0 + len);
+        uint64_t wv = i0 < i1 ? wr[i0 >> 6] : 0ull;
+#pragma unroll 4
+        for (int i = i0; i < i1; ++i) {
+            if ((i & 63) == 0) wv = wr[i >> 6];
+            const int dv = D[static_cast<long long>(i) * ld + u];
+            h += ((wv >> (i & 63)) & 1ull) ? dv : -dv;
+        }
+    }
+    part[sl][ul] = h;
+    __syncthreads();
+    if (sl == 0 && u < cnt) {
+        long long t = 0;
+        for (int q = 0; q < 8; ++q) t += part[q][ul];
+        out[(U0 + u) * K + layer] = 0.5 * (W - 0.5 * static_cast<double>(t));
+    }
 }
 
 bool eval_gemm_ok(const Ctx& c)
@@ -528,15 +554,22 @@ void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, 
     DenseScratch& d = dscratch(c);
     const int n = c.n, K = c.k, wpc = (n + 63) / 64;
     const int chunk = 16384;
-    d.s8.reserve(static_cast<size_t>(chunk) * n + static_cast<size_t>(n) * n);
+    d.s8.reserve(static_cast<size_t>(chunk) * n);
     d.D.reserve(static_cast<size_t>(chunk) * n);
-    signed char* Wk = d.s8.p + static_cast<size_t>(chunk) * n;
+    if (d.wk_gen != c.inst_gen) {  // dense int8 layers, built once per instance
+        d.wk.reserve(static_cast<size_t>(K) * n * n);
+        for (int layer = 0; layer < K; ++layer) {
+            k_build_layer<<<n, 256, 0, c.stream>>>(n, K, layer, c.d_rowptr.p, c.d_col.p, c.d_eidx.p, c.d_wi.p,
+                                                   d.wk.p + static_cast<size_t>(layer) * n * n);
+            c.launches++;
+        }
+        d.wk_gen = c.inst_gen;
+    }
     std::vector<double> W(static_cast<size_t>(K), 0.0);
     for (int e = 0; e < c.m; ++e)
         for (int q = 0; q < K; ++q) W[static_cast<size_t>(q)] += c.h_w[static_cast<size_t>(e) * K + q];
     for (int layer = 0; layer < K; ++layer) {
-        k_build_layer<<<n, 256, 0, c.stream>>>(n, K, layer, c.d_rowptr.p, c.d_col.p, c.d_eidx.p, c.d_wi.p, Wk);
-        c.launches++;
+        const signed char* Wk = d.wk.p + static_cast<size_t>(layer) * n * n;
         for (long long u0 = 0; u0 < U; u0 += chunk) {
             const int cnt = static_cast<int>(std::min<long long>(chunk, U - u0));
             const int cntp = (cnt + 15) / 16 * 16;
@@ -546,8 +579,8 @@ void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, 
                    "memset");
             c.launches++;
             gemm_i8_batched(c, d.gemm, cntp, n, n, d.s8.p, 0, Wk, 0, d.D.p, 0, 1);
-            k_cut_from_gemm<<<(cnt + 127) / 128, 128, 0, c.stream>>>(d.D.p, d.s8.p, cnt, cntp, n, K, layer,
-                                                                      W[static_cast<size_t>(layer)], u0, d_out);
+            k_cut_from_gemm<<<(cnt + 31) / 32, 256, 0, c.stream>>>(d.D.p, d_words, d_idx, cnt, cntp, n, wpc, K,
+                                                                    layer, W[static_cast<size_t>(layer)], u0, d_out);
             c.launches++;
         }
     }
