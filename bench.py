@@ -221,10 +221,18 @@ def main():
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    # functional check of the multi-rank path on a one-GPU box: MOMC_BENCH_DEVICE pins every
+    # rank to one device and MOMC_DIST_BACKEND=gloo replaces NCCL (never used for numbers)
+    if os.environ.get("MOMC_BENCH_DEVICE") is not None:
+        local = env_int("MOMC_BENCH_DEVICE", 0)
+    backend = os.environ.get("MOMC_DIST_BACKEND", "nccl")
     warmup = max(args.warmup, 3)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     inst = load_heavy_hex(4)
     weights = api.build_weights(4, resolution=13)
@@ -258,6 +266,11 @@ def main():
             rep["archive_size"] = s.archive_size()
         return rep
 
+    def max_over_ranks(v: float) -> float:
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     def sync_all():
         torch.cuda.synchronize(local)
         if world > 1:
@@ -287,9 +300,7 @@ def main():
     launches = (s.launches() - launches0) // max(args.steps, 1)
     total_ms = float(np.sum(step_ms))
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / args.steps
     value = samples_total / (ms_per_step * 1e-3)
     last = reps[-1]
@@ -346,9 +357,7 @@ def main():
             torch.cuda.synchronize(local)
             secs = time.perf_counter() - t0
             if world > 1:
-                t = torch.tensor([secs], dtype=torch.float64, device=f"cuda:{local}")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                secs = float(t.item())
+                secs = max_over_ranks(secs)
             tto[f"k{k}"] = {"seconds": secs if res["reached"] else None, "reached": res["reached"],
                             "runs": res["runs"], "samples": res["samples"], "hv": res["hv"], "hv_star": target,
                             "archive": res["archive"], "front_exact": int(g["values"].shape[0]),

@@ -26,7 +26,9 @@ def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
 
 def allgather_rows(local: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather a variable number of rows (dim 0) across ranks; returns the concatenation
-    in rank order. Sizes first, then one padded collective."""
+    in rank order. Sizes first, then one padded collective. (gloo: through host memory.)"""
+    if local.is_cuda and dist.get_backend(group) == "gloo":
+        return allgather_rows(local.cpu(), group).to(local.device)
     world = dist.get_world_size(group)
     n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
