@@ -61,10 +61,13 @@ DevArchive& running_archive(Ctx& c)
     return *static_cast<DevArchive*>(c.running.get());
 }
 
-// running <- front(running U (vals, words)); unordered (internal use); returns the new size
-long long running_merge(Ctx& c, const double* d_vals, const uint64_t* d_words, long long M, int K, int wpc)
+// running <- front(running U (vals, words)); unordered (internal use); returns the new size.
+// *changed: whether the running archive's value set changed (its HV can only change then).
+long long running_merge(Ctx& c, const double* d_vals, const uint64_t* d_words, long long M, int K, int wpc,
+                        bool* changed = nullptr)
 {
     DevArchive& R = running_archive(c);
+    if (changed) *changed = M > 0;
     if (M <= 0) return R.F;
     if (R.F == 0) {  // first front: copy
         R.F = M;
@@ -91,6 +94,7 @@ long long running_merge(Ctx& c, const double* d_vals, const uint64_t* d_words, l
         ck(cudaMemcpyAsync(cw.p + R.F * wpc, d_words, sizeof(uint64_t) * M * wpc, cudaMemcpyDeviceToDevice, c.stream),
            "D2D");
     }
+    const long long F_old = R.F;
     const bool so = c.skip_order;
     c.skip_order = true;
     try {
@@ -100,6 +104,7 @@ long long running_merge(Ctx& c, const double* d_vals, const uint64_t* d_words, l
         throw;
     }
     c.skip_order = so;
+    if (changed) *changed = !same_value_set(c, cv.p, F_old, R.vals.p, R.F, K);  // old rows lead cv
     cv.release();
     cw.release();
     return R.F;
@@ -1077,6 +1082,7 @@ int momc_b200_running_reset(momc_ctx* ctx, char* err, size_t errlen)
     return guarded(err, errlen, [&] {
         DevArchive& R = running_archive(*ctx);
         R.F = 0;
+        ctx->running_hv_ref.clear();
     });
 }
 
@@ -1099,29 +1105,44 @@ int momc_b200_stream_step(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, l
         rp->sampling_s = ss;
         rp->pool_size = ctx->pool_size;
         const auto tf = clk::now();
-        DevArchive& a = resident_archive(*ctx);
-        ParetoTimings tm;
         const bool so = ctx->skip_order;
-        ctx->skip_order = true;  // the run's front is only merged: no archive order
-        try {
+        ctx->skip_order = true;  // internal fronts: no archive order
+        struct Restore {
+            Ctx& c;
+            bool v;
+            ~Restore() { c.skip_order = v; }
+        } restore{*ctx, so};
+        if (!merge) {  // the run's front into the resident archive (unordered)
+            DevArchive& a = resident_archive(*ctx);
+            ParetoTimings tm;
             filter_pool_device(*ctx, ctx->d_words.p, ctx->pool_size, a, &tm);
-        } catch (...) {
-            ctx->skip_order = so;
-            throw;
-        }
-        ctx->skip_order = so;
-        rp->unique_configs = tm.unique_configs;
-        rp->unique_vectors = tm.unique_vectors;
-        rp->archive_size = a.F;
-        if (!merge) {  // the run's front stays in the resident archive (unordered)
+            rp->unique_configs = tm.unique_configs;
+            rp->unique_vectors = tm.unique_vectors;
+            rp->archive_size = a.F;
             ck(cudaStreamSynchronize(ctx->stream), "stream front");
+            rp->pareto_filtering_s = std::chrono::duration<double>(clk::now() - tf).count();
+            rp->end_to_end_s = std::chrono::duration<double>(clk::now() - t0).count();
             return;
         }
-        const long long F = running_merge(*ctx, a.vals.p, a.words.p, a.F, a.K, a.wpc);
-        if (running_F) *running_F = F;
+        // one collapse + front over (this run's configs U the running archive)
+        DevArchive& R = running_archive(*ctx);
+        const long long X = R.F;
+        DevBuf<double> all;
+        filter_pool_merge_device(*ctx, ctx->d_words.p, ctx->pool_size, R.vals.p, R.words.p, X, R, all);
+        R.K = ctx->k;
+        R.wpc = (ctx->n + 63) / 64;
+        const bool changed = X == 0 || !same_value_set(*ctx, all.p, X, R.vals.p, R.F, ctx->k);
+        all.release();
+        rp->archive_size = R.F;
+        if (running_F) *running_F = R.F;
         if (r && hv) {
-            const DevArchive& R = running_archive(*ctx);
-            *hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, std::vector<double>(r, r + R.K));
+            // the HV of an unchanged value set at the same r is the cached one
+            const std::vector<double> rv(r, r + ctx->k);
+            if (changed || rv != ctx->running_hv_ref) {
+                ctx->running_hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, rv);
+                ctx->running_hv_ref = rv;
+            }
+            *hv = ctx->running_hv;
             rp->hv = *hv;
         }
         rp->pareto_filtering_s = std::chrono::duration<double>(clk::now() - tf).count();
@@ -1134,11 +1155,17 @@ int momc_b200_running_merge_values(momc_ctx* ctx, const double* d_vals, const ui
 {
     return guarded(err, errlen, [&] {
         bind(*ctx);
-        const long long F = running_merge(*ctx, d_vals, d_words, static_cast<long long>(M), k, wpc);
+        bool changed = true;
+        const long long F = running_merge(*ctx, d_vals, d_words, static_cast<long long>(M), k, wpc, &changed);
         if (running_F) *running_F = F;
         if (r && hv) {
-            const DevArchive& R = running_archive(*ctx);
-            *hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, std::vector<double>(r, r + R.K));
+            const std::vector<double> rv(r, r + k);
+            if (changed || rv != ctx->running_hv_ref) {
+                const DevArchive& R = running_archive(*ctx);
+                ctx->running_hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, rv);
+                ctx->running_hv_ref = rv;
+            }
+            *hv = ctx->running_hv;
         }
         ck(cudaStreamSynchronize(ctx->stream), "running merge");
     });

@@ -105,6 +105,8 @@ struct Ctx {
     std::shared_ptr<void> csv_scratch;            // csv.cu parsed pool
     std::shared_ptr<void> archive;
     std::shared_ptr<void> running;                // streaming: running archive (unordered)
+    double running_hv = 0.0;                      // its HV at running_hv_ref (cached)
+    std::vector<double> running_hv_ref;
     bool skip_order = false;                      // fronts for internal use: no archive order                // resident DevArchive (pareto.cuh)
 
     ~Ctx();

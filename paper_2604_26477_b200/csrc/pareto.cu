@@ -1005,14 +1005,19 @@ void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, 
 
 void evaluate_cuts_device(Ctx& c, const uint64_t* d_words, long long U, double* d_out)
 {
+    evaluate_cuts_rows(c, d_words, nullptr, U, d_out);
+}
+
+void evaluate_cuts_rows(Ctx& c, const uint64_t* d_words, const uint32_t* idx, long long U, double* d_out)
+{
     const int wpc = (c.n + 63) / 64;
     if (c.k > kMaxK) usage("the GPU path supports at most 16 objectives");
     if (U == 0) return;
     if (eval_gemm_ok(c)) {
-        evaluate_cuts_gemm(c, d_words, nullptr, U, d_out);
+        evaluate_cuts_gemm(c, d_words, idx, U, d_out);
     } else if (c.integer_weights) {
         const int sm = c.m * (2 + c.k) <= 12000 ? c.m * (2 + c.k) * 4 : 0;
-        k_eval_int<<<grid_blocks(U), 256, sm, c.stream>>>(d_words, nullptr, U, wpc, c.m, c.k, c.d_ei.p, c.d_ej.p,
+        k_eval_int<<<grid_blocks(U), 256, sm, c.stream>>>(d_words, idx, U, wpc, c.m, c.k, c.d_ei.p, c.d_ej.p,
                                                            c.d_wi.p, d_out);
     } else {
         std::vector<double> W(static_cast<size_t>(c.k), 0.0);
@@ -1021,7 +1026,7 @@ void evaluate_cuts_device(Ctx& c, const uint64_t* d_words, long long U, double* 
         DevBuf<double> dW;
         dW.reserve(static_cast<size_t>(c.k));
         ck(cudaMemcpyAsync(dW.p, W.data(), sizeof(double) * c.k, cudaMemcpyHostToDevice, c.stream), "H2D");
-        k_eval_dbl<<<grid_blocks(U, 128), 128, 0, c.stream>>>(d_words, nullptr, U, wpc, c.n, c.k, c.d_rowptr.p,
+        k_eval_dbl<<<grid_blocks(U, 128), 128, 0, c.stream>>>(d_words, idx, U, wpc, c.n, c.k, c.d_rowptr.p,
                                                                c.d_col.p, c.d_eidx.p, c.d_w.p, dW.p, d_out);
         ck(cudaStreamSynchronize(c.stream), "eval");
         dW.release();
@@ -1122,6 +1127,51 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     vv.release();
     vcfg.release();
     for (auto ev : {e0, e1, e2, e3}) cudaEventDestroy(ev);
+}
+
+__global__ void k_gather_words(const uint64_t* __restrict__ words, const uint32_t* __restrict__ idx, long long U, int wpc,
+                               uint64_t* out)
+{
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < U * wpc;
+         q += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[q] = words[static_cast<long long>(idx[q / wpc]) * wpc + q % wpc];
+}
+
+// front of (the M pool configs U the X rows xv / xw) into `out` in one collapse + front pass:
+// the streaming step's "run front merged into the running archive" without a separate run
+// front. xv / xw may alias `out` (they are copied first).
+void filter_pool_merge_device(Ctx& c, const uint64_t* d_words, long long M, const double* xv, const uint64_t* xw,
+                              long long X, DevArchive& out, DevBuf<double>& all_vals)
+{
+    if (M <= 0) usage("non-dominated filter needs a non-empty pool");
+    if (c.k > kMaxK) usage("the GPU path supports at most 16 objectives");
+    if (M >= 0xFFFFFFFFll) usage("pool too large for one device pass (shard it)");
+    Scratch& s = scratch(c);
+    const int wpc = (c.n + 63) / 64;
+    const int K = c.k;
+    const uint64_t tsize = pow2_at_least(2ull * static_cast<uint64_t>(M));
+    s.table.reserve(tsize);
+    s.uniq.reserve(static_cast<size_t>(M));
+    s.counters.reserve(8);
+    ck(cudaMemsetAsync(s.table.p, 0xFF, sizeof(uint32_t) * tsize, c.stream), "memset");
+    ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long) * 8, c.stream), "memset");
+    k_dedup<<<grid_blocks(M), 256, 0, c.stream>>>(d_words, M, wpc, s.table.p, tsize - 1, s.uniq.p, s.counters.p);
+    c.launches++;
+    const long long U = static_cast<long long>(read_counter(c, s.counters.p));
+    const long long T = U + X;
+    all_vals.reserve(static_cast<size_t>(T) * K + 1);
+    DevBuf<uint64_t> aw;
+    aw.reserve(static_cast<size_t>(T) * wpc + 1);
+    // the X rows first (rows [0, X): the caller compares them with the result), then the pool
+    if (X) {
+        ck(cudaMemcpyAsync(all_vals.p, xv, sizeof(double) * X * K, cudaMemcpyDeviceToDevice, c.stream), "D2D");
+        ck(cudaMemcpyAsync(aw.p, xw, sizeof(uint64_t) * X * wpc, cudaMemcpyDeviceToDevice, c.stream), "D2D");
+    }
+    evaluate_cuts_rows(c, d_words, s.uniq.p, U, all_vals.p + X * K);
+    k_gather_words<<<grid_blocks(U * wpc), 256, 0, c.stream>>>(d_words, s.uniq.p, U, wpc, aw.p + X * wpc);
+    c.launches++;
+    filter_values_device(c, all_vals.p, aw.p, wpc, c.n, T, K, out, nullptr);
+    aw.release();
 }
 
 void filter_values_device(Ctx& c, const double* d_vals, const uint64_t* d_words, int wpc, int n_spins, long long M,
@@ -1270,6 +1320,75 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
         tot = t;
     }
     return tot;
+}
+
+namespace {
+
+__device__ __forceinline__ uint64_t row_hash(const double* v, int K)
+{
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+    for (int k = 0; k < K; ++k) {
+        const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v[k] == 0.0 ? 0.0 : v[k]));
+        h ^= b + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+        h *= 0xBF58476D1CE4E5B9ull;
+    }
+    return h ^ (h >> 31);
+}
+
+__global__ void k_set_insert(const double* __restrict__ v, long long F, int K, uint32_t* table, uint64_t mask)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        uint64_t q = row_hash(v + i * K, K) & mask;
+        while (atomicCAS(&table[q], 0xFFFFFFFFu, static_cast<uint32_t>(i)) != 0xFFFFFFFFu) q = (q + 1) & mask;
+    }
+}
+
+__global__ void k_set_missing(const double* __restrict__ a, const uint32_t* __restrict__ table, uint64_t mask,
+                              const double* __restrict__ b, long long F, int K, unsigned long long* missing)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double* v = b + i * K;
+        uint64_t q = row_hash(v, K) & mask;
+        bool found = false;
+        for (;;) {
+            const uint32_t r = table[q];
+            if (r == 0xFFFFFFFFu) break;
+            bool eq = true;
+            for (int k = 0; k < K; ++k) eq &= a[static_cast<long long>(r) * K + k] == v[k];
+            if (eq) {
+                found = true;
+                break;
+            }
+            q = (q + 1) & mask;
+        }
+        if (!found) atomicAdd(missing, 1ull);
+    }
+}
+
+}  // namespace
+
+// true when the distinct vector sets a (Fa x K) and b (Fb x K) are equal (exact compare)
+bool same_value_set(Ctx& c, const double* a, long long Fa, const double* b, long long Fb, int K)
+{
+    if (Fa != Fb) return false;
+    if (Fa == 0) return true;
+    uint64_t size = 1;
+    while (size < 2ull * static_cast<uint64_t>(Fa) + 16) size <<= 1;
+    DevBuf<uint32_t> table;
+    DevBuf<unsigned long long> miss;
+    table.reserve(size);
+    miss.reserve(1);
+    ck(cudaMemsetAsync(table.p, 0xFF, sizeof(uint32_t) * size, c.stream), "memset");
+    ck(cudaMemsetAsync(miss.p, 0, sizeof(unsigned long long), c.stream), "memset");
+    k_set_insert<<<grid_blocks(Fa), 256, 0, c.stream>>>(a, Fa, K, table.p, size - 1);
+    k_set_missing<<<grid_blocks(Fb), 256, 0, c.stream>>>(a, table.p, size - 1, b, Fb, K, miss.p);
+    c.launches += 2;
+    const unsigned long long m = read_counter(c, miss.p);
+    table.release();
+    miss.release();
+    return m == 0;
 }
 
 }  // namespace momc_b200

@@ -35,8 +35,18 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
 void filter_values_device(Ctx& c, const double* d_vals, const uint64_t* d_words, int wpc, int n_spins,
                           long long M, int K, DevArchive& out, ParetoTimings* tm);
 
+// exact equality of two sets of distinct vectors (streaming: did the running archive change?)
+bool same_value_set(Ctx& c, const double* a, long long Fa, const double* b, long long Fb, int K);
+
+// front of (M pool configs U X extra rows xv/xw) into `out` in one pass (streaming merge);
+// all_vals receives the combined values, the X extra rows first
+void filter_pool_merge_device(Ctx& c, const uint64_t* d_words, long long M, const double* xv, const uint64_t* xw,
+                              long long X, DevArchive& out, DevBuf<double>& all_vals);
+
 // detail::evaluate_cuts (pareto.hpp:330-363) for U configs: d_out U x K.
 void evaluate_cuts_device(Ctx& c, const uint64_t* d_words, long long U, double* d_out);
+// the same for rows idx[0..U) of d_words
+void evaluate_cuts_rows(Ctx& c, const uint64_t* d_words, const uint32_t* idx, long long U, double* d_out);
 
 // reference_point_sampled (pareto.hpp:620-642)
 std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed);
