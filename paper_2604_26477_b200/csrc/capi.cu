@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_set>
@@ -603,6 +604,14 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     ck(cudaStreamSynchronize(ss), "sampler");
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, c.ev0, c.ev1), "event");
+    // test hook: MOMC_TEST_FORCE_FALLBACK=k re-runs every k-th register-path block on the
+    // sequential path (its words must be identical); never set in production
+    if (regpath) {
+        const char* f = std::getenv("MOMC_TEST_FORCE_FALLBACK");
+        const long long every = f ? std::atoll(f) : 0;
+        if (every > 0)
+            for (long long b = 0; b < nblocks; b += every) flags[static_cast<size_t>(b)] |= 2;
+    }
     bool refixed = false;
     for (long long b = 0; b < nblocks; ++b) {
         if (!(flags[static_cast<size_t>(b)] & 2)) continue;

@@ -141,3 +141,28 @@ def test_config_validation_messages(session):
         api.run_sampler(inst, [api.WeightVector([1], 1)], SolverConfig(), 0, session=session)
     with pytest.raises(InvalidArgument, match="at least one weight vector"):
         api.run_sampler(inst, [], SolverConfig(), 1, session=session)
+
+
+@pytest.mark.parametrize("variant", ["dsb", "bsb", "simcim"])
+def test_register_path_fallback_blocks_are_identical(session, variant):
+    """blocks re-run on the exact sequential path (the register path's overflow fallback)
+    produce the same words as the register path (MOMC_TEST_FORCE_FALLBACK re-runs every
+    3rd block)"""
+    import os
+    from paper_2604_26477_b200.instances import load_heavy_hex
+    inst = load_heavy_hex(4)
+    s = session
+    s.set_instance(inst)
+    s.set_weights(api.build_weights(4, resolution=5))
+    cfg = SolverConfig(variant=api.parse_variant(variant), batch_size=300, seed=11)
+    s.sample(cfg, 1)
+    a = s.pool(stamps=False).words.copy()
+    before = s.fallback_blocks() & ((1 << 40) - 1)
+    os.environ["MOMC_TEST_FORCE_FALLBACK"] = "3"
+    try:
+        s.sample(cfg, 1)
+    finally:
+        del os.environ["MOMC_TEST_FORCE_FALLBACK"]
+    b = s.pool(stamps=False).words
+    assert (s.fallback_blocks() & ((1 << 40) - 1)) > before
+    assert np.array_equal(a, b)
