@@ -168,6 +168,11 @@ int momc_b200_convergence_trace(momc_ctx* ctx, const uint64_t* words, const int6
                                 const double* r, int checkpoints, double* elapsed_s, double* hv, int64_t* samples,
                                 char* err, size_t errlen);
 
+/* Self-test of the hand-written tcgen05 int8 blocks: D (128 x 128 int32, row-major) =
+ * A (128 x K int8, row-major) . B (128 x K int8, row-major)^T, K a multiple of 128. */
+int momc_b200_tc_i8_selftest(momc_ctx* ctx, const int8_t* A, const int8_t* B, int K, int32_t* D, char* err,
+                             size_t errlen);
+
 /* ---------------------------------------------------------------- pool CSV (solver.hpp:357-432) */
 /* The record rows of save_pool_csv, formatted on the device: for each of M records
  * "run,weight,trajectory,timestamp_ns,<16 hex nibbles per word>\n". With out == NULL only

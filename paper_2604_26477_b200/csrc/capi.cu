@@ -1204,6 +1204,15 @@ int momc_b200_running_to_archive(momc_ctx* ctx, int64_t* out_F, char* err, size_
     });
 }
 
+int momc_b200_tc_i8_selftest(momc_ctx* ctx, const int8_t* A, const int8_t* B, int K, int32_t* D, char* err,
+                             size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        tc_i8_selftest(*ctx, A, B, K, D);
+    });
+}
+
 int momc_b200_clamp_reference(momc_ctx* ctx, double* r, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {
