@@ -20,14 +20,17 @@
 // The GEMM is cuBLASLt's int8 batched matmul (a plain library GEMM); the fused tcgen05
 // kernel with the SB update in its epilogue is the next step.
 #include <cublasLt.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "ctx.cuh"
+#include "tc_i8.cuh"
 #include "rng.cuh"
 #include "sampler.cuh"
 
@@ -117,9 +120,20 @@ struct WordRing {
     __device__ __forceinline__ uint32_t at(int i) const { return r[((head + i) & 15) * 128]; }
 };
 
-// next_normal (rng.hpp:156-185) from the ring
-__device__ __forceinline__ double ring_normal(WordRing& w, const ZigTables* __restrict__ z)
+// next_normal (rng.hpp:156-185) from the ring: the fast path inline, the rest (wedge and
+// tail attempts, ~2.75 % of words) out of line. The slow path takes the ring state by value
+// and returns it, so the caller's WordRing stays in registers.
+struct RingSlow {
+    double v;
+    int head, tail;
+    uint32_t blk;
+};
+
+__device__ __noinline__ RingSlow ring_normal_slow(uint32_t* r, uint32_t k0, uint32_t k1, uint32_t lo, uint32_t mid,
+                                                  uint32_t hi, uint32_t blk, int head, int tail,
+                                                  const ZigTables* __restrict__ z)
 {
+    WordRing w{r, k0, k1, lo, mid, hi, blk, head, tail};
     for (;;) {
         w.ensure(1);
         const uint32_t u = w.at(0);
@@ -128,17 +142,18 @@ __device__ __forceinline__ double ring_normal(WordRing& w, const ZigTables* __re
         const uint32_t mag = hz < 0 ? 0u - u : u;
         if (mag < z->kn[iz]) {
             ++w.head;
-            return __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+            return {__dmul_rn(static_cast<double>(hz), z->wn[iz]), w.head, w.tail, w.blk};
         }
         if (iz == 0) {  // tail: (x, y) trials of 4 words each
             ++w.head;
-            const double r = 3.442619855899;
+            const double rr = 3.442619855899;
             for (;;) {
                 w.ensure(4);
-                const double xx = __ddiv_rn(-log(u01_open_from(w.at(0), w.at(1))), r);
+                const double xx = __ddiv_rn(-log(u01_open_from(w.at(0), w.at(1))), rr);
                 const double yy = -log(u01_open_from(w.at(2), w.at(3)));
                 w.head += 4;
-                if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) return hz > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
+                if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx))
+                    return {hz > 0 ? __dadd_rn(rr, xx) : -__dadd_rn(rr, xx), w.head, w.tail, w.blk};
             }
         }
         w.ensure(3);
@@ -154,8 +169,27 @@ __device__ __forceinline__ double ring_normal(WordRing& w, const ZigTables* __re
         if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) accept = true;
         else if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) accept = false;
         else accept = lhs < exp(targ);
-        if (accept) return xv;
+        if (accept) return {xv, w.head, w.tail, w.blk};
     }
+}
+
+__device__ __forceinline__ double ring_normal(WordRing& w, const ZigTables* __restrict__ z)
+{
+    if (w.tail - w.head >= 1) {
+        const uint32_t u = w.at(0);
+        const int32_t hz = static_cast<int32_t>(u);
+        const uint32_t iz = u & 127u;
+        const uint32_t mag = hz < 0 ? 0u - u : u;
+        if (mag < z->kn[iz]) {
+            ++w.head;
+            return __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        }
+    }
+    const RingSlow r = ring_normal_slow(w.r, w.k0, w.k1, w.lo, w.mid, w.hi, w.blk, w.head, w.tail, z);
+    w.head = r.head;
+    w.tail = r.tail;
+    w.blk = r.blk;
+    return r.v;
 }
 
 constexpr int kDenseTile = 64;  // spins per shared-memory phi tile
@@ -249,6 +283,191 @@ __global__ void __launch_bounds__(128, 9) k_dense_update(int n, int batch_pad, i
         __syncthreads();
     }
     if (nonfinite) atomicMin(bad, t_step + 1);
+}
+
+// ---- fused tensor-core step (the default dense path): one CTA owns 128 trajectories of
+// one (run, weight) pair and walks the output spins in tiles of 128. Per tile, the
+// contraction D (128 traj x 128 spins) = Phi_t (128 x n, int8) . (H J)^T (n x 128, int8) runs
+// on the tensor cores: thread 0 streams 128-wide K chunks of both operands with TMA
+// (128-byte swizzle, two smem stages, mbarrier completion) and issues tcgen05.mma kind::i8
+// into a TMEM accumulator; the epilogue thread of trajectory t then reads its row of D
+// (tcgen05.ld) and applies the dSB update to the tile's spins in order (the noise stream is
+// sequential in the spin index), writing x, y and Phi_{t+1}. D never touches HBM.
+constexpr int kTcN = 128;
+constexpr int kTcStage = 2 * 128 * tc::kChunkK;  // A + B chunk
+constexpr int kTcSmem = 1024 + 2 * kTcStage + 128 * (kTcN + 4) + 16 * 128 * 4 + static_cast<int>(sizeof(ZigTables));
+
+__global__ void __launch_bounds__(128) k_dense_tc_step(const __grid_constant__ CUtensorMap tmA,
+                                                       const __grid_constant__ CUtensorMap tmB, int n, int batch_pad,
+                                                       int H, const PairOf* __restrict__ pairs, uint64_t seed,
+                                                       int t_step, int T, double dt, double a0, double alpha,
+                                                       double sdt, const double* __restrict__ c0s,
+                                                       const ZigTables* __restrict__ zig, signed char* phi_next,
+                                                       double* x, double* y, int* bad)
+{
+    extern __shared__ uint8_t sm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    __shared__ uint64_t full[2], done[2], tile_done;
+    __shared__ uint32_t tslot;
+    auto tile = reinterpret_cast<signed char(*)[kTcN + 4]>(sm + 2 * kTcStage);
+    uint32_t* ring = reinterpret_cast<uint32_t*>(sm + 2 * kTcStage + 128 * (kTcN + 4));
+    ZigTables* z = reinterpret_cast<ZigTables*>(sm + 2 * kTcStage + 128 * (kTcN + 4) + 16 * 128 * 4);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int q = tid; q < static_cast<int>(sizeof(ZigTables) / 4); q += blockDim.x)
+        reinterpret_cast<uint32_t*>(z)[q] = reinterpret_cast<const uint32_t*>(zig)[q];
+    if (warp == 0) tc::tmem_alloc<128>(&tslot);
+    if (tid == 0) {
+        tc::prefetch_tmap(&tmA);
+        tc::prefetch_tmap(&tmB);
+        for (int q = 0; q < 2; ++q) {
+            tc::mbar_init(&full[q], 1);
+            tc::mbar_init(&done[q], 1);
+        }
+        tc::mbar_init(&tile_done, 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = tslot;
+
+    const PairOf pr = pairs[blockIdx.y];
+    const long long pb = blockIdx.y;
+    const int t0 = blockIdx.x * 128;
+    const int t = t0 + tid;
+    const bool active = t < pr.count;
+    const double c0h = __ddiv_rn(c0s[pr.l], static_cast<double>(H));
+    const double a_t = __ddiv_rn(static_cast<double>(t_step + 1), static_cast<double>(T));
+    const double neg_drift = -__dsub_rn(a0, a_t);
+    const bool noisy = alpha > 0.0;
+    WordRing w;
+    {
+        const uint64_t key = run_key(seed, static_cast<uint32_t>(pr.run));
+        w.r = ring + tid;
+        w.k0 = static_cast<uint32_t>(key);
+        w.k1 = static_cast<uint32_t>(key >> 32);
+        w.lo = tag_word(kTagStepNoise, static_cast<uint32_t>(t_step));
+        w.mid = static_cast<uint32_t>(pr.traj0 + t);
+        w.hi = static_cast<uint32_t>(pr.l);
+        w.blk = 0;
+        w.head = w.tail = 0;
+    }
+    double* xs = x + pb * n * static_cast<long long>(batch_pad);
+    double* ys = y + pb * n * static_cast<long long>(batch_pad);
+    constexpr uint32_t idesc = tc::idesc_i8(128, kTcN);
+    const int nk = (n + tc::kChunkK - 1) / tc::kChunkK;
+    const int arow = static_cast<int>(pb * batch_pad + t0), brow = pr.l * n;
+    // chunk g (global over tiles) uses stage g & 1; its full / done barriers complete their
+    // (g >> 1)-th phase
+    auto issue_tma = [&](int g, int kc, int nb) {
+        const int st = g & 1;
+        if (g >= 2) tc::mbar_wait(&done[st], ((g - 2) >> 1) & 1);  // the MMAs that read this stage
+        uint8_t* sa = sm + st * kTcStage;
+        tc::mbar_expect_tx(&full[st], kTcStage);
+        tc::tma_load_2d(sa, &tmA, kc * tc::kChunkK, arow, &full[st]);
+        tc::tma_load_2d(sa + 128 * tc::kChunkK, &tmB, kc * tc::kChunkK, brow + nb, &full[st]);
+    };
+    bool nonfinite = false;
+    int g = 0;
+    for (int nb = 0; nb < n; nb += kTcN, g += nk) {
+        if (tid == 0) {
+            issue_tma(g, 0, nb);
+            for (int kc = 0; kc < nk; ++kc) {
+                if (kc + 1 < nk) issue_tma(g + kc + 1, kc + 1, nb);
+                const int gc = g + kc, st = gc & 1;
+                tc::mbar_wait(&full[st], (gc >> 1) & 1);
+                tc::fence_after();
+                const uint32_t a_s = tc::smem_u32(sm + st * kTcStage), b_s = a_s + 128 * tc::kChunkK;
+#pragma unroll
+                for (int k = 0; k < tc::kChunkK / 32; ++k)
+                    tc::mma_i8(tbase, tc::smem_desc_sw128(a_s + 32 * k), tc::smem_desc_sw128(b_s + 32 * k), idesc,
+                               kc > 0 || k > 0);
+                tc::commit(&done[st]);
+            }
+            tc::commit(&tile_done);  // completes once per tile: waiters are never a phase behind
+        }
+        tc::mbar_wait(&tile_done, (nb / kTcN) & 1);
+        tc::fence_after();
+        // ---- epilogue: trajectory t updates the tile's spins in order
+        const int lim = min(kTcN, n - nb);
+        for (int c0 = 0; c0 < kTcN; c0 += 32) {
+            uint32_t v[32];
+            tc::tmem_ld32(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+            if (c0 >= lim) continue;
+            if (active) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int c = c0 + j;
+                    if (c >= lim) continue;
+                    if (noisy && (c & 3) == 0) {
+                        while (w.tail - w.head < 8) w.block();  // warp-synchronous top-up
+                    }
+                    const long long o = static_cast<long long>(nb + c) * batch_pad + t;
+                    double xi = xs[o], yi = ys[o];
+                    const double eta = noisy ? ring_normal(w, z) : 0.0;
+                    double d = __dsub_rn(__dmul_rn(neg_drift, xi),
+                                         __dmul_rn(c0h, static_cast<double>(static_cast<int32_t>(v[j]))));
+                    if (noisy) d = __dadd_rn(d, __dmul_rn(alpha, eta));
+                    yi = __dadd_rn(yi, __dmul_rn(dt, d));
+                    xi = __dadd_rn(xi, __dmul_rn(sdt, yi));
+                    if (fabs(xi) > 1.0) {  // wall + clamp (both fire exactly when |x| > 1)
+                        yi = 0.0;
+                        xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
+                    }
+                    nonfinite |= !isfinite(xi) || !isfinite(yi);
+                    xs[o] = xi;
+                    ys[o] = yi;
+                    tile[tid][c] = xi < 0.0 ? -1 : 1;
+                }
+            } else {
+                for (int j = 0; j < 32 && c0 + j < lim; ++j) tile[tid][c0 + j] = 1;  // padding rows stay +1
+            }
+        }
+        tc::fence_before();
+        __syncthreads();  // the tile's TMEM reads are done before the next tile's MMAs
+        // coalesced store of Phi_{t+1} for the tile: rows of `lim` bytes, 4 bytes per thread and step
+        for (int q = tid; q < 128 * (kTcN / 4); q += blockDim.x) {
+            const int r = q / (kTcN / 4), c4 = (q % (kTcN / 4)) * 4;
+            if (t0 + r < batch_pad && c4 < lim) {
+                const uint32_t val = *reinterpret_cast<const uint32_t*>(&tile[r][c4]);
+                *reinterpret_cast<uint32_t*>(phi_next + (pb * batch_pad + t0 + r) * n + nb + c4) = val;
+            }
+        }
+        __syncthreads();
+        tc::fence_after();
+    }
+    if (nonfinite) atomicMin(bad, t_step + 1);
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<128>(tbase);
+}
+
+// TMA descriptor of a row-major int8 matrix (rows x cols, cols % 16 == 0): 128 x 128 boxes,
+// 128-byte swizzle, zero fill outside
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+CUtensorMap make_tmap_i8(const void* base, long long rows, int cols)
+{
+    static PFN_encodeTiled encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q), "driver entry point");
+        if (!fn || q != cudaDriverEntryPointSuccess) runtime("cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_encodeTiled>(fn);
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols)};
+    const cuuint32_t box[2] = {128, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) runtime("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return m;
 }
 
 __global__ void k_dense_readout(int n, int batch_pad, int batch, int L, const PairOf* __restrict__ pairs,
@@ -352,7 +571,7 @@ void gemm_i8_batched(Ctx& c, LtGemm& g, int m, int n, int k, const signed char* 
 
 struct DenseScratch {
     LtGemm gemm;
-    DevBuf<signed char> hj, phi, s8;
+    DevBuf<signed char> hj, phi, phi2, s8;
     DevBuf<int> D, flags;
     DevBuf<double> x, y;
     DevBuf<PairOf> pairs;
@@ -366,7 +585,7 @@ DenseScratch& dscratch(Ctx& c)
 {
     if (!c.dense_scratch) c.dense_scratch = std::shared_ptr<void>(new DenseScratch(), [](void* p) {
         auto* d = static_cast<DenseScratch*>(p);
-        d->hj.release(); d->phi.release(); d->s8.release(); d->D.release(); d->flags.release(); d->wk.release();
+        d->hj.release(); d->phi.release(); d->phi2.release(); d->s8.release(); d->D.release(); d->flags.release(); d->wk.release();
         d->x.release(); d->y.release(); d->pairs.release();
         delete d;
     });
@@ -434,6 +653,9 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
     int maxc = 0;
     for (auto& q : pairs) maxc = std::max(maxc, q.count);
     const int batch_pad = (maxc + 15) / 16 * 16;
+    // the fused tcgen05 step (default) or, for cross-checks (MOMC_DENSE_LT=1), cuBLASLt's int8
+    // GEMM followed by the update kernel; both give identical words (D is exact)
+    const bool use_tc = std::getenv("MOMC_DENSE_LT") == nullptr;
     // process pairs in groups bounded by memory (~24 GB of state)
     const size_t per_pair = static_cast<size_t>(n) * batch_pad * (8 + 8 + 4 + 1);
     const size_t group = std::max<size_t>(1, (24ull << 30) / per_pair);
@@ -444,7 +666,7 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
         const size_t cells = static_cast<size_t>(G) * n * batch_pad;
         d.x.reserve(cells);
         d.y.reserve(cells);
-        d.D.reserve(cells);
+        if (!use_tc) d.D.reserve(cells);
         d.phi.reserve(cells);
         d.flags.reserve(4);
         ck(cudaMemsetAsync(d.flags.p, 0x7f, sizeof(int), c.stream), "memset");
@@ -454,21 +676,37 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
         c.launches++;
         // all pairs of a group must share the weight stride pattern: B operand per pair = HJ of its weight
         // -> run one strided-batch GEMM per maximal run of consecutive weights within the group
-        for (int t = 0; t < p.T; ++t) {
-            int q0 = 0;
-            while (q0 < G) {
-                int q1 = q0 + 1;
-                const PairOf& a = pairs[g0 + q0];
-                while (q1 < G && pairs[g0 + q1].l == pairs[g0 + q1 - 1].l + 1 && pairs[g0 + q1].run == a.run) ++q1;
-                const long long pstride = static_cast<long long>(n) * batch_pad;
-                gemm_i8_batched(c, d.gemm, batch_pad, n, n, d.phi.p + q0 * pstride, pstride,
-                                d.hj.p + static_cast<long long>(a.l) * n * n, static_cast<long long>(n) * n,
-                                d.D.p + q0 * pstride, pstride, q1 - q0);
-                q0 = q1;
+        if (use_tc) {
+            d.phi2.reserve(cells);
+            ck(cudaFuncSetAttribute(k_dense_tc_step, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem), "smem");
+            const dim3 tgrid(static_cast<unsigned>((batch_pad + 127) / 128), static_cast<unsigned>(G));
+            const long long rows = static_cast<long long>(G) * batch_pad;
+            const CUtensorMap tm_phi[2] = {make_tmap_i8(d.phi.p, rows, n), make_tmap_i8(d.phi2.p, rows, n)};
+            const CUtensorMap tm_hj = make_tmap_i8(d.hj.p, static_cast<long long>(L) * n, n);
+            signed char* bufs[2] = {d.phi.p, d.phi2.p};
+            for (int t = 0; t < p.T; ++t) {
+                k_dense_tc_step<<<tgrid, 128, kTcSmem, c.stream>>>(tm_phi[t & 1], tm_hj, n, batch_pad, c.H, d.pairs.p,
+                                                                   p.seed, t, p.T, p.dt, p.a0, p.alpha, p.s_dt_a0, p.c0,
+                                                                   p.zig, bufs[(t + 1) & 1], d.x.p, d.y.p, d.flags.p);
+                c.launches++;
             }
-            k_dense_update<<<grid, 128, 0, c.stream>>>(n, batch_pad, c.H, d.pairs.p, p.seed, t, p.T, p.dt, p.a0, p.alpha,
-                                                       p.s_dt_a0, p.c0, p.zig, d.D.p, d.x.p, d.y.p, d.phi.p, d.flags.p);
-            c.launches++;
+        } else {
+            for (int t = 0; t < p.T; ++t) {
+                int q0 = 0;
+                while (q0 < G) {
+                    int q1 = q0 + 1;
+                    const PairOf& a = pairs[g0 + q0];
+                    while (q1 < G && pairs[g0 + q1].l == pairs[g0 + q1 - 1].l + 1 && pairs[g0 + q1].run == a.run) ++q1;
+                    const long long pstride = static_cast<long long>(n) * batch_pad;
+                    gemm_i8_batched(c, d.gemm, batch_pad, n, n, d.phi.p + q0 * pstride, pstride,
+                                    d.hj.p + static_cast<long long>(a.l) * n * n, static_cast<long long>(n) * n,
+                                    d.D.p + q0 * pstride, pstride, q1 - q0);
+                    q0 = q1;
+                }
+                k_dense_update<<<grid, 128, 0, c.stream>>>(n, batch_pad, c.H, d.pairs.p, p.seed, t, p.T, p.dt, p.a0, p.alpha,
+                                                           p.s_dt_a0, p.c0, p.zig, d.D.p, d.x.p, d.y.p, d.phi.p, d.flags.p);
+                c.launches++;
+            }
         }
         k_dense_readout<<<grid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, p.row0, d.flags.p + 1);
         c.launches++;

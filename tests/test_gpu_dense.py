@@ -54,3 +54,24 @@ def test_dense_reference_point_matches_reference(ref, session):
     inst = session.generate_uniform_instance(512, 0.5, 3, 12)
     ri = ref.generate_uniform(512, 0.5, 3, 12)
     assert api.reference_point_sampled(inst, 333, 7, session=session) == ref.reference_point_sampled(ri, 333, 7).tolist()
+
+
+def test_tcgen05_step_matches_cublaslt_path(session):
+    """the fused tcgen05 step (default) and the cuBLASLt GEMM + update kernels compute the
+    same exact D = (H J) sgn(X) and the same update: identical words"""
+    import os
+    n, H = 384, 4
+    session.generate_uniform_instance(n, 0.6, 3, 21)
+    nums = [[a, b, H - a - b] for a in range(1, H) for b in range(1, H - a)]
+    session.set_dense_threshold(256)
+    session.set_weights([api.WeightVector(r, H) for r in nums])
+    cfg = api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=200, seed=4)
+    session.sample(cfg, 1)
+    a = session.pool(stamps=False).words.copy()
+    os.environ["MOMC_DENSE_LT"] = "1"
+    try:
+        session.sample(cfg, 1)
+    finally:
+        del os.environ["MOMC_DENSE_LT"]
+    b = session.pool(stamps=False).words
+    assert np.array_equal(a, b)
