@@ -173,6 +173,45 @@ __device__ __noinline__ RingSlow ring_normal_slow(uint32_t* r, uint32_t k0, uint
     }
 }
 
+// all inline (the update kernel, register-capped at 56: a call would spill the ring state)
+__device__ __forceinline__ double ring_normal_inline(WordRing& w, const ZigTables* __restrict__ z)
+{
+    for (;;) {
+        w.ensure(1);
+        const uint32_t u = w.at(0);
+        const int32_t hz = static_cast<int32_t>(u);
+        const uint32_t iz = u & 127u;
+        const uint32_t mag = hz < 0 ? 0u - u : u;
+        if (mag < z->kn[iz]) {
+            ++w.head;
+            return __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        }
+        if (iz == 0) {
+            ++w.head;
+            const double rr = 3.442619855899;
+            for (;;) {
+                w.ensure(4);
+                const double xx = __ddiv_rn(-log(u01_open_from(w.at(0), w.at(1))), rr);
+                const double yy = -log(u01_open_from(w.at(2), w.at(3)));
+                w.head += 4;
+                if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) return hz > 0 ? __dadd_rn(rr, xx) : -__dadd_rn(rr, xx);
+            }
+        }
+        w.ensure(3);
+        const double xv = __dmul_rn(static_cast<double>(hz), z->wn[iz]);
+        const double u01 = u01_from(w.at(1), w.at(2));
+        w.head += 3;
+        const double lhs = __dadd_rn(z->fn[iz], __dmul_rn(u01, __dsub_rn(z->fn[iz - 1], z->fn[iz])));
+        const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
+        const float ef = __expf(static_cast<float>(targ));
+        bool accept;
+        if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) accept = true;
+        else if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) accept = false;
+        else accept = lhs < exp(targ);
+        if (accept) return xv;
+    }
+}
+
 __device__ __forceinline__ double ring_normal(WordRing& w, const ZigTables* __restrict__ z)
 {
     if (w.tail - w.head >= 1) {
@@ -255,7 +294,7 @@ __global__ void __launch_bounds__(128, 9) k_dense_update(int n, int batch_pad, i
                     xn = xs[o];
                     yn = ys[o];
                 }
-                const double eta = noisy ? ring_normal(w, &z) : 0.0;
+                const double eta = noisy ? ring_normal_inline(w, &z) : 0.0;
                 double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0h, static_cast<double>(dq)));
                 if (noisy) d = __dadd_rn(d, __dmul_rn(alpha, eta));
                 yi = __dadd_rn(yi, __dmul_rn(dt, d));
@@ -388,22 +427,28 @@ __global__ void __launch_bounds__(128) k_dense_tc_step(const __grid_constant__ C
         }
         tc::mbar_wait(&tile_done, (nb / kTcN) & 1);
         tc::fence_after();
-        // ---- epilogue: trajectory t updates the tile's spins in order
+        // ---- epilogue: trajectory t updates the tile's spins in order, 8 at a time: the 16
+        //      x / y loads of a group are issued together (memory parallelism at 8 warps/SM)
         const int lim = min(kTcN, n - nb);
-        for (int c0 = 0; c0 < kTcN; c0 += 32) {
-            uint32_t v[32];
-            tc::tmem_ld32(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
-            if (c0 >= lim) continue;
+        for (int c0 = 0; c0 < lim; c0 += 8) {
+            uint32_t v[8];
+            tc::tmem_ld8(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
             if (active) {
+                double xg[8], yg[8];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
+                for (int j = 0; j < 8; ++j) {
+                    const long long o = static_cast<long long>(nb + c0 + j) * batch_pad + t;
+                    xg[j] = c0 + j < lim ? xs[o] : 0.0;
+                    yg[j] = c0 + j < lim ? ys[o] : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
                     const int c = c0 + j;
-                    if (c >= lim) continue;
+                    if (c >= lim) break;
                     if (noisy && (c & 3) == 0) {
                         while (w.tail - w.head < 8) w.block();  // warp-synchronous top-up
                     }
-                    const long long o = static_cast<long long>(nb + c) * batch_pad + t;
-                    double xi = xs[o], yi = ys[o];
+                    double xi = xg[j], yi = yg[j];
                     const double eta = noisy ? ring_normal(w, z) : 0.0;
                     double d = __dsub_rn(__dmul_rn(neg_drift, xi),
                                          __dmul_rn(c0h, static_cast<double>(static_cast<int32_t>(v[j]))));
@@ -415,12 +460,13 @@ __global__ void __launch_bounds__(128) k_dense_tc_step(const __grid_constant__ C
                         xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
                     }
                     nonfinite |= !isfinite(xi) || !isfinite(yi);
+                    const long long o = static_cast<long long>(nb + c) * batch_pad + t;
                     xs[o] = xi;
                     ys[o] = yi;
                     tile[tid][c] = xi < 0.0 ? -1 : 1;
                 }
             } else {
-                for (int j = 0; j < 32 && c0 + j < lim; ++j) tile[tid][c0 + j] = 1;  // padding rows stay +1
+                for (int j = 0; j < 8 && c0 + j < lim; ++j) tile[tid][c0 + j] = 1;  // padding rows stay +1
             }
         }
         tc::fence_before();
@@ -653,9 +699,11 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
     int maxc = 0;
     for (auto& q : pairs) maxc = std::max(maxc, q.count);
     const int batch_pad = (maxc + 15) / 16 * 16;
-    // the fused tcgen05 step (default) or, for cross-checks (MOMC_DENSE_LT=1), cuBLASLt's int8
-    // GEMM followed by the update kernel; both give identical words (D is exact)
-    const bool use_tc = std::getenv("MOMC_DENSE_LT") == nullptr;
+    // cuBLASLt's int8 GEMM followed by the update kernel (default), or the fused tcgen05 step
+    // (MOMC_DENSE_TC=1): identical words (D is exact). The fused step is correct but its
+    // epilogue runs at 8 warps/SM (2 CTAs: TMA stages + TMEM), 2x slower for now.
+    const char* tc_env = std::getenv("MOMC_DENSE_TC");
+    const bool use_tc = tc_env != nullptr && tc_env[0] == '1';
     // process pairs in groups bounded by memory (~24 GB of state)
     const size_t per_pair = static_cast<size_t>(n) * batch_pad * (8 + 8 + 4 + 1);
     const size_t group = std::max<size_t>(1, (24ull << 30) / per_pair);

@@ -57,8 +57,8 @@ def test_dense_reference_point_matches_reference(ref, session):
 
 
 def test_tcgen05_step_matches_cublaslt_path(session):
-    """the fused tcgen05 step (default) and the cuBLASLt GEMM + update kernels compute the
-    same exact D = (H J) sgn(X) and the same update: identical words"""
+    """the fused tcgen05 step (MOMC_DENSE_TC=1) and the cuBLASLt GEMM + update kernels
+    (default) compute the same exact D = (H J) sgn(X) and the same update: identical words"""
     import os
     n, H = 384, 4
     session.generate_uniform_instance(n, 0.6, 3, 21)
@@ -68,10 +68,10 @@ def test_tcgen05_step_matches_cublaslt_path(session):
     cfg = api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=200, seed=4)
     session.sample(cfg, 1)
     a = session.pool(stamps=False).words.copy()
-    os.environ["MOMC_DENSE_LT"] = "1"
+    os.environ["MOMC_DENSE_TC"] = "1"
     try:
         session.sample(cfg, 1)
     finally:
-        del os.environ["MOMC_DENSE_LT"]
+        del os.environ["MOMC_DENSE_TC"]
     b = session.pool(stamps=False).words
     assert np.array_equal(a, b)
