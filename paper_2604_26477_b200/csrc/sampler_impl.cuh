@@ -269,7 +269,23 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
             int gen = G::kNU;  // words present in ub
             int pos = 0;       // next attempt position
             int slow = 0;      // words taken by the listed slow attempts
+            // fast walk: wedges whose words lie inside the mask (the common case); anything
+            // else (a tail, words beyond the mask, a full list) continues in the general walk
+            bool general = false;
             for (;;) {
+                const int lastq = n - 1 + slow;
+                const int q = next_slow<G::kNU>(F0, F1, pos);  // kNU when none is left
+                if (q > lastq) break;
+                if (q + 2 >= G::kNU || m >= G::kECAP || (ub[q] & 127u) == 0) {
+                    general = true;
+                    break;
+                }
+                en[m * TPC] = static_cast<uint32_t>(q);
+                ++m;
+                slow += 3;
+                pos = q + 3;
+            }
+            for (; general;) {
                 const int lastq = n - 1 + slow;  // fast normals before q = q - slow must stay < n
                 int q = next_slow<G::kNU>(F0, F1, pos);
                 if (q >= G::kNU) {  // beyond the mask: extend the word buffer, test on demand
