@@ -73,7 +73,6 @@ struct Geo {
     static constexpr int zig = 0;                                           // ZigTables (2560 B)
     static constexpr int ubuf = 2560;                                       // kTPC x kUS u32
     static constexpr int ent = ubuf + kTPC * kUS * 4;                       // kECAP x kTPC u32
-    static constexpr int entv = ent + kECAP * kTPC * 4;                     // kECAP x kTPC f64
     // phi(x_j) rows, trajectory-major: dSB keeps the sign as a u32 mask (J_ij phi_j is J_ij
     // with its sign flipped), bSB / SimCIM keep x as f64. Row strides put the 4 lanes x 8
     // trajectories of a warp on distinct banks for both the writes (spin s0 + s of lane h) and
@@ -81,7 +80,7 @@ struct Geo {
     // == 2 mod 16 elements.
     static constexpr int kPhiW = VAR == 1 ? 4 : 8;
     static constexpr int kPStr = VAR == 1 ? (kNP + 27) / 32 * 32 + 4 : (kNP + 13) / 16 * 16 + 2;
-    static constexpr int phi = entv + kECAP * kTPC * 8;                     // kTPC x kPStr phi entries
+    static constexpr int phi = ent + kECAP * kTPC * 4;                      // kTPC x kPStr phi entries
     static constexpr int csr = (phi + kTPC * kPStr * kPhiW + 15) / 16 * 16;
     static_assert(kNU <= 128, "mask covers at most 128 words");
     static_assert(kNA <= 255, "word positions are stored in 8 bits");
@@ -135,7 +134,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     ZigTables* zig = reinterpret_cast<ZigTables*>(smem + G::zig);
     uint32_t* ubuf = reinterpret_cast<uint32_t*>(smem + G::ubuf);
     uint32_t* ent = reinterpret_cast<uint32_t*>(smem + G::ent);
-    double* entv = reinterpret_cast<double*>(smem + G::entv);
     unsigned char* phis = smem + G::phi;
     unsigned char* csr = smem + G::csr;
     // DMAX == 0: rp[NP+1] | cv[nnz] | cc[nnz];  DMAX == 3: one 48-byte record per spin,
@@ -228,7 +226,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     const double* fn = zig->fn;
     uint32_t* ub = ubuf + t_loc * US;  // this trajectory's word row
     uint32_t* en = ent + t_loc;   // this trajectory's event column, stride TPC
-    double* ev = entv + t_loc;
     const uint4* recs = reinterpret_cast<const uint4*>(csr) + s0 * 3;  // this lane's coupling records
     bool overflow = false;
     int ovf_code = 0;  // which buffer overflowed (diagnostics)
@@ -338,7 +335,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                     }
                     if (overflow) break;
                     en[m * TPC] = static_cast<uint32_t>(q) | (static_cast<uint32_t>(qq - q) << 8) | (1u << 16);
-                    ev[m * TPC] = sval;
+                    // the tail's value goes into its last two words (read by the normal's spin in B:
+                    // lo at the normal's word, hi just before it; no other attempt reads them)
+                    ub[qq - 1] = static_cast<uint32_t>(__double2loint(sval));
+                    ub[qq - 2] = static_cast<uint32_t>(__double2hiint(sval));
                     slow += qq - q;
                     pos = qq;
                 } else {
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
 
         // ---- A2e: walk the candidates with their outcomes; every lane keeps the word offset
         //      of each of its spins packed 6 bits per field (10 fields per u64) and a mask of its
-        //      tail normals, whose value goes into the tail's last two words
+        //      tail normals (their value already sits in the tail's last two words)
         uint64_t P0 = 0, P1 = 0;  // fields 0..9 and 10..15
         uint32_t specm = 0;
         {
@@ -415,12 +415,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                         const uint64_t msk = (kF36 << (6 * (jl - 10))) & kF36;
                         P1 = (P1 & ~msk) | (val & msk);
                     }
-                    if (tail && jl >= 0) {
-                        specm |= 1u << jl;
-                        const double sv = ev[j * TPC];
-                        ub[new_pos - 1] = static_cast<uint32_t>(__double2loint(sv));
-                        ub[new_pos - 2] = static_cast<uint32_t>(__double2hiint(sv));
-                    }
+                    if (tail && jl >= 0) specm |= 1u << jl;
                 }
                 pos = new_pos;
                 i = new_i;
