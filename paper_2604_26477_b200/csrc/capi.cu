@@ -345,6 +345,27 @@ void set_instance(Ctx& c, const momc_instance_view* iv)
     for (double a : absum)
         if (!(a < 2147483647.0)) integral = false;
     c.integer_weights = integral;
+    // cut value ranges (a cut sums a subset of the edges' weights): with integer weights and
+    // at most 64 bits for all K offsets, archive orders sort one packed key
+    c.cut_pack = false;
+    c.cut_lo.assign(static_cast<size_t>(c.k), 0);
+    c.cut_bits.assign(static_cast<size_t>(c.k), 0);
+    if (integral) {
+        int total = 0;
+        for (int q = 0; q < c.k; ++q) {
+            long long lo = 0, hi = 0;
+            for (int e = 0; e < c.m; ++e) {
+                const long long w = static_cast<long long>(c.h_w[static_cast<size_t>(e) * c.k + q]);
+                (w < 0 ? lo : hi) += w;
+            }
+            int bits = 1;
+            while (bits < 62 && (1ll << bits) <= hi - lo) ++bits;
+            c.cut_lo[static_cast<size_t>(q)] = lo;
+            c.cut_bits[static_cast<size_t>(q)] = bits;
+            total += bits;
+        }
+        c.cut_pack = total <= 64;
+    }
     // CSR of the symmetric graph, rows i, columns ascending; eidx maps a slot to its edge
     c.nnz = 2 * c.m;
     std::vector<int> deg(static_cast<size_t>(c.n) + 1, 0);

@@ -73,6 +73,10 @@ struct Ctx {
     int n = 0, k = 0, m = 0, nnz = 0;
     long long inst_gen = 0;  // bumped by every set_instance (caches keyed on the instance)
     bool integer_weights = false;  // every weight integral and sum |w| < 2^31 (exact int32 cut path)
+    bool cut_pack = false;         // cut values of all K objectives fit one 64-bit key (offsets)
+    std::vector<long long> cut_lo; // per objective: smallest possible cut value
+    std::vector<int> cut_bits;     // per objective: key bits
+    bool values_are_cuts = false;  // the filter in progress orders this instance's cut values
     std::vector<int> h_ei, h_ej;
     std::vector<double> h_w;
     DevBuf<int> d_ei, d_ej, d_rowptr, d_col, d_eidx;

@@ -911,9 +911,61 @@ __global__ void k_map_u32(const uint32_t* __restrict__ idx, const uint32_t* __re
 }
 
 // rank[i] = position of row i in the lexicographically descending order (rows distinct)
+struct PackGeo {
+    long long lo[kMaxK];
+    int shift[kMaxK];
+};
+
+// packed lexicographic key: objective 0 in the most significant bits (exact: integer cut
+// values within their ranges)
+__global__ void k_packed_keys(const double* __restrict__ vals, long long F, int K, PackGeo g, unsigned long long* keys,
+                              uint32_t* idx)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        unsigned long long key = 0;
+        for (int k = 0; k < K; ++k)
+            key |= static_cast<unsigned long long>(static_cast<long long>(vals[i * K + k]) - g.lo[k]) << g.shift[k];
+        keys[i] = key;
+        idx[i] = static_cast<uint32_t>(i);
+    }
+}
+
 void lex_desc_rank(Ctx& c, const double* d_vals, long long F, int K, long long* rank)
 {
     if (F <= 0) return;
+    if (c.values_are_cuts && c.cut_pack && K == c.k) {  // one radix pass over packed keys
+        PackGeo g{};
+        int sh = 64;
+        for (int k = 0; k < K; ++k) {
+            sh -= c.cut_bits[static_cast<size_t>(k)];
+            g.lo[k] = c.cut_lo[static_cast<size_t>(k)];
+            g.shift[k] = sh;
+        }
+        DevBuf<uint32_t> ia, ib;
+        DevBuf<unsigned long long> ka, kb;
+        ia.reserve(static_cast<size_t>(F));
+        ib.reserve(static_cast<size_t>(F));
+        ka.reserve(static_cast<size_t>(F));
+        kb.reserve(static_cast<size_t>(F));
+        k_packed_keys<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, F, K, g, ka.p, ia.p);
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, ka.p, kb.p, ia.p, ib.p, static_cast<int>(F), sh, 64,
+                                                  c.stream);
+        DevBuf<unsigned char> tmp;
+        tmp.reserve(tb + 1);
+        ck(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, ka.p, kb.p, ia.p, ib.p, static_cast<int>(F), sh, 64,
+                                                     c.stream),
+           "sort");
+        k_rank_of<<<grid_blocks(F), 256, 0, c.stream>>>(ib.p, F, rank);
+        c.launches += 3;
+        ia.release();
+        ib.release();
+        ka.release();
+        kb.release();
+        tmp.release();
+        return;
+    }
     DevBuf<uint32_t> ia, ib;
     DevBuf<unsigned long long> ka, kb;
     ia.reserve(static_cast<size_t>(F));
@@ -1120,7 +1172,14 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
         tm->unique_configs = U;
     }
     trace("filter_pool: finish_archive");
-    finish_archive(c, s, vv.p, V, K, d_words, vcfg.p, wpc, out, tm);
+    c.values_are_cuts = true;
+    try {
+        finish_archive(c, s, vv.p, V, K, d_words, vcfg.p, wpc, out, tm);
+    } catch (...) {
+        c.values_are_cuts = false;
+        throw;
+    }
+    c.values_are_cuts = false;
     trace("filter_pool: archive done");
     vrow.release();
     vown.release();
