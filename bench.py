@@ -45,6 +45,9 @@ WORKLOAD = "C2: 42-node heavy-hex K=4 MO-MaxCut, dSB, 220 weights (H=13) x batch
 GOLDEN = os.path.join(ROOT, "tests", "golden", "c2_heavyhex_k4_dsb.npz")
 EXACT = os.path.join(ROOT, "tests", "golden", "heavyhex42_k{k}_exact.npz")
 TTO_MAX_RUNS = {4: 512, 3: 64}  # bound on the streaming run (K=4 needs ~104 runs, K=3 ~3)
+# runs sampled per streaming step (one launch, one merge, one HV check): the K=4 stream
+# checks every 2 runs (merge + HV ~1.2 ms against a 10.7 ms run), the short K=3 one every run
+TTO_RUNS_PER_STEP = {4: 2, 3: 1}
 CPU_SAMPLE_BATCH = 512  # reference arm / cpu_baseline: 220 x 512 = 112,640 samples per step
 
 # Algorithmic lane-operations of one SB sample at n=42, |E|=45, T=50:
@@ -353,7 +356,7 @@ def main():
                 sk.set_instance(ik)  # model build inside the clock
                 sk.set_weights(wk)
             res = streaming.time_to_target(sessions[0], ck, r_frozen, target, TTO_MAX_RUNS[k], world, rank,
-                                           torch.device("cuda", local))
+                                           torch.device("cuda", local), runs_per_step=TTO_RUNS_PER_STEP[k])
             torch.cuda.synchronize(local)
             secs = time.perf_counter() - t0
             if world > 1:
@@ -361,7 +364,7 @@ def main():
             tto[f"k{k}"] = {"seconds": secs if res["reached"] else None, "reached": res["reached"],
                             "runs": res["runs"], "samples": res["samples"], "hv": res["hv"], "hv_star": target,
                             "archive": res["archive"], "front_exact": int(g["values"].shape[0]),
-                            "reference_frozen": r_frozen, "contexts": len(sessions),
+                            "reference_frozen": r_frozen, "runs_per_check": TTO_RUNS_PER_STEP[k] * world,
                             "shape": "C2 (K=4 dSB, 220 x 4546)" if k == 4 else "C1 (K=3 bSB, 190 x 3000)"}
             del sessions
 

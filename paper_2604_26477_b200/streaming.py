@@ -26,7 +26,7 @@ def _packed_front(session, device):
 
 
 def time_to_target(session, cfg, reference, hv_target: float, max_runs: int, world: int = 1, rank: int = 0,
-                   device=None, trace: list | None = None) -> dict:
+                   device=None, trace: list | None = None, runs_per_step: int = 1) -> dict:
     """Runs rounds until the running archive's HV at `reference` equals `hv_target` (exact
     arithmetic for integer weights) or `max_runs` runs are spent. Returns the number of
     runs / samples used, the wall time (device-synchronised, this rank) and the final HV.
@@ -35,7 +35,9 @@ def time_to_target(session, cfg, reference, hv_target: float, max_runs: int, wor
 
     One GPU: one C-ABI call per run (momc_b200_stream_step: sample -> front -> merge into the
     context's running archive -> HV). N ranks: each rank's run front is all-gathered (NCCL)
-    and merged into every rank's running archive (momc_b200_running_merge_values)."""
+    and merged into every rank's running archive (momc_b200_running_merge_values).
+    `runs_per_step` runs are sampled per call (one launch, one merge, one HV check), so the
+    check happens every runs_per_step x world runs."""
     device = device or torch.device("cuda", torch.cuda.current_device())
     k = session.inst.k()
     per_run = session.num_blocks(cfg, 1)
@@ -43,20 +45,21 @@ def time_to_target(session, cfg, reference, hv_target: float, max_runs: int, wor
     session.running_reset()
     hv, F, runs_done = 0.0, 0, 0
     t0 = time.perf_counter()
-    rounds = (max_runs + world - 1) // world
+    R = max(1, int(runs_per_step))
+    rounds = (max_runs + world * R - 1) // (world * R)
     for q in range(rounds):
-        run = q * world + rank
+        run = (q * world + rank) * R  # this rank's first run of the round
         if world == 1:
-            hv, F, _ = session.stream_step(cfg, run + 1, run * per_run, (run + 1) * per_run, reference)
+            hv, F, _ = session.stream_step(cfg, run + R, run * per_run, (run + R) * per_run, reference)
         else:
-            session.stream_step(cfg, run + 1, run * per_run, (run + 1) * per_run, None, merge=False)
+            session.stream_step(cfg, run + R, run * per_run, (run + R) * per_run, None, merge=False)
             rows = mdist.allgather_rows(_packed_front(session, device))
             vals = rows[:, :k].contiguous().view(torch.float64)
             words = rows[:, k:].contiguous()
             torch.cuda.current_stream(device).synchronize()
             hv, F = session.running_merge_values(vals.data_ptr(), words.data_ptr(), words.shape[1], vals.shape[0], k,
                                                  reference)
-        runs_done = (q + 1) * world
+        runs_done = (q + 1) * world * R
         if trace is not None:
             trace.append({"runs": runs_done, "samples": runs_done * samples_per_run, "archive": F, "hv": hv,
                           "wall_s": time.perf_counter() - t0})
