@@ -386,6 +386,17 @@ def main():
                 "note": "neither HBM- nor tensor-bound: integer Philox + FP64 update; peak = SMs x 128 lanes "
                         "x sm_max_mhz dispatch rate; algorithmic ops/sample in DESIGN.md",
                 "kernel_share_of_step": sampling_s / (ms_per_step * 1e-3)}
+    # calibration: the sampler's per-word noise work alone, at full occupancy
+    try:
+        nps = s.rng_calibrate(2048)
+        words = 42 * 50 * 1.08 + 4 * 42  # step normals incl. slow-attempt words, + init draws
+        roofline["rng_calibration"] = {
+            "normals_per_s": nps, "words_per_sample": words,
+            "rng_only_ms_per_step": samples_total / world * words / nps * 1e3,
+            "sampler_ms_per_step": sampling_s * 1e3,
+            "note": "Philox + ziggurat fast path + eta only (calib.cu): the RNG share of the sampler's floor"}
+    except Exception as ex:  # informational only
+        roofline["rng_calibration"] = {"unavailable": str(ex)}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

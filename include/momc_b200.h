@@ -173,6 +173,10 @@ int momc_b200_convergence_trace(momc_ctx* ctx, const uint64_t* words, const int6
 int momc_b200_tc_i8_selftest(momc_ctx* ctx, const int8_t* A, const int8_t* B, int K, int32_t* D, char* err,
                              size_t errlen);
 
+/* Roofline calibration: normals/s of a kernel doing only the sampler's per-word noise work
+ * (Philox block per 4 words, ziggurat fast test, eta = hz * wn[iz]). */
+int momc_b200_rng_calibrate(momc_ctx* ctx, int blocks_per_thread, double* normals_per_s, char* err, size_t errlen);
+
 /* ---------------------------------------------------------------- pool CSV (solver.hpp:357-432) */
 /* The record rows of save_pool_csv, formatted on the device: for each of M records
  * "run,weight,trajectory,timestamp_ns,<16 hex nibbles per word>\n". With out == NULL only

@@ -114,6 +114,7 @@ SIGNATURES = [
                                                          C.c_char_p, C.c_size_t]),
     ("momc_b200_measured_correlation", C.c_int, [vp, C.c_int, C.c_uint64, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_tc_i8_selftest", C.c_int, [vp, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_char_p, C.c_size_t]),
+    ("momc_b200_rng_calibrate", C.c_int, [vp, C.c_int, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_running_reset", C.c_int, [vp, C.c_char_p, C.c_size_t]),
     ("momc_b200_stream_step", C.c_int, [vp, C.POINTER(SolverCfgC), C.c_int, C.c_longlong, C.c_longlong, C.c_int, dp,
                                         dp, i64p, C.POINTER(BenchReportC), C.c_char_p, C.c_size_t]),

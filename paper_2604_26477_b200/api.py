@@ -658,6 +658,13 @@ class Session:
                                                     C.byref(F), err, 2048), err)
         return F.value
 
+    def rng_calibrate(self, blocks_per_thread: int = 2048) -> float:
+        """normals/s of the RNG-only calibration kernel (roofline: the sampler's noise share)"""
+        out = C.c_double()
+        err = _errbuf()
+        _raise(self.lib.momc_b200_rng_calibrate(self.h, blocks_per_thread, C.byref(out), err, 2048), err)
+        return out.value
+
     # ---- streaming (running archive on the context)
     def running_reset(self):
         err = _errbuf()

@@ -1234,6 +1234,15 @@ int momc_b200_tc_i8_selftest(momc_ctx* ctx, const int8_t* A, const int8_t* B, in
     });
 }
 
+int momc_b200_rng_calibrate(momc_ctx* ctx, int blocks_per_thread, double* normals_per_s, char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        if (blocks_per_thread < 1) usage("blocks_per_thread must be positive");
+        *normals_per_s = rng_calibrate(*ctx, blocks_per_thread);
+    });
+}
+
 int momc_b200_clamp_reference(momc_ctx* ctx, double* r, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {

@@ -144,6 +144,8 @@ long long parse_pool_rows(Ctx& c, const char* text, size_t len, int n, int first
 void parsed_pool_get(Ctx& c, uint32_t* run, uint32_t* wt, uint32_t* tr, int64_t* ts, uint64_t* words);
 // tc_selftest.cu: D = A . B^T (128 x 128, int8 -> int32) through the hand-written tcgen05 path
 void tc_i8_selftest(Ctx& c, const int8_t* hA, const int8_t* hB, int K, int32_t* hD);
+// calib.cu: normals/s of the RNG-only calibration kernel
+double rng_calibrate(Ctx& c, int blocks_per_thread);
 // capi.cu: the ziggurat tables on the device (uploaded once)
 const ZigTables* device_zig(Ctx& c);
 // instance_gen.cu

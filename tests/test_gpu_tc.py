@@ -20,3 +20,10 @@ def test_tc_i8_gemm_exact(session, K, seed):
     assert rc == 0, err.value
     want = A.astype(np.int64) @ B.astype(np.int64).T
     assert np.array_equal(D.astype(np.int64), want)
+
+
+def test_rng_calibration_rate(session):
+    """calib.cu: the noise-only microkernel behind roofline.rng_calibration runs and reports
+    a rate in a plausible band for one B200 (measured 1.0e12 normals/s)"""
+    nps = session.rng_calibrate(256)
+    assert 1e11 < nps < 1e13
