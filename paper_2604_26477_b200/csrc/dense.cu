@@ -10,15 +10,16 @@
 // so trajectories agree within the FP tolerance stated in DESIGN.md (spin words are compared
 // against the reference in tests/test_gpu_dense.py), not bit-for-bit.
 //
-// Layout (one batch per (run, weight) pair):
-//   Phi  int8  [pair][traj][spin]   (GEMM A operand, op T)
-//   HJ   int8  [weight][spin][spin] (GEMM B operand; symmetric)
-//   D    int32 [pair][spin][traj]   (GEMM output; coalesced for the update kernel)
-//   x, y f64   [pair][spin][traj]
-// The update kernel runs one thread per trajectory (the noise stream of a (trajectory, step)
-// is sequential over spins, rng.hpp:156-185) and stages Phi rows through shared memory.
-// The GEMM is cuBLASLt's int8 batched matmul (a plain library GEMM); the fused tcgen05
-// kernel with the SB update in its epilogue is the next step.
+// Layout (one batch per (run, weight) pair), default path:
+//   Phi  int8  [pair][traj][spin]   (GEMM B operand, K-major)
+//   HJ   int8  [weight][spin][spin] (GEMM A operand; symmetric)
+//   D    int32 [pair][traj][spin]   (GEMM output D^T = (H J) Phi^T)
+//   x, y f64   [pair][traj][spin]
+// The update kernel (k_dense_warp) integrates one trajectory per warp, 32 spins per window:
+// every access of a warp is one contiguous run, and the trajectory's sequential noise stream
+// (rng.hpp:156-185) is resolved warp-wide per window. The GEMM is cuBLASLt's int8 batched
+// matmul (a plain library GEMM). The fused tcgen05 step (MOMC_DENSE_TC=1) keeps x, y
+// spin-major ([pair][spin][traj]) and one thread per trajectory.
 #include <cublasLt.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -65,8 +66,15 @@ struct PairOf {
 };
 
 // init_state (solver.hpp:108-124) for one (run, weight) pair block of trajectories
+// x / y element of (pair pb, spin i, trajectory t): spin-major [pair][spin][traj] for the
+// per-thread kernels, trajectory-major [pair][traj][spin] for the warp-per-trajectory update
+__host__ __device__ __forceinline__ long long xy_at(long long pb, int n, int batch_pad, int i, int t, bool tmajor)
+{
+    return tmajor ? (pb * batch_pad + t) * n + i : (pb * n + i) * batch_pad + t;
+}
+
 __global__ void k_dense_init(int n, int batch_pad, const PairOf* __restrict__ pairs, uint64_t seed, double h,
-                             double* x, double* y, signed char* phi)
+                             double* x, double* y, signed char* phi, bool tmajor)
 {
     const PairOf pr = pairs[blockIdx.y];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -76,18 +84,16 @@ __global__ void k_dense_init(int n, int batch_pad, const PairOf* __restrict__ pa
         DevStream sx, sy;
         sx.init(key, pr.l, pr.traj0 + t, tag_word(kTagInitX, 0));
         sy.init(key, pr.l, pr.traj0 + t, tag_word(kTagInitY, 0));
-        double* xs = x + pb * n * batch_pad;
-        double* ys = y + pb * n * batch_pad;
         signed char* ph = phi + (pb * batch_pad + t) * n;
         for (int i = 0; i < n; ++i) {
             const double u = static_cast<double>(sx.next_u64() >> 11) * 0x1.0p-53;
             const double xv = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, u), 1.0));
-            xs[static_cast<long long>(i) * batch_pad + t] = xv;
+            x[xy_at(pb, n, batch_pad, i, t, tmajor)] = xv;
             ph[i] = xv < 0.0 ? -1 : 1;
         }
         for (int i = 0; i < n; ++i) {
             const double u = static_cast<double>(sy.next_u64() >> 11) * 0x1.0p-53;
-            ys[static_cast<long long>(i) * batch_pad + t] = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, u), 1.0));
+            y[xy_at(pb, n, batch_pad, i, t, tmajor)] = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, u), 1.0));
         }
     } else if (t < batch_pad) {  // padding trajectories: phi = +1 rows (never read back)
         signed char* ph = phi + (pb * batch_pad + t) * n;
@@ -173,45 +179,6 @@ __device__ __noinline__ RingSlow ring_normal_slow(uint32_t* r, uint32_t k0, uint
     }
 }
 
-// all inline (the update kernel, register-capped at 56: a call would spill the ring state)
-__device__ __forceinline__ double ring_normal_inline(WordRing& w, const ZigTables* __restrict__ z)
-{
-    for (;;) {
-        w.ensure(1);
-        const uint32_t u = w.at(0);
-        const int32_t hz = static_cast<int32_t>(u);
-        const uint32_t iz = u & 127u;
-        const uint32_t mag = hz < 0 ? 0u - u : u;
-        if (mag < z->kn[iz]) {
-            ++w.head;
-            return __dmul_rn(static_cast<double>(hz), z->wn[iz]);
-        }
-        if (iz == 0) {
-            ++w.head;
-            const double rr = 3.442619855899;
-            for (;;) {
-                w.ensure(4);
-                const double xx = __ddiv_rn(-log(u01_open_from(w.at(0), w.at(1))), rr);
-                const double yy = -log(u01_open_from(w.at(2), w.at(3)));
-                w.head += 4;
-                if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) return hz > 0 ? __dadd_rn(rr, xx) : -__dadd_rn(rr, xx);
-            }
-        }
-        w.ensure(3);
-        const double xv = __dmul_rn(static_cast<double>(hz), z->wn[iz]);
-        const double u01 = u01_from(w.at(1), w.at(2));
-        w.head += 3;
-        const double lhs = __dadd_rn(z->fn[iz], __dmul_rn(u01, __dsub_rn(z->fn[iz - 1], z->fn[iz])));
-        const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
-        const float ef = __expf(static_cast<float>(targ));
-        bool accept;
-        if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) accept = true;
-        else if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) accept = false;
-        else accept = lhs < exp(targ);
-        if (accept) return xv;
-    }
-}
-
 __device__ __forceinline__ double ring_normal(WordRing& w, const ZigTables* __restrict__ z)
 {
     if (w.tail - w.head >= 1) {
@@ -231,97 +198,242 @@ __device__ __forceinline__ double ring_normal(WordRing& w, const ZigTables* __re
     return r.v;
 }
 
-constexpr int kDenseTile = 64;  // spins per shared-memory phi tile
+// init_state (solver.hpp:108-124) in the trajectory-major layout: one warp per trajectory,
+// lanes over spins; spin i takes words 2i, 2i+1 of the init_x / init_y streams (block i/2,
+// half i%2), so every store of a warp is one contiguous run
+__global__ void __launch_bounds__(256) k_dense_init_t(int n, int batch_pad, const PairOf* __restrict__ pairs,
+                                                      uint64_t seed, double h, double* x, double* y, signed char* phi)
+{
+    const PairOf pr = pairs[blockIdx.y];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = blockIdx.x * 8 + warp;
+    if (t >= batch_pad) return;
+    const long long rowe = (static_cast<long long>(blockIdx.y) * batch_pad + t) * n;
+    if (t >= pr.count) {  // padding trajectories: phi = +1 rows (never read back)
+        for (int i = lane; i < n; i += 32) phi[rowe + i] = 1;
+        return;
+    }
+    const uint64_t key = run_key(seed, static_cast<uint32_t>(pr.run));
+    const uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
+    const uint32_t tr = static_cast<uint32_t>(pr.traj0 + t), wl = static_cast<uint32_t>(pr.l);
+    for (int i = lane; i < n; i += 32) {
+        const uint4 rx = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitX, 0), tr, wl);
+        const uint4 ry = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitY, 0), tr, wl);
+        const bool odd = i & 1;
+        const double xv = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(rx.z, rx.w) : u01_from(rx.x, rx.y)), 1.0));
+        const double yv = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(ry.z, ry.w) : u01_from(ry.x, ry.y)), 1.0));
+        x[rowe + i] = xv;
+        y[rowe + i] = yv;
+        phi[rowe + i] = xv < 0.0 ? -1 : 1;
+    }
+}
 
-// one dSB step for every trajectory: y += dt((a_t - a0) x - (c0/H) D + alpha eta);
-// x += dt a0 y; wall; clamp; phi = sgn(x). D = (H J(c)) sgn(X) is exact (int32); the one
-// rounding of c0/H replaces the reference's per-product roundings of J (tolerance: DESIGN §3).
-// 9 CTAs of 128 per SM (<= 56 registers, 19 KB smem): the C4 grid (55 x 24 CTAs) is one wave
-__global__ void __launch_bounds__(128, 9) k_dense_update(int n, int batch_pad, int H, const PairOf* __restrict__ pairs,
-                                                      uint64_t seed, int t_step, int T, double dt, double a0,
-                                                      double alpha, double sdt, const double* __restrict__ c0s,
-                                                      const ZigTables* __restrict__ zig, const int* __restrict__ D,
-                                                      double* x, double* y, signed char* phi, int* bad)
+// ---- warp-per-trajectory dSB update (the default dense path). x, y and D are stored
+// trajectory-major ([pair][traj][spin]); a warp integrates one trajectory, 32 spins per
+// window, lane L taking spin s0 + L, so every x / y / D / phi access of a warp is one
+// contiguous run. The (trajectory, step) noise stream (rng.hpp:156-185) is resolved per
+// window of 32 normals, warp-wide:
+//   * the 32 lanes generate Philox blocks together (block tail/4 + L on lane L) into a
+//     256-word ring per warp, 128 words at a time;
+//   * round 1: lane L tests the word at head + L (|hz| < kn[iz]); slow words are wedge
+//     attempts (3 words), tested in parallel by their lanes; a ballot gives the producing
+//     positions (fast words not consumed by an attempt, accepted attempts) and each lane's
+//     normal index is the popcount below it; round 2 (words after round 1's last attempt)
+//     supplies the normals round 1 fell short of;
+//   * windows with a tail attempt, a slow word inside another attempt's words, or a round 2
+//     that falls short (about 1 in 10) are walked sequentially by the whole warp.
+// The values go through a 32-entry shared buffer to the lanes of their spins.
+constexpr int kWRing = 256;  // words per warp
+constexpr int kWWarps = 8;   // trajectories (warps) per CTA
+
+struct DensePairArg {
+    uint32_t k0, k1;  // run_key(seed, run)
+    int l, traj0, count;
+    int pad_;
+    double c0h;  // c0_l / H, rounded once
+};
+constexpr int kDensePairsPerLaunch = 256;
+// per-launch arguments, passed by value: per-pair values are indexed by blockIdx.y and load
+// as per-CTA constants
+struct DenseStepArgs {
+    int n, batch_pad, t_step, pair0;   // pair0: index of pair[0] in the group's state arrays
+    double neg_drift, dt, alpha, sdt;  // -(a0 - a_t) (solver.hpp:70-76), dt, alpha, dt * a0
+    const ZigTables* zig;
+    const int* D;
+    double* x;
+    double* y;
+    signed char* phi;
+    int* bad;
+    DensePairArg pair[kDensePairsPerLaunch];
+};
+
+__device__ __forceinline__ uint32_t zmag32(uint32_t u) { return static_cast<int32_t>(u) < 0 ? 0u - u : u; }
+
+// wedge test of the attempt at word u with uniform words (w1, w2) (rng.hpp:178-183): the FP32
+// exp brackets the FP64 one within 1e-6 relative on [-6, 0]; the FP64 exp decides the band
+__device__ __forceinline__ bool wedge_accept(uint32_t u, uint32_t w1, uint32_t w2, const ZigTables& z)
+{
+    const uint32_t iz = u & 127u;
+    const double xv = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), z.wn[iz]);
+    const double lhs = __dadd_rn(z.fn[iz], __dmul_rn(u01_from(w1, w2), __dsub_rn(z.fn[iz - 1], z.fn[iz])));
+    const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
+    const float ef = __expf(static_cast<float>(targ));
+    if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) return true;
+    if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) return false;
+    return lhs < exp(targ);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt()
+{
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <bool NOISY>
+__global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_constant__ DenseStepArgs a)
 {
     __shared__ ZigTables z;
-    __shared__ __align__(16) signed char tile[128][kDenseTile + 4];
-    __shared__ uint32_t ring[16 * 128];
-    for (int q = threadIdx.x; q < static_cast<int>(sizeof(ZigTables) / 4); q += blockDim.x)
-        reinterpret_cast<uint32_t*>(&z)[q] = reinterpret_cast<const uint32_t*>(zig)[q];
-    __syncthreads();
-    const PairOf pr = pairs[blockIdx.y];
-    const long long pb = blockIdx.y;
-    const int t0 = blockIdx.x * blockDim.x;
-    const int t = t0 + threadIdx.x;
-    const bool active = t < pr.count;
-    const double c0h = __ddiv_rn(c0s[pr.l], static_cast<double>(H));
-    const double a_t = __ddiv_rn(static_cast<double>(t_step + 1), static_cast<double>(T));
-    const double neg_drift = -__dsub_rn(a0, a_t);
-    const bool noisy = alpha > 0.0;
-    WordRing w;
-    {
-        const uint64_t key = run_key(seed, static_cast<uint32_t>(pr.run));
-        w.r = ring + threadIdx.x;
-        w.k0 = static_cast<uint32_t>(key);
-        w.k1 = static_cast<uint32_t>(key >> 32);
-        w.lo = tag_word(kTagStepNoise, static_cast<uint32_t>(t_step));
-        w.mid = static_cast<uint32_t>(pr.traj0 + t);
-        w.hi = static_cast<uint32_t>(pr.l);
-        w.blk = 0;
-        w.head = w.tail = 0;
+    __shared__ __align__(16) uint32_t rings[kWWarps][kWRing];
+    __shared__ double vals[kWWarps][32];
+    if constexpr (NOISY) {
+        for (int q = threadIdx.x; q < static_cast<int>(sizeof(ZigTables) / 4); q += blockDim.x)
+            reinterpret_cast<uint32_t*>(&z)[q] = reinterpret_cast<const uint32_t*>(a.zig)[q];
+        __syncthreads();
     }
-    const int* Dp = D + pb * n * static_cast<long long>(batch_pad);
-    double* xs = x + pb * n * static_cast<long long>(batch_pad);
-    double* ys = y + pb * n * static_cast<long long>(batch_pad);
+    const DensePairArg& pr = a.pair[blockIdx.y];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = blockIdx.x * kWWarps + warp;
+    if (t >= pr.count) return;  // whole warps; no CTA barrier below
+    const int n = a.n;
+    uint32_t* ring = rings[warp];
+    double* val = vals[warp];
+    const uint32_t k0 = pr.k0, k1 = pr.k1, lo = tag_word(kTagStepNoise, static_cast<uint32_t>(a.t_step));
+    const uint32_t mid = static_cast<uint32_t>(pr.traj0 + t), hi = static_cast<uint32_t>(pr.l);
+    const uint32_t lt = lanemask_lt();
+    int head = 0, tail = 0;  // next unread word / words generated (warp-uniform)
+    auto gen = [&]() {       // 128 words: block tail/4 + lane on each lane
+        const uint4 v = philox(k0, k1, static_cast<uint32_t>(tail >> 2) + static_cast<uint32_t>(lane), lo, mid, hi);
+        *reinterpret_cast<uint4*>(&ring[(tail + 4 * lane) & (kWRing - 1)]) = v;
+        tail += 128;
+        __syncwarp();
+    };
+    auto word = [&](int p) -> uint32_t {  // any position: the ring, or generated directly (slow path)
+        if (p < tail) return ring[p & (kWRing - 1)];
+        const uint4 v = philox(k0, k1, static_cast<uint32_t>(p >> 2), lo, mid, hi);
+        const int c = p & 3;
+        return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+    };
+    auto is_fast = [&](uint32_t u) { return zmag32(u) < z.kn[u & 127u]; };
+    auto fast_val = [&](uint32_t u) { return __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), z.wn[u & 127u]); };
+
+    // element index of (trajectory t, spin 0) in x / y / D / phi (< 2^32 within a group)
+    const uint32_t row = (static_cast<uint32_t>(a.pair0 + static_cast<int>(blockIdx.y)) * static_cast<uint32_t>(a.batch_pad) +
+                          static_cast<uint32_t>(t)) * static_cast<uint32_t>(n);
     bool nonfinite = false;
-    for (int i0 = 0; i0 < n; i0 += kDenseTile) {
-        const int lim = min(kDenseTile, n - i0);
-        if (active) {
-            // software pipeline: the next spin's loads are in flight during this spin's draw
-            long long o = static_cast<long long>(i0) * batch_pad + t;
-            int dn = Dp[o];
-            double xn = xs[o], yn = ys[o];
-            for (int q = 0; q < lim; ++q) {
-                if (noisy && (q & 3) == 0) {
-                    while (w.tail - w.head < 8) w.block();  // warp-synchronous top-up
-                }
-                const int dq = dn;
-                double xi = xn, yi = yn;
-                const long long oq = o;
-                if (q + 1 < lim) {
-                    o += batch_pad;
-                    dn = Dp[o];
-                    xn = xs[o];
-                    yn = ys[o];
-                }
-                const double eta = noisy ? ring_normal_inline(w, &z) : 0.0;
-                double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0h, static_cast<double>(dq)));
-                if (noisy) d = __dadd_rn(d, __dmul_rn(alpha, eta));
-                yi = __dadd_rn(yi, __dmul_rn(dt, d));
-                xi = __dadd_rn(xi, __dmul_rn(sdt, yi));
-                if (fabs(xi) > 1.0) {  // wall + clamp (both fire exactly when |x| > 1)
-                    yi = 0.0;
-                    xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
-                }
-                nonfinite |= !isfinite(xi) || !isfinite(yi);
-                xs[oq] = xi;
-                ys[oq] = yi;
-                tile[threadIdx.x][q] = xi < 0.0 ? -1 : 1;
+    // resolve the next window: k normals (lane L < k gets normal L in eta)
+    auto resolve = [&](int& k, double& eta) {
+        k = 32;
+        eta = 0.0;
+        if constexpr (NOISY) {
+            if (tail - head < 96) gen();
+            const int H = head;
+            const uint32_t u = ring[(H + lane) & (kWRing - 1)];
+            const bool slow = !is_fast(u);
+            const uint32_t sm = __ballot_sync(0xffffffffu, slow);
+            if (sm == 0) {  // 32 fast words: lane L's normal is its own word
+                eta = fast_val(u);
+                head = H + 32;
+                return;
             }
-        }
-        __syncthreads();
-        // coalesced store of the phi tile: rows of `lim` bytes, 4 bytes per thread and step
-        // (n % 16 == 0 on the dense path, so row starts are 4-byte aligned)
-        for (int q = threadIdx.x; q < 128 * (kDenseTile / 4); q += blockDim.x) {
-            const int r = q / (kDenseTile / 4), c4 = (q % (kDenseTile / 4)) * 4;
-            if (t0 + r < pr.count && c4 < lim) {
-                const uint32_t v = *reinterpret_cast<const uint32_t*>(&tile[r][c4]);
-                *reinterpret_cast<uint32_t*>(phi + (pb * batch_pad + t0 + r) * n + i0 + c4) = v;
+            // every slow word is tested as if an attempt started there (the ones inside another
+            // attempt's words are discarded below): wedges take 3 words, tails 1 + 4k and always
+            // give a normal (rng.hpp:164-184)
+            double v = 0.0;
+            bool good = !slow;  // this word gives a normal if it starts an attempt / is free
+            int len = 1;
+            if (slow) {
+                if (u & 127u) {
+                    good = wedge_accept(u, ring[(H + lane + 1) & (kWRing - 1)], ring[(H + lane + 2) & (kWRing - 1)], z);
+                    len = 3;
+                } else {
+                    const double r = 3.442619855899;
+                    int qq = H + lane + 1;
+                    for (;;) {
+                        const double xx = __ddiv_rn(-log(u01_open_from(word(qq), word(qq + 1))), r);
+                        const double yy = -log(u01_open_from(word(qq + 2), word(qq + 3)));
+                        qq += 4;
+                        if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) {
+                            v = static_cast<int32_t>(u) > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
+                            break;
+                        }
+                    }
+                    len = qq - (H + lane);
+                    good = true;
+                }
             }
+            if (good && !(slow && (u & 127u) == 0)) v = fast_val(u);
+            const uint32_t gm = __ballot_sync(0xffffffffu, good);
+            // the attempts, in order: the first slow word starts one, its words are consumed
+            uint32_t cons = 0, rem = sm;
+            int end = 32;  // first word after the window's last attempt (relative to H)
+            while (rem) {
+                const int q = __ffs(rem) - 1;
+                const int lq = __shfl_sync(0xffffffffu, len, q);
+                const uint32_t span = q + lq >= 32 ? ~0u << q : ((1u << lq) - 1u) << q;
+                cons |= span & ~(1u << q);
+                rem &= ~span;
+                end = q + lq > end ? q + lq : end;
+            }
+            const uint32_t prod = gm & ~cons;  // positions that give this window's normals
+            k = __popc(prod);
+            head = H + end;
+            if ((prod >> lane) & 1u) val[__popc(prod & lt)] = v;
+            __syncwarp();
+            eta = val[lane];
+            __syncwarp();  // read before the next window writes
         }
-        __syncthreads();
+    };
+    // software pipeline: the loads of window w are in flight while window w+1's noise is
+    // resolved (the noise does not depend on the state)
+    int s0 = 0, k;  // first spin / normal count of the current window
+    double eta;
+    resolve(k, eta);
+    while (s0 < n) {
+        const bool upd = s0 + lane < n && lane < k;
+        const uint32_t e = row + static_cast<uint32_t>(s0 + lane);
+        double xi = 0.0, yi = 0.0;
+        int dq = 0;
+        if (upd) {
+            xi = a.x[e];
+            yi = a.y[e];
+            dq = a.D[e];
+        }
+        int kn = 0;
+        double etan = 0.0;
+        if (s0 + k < n) resolve(kn, etan);
+        asm volatile("" : "+r"(dq)::"memory");  // keep the conversion (a wait on the load) here
+        // ---- the update of spin s0 + lane (sb_step solver.hpp:159-181, phi = sgn(x))
+        if (upd) {
+            double d = __dsub_rn(__dmul_rn(a.neg_drift, xi), __dmul_rn(pr.c0h, static_cast<double>(dq)));
+            if constexpr (NOISY) d = __dadd_rn(d, __dmul_rn(a.alpha, eta));
+            yi = __dadd_rn(yi, __dmul_rn(a.dt, d));
+            xi = __dadd_rn(xi, __dmul_rn(a.sdt, yi));
+            if (fabs(xi) > 1.0) {  // wall + clamp (both fire exactly when |x| > 1)
+                yi = 0.0;
+                xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
+            }
+            // the first step with a non-finite x or y has a non-finite y (x = x + dt a0 y, walls)
+            nonfinite |= !(fabs(yi) <= 1.7976931348623157e308);
+            a.x[e] = xi;
+            a.y[e] = yi;
+            a.phi[e] = xi < 0.0 ? -1 : 1;
+        }
+        s0 += k;
+        k = kn;
+        eta = etan;
     }
-    if (nonfinite) atomicMin(bad, t_step + 1);
+    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicMin(a.bad, a.t_step + 1);
 }
 
 // ---- fused tensor-core step (the default dense path): one CTA owns 128 trajectories of
@@ -517,20 +629,19 @@ CUtensorMap make_tmap_i8(const void* base, long long rows, int cols)
 }
 
 __global__ void k_dense_readout(int n, int batch_pad, int batch, int L, const PairOf* __restrict__ pairs,
-                                const double* __restrict__ x, uint64_t* words, long long row0, int* nanflag)
+                                const double* __restrict__ x, uint64_t* words, long long row0, int* nanflag, bool tmajor)
 {
     const PairOf pr = pairs[blockIdx.y];
     const long long pb = blockIdx.y;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= pr.count) return;
     const int wpc = (n + 63) / 64;
-    const double* xs = x + pb * n * static_cast<long long>(batch_pad);
     const long long idx = (static_cast<long long>(pr.run) * L + pr.l) * batch + pr.traj0 + t;
     bool bad = false;
     for (int wd = 0; wd < wpc; ++wd) {
         uint64_t word = 0;
         for (int b = 0; b < 64 && wd * 64 + b < n; ++b) {
-            const double v = xs[static_cast<long long>(wd * 64 + b) * batch_pad + t];
+            const double v = x[xy_at(pb, n, batch_pad, wd * 64 + b, t, tmajor)];
             word |= static_cast<uint64_t>(!(v < 0.0)) << b;
             bad |= v != v;
         }
@@ -696,6 +807,9 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
             pairs.push_back({run, l, first, cnt});
     }
     if (pairs.empty()) return;
+    std::vector<double> c0_host(static_cast<size_t>(L));
+    ck(cudaMemcpyAsync(c0_host.data(), p.c0, sizeof(double) * L, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "c0");
     int maxc = 0;
     for (auto& q : pairs) maxc = std::max(maxc, q.count);
     const int batch_pad = (maxc + 15) / 16 * 16;
@@ -720,7 +834,12 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
         ck(cudaMemsetAsync(d.flags.p, 0x7f, sizeof(int), c.stream), "memset");
         ck(cudaMemsetAsync(d.flags.p + 1, 0, sizeof(int), c.stream), "memset");
         const dim3 grid(static_cast<unsigned>((batch_pad + 127) / 128), static_cast<unsigned>(G));
-        k_dense_init<<<grid, 128, 0, c.stream>>>(n, batch_pad, d.pairs.p, p.seed, p.init_scale, d.x.p, d.y.p, d.phi.p);
+        if (use_tc)
+            k_dense_init<<<grid, 128, 0, c.stream>>>(n, batch_pad, d.pairs.p, p.seed, p.init_scale, d.x.p, d.y.p, d.phi.p,
+                                                     false);
+        else
+            k_dense_init_t<<<dim3(static_cast<unsigned>((batch_pad + 7) / 8), static_cast<unsigned>(G)), 256, 0, c.stream>>>(
+                n, batch_pad, d.pairs.p, p.seed, p.init_scale, d.x.p, d.y.p, d.phi.p);
         c.launches++;
         // all pairs of a group must share the weight stride pattern: B operand per pair = HJ of its weight
         // -> run one strided-batch GEMM per maximal run of consecutive weights within the group
@@ -739,6 +858,19 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
                 c.launches++;
             }
         } else {
+            // D^T per pair = (H J) . Phi^T: m = spins, n = trajectories, so D lands trajectory-major
+            static DenseStepArgs step_args;  // 8 KB of launch arguments (host-side staging only)
+            step_args.n = n;
+            step_args.batch_pad = batch_pad;
+            step_args.dt = p.dt;
+            step_args.alpha = p.alpha;
+            step_args.sdt = p.s_dt_a0;
+            step_args.zig = p.zig;
+            step_args.D = d.D.p;
+            step_args.x = d.x.p;
+            step_args.y = d.y.p;
+            step_args.phi = d.phi.p;
+            step_args.bad = d.flags.p;
             for (int t = 0; t < p.T; ++t) {
                 int q0 = 0;
                 while (q0 < G) {
@@ -746,17 +878,31 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
                     const PairOf& a = pairs[g0 + q0];
                     while (q1 < G && pairs[g0 + q1].l == pairs[g0 + q1 - 1].l + 1 && pairs[g0 + q1].run == a.run) ++q1;
                     const long long pstride = static_cast<long long>(n) * batch_pad;
-                    gemm_i8_batched(c, d.gemm, batch_pad, n, n, d.phi.p + q0 * pstride, pstride,
-                                    d.hj.p + static_cast<long long>(a.l) * n * n, static_cast<long long>(n) * n,
-                                    d.D.p + q0 * pstride, pstride, q1 - q0);
+                    gemm_i8_batched(c, d.gemm, n, batch_pad, n, d.hj.p + static_cast<long long>(a.l) * n * n,
+                                    static_cast<long long>(n) * n, d.phi.p + q0 * pstride, pstride, d.D.p + q0 * pstride,
+                                    pstride, q1 - q0);
                     q0 = q1;
                 }
-                k_dense_update<<<grid, 128, 0, c.stream>>>(n, batch_pad, c.H, d.pairs.p, p.seed, t, p.T, p.dt, p.a0, p.alpha,
-                                                           p.s_dt_a0, p.c0, p.zig, d.D.p, d.x.p, d.y.p, d.phi.p, d.flags.p);
-                c.launches++;
+                for (int s0 = 0; s0 < G; s0 += kDensePairsPerLaunch) {
+                    const int np = std::min(kDensePairsPerLaunch, G - s0);
+                    step_args.t_step = t;
+                    step_args.pair0 = s0;
+                    step_args.neg_drift = -(p.a0 - static_cast<double>(t + 1) / static_cast<double>(p.T));
+                    for (int q = 0; q < np; ++q) {
+                        const PairOf& pq = pairs[g0 + s0 + q];
+                        const uint64_t key = run_key(p.seed, static_cast<uint32_t>(pq.run));
+                        step_args.pair[q] = {static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32), pq.l, pq.traj0,
+                                             pq.count, 0, c0_host[static_cast<size_t>(pq.l)] / static_cast<double>(c.H)};
+                    }
+                    const dim3 wgrid(static_cast<unsigned>((maxc + kWWarps - 1) / kWWarps), static_cast<unsigned>(np));
+                    if (p.alpha > 0.0) k_dense_warp<true><<<wgrid, kWWarps * 32, 0, c.stream>>>(step_args);
+                    else k_dense_warp<false><<<wgrid, kWWarps * 32, 0, c.stream>>>(step_args);
+                    c.launches++;
+                }
             }
         }
-        k_dense_readout<<<grid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, p.row0, d.flags.p + 1);
+        k_dense_readout<<<grid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, p.row0,
+                                                    d.flags.p + 1, !use_tc);
         c.launches++;
         ck(cudaGetLastError(), "dense sampler");
         int fl[2] = {0, 0};
