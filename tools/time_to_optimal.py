@@ -36,8 +36,10 @@ def main():
     s.set_weights(api.build_weights(k, resolution=H))
     cfg = api.SolverConfig(variant=variant, batch_size=batch, seed=7)
     from paper_2604_26477_b200 import streaming
+    rps = 2 if k == 4 else 1  # runs per C-ABI call, as bench.py (TTO_RUNS_PER_STEP)
+    streaming.time_to_target(s, cfg, r, hv_star, 2 * rps, runs_per_step=rps)  # warm-up (allocations, plans)
     trace = []
-    res = streaming.time_to_target(s, cfg, r, hv_star, max_runs, trace=trace)
+    res = streaming.time_to_target(s, cfg, r, hv_star, max_runs, trace=trace, runs_per_step=rps)
     reached = res["runs"] if res["reached"] else None
     arc = s.archive(with_configs=False)
     missing = [list(x) for x in exact - {tuple(v) for v in arc.values}]
