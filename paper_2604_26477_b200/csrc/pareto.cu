@@ -332,18 +332,25 @@ __global__ void k_grid_scatter(const double* __restrict__ vals, long long V, int
 }
 
 // suffix max along one axis: S[.., a, ..] = max(S[.., a, ..], S[.., a+1, ..])
+// (consecutive threads take consecutive lines: coalesced; each thread loads 8 cells of its
+// line before it stores any, so 8 loads are in flight instead of one dependent chain)
 __global__ void k_suffix_max(uint32_t* S, long long cells, long long stride, int D)
 {
     const long long lines = cells / D;
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < lines;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long inner = t % stride, outer = t / stride;
-        long long p = outer * stride * D + inner + static_cast<long long>(D - 1) * stride;
-        uint32_t run = S[p];
-        for (int a = D - 2; a >= 0; --a) {
-            p -= stride;
-            run = max(run, S[p]);
-            S[p] = run;
+        uint32_t* line = S + outer * stride * D + inner;
+        uint32_t run = 0;
+        for (int a = D - 1; a >= 0; a -= 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = a - j >= 0 ? line[static_cast<long long>(a - j) * stride] : 0u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                run = max(run, v[j]);
+                if (a - j >= 0) line[static_cast<long long>(a - j) * stride] = run;
+            }
         }
     }
 }
