@@ -588,6 +588,28 @@ __global__ void k_ref_check(const double* __restrict__ vals, long long F, int K,
             if (r[k] > vals[i * K + k]) atomicMin(first, static_cast<unsigned long long>(i * K + k));
 }
 
+// integrality of the archive values and the largest gain v - r (decides the exact __int128 HV
+// sum): flags[0] &= every value is an integer below 9e15, flags[1] = max dkey(gain)
+__global__ void k_hv_stats(const double* __restrict__ vals, long long F, int K, const double* __restrict__ r,
+                           unsigned long long* flags)
+{
+    bool integral = true;
+    unsigned long long gmax = dkey(0.0);
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F * K;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double v = vals[i];
+        integral &= floor(v) == v && fabs(v) < 9.0e15;
+        const unsigned long long g = dkey(v - r[i % K]);
+        gmax = g > gmax ? g : gmax;
+    }
+    if (!__all_sync(0xffffffffu, integral) && (threadIdx.x & 31) == 0) atomicAnd(&flags[0], 0ull);
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long u = __shfl_xor_sync(0xffffffffu, gmax, o);
+        gmax = u > gmax ? u : gmax;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(&flags[1], gmax);
+}
+
 // MOMC_TRACE=1: host timestamps of the Pareto stage on stderr (diagnostics)
 void trace(const char* what)
 {
@@ -1278,7 +1300,8 @@ void filter_values_device(Ctx& c, const double* d_vals, const uint64_t* d_words,
     vv.release();
 }
 
-std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed)
+std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed, const double* clamp_vals,
+                                                   long long clamp_rows)
 {
     if (count < 1) usage("sampled reference needs count >= 1");
     if (c.n > 4096) usage("reference sampling on the GPU path supports n <= 4096");
@@ -1299,12 +1322,15 @@ std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t s
         evaluate_cuts_gemm(c, wd.p, nullptr, count, cv.p);
         k_col_min<<<grid_blocks(static_cast<long long>(count) * c.k), 256, 0, c.stream>>>(cv.p, count, c.k, rmin.p);
         c.launches++;
-        ck(cudaStreamSynchronize(c.stream), "reference point");
-        wd.release();
+        wd.release();  // stream-ordered: no host sync needed
         cv.release();
     } else {
         k_ref_sample<<<grid_blocks(count, 128), 128, 0, c.stream>>>(count, derive_key(seed, 0x70617265u), c.n, c.m, c.k,
                                                                      c.d_ei.p, c.d_ej.p, c.d_w.p, rmin.p);
+        c.launches++;
+    }
+    if (clamp_vals && clamp_rows > 0) {  // clamp_reference (pareto.hpp:647-655): min with every archive row
+        k_col_min<<<grid_blocks(clamp_rows * c.k), 256, 0, c.stream>>>(clamp_vals, clamp_rows, c.k, rmin.p);
         c.launches++;
     }
     std::vector<unsigned long long> h(static_cast<size_t>(c.k));
@@ -1331,30 +1357,34 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
     ck(cudaMemcpyAsync(s.rdev.p, r.data(), sizeof(double) * K, cudaMemcpyHostToDevice, c.stream), "H2D");
     const unsigned long long none = ~0ull;
     ck(cudaMemcpyAsync(s.counters.p + 3, &none, sizeof none, cudaMemcpyHostToDevice, c.stream), "H2D");
+    const unsigned long long stats_init[2] = {~0ull, dkey(0.0)};
+    ck(cudaMemcpyAsync(s.counters.p + 4, stats_init, sizeof stats_init, cudaMemcpyHostToDevice, c.stream), "H2D");
     k_ref_check<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, F, K, s.rdev.p, s.counters.p + 3);
-    c.launches++;
-    const unsigned long long bad = read_counter(c, s.counters.p + 3);
+    // gains are exact integers when every value and r is integral (n=42 configs): then the
+    // __int128 cell sum is the exact hypervolume, i.e. the reference's exact double result
+    k_hv_stats<<<grid_blocks(F * K), 256, 0, c.stream>>>(d_vals, F, K, s.rdev.p, s.counters.p + 4);
+    c.launches += 2;
+    unsigned long long st[3];
+    ck(cudaMemcpyAsync(st, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    const unsigned long long bad = st[0];
     if (bad != none)
         usage("reference point not dominated by archive entry " + std::to_string(bad / K) + " (objective " +
               std::to_string(bad % K) + ")");
-    // gains are exact integers when every value and r is integral (n=42 configs): then the
-    // __int128 cell sum is the exact hypervolume, i.e. the reference's exact double result
-    std::vector<double> hv(static_cast<size_t>(F) * K);
-    ck(cudaMemcpyAsync(hv.data(), d_vals, sizeof(double) * F * K, cudaMemcpyDeviceToHost, c.stream), "D2H");
-    ck(cudaStreamSynchronize(c.stream), "sync");
-    bool integral = true;
-    double maxg = 0;
-    for (long long i = 0; i < F; ++i)
-        for (int k = 0; k < K; ++k) {
-            const double g = hv[static_cast<size_t>(i * K + k)] - r[static_cast<size_t>(k)];
-            integral &= std::floor(hv[static_cast<size_t>(i * K + k)]) == hv[static_cast<size_t>(i * K + k)] &&
-                        std::fabs(hv[static_cast<size_t>(i * K + k)]) < 9.0e15;
-            maxg = std::max(maxg, g);
-        }
+    bool integral = st[1] != 0;
+    double maxg;
+    {
+        const uint64_t key = st[2];
+        const uint64_t b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
+        std::memcpy(&maxg, &b, 8);
+    }
     for (int k = 0; k < K; ++k) integral &= std::floor(r[static_cast<size_t>(k)]) == r[static_cast<size_t>(k)];
     if (integral && K * std::log2(std::max(maxg, 1.0)) > 120.0) integral = false;  // keep __int128 exact
     if (K == 1) {
         double best = 0;  // pareto.hpp:544-548
+        std::vector<double> hv(static_cast<size_t>(F));
+        ck(cudaMemcpyAsync(hv.data(), d_vals, sizeof(double) * F, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        ck(cudaStreamSynchronize(c.stream), "sync");
         for (long long i = 0; i < F; ++i) best = std::max(best, hv[static_cast<size_t>(i)] - r[0]);
         return best;
     }

@@ -49,7 +49,8 @@ void evaluate_cuts_device(Ctx& c, const uint64_t* d_words, long long U, double* 
 void evaluate_cuts_rows(Ctx& c, const uint64_t* d_words, const uint32_t* idx, long long U, double* d_out);
 
 // reference_point_sampled (pareto.hpp:620-642)
-std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed);
+std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed, const double* clamp_vals = nullptr,
+                                                   long long clamp_rows = 0);
 
 // hypervolume (pareto.hpp:540-552) of F x K values (device) against r (host); validates r
 // (pareto.hpp:103-118) and throws the reference's messages.
