@@ -30,3 +30,7 @@ def test_bench_two_ranks_functional():
     tto = d["time_to_optimal"]
     assert tto["k4"]["reached"] and tto["k4"]["hv"] == tto["k4"]["hv_star"]
     assert tto["k3"]["reached"] and tto["k3"]["runs"] % 2 == 0
+    # e2e through the public API with host buffers on every rank (not a copy of the device time)
+    e = d["e2e"]
+    assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] >= 1000120 * 8
+    assert e["value"] > 0 and e["ms_per_step"] != d["ms_per_step"]
