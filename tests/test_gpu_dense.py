@@ -23,13 +23,14 @@ def test_device_generator_matches_reference(ref, session, n, density, k, kind, l
     assert np.array_equal(inst.edge_i, ei) and np.array_equal(inst.edge_j, ej) and np.array_equal(inst.weights, w)
 
 
-def test_dense_dsb_agrees_with_reference(ref, session):
-    n, H = 512, 4
-    inst = session.generate_uniform_instance(n, 0.5, 3, 5)
-    ri = ref.generate_uniform(n, 0.5, 3, 5)
+@pytest.mark.parametrize("n,batch,seed", [(512, 48, 5), (272, 37, 6)])
+def test_dense_dsb_agrees_with_reference(ref, session, n, batch, seed):
+    """n = 272 leaves a half window (272 = 8 x 32 + 16) and batch 37 a partial CTA of warps"""
+    H = 4
+    inst = session.generate_uniform_instance(n, 0.5, 3, seed)
+    ri = ref.generate_uniform(n, 0.5, 3, seed)
     nums = ref.das_dennis(3, H)
     weights = [api.WeightVector(list(r), H) for r in nums]
-    batch = 48
     want = ref.run_sampler(ri, nums, H, make_cfg("dsb", batch_size=batch, seed=9, threads=16), 1)["words"]
     session.set_dense_threshold(256)
     session.set_weights(weights)
