@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -859,7 +860,9 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
             }
         } else {
             // D^T per pair = (H J) . Phi^T: m = spins, n = trajectories, so D lands trajectory-major
-            static DenseStepArgs step_args;  // 8 KB of launch arguments (host-side staging only)
+            // 8 KB of launch arguments, per call (contexts may sample from several host threads)
+            const auto step_args_p = std::make_unique<DenseStepArgs>();
+            DenseStepArgs& step_args = *step_args_p;
             step_args.n = n;
             step_args.batch_pad = batch_pad;
             step_args.dt = p.dt;
