@@ -1,0 +1,56 @@
+"""Size-independent properties at C5 scale (the 1e8-sample Pareto stress),
+on 16 runs of the C2 lattice (1.6e7 samples) so the test stays short:
+
+* one filter over the whole 1.6e7-sample pool equals the streaming merge of the 16 per-run
+  fronts (filter(union) = filter(union of filters), test_pareto.cpp:115-125), values and
+  configs bit-identical, and the HVs agree;
+* every archive vector is weakly dominated by a point of the exact front (all 2^41
+  configurations, tests/golden/heavyhex42_k4_exact.npz): no evaluated cut exceeds the
+  true optimum;
+* the HV at the frozen reference point never exceeds HV*.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2604_26477_b200 import api, streaming
+from paper_2604_26477_b200.instances import load_heavy_hex
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+RUNS = 16
+
+
+def test_c5_scale_pool_filter_equals_streaming_merge():
+    g = np.load(os.path.join(ROOT, "tests", "golden", "heavyhex42_k4_exact.npz"))
+    r = [float(x) for x in g["reference"]]
+    hv_star = float(g["hv_star"])
+    front = g["values"].astype(np.float64)
+    inst = load_heavy_hex(4)
+    w = api.build_weights(4, resolution=13)
+    cfg = api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=4546, seed=7)
+
+    whole = api.Session(0)
+    whole.set_instance(inst)
+    whole.set_weights(w)
+    rep = whole.pipeline(cfg, RUNS, 0, -1, do_hv=True, ref_count=4096, fixed_reference=r)
+    assert rep["pool_size"] == RUNS * 220 * 4546
+    a = whole.archive()
+
+    st = api.Session(0)
+    st.set_instance(inst)
+    st.set_weights(w)
+    res = streaming.time_to_target(st, cfg, r, -1.0, RUNS)  # unreachable target: all RUNS runs
+    assert res["runs"] == RUNS
+    b = st.archive()
+    assert np.array_equal(a.values, b.values) and np.array_equal(a.configs, b.configs)
+    assert res["hv"] == rep["hv"]
+
+    # weak dominance by the exact front, in chunks (archive ~1e4 x front ~1e4 x K)
+    vals = a.values
+    for i in range(0, vals.shape[0], 512):
+        chunk = vals[i:i + 512]
+        covered = (front[None, :, :] >= chunk[:, None, :]).all(axis=2).any(axis=1)
+        assert covered.all(), f"archive rows {np.flatnonzero(~covered)[:5] + i} beat the exact front"
+    assert rep["hv"] <= hv_star
