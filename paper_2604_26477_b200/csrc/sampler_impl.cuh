@@ -379,13 +379,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         acc = static_cast<uint32_t>(lane_or<LANES>(wmask, acc));
 
         // ---- A2e: walk the candidates with their outcomes; every lane keeps the word offset
-        //      of each of its spins packed 6 bits per field (10 fields per u64) and a mask of its
+        //      of each of its spins as a byte offset (4 x word offset) in 8-bit fields (fields 0..7
+        //      in P0, 8..15 in P1: one byte-permute extracts a field in B) and a mask of its
         //      tail normals (their value already sits in the tail's last two words)
-        uint64_t P0 = 0, P1 = 0;  // fields 0..9 and 10..15
+        uint64_t P0 = 0, P1 = 0;  // fields 0..7 and 8..15
         uint32_t specm = 0;
         {
-            constexpr uint64_t kRep = 0x041041041041041ull;  // one in each of 10 fields
-            constexpr uint64_t kF60 = (1ull << 60) - 1, kF36 = (1ull << 36) - 1;
+            constexpr uint64_t kRep = 0x0101010101010101ull;  // one in each of 8 fields
             int pos = 0, i = 0;
             for (int j = 0; j < m; ++j) {
                 const uint32_t e = en[j * TPC];
@@ -403,16 +403,16 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                         overflow = true;
                         ovf_code |= 16;
                     }
-                    const uint64_t val = static_cast<uint64_t>(off & 63) * kRep;
+                    const uint64_t val = static_cast<uint64_t>(4 * (off & 63)) * kRep;
                     if (jl <= 0) {
                         P0 = val;
-                        P1 = val & kF36;
-                    } else if (jl < 10) {
-                        const uint64_t msk = (kF60 << (6 * jl)) & kF60;
+                        P1 = val;
+                    } else if (jl < 8) {
+                        const uint64_t msk = ~0ull << (8 * jl);
                         P0 = (P0 & ~msk) | (val & msk);
-                        P1 = val & kF36;
+                        P1 = val;
                     } else {
-                        const uint64_t msk = (kF36 << (6 * (jl - 10))) & kF36;
+                        const uint64_t msk = ~0ull << (8 * (jl - 8));
                         P1 = (P1 & ~msk) | (val & msk);
                     }
                     if (tail && jl >= 0) specm |= 1u << jl;
@@ -427,8 +427,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         const uint32_t* ubs = ub + s0;
 #pragma unroll
         for (int s = 0; s < NQ; ++s) {
-            const int off = static_cast<int>(((s < 10 ? P0 >> (6 * s) : P1 >> (6 * (s - 10)))) & 63u);
-            const uint32_t* wp = ubs + s + off;
+            const uint64_t Pq = s < 8 ? P0 : P1;
+            const int sq = s & 7;
+            const uint32_t half = sq < 4 ? static_cast<uint32_t>(Pq) : static_cast<uint32_t>(Pq >> 32);
+            const uint32_t boff = __byte_perm(half, 0u, 0x4440u + static_cast<uint32_t>(sq & 3));
+            const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(ubs + s) + boff);
             const uint32_t u = wp[0];
             double eta = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), wn[u & 127u]);
             if (specm & (1u << s)) eta = __hiloint2double(static_cast<int>(wp[-1]), static_cast<int>(u));
