@@ -381,14 +381,17 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         acc = static_cast<uint32_t>(lane_or<LANES>(wmask, acc));
 
         // ---- A2e: walk the candidates with their outcomes; every lane keeps the word offset
-        //      of each of its spins as a byte offset (4 x word offset) in 8-bit fields (fields 0..7
-        //      in P0, 8..15 in P1: one byte-permute extracts a field in B) and a mask of its
-        //      tail normals (their value already sits in the tail's last two words)
-        uint64_t P0 = 0, P1 = 0;  // fields 0..7 and 8..15
+        //      of each of its spins as a byte offset (4 x word offset) in 8-bit fields of four
+        //      words (spins 0..3, 4..7, 8..11, 12..15: one byte-permute extracts a field in B),
+        //      and a mask of its tail normals (their value already sits in the tail's last two
+        //      words). Offsets only grow along the stream, so each attempt adds its increase to
+        //      the fields from its normal on (bytes never carry: offsets stay <= 63).
+        uint32_t W0 = 0, W1 = 0, W2 = 0, W3 = 0;
         uint32_t specm = 0;
         {
-            constexpr uint64_t kRep = 0x0101010101010101ull;  // one in each of 8 fields
-            int pos = 0, i = 0;
+            // fields from bit b on (b may be <= 0: all of them, >= 32: none)
+            auto from = [](int b) -> uint32_t { return b <= 0 ? ~0u : (b >= 32 ? 0u : ~0u << b); };
+            int pos = 0, i = 0, cur = 0;  // cur: the word offset of the next fast normal
             for (int j = 0; j < m; ++j) {
                 const uint32_t e = en[j * TPC];
                 const int q = static_cast<int>(e & 0xFFu);
@@ -405,20 +408,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                         overflow = true;
                         ovf_code |= 16;
                     }
-                    const uint64_t val = static_cast<uint64_t>(4 * (off & 63)) * kRep;
-                    if (jl <= 0) {
-                        P0 = val;
-                        P1 = val;
-                    } else if (jl < 8) {
-                        const uint64_t msk = ~0ull << (8 * jl);
-                        P0 = (P0 & ~msk) | (val & msk);
-                        P1 = val;
-                    } else {
-                        const uint64_t msk = ~0ull << (8 * (jl - 8));
-                        P1 = (P1 & ~msk) | (val & msk);
-                    }
+                    const uint32_t rep = static_cast<uint32_t>(off - cur) * 0x04040404u;
+                    const int bb = 8 * jl;
+                    W0 += rep & from(bb);
+                    if constexpr (NQ > 4) W1 += rep & from(bb - 32);
+                    if constexpr (NQ > 8) W2 += rep & from(bb - 64);
+                    if constexpr (NQ > 12) W3 += rep & from(bb - 96);
                     if (tail && jl >= 0) specm |= 1u << jl;
                 }
+                cur = off;
                 pos = new_pos;
                 i = new_i;
                 if (i >= n) break;
@@ -429,10 +427,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         const uint32_t* ubs = ub + s0;
 #pragma unroll
         for (int s = 0; s < NQ; ++s) {
-            const uint64_t Pq = s < 8 ? P0 : P1;
-            const int sq = s & 7;
-            const uint32_t half = sq < 4 ? static_cast<uint32_t>(Pq) : static_cast<uint32_t>(Pq >> 32);
-            const uint32_t boff = __byte_perm(half, 0u, 0x4440u + static_cast<uint32_t>(sq & 3));
+            const uint32_t Wq = s < 4 ? W0 : s < 8 ? W1 : s < 12 ? W2 : W3;
+            const uint32_t boff = __byte_perm(Wq, 0u, 0x4440u + static_cast<uint32_t>(s & 3));
             const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(ubs + s) + boff);
             const uint32_t u = wp[0];
             double eta = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), wn[u & 127u]);
