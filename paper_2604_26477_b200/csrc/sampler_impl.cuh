@@ -389,8 +389,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         uint32_t W0 = 0, W1 = 0, W2 = 0, W3 = 0;
         uint32_t specm = 0;
         {
-            // fields from bit b on (b may be <= 0: all of them, >= 32: none)
-            auto from = [](int b) -> uint32_t { return b <= 0 ? ~0u : (b >= 32 ? 0u : ~0u << b); };
+            // fields from bit b on (b <= 0: all of them, >= 32: none): the funnel shift clamps
+            // its count to 32
+            auto from = [](int b) -> uint32_t { return __funnelshift_lc(0u, ~0u, static_cast<uint32_t>(max(b, 0))); };
             int pos = 0, i = 0, cur = 0;  // cur: the word offset of the next fast normal
             for (int j = 0; j < m; ++j) {
                 const uint32_t e = en[j * TPC];
