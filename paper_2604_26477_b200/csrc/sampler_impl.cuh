@@ -271,18 +271,37 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
             // fast walk: wedges whose words lie inside the mask (the common case); anything
             // else (a tail, words beyond the mask, a full list) continues in the general walk
             bool general = false;
-            for (;;) {
-                const int lastq = n - 1 + slow;
-                const int q = next_slow<G::kNU>(F0, F1, pos);  // kNU when none is left
-                if (q > lastq) break;
-                if (q + 2 >= G::kNU || m >= G::kECAP || (ub[q] & 127u) == 0) {
-                    general = true;
-                    break;
+            if constexpr (G::kNU <= 64) {
+                // the remaining slow words as one mask, consumed from the bottom
+                uint64_t rem = ~F0 & (G::kNU >= 64 ? ~0ull : ((1ull << (G::kNU & 63)) - 1));
+                for (;;) {
+                    const int lastq = n - 1 + slow;
+                    const int q = rem ? __ffsll(static_cast<long long>(rem)) - 1 : G::kNU;  // kNU when none is left
+                    if (q > lastq) break;
+                    if (q + 2 >= G::kNU || m >= G::kECAP || (ub[q] & 127u) == 0) {
+                        general = true;
+                        break;
+                    }
+                    en[m * TPC] = static_cast<uint32_t>(q);
+                    ++m;
+                    slow += 3;
+                    pos = q + 3;
+                    rem = pos >= 64 ? 0ull : rem & (~0ull << pos);  // pos <= kNU here (q + 2 < kNU)
                 }
-                en[m * TPC] = static_cast<uint32_t>(q);
-                ++m;
-                slow += 3;
-                pos = q + 3;
+            } else {
+                for (;;) {
+                    const int lastq = n - 1 + slow;
+                    const int q = next_slow<G::kNU>(F0, F1, pos);  // kNU when none is left
+                    if (q > lastq) break;
+                    if (q + 2 >= G::kNU || m >= G::kECAP || (ub[q] & 127u) == 0) {
+                        general = true;
+                        break;
+                    }
+                    en[m * TPC] = static_cast<uint32_t>(q);
+                    ++m;
+                    slow += 3;
+                    pos = q + 3;
+                }
             }
             for (; general;) {
                 const int lastq = n - 1 + slow;  // fast normals before q = q - slow must stay < n
