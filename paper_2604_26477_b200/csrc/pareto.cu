@@ -679,23 +679,33 @@ bool build_grid(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, Gr
 {
     g.dims = K - 1;
     const uint64_t tsize = pow2_at_least(2ull * static_cast<uint64_t>(V) + 16);
-    s.dtable.reserve(tsize);
-    s.axisbuf.reserve(static_cast<size_t>(kDistinctCap));
+    // the K axes' distinct values in one pass of launches and one read-back (tables and
+    // counters per axis; counters from slot 8 on)
+    s.dtable.reserve(tsize * K);
+    s.axisbuf.reserve(static_cast<size_t>(kDistinctCap) * K);
     s.axis_sorted.reserve(static_cast<size_t>(kDistinctCap) * K);
-    s.counters.reserve(8);
+    s.counters.reserve(8 + kMaxK);
+    ck(cudaMemsetAsync(s.dtable.p, 0, sizeof(unsigned long long) * tsize * K, c.stream), "memset");
+    ck(cudaMemsetAsync(s.counters.p + 8, 0, sizeof(unsigned long long) * K, c.stream), "memset");
+    for (int a = 0; a < K; ++a) {
+        k_distinct<<<grid_blocks(V), 256, 0, c.stream>>>(d_vals, V, K, a, s.dtable.p + tsize * a, tsize - 1,
+                                                           s.axisbuf.p + static_cast<size_t>(kDistinctCap) * a,
+                                                           s.counters.p + 8 + a, kDistinctCap);
+        c.launches++;
+    }
+    std::vector<unsigned long long> dcount(static_cast<size_t>(K));
+    ck(cudaMemcpyAsync(dcount.data(), s.counters.p + 8, sizeof(unsigned long long) * K, cudaMemcpyDeviceToHost,
+                       c.stream),
+       "D2H");
+    ck(cudaStreamSynchronize(c.stream), "sync");
     long long prod = 1;
     for (int a = 0; a < K; ++a) {
-        ck(cudaMemsetAsync(s.dtable.p, 0, sizeof(unsigned long long) * tsize, c.stream), "memset");
-        ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long), c.stream), "memset");
-        k_distinct<<<grid_blocks(V), 256, 0, c.stream>>>(d_vals, V, K, a, s.dtable.p, tsize - 1, s.axisbuf.p,
-                                                           s.counters.p, kDistinctCap);
-        c.launches++;
-        const long long D = static_cast<long long>(read_counter(c, s.counters.p));
+        const long long D = static_cast<long long>(dcount[static_cast<size_t>(a)]);
         if (D > kDistinctCap) return false;
         g.D[a] = static_cast<int>(D);
         double* sorted = s.axis_sorted.p + static_cast<size_t>(a) * kDistinctCap;
-        k_rank_sort_asc<<<grid_blocks(D, 256), 256, 256 * sizeof(double), c.stream>>>(s.axisbuf.p, static_cast<int>(D),
-                                                                                       sorted);
+        k_rank_sort_asc<<<grid_blocks(D, 256), 256, 256 * sizeof(double), c.stream>>>(
+            s.axisbuf.p + static_cast<size_t>(kDistinctCap) * a, static_cast<int>(D), sorted);
         c.launches++;
         g.axis[a] = sorted;
         if (a < K - 1) {
