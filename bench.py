@@ -408,7 +408,7 @@ def main():
     peak_ops = n_sm * 128 * sm_clk * 1e6  # lane-ops/s: 4 schedulers x 32 lanes per SM per clock
     sampling_s = float(np.mean([r["sampling_s"] for r in reps]))
     achieved = ALG_OPS_PER_SAMPLE * (samples_total / world) / sampling_s
-    roofline = {"bound": "issue", "kernel": "sb_small_kernel<42,4,1,3> (SB sampler, dominant)",
+    roofline = {"bound": "issue", "kernel": "sb_small_kernel<42,4,1,3,true> (SB sampler, dominant)",
                 "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tlane-op/s",
                 "frac": achieved / peak_ops, "traffic": profile_traffic(),
                 "note": "neither HBM- nor tensor-bound: integer Philox + FP64 update; peak = SMs x 128 lanes "
