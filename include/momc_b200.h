@@ -54,7 +54,10 @@ typedef struct {
     const double* w;
 } momc_instance_view;
 
-/* ---------------------------------------------------------------- context */
+/* ---------------------------------------------------------------- context
+ * No reference counterpart: the reference is stateless and run_sampler owns a transient
+ * thread pool (solver.hpp:463-467). A context is one device, its streams and the resident
+ * buffers (instance, lattice, pool, archive) the calls below share. */
 int momc_b200_ctx_create(int device, momc_ctx** out, char* err, size_t errlen);
 void momc_b200_ctx_destroy(momc_ctx* ctx);
 int momc_b200_ctx_sync(momc_ctx* ctx, char* err, size_t errlen);
@@ -107,7 +110,8 @@ long long momc_b200_pool_size(momc_ctx* ctx);
 int momc_b200_pool_get(momc_ctx* ctx, uint64_t* words, int64_t* stamps_ns, char* err, size_t errlen);
 const uint64_t* momc_b200_pool_device(momc_ctx* ctx);
 
-/* Host-to-host drop-in for run_sampler: instance + weights + sample + copy back. */
+/* Host-to-host drop-in for run_sampler (solver.hpp:439-529): instance + weights + sample +
+ * copy back; words / records in the reference's canonical order (solver.hpp:493-495). */
 int momc_b200_run_sampler(momc_ctx* ctx, const momc_instance_view* inst, const int32_t* nums, int L, int H,
                           const momc_solver_cfg* cfg, int runs, uint64_t* out_words, int64_t* out_stamps_ns,
                           double* out_seconds /* [model_construction, sampling] */, char* err, size_t errlen);
@@ -130,7 +134,8 @@ int momc_b200_filter_values(momc_ctx* ctx, const double* vals, size_t M, int k, 
  * device configs M x wpc; equal vectors keep the lexicographically smallest config. */
 int momc_b200_filter_values_dev(momc_ctx* ctx, const double* d_vals, const uint64_t* d_words, int wpc, size_t M,
                                 int k, int64_t* out_F, char* err, size_t errlen);
-/* resident archive: size, host copy, device pointers, device-to-device copy */
+/* resident archive (the ParetoArchive entries of non_dominated_filter, pareto.hpp:370-410):
+ * size, host copy, device pointers, device-to-device copy */
 int64_t momc_b200_archive_size(momc_ctx* ctx);
 int momc_b200_archive_get(momc_ctx* ctx, double* vals, uint64_t* words, char* err, size_t errlen);
 int momc_b200_archive_copy_device(momc_ctx* ctx, double* d_vals, uint64_t* d_words, char* err, size_t errlen);
@@ -173,8 +178,9 @@ int momc_b200_convergence_trace(momc_ctx* ctx, const uint64_t* words, const int6
 int momc_b200_tc_i8_selftest(momc_ctx* ctx, const int8_t* A, const int8_t* B, int K, int32_t* D, char* err,
                              size_t errlen);
 
-/* Roofline calibration: normals/s of a kernel doing only the sampler's per-word noise work
- * (Philox block per 4 words, ziggurat fast test, eta = hz * wn[iz]). */
+/* Roofline calibration (no reference counterpart): normals/s of a kernel doing
+ * only the sampler's per-word noise work (Philox block per 4 words, rng.hpp:113-121; the
+ * ziggurat fast test and eta = hz * wn[iz], rng.hpp:156-163). */
 int momc_b200_rng_calibrate(momc_ctx* ctx, int blocks_per_thread, double* normals_per_s, char* err, size_t errlen);
 
 /* ---------------------------------------------------------------- pool CSV (solver.hpp:357-432) */
@@ -224,7 +230,8 @@ int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t
 int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long long block_begin,
                        long long block_end, int do_hv, int ref_count, const double* fixed_ref,
                        momc_bench_report* report, char* err, size_t errlen);
-/* Streaming (time-to-optimal): a running archive on the context. stream_step samples
+/* Streaming (time-to-optimal; the running archive of archive_insert pareto.hpp:702-710 and
+ * samples_to_reach :763-781, kept on the device): a running archive on the context. stream_step samples
  * blocks [block_begin, block_end) of a `runs`-run job (compact pool), filters them into the
  * resident archive (unordered) and, with merge != 0, merges that front into the running
  * archive and (r, hv non-NULL) returns the running archive's hypervolume at r. running_merge_values merges device rows (another context's or
@@ -239,7 +246,8 @@ int momc_b200_archive_device_ptrs(momc_ctx* ctx, const double** vals, const uint
 int momc_b200_running_merge_values(momc_ctx* ctx, const double* d_vals, const uint64_t* d_words, int wpc, size_t M,
                                    int k, const double* r, double* hv, int64_t* running_F, char* err, size_t errlen);
 int momc_b200_running_to_archive(momc_ctx* ctx, int64_t* out_F, char* err, size_t errlen);
-/* flattened (run, weight, chunk) block count of a run configuration on this context */
+/* flattened (run, weight, chunk) block count of a run configuration on this context: the
+ * sharding unit (the reference's (run, weight, 512-trajectory) tasks, solver.hpp:481-499) */
 long long momc_b200_num_blocks(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs);
 
 #ifdef __cplusplus
