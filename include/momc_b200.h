@@ -247,7 +247,7 @@ int momc_b200_running_merge_values(momc_ctx* ctx, const double* d_vals, const ui
                                    int k, const double* r, double* hv, int64_t* running_F, char* err, size_t errlen);
 int momc_b200_running_to_archive(momc_ctx* ctx, int64_t* out_F, char* err, size_t errlen);
 /* flattened (run, weight, chunk) block count of a run configuration on this context: the
- * sharding unit (the reference's (run, weight, 512-trajectory) tasks, solver.hpp:481-499) */
+ * sharding unit (the reference's (run, weight, 512-trajectory) tasks, solver.hpp:455-499) */
 long long momc_b200_num_blocks(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs);
 
 #ifdef __cplusplus
