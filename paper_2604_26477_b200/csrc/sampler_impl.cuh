@@ -195,16 +195,34 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
 
     // ---- init_state (solver.hpp:108-124): spin i uses words 2i, 2i+1 of the init_x /
     //      init_y streams (block i/2, half i%2)
+    //      Block c = s0/2 + c' serves slots 2c'-1 .. 2c'+1 depending on the parity of s0, so
+    //      each block is generated once (NQ/2 + 1 per stream instead of NQ).
     double x[NQ];
     double y[NQ];
+    {
+        const bool par = s0 & 1;  // odd first spin: slot s takes block (s + 1) / 2
+        const uint32_t bx = static_cast<uint32_t>(s0 >> 1);
+        const uint32_t tx = tag_word(kTagInitX, 0), ty = tag_word(kTagInitY, 0);
+        auto init_val = [&](uint32_t lo, uint32_t hi) {
+            return __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, u01_from(lo, hi)), 1.0));
+        };
+        uint4 px = philox(k0, k1, bx, tx, tr, wl), py = philox(k0, k1, bx, ty, tr, wl);
+        x[0] = init_val(par ? px.z : px.x, par ? px.w : px.y);
+        y[0] = init_val(par ? py.z : py.x, par ? py.w : py.y);
 #pragma unroll
-    for (int s = 0; s < NQ; ++s) {
-        const int i = s0 + s;
-        const uint4 rx = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitX, 0), tr, wl);
-        const uint4 ry = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitY, 0), tr, wl);
-        const bool odd = i & 1;
-        x[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(rx.z, rx.w) : u01_from(rx.x, rx.y)), 1.0));
-        y[s] = __dmul_rn(p.init_scale, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(ry.z, ry.w) : u01_from(ry.x, ry.y)), 1.0));
+        for (int c = 1; c <= NQ / 2; ++c) {
+            const uint4 cx = philox(k0, k1, bx + c, tx, tr, wl), cy = philox(k0, k1, bx + c, ty, tr, wl);
+            if (2 * c - 1 < NQ) {  // slot 2c-1: the previous block's high half, or this block's low half
+                x[2 * c - 1] = init_val(par ? cx.x : px.z, par ? cx.y : px.w);
+                y[2 * c - 1] = init_val(par ? cy.x : py.z, par ? cy.y : py.w);
+            }
+            if (2 * c < NQ) {  // slot 2c: this block's low half, or its high half
+                x[2 * c] = init_val(par ? cx.z : cx.x, par ? cx.w : cx.y);
+                y[2 * c] = init_val(par ? cy.z : cy.x, par ? cy.w : cy.y);
+            }
+            px = cx;
+            py = cy;
+        }
     }
 
     unsigned char* phb = phis + t_loc * G::kPStr * G::kPhiW;  // this trajectory's phi row
