@@ -68,6 +68,21 @@ def test_pool_matches_reference(ref, session, variant, n, density, k, seed):
     assert mismatch(pool.words, expect) <= MAX_WORD_MISMATCH
 
 
+@pytest.mark.parametrize("variant", ["bsb", "dsb", "simcim"])
+@pytest.mark.parametrize("dt,a0", [(0.5, 1.0), (1.0, 0.8), (0.7, 1.3)])
+def test_non_unit_time_step_matches_reference(ref, session, variant, dt, a0):
+    """dt != 1 or dt*a0 != 1 takes the general update (the unit-dt specialisation skips the
+    exact products dt*d and dt*a0*y only when both are 1)"""
+    ri = ref.generate_uniform(42, 0.2, 3, 9)
+    inst = inst_from_ref(ri)
+    nums = ref.das_dennis(3, 4)
+    c = make_cfg(variant, batch_size=200, seed=21, threads=8, dt=dt, a0=a0)
+    expect = ref.run_sampler(ri, nums, 4, c, 1)["words"]
+    pool = api.run_sampler(inst, weights_of(nums, 4), cfg_of(variant, batch_size=200, seed=21, dt=dt, a0=a0), 1,
+                           session=session)
+    assert mismatch(pool.words, expect) <= MAX_WORD_MISMATCH
+
+
 @pytest.mark.parametrize("variant", ["bsb", "dsb"])
 def test_heavy_hex_k4_matches_reference(ref, session, variant):
     inst = load_heavy_hex(4)
