@@ -41,6 +41,22 @@ def test_dense_dsb_agrees_with_reference(ref, session, n, batch, seed):
     assert mm <= MAX_DENSE_WORD_MISMATCH
 
 
+def test_dense_dsb_non_unit_dt_agrees_with_reference(ref, session):
+    """dt = 0.5, a0 = 1.2: the general update of the warp-per-trajectory kernel"""
+    n, H = 288, 4
+    session.generate_uniform_instance(n, 0.5, 3, 8)
+    ri = ref.generate_uniform(n, 0.5, 3, 8)
+    nums = ref.das_dennis(3, H)
+    batch = 33
+    want = ref.run_sampler(ri, nums, H, make_cfg("dsb", batch_size=batch, seed=4, threads=16, dt=0.5, a0=1.2),
+                           1)["words"]
+    session.set_dense_threshold(256)
+    session.set_weights([api.WeightVector(list(r), H) for r in nums])
+    session.sample(api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=batch, seed=4, dt=0.5, a0=1.2), 1)
+    got = session.pool(stamps=False).words
+    assert float(np.mean(np.any(got != want, axis=1))) <= MAX_DENSE_WORD_MISMATCH
+
+
 def test_dense_eval_gemm_exact(ref, session):
     n = 512
     inst = session.generate_uniform_instance(n, 0.7, 3, 8)
