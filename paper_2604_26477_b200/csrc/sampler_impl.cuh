@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                 uint64_t rem = ~F0 & (G::kNU >= 64 ? ~0ull : ((1ull << (G::kNU & 63)) - 1));
                 for (;;) {
                     const int lastq = n - 1 + slow;
-                    const int q = rem ? __ffsll(static_cast<long long>(rem)) - 1 : G::kNU;  // kNU when none is left
+                    const uint32_t rlo = static_cast<uint32_t>(rem), rhi = static_cast<uint32_t>(rem >> 32);
+                    const int q = rlo ? __ffs(rlo) - 1 : (rhi ? 31 + __ffs(rhi) : G::kNU);  // kNU when none is left
                     if (q > lastq) break;
                     if (q + 2 >= G::kNU || m >= G::kECAP || (ub[q] & 127u) == 0) {
                         general = true;
