@@ -1203,13 +1203,7 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     k_map_u32<<<grid_blocks(V), 256, 0, c.stream>>>(vown.p, s.uniq.p, V, vcfg.p);
     c.launches++;
     cudaEventRecord(e3, c.stream);
-    ck(cudaStreamSynchronize(c.stream), "collapse");
-    if (tm) {
-        tm->dedup_s = seconds_between(e0, e1);
-        tm->eval_s = seconds_between(e1, e2);
-        tm->collapse_s = seconds_between(e2, e3);
-        tm->unique_configs = U;
-    }
+    if (tm) tm->unique_configs = U;
     trace("filter_pool: finish_archive");
     c.values_are_cuts = true;
     try {
@@ -1219,6 +1213,12 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
         throw;
     }
     c.values_are_cuts = false;
+    if (tm) {  // the events completed: finish_archive read results back after them
+        ck(cudaEventSynchronize(e3), "events");
+        tm->dedup_s = seconds_between(e0, e1);
+        tm->eval_s = seconds_between(e1, e2);
+        tm->collapse_s = seconds_between(e2, e3);
+    }
     trace("filter_pool: archive done");
     vrow.release();
     vown.release();
