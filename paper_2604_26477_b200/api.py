@@ -340,12 +340,11 @@ def _weights_array(weights, k):
     if len(weights) == 0:
         raise InvalidArgument("run_sampler needs at least one weight vector")
     H = weights[0].resolution()
-    for w in weights:
-        if w.size() != k:
-            raise InvalidArgument("weight vector length does not match objective count")
-        if w.resolution() != H:
-            raise InvalidArgument("all weight vectors must share one resolution")
-    nums = np.asarray([[w.numerator(q) for q in range(k)] for w in weights], dtype=np.int32)
+    if any(len(w._num) != k for w in weights):
+        raise InvalidArgument("weight vector length does not match objective count")
+    if any(w._h != H for w in weights):
+        raise InvalidArgument("all weight vectors must share one resolution")
+    nums = np.asarray([w._num for w in weights], dtype=np.int32)  # one pass: this runs every bench call
     return nums, H
 
 
