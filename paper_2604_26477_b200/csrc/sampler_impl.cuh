@@ -46,12 +46,6 @@ __device__ __forceinline__ unsigned long long globaltimer()
     return t;
 }
 
-// exact int32 -> double without the XU conversion pipe: (2^52 + 2^31 + v) - (2^52 + 2^31)
-__device__ __forceinline__ double i32_to_f64(int32_t v)
-{
-    return __dsub_rn(__hiloint2double(0x43300000, static_cast<uint32_t>(v) ^ 0x80000000u), 4503601774854144.0);
-}
-
 // |hz| as in rng.hpp:161-163 (INT_MIN -> 2^31)
 __device__ __forceinline__ uint32_t zmag(uint32_t u)
 {
