@@ -57,6 +57,21 @@ def test_dense_dsb_non_unit_dt_agrees_with_reference(ref, session):
     assert float(np.mean(np.any(got != want, axis=1))) <= MAX_DENSE_WORD_MISMATCH
 
 
+def test_dense_dsb_noiseless_agrees_with_reference(ref, session):
+    """alpha = 0: the noise-free instantiation of the update kernel"""
+    n, H = 256, 4
+    session.generate_uniform_instance(n, 0.6, 3, 13)
+    ri = ref.generate_uniform(n, 0.6, 3, 13)
+    nums = ref.das_dennis(3, H)
+    batch = 24
+    want = ref.run_sampler(ri, nums, H, make_cfg("dsb", batch_size=batch, seed=2, threads=16, alpha=0.0), 1)["words"]
+    session.set_dense_threshold(256)
+    session.set_weights([api.WeightVector(list(r), H) for r in nums])
+    session.sample(api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=batch, seed=2, alpha=0.0), 1)
+    got = session.pool(stamps=False).words
+    assert float(np.mean(np.any(got != want, axis=1))) <= MAX_DENSE_WORD_MISMATCH
+
+
 def test_dense_eval_gemm_exact(ref, session):
     n = 512
     inst = session.generate_uniform_instance(n, 0.7, 3, 8)
