@@ -436,6 +436,7 @@ void set_instance(Ctx& c, const momc_instance_view* iv)
 
 void set_weights(Ctx& c, const int32_t* nums, int L, int H)
 {
+    ++c.weights_gen;
     if (c.n == 0) usage("no instance set");
     if (L < 1) usage("block system needs at least one weight vector");
     if (H < 1) usage("lattice resolution must be positive");

@@ -734,8 +734,7 @@ struct DenseScratch {
     DevBuf<int> D, flags;
     DevBuf<double> x, y;
     DevBuf<PairOf> pairs;
-    int hj_L = -1, hj_n = 0;
-    const void* hj_key = nullptr;
+    long long hj_inst = -1, hj_weights = -1;  // H*J(c) built for this instance / lattice generation
     DevBuf<signed char> wk;  // the K weight layers as dense int8 (evaluate_cuts), per instance
     long long wk_gen = -1;
 };
@@ -779,7 +778,7 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
     DenseScratch& d = dscratch(c);
     const int n = c.n, L = c.L;
     // H*J(c_l) in int8 (rebuilt when the weights change)
-    if (d.hj_L != L || d.hj_n != n || d.hj_key != static_cast<const void*>(c.d_vals.p)) {
+    if (d.hj_inst != c.inst_gen || d.hj_weights != c.weights_gen) {
         d.hj.reserve(static_cast<size_t>(L) * n * n);
         d.flags.reserve(4);
         ck(cudaMemsetAsync(d.flags.p, 0, sizeof(int) * 4, c.stream), "memset");
@@ -790,9 +789,8 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
         ck(cudaMemcpyAsync(&ovf, d.flags.p, sizeof ovf, cudaMemcpyDeviceToHost, c.stream), "D2H");
         ck(cudaStreamSynchronize(c.stream), "hj");
         if (ovf) runtime("dense path: H*J(c) exceeds int8");
-        d.hj_L = L;
-        d.hj_n = n;
-        d.hj_key = c.d_vals.p;
+        d.hj_inst = c.inst_gen;
+        d.hj_weights = c.weights_gen;
     }
     // group the block range into (run, weight) pairs of contiguous trajectories
     std::vector<PairOf> pairs;

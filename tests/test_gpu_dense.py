@@ -72,6 +72,22 @@ def test_dense_dsb_noiseless_agrees_with_reference(ref, session):
     assert float(np.mean(np.any(got != want, axis=1))) <= MAX_DENSE_WORD_MISMATCH
 
 
+def test_dense_dsb_two_runs_agree_with_reference(ref, session):
+    """runs = 2: pairs of both runs in one launch group (per-pair run keys, pair offsets)"""
+    n, H = 256, 4
+    session.generate_uniform_instance(n, 0.5, 3, 14)
+    ri = ref.generate_uniform(n, 0.5, 3, 14)
+    nums = ref.das_dennis(3, H)
+    batch = 20
+    want = ref.run_sampler(ri, nums, H, make_cfg("dsb", batch_size=batch, seed=6, threads=16), 2)["words"]
+    session.set_dense_threshold(256)
+    session.set_weights([api.WeightVector(list(r), H) for r in nums])
+    session.sample(api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=batch, seed=6), 2)
+    got = session.pool(stamps=False).words
+    assert got.shape == want.shape
+    assert float(np.mean(np.any(got != want, axis=1))) <= MAX_DENSE_WORD_MISMATCH
+
+
 def test_dense_eval_gemm_exact(ref, session):
     n = 512
     inst = session.generate_uniform_instance(n, 0.7, 3, 8)
