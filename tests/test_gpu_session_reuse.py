@@ -1,0 +1,38 @@
+"""One context reused across instances, lattices and paths must give the same results as a
+fresh context for each (guards every cache keyed on the instance or the lattice: the dense
+H*J(c), the int8 weight layers, padded rows, cut packing)."""
+import numpy as np
+import pytest
+
+from paper_2604_26477_b200 import api
+from paper_2604_26477_b200.instances import load_heavy_hex
+
+pytestmark = pytest.mark.gpu
+
+
+def _dense_run(s, seed, H):
+    s.generate_uniform_instance(256, 0.5, 3, seed)
+    s.set_dense_threshold(256)
+    s.set_weights(api.build_weights(3, resolution=H))
+    rep = s.pipeline(api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=24, seed=seed), 1, 0, -1,
+                     True, 256)
+    return s.pool(stamps=False).words.copy(), s.archive().values.copy(), rep["hv"]
+
+
+def _hh_run(s, k, variant):
+    s.set_instance(load_heavy_hex(k))
+    s.set_weights(api.build_weights(k, resolution=5 if k == 4 else 7))
+    rep = s.pipeline(api.SolverConfig(variant=variant, batch_size=70, seed=3), 1, 0, -1, True, 512)
+    return s.pool(stamps=False).words.copy(), s.archive().values.copy(), rep["hv"]
+
+
+def test_context_reuse_matches_fresh_contexts():
+    plan = [("dense", 31, 4), ("hh", 4, api.SolverVariant.discrete_sb), ("dense", 32, 4), ("dense", 32, 5),
+            ("hh", 3, api.SolverVariant.ballistic_sb), ("dense", 31, 4), ("hh", 4, api.SolverVariant.simcim)]
+    shared = api.Session(0)
+    for kind, a, b in plan:
+        run = _dense_run if kind == "dense" else _hh_run
+        got = run(shared, a, b)
+        want = run(api.Session(0), a, b)
+        for g, w in zip(got, want):
+            assert np.array_equal(np.asarray(g), np.asarray(w)), (kind, a, b)
