@@ -436,7 +436,6 @@ void set_instance(Ctx& c, const momc_instance_view* iv)
 
 void set_weights(Ctx& c, const int32_t* nums, int L, int H)
 {
-    ++c.weights_gen;
     if (c.n == 0) usage("no instance set");
     if (L < 1) usage("block system needs at least one weight vector");
     if (H < 1) usage("lattice resolution must be positive");
@@ -447,6 +446,18 @@ void set_weights(Ctx& c, const int32_t* nums, int L, int H)
             s += nums[static_cast<size_t>(l) * c.k + q];
         }
         if (s != H) usage("weight numerators must sum to the resolution");
+    }
+    {  // a new lattice (or a new instance) invalidates lattice-keyed caches; re-scalarising
+       // the same lattice (every pipeline call) does not
+        const bool same = c.weights_inst == c.inst_gen && c.h_H_last == H &&
+                          c.h_nums_last.size() == static_cast<size_t>(L) * c.k &&
+                          std::equal(c.h_nums_last.begin(), c.h_nums_last.end(), nums);
+        if (!same) {
+            ++c.weights_gen;
+            c.weights_inst = c.inst_gen;
+            c.h_H_last = H;
+            c.h_nums_last.assign(nums, nums + static_cast<size_t>(L) * c.k);
+        }
     }
     c.L = L;
     c.H = H;

@@ -72,7 +72,10 @@ struct Ctx {
     // instance
     int n = 0, k = 0, m = 0, nnz = 0;
     long long inst_gen = 0;     // bumped by every set_instance (caches keyed on the instance)
-    long long weights_gen = 0;  // bumped by every set_weights (caches keyed on the lattice)
+    long long weights_gen = 0;  // bumped when set_weights changes the lattice (caches keyed on it)
+    long long weights_inst = -1;          // inst_gen the current lattice was set for
+    std::vector<int32_t> h_nums_last;     // the current lattice's numerators (change detection)
+    int h_H_last = 0;
     bool integer_weights = false;  // every weight integral and sum |w| < 2^31 (exact int32 cut path)
     bool cut_pack = false;         // cut values of all K objectives fit one 64-bit key (offsets)
     std::vector<long long> cut_lo; // per objective: smallest possible cut value
