@@ -36,3 +36,28 @@ def test_context_reuse_matches_fresh_contexts():
         want = run(api.Session(0), a, b)
         for g, w in zip(got, want):
             assert np.array_equal(np.asarray(g), np.asarray(w)), (kind, a, b)
+
+
+def test_streaming_and_enumeration_after_other_work():
+    """the running archive and the enumerator on a context that sampled other instances first"""
+    from paper_2604_26477_b200 import streaming
+
+    def stream(s):
+        s.set_instance(load_heavy_hex(3))
+        s.set_weights(api.build_weights(3, resolution=7))
+        cfg = api.SolverConfig(variant=api.SolverVariant.ballistic_sb, batch_size=60, seed=9)
+        res = streaming.time_to_target(s, cfg, [-60.0, -60.0, -60.0], -1.0, 3)
+        return res["hv"], s.archive().values.copy()
+
+    shared = api.Session(0)
+    _dense_run(shared, 33, 4)
+    _hh_run(shared, 4, api.SolverVariant.discrete_sb)
+    hv_a, arc_a = stream(shared)
+    hv_b, arc_b = stream(api.Session(0))
+    assert hv_a == hv_b and np.array_equal(arc_a, arc_b)
+
+    g = api.Session(0).generate_uniform_instance(16, 0.6, 2, 5)
+    fresh = api.brute_force_pareto(g, session=api.Session(0))
+    shared.generate_uniform_instance(16, 0.6, 2, 5)
+    again = api.brute_force_pareto(g, session=shared)
+    assert np.array_equal(fresh.values, again.values) and np.array_equal(fresh.configs, again.configs)
