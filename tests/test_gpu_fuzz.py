@@ -47,3 +47,33 @@ def test_random_configurations_match_reference(ref, session, seed):
                                                alpha=alpha, dt=dt, a0=a0, runs=runs)
         compared += 1
     assert compared >= 30
+
+
+@pytest.mark.parametrize("seed", [303, 404])
+def test_random_pools_filter_and_hv_match_reference(ref, session, seed):
+    """the Pareto stage on random pools of random instances (integer and real weights,
+    K = 2..5, duplicates): archive values / configs / order, evaluate_cuts and the HV at the
+    clamped sampled reference point (pareto.hpp:253-410, :540-655)"""
+    from test_gpu_pareto import check_archive, inst_from_ref, random_words
+
+    rnd = random.Random(seed)
+    for _ in range(12):
+        n = rnd.choice([5, 9, 16, 30, 42, 64, 65, 90])
+        k = rnd.choice([2, 3, 4, 5])
+        kind = rnd.choice(["int", "int", "real"])
+        ri = ref.generate_uniform(n, rnd.choice([0.2, 0.5, 1.0]), k, rnd.randrange(1000), kind=kind,
+                                  lo=1.0 if kind == "int" else -1.0, hi=10.0 if kind == "int" else 1.0)
+        if len(ri.edges()[0]) == 0:
+            continue
+        inst = inst_from_ref(ri)
+        M = rnd.choice([1, 7, 500, 20000])
+        words = random_words(n, M, rnd.randrange(10**6))
+        if M > 1:
+            words[M // 2:] = words[: M - M // 2]
+        assert np.array_equal(api.evaluate_cuts(inst, words, session=session), ref.evaluate_cuts(ri, words))
+        got = api.non_dominated_filter(api.SamplePool(n, words), inst, session=session)
+        want = ref.filter_pool(ri, words)
+        check_archive(got, want)
+        r = api.clamp_reference(api.reference_point_sampled(inst, 256, 5, session=session), got)
+        h = api.hypervolume(got, r, session=session)
+        assert h == pytest.approx(ref.hypervolume(want.values, np.asarray(r)), rel=1e-12)
