@@ -77,3 +77,35 @@ def test_random_pools_filter_and_hv_match_reference(ref, session, seed):
         r = api.clamp_reference(api.reference_point_sampled(inst, 256, 5, session=session), got)
         h = api.hypervolume(got, r, session=session)
         assert h == pytest.approx(ref.hypervolume(want.values, np.asarray(r)), rel=1e-12)
+
+
+def test_random_dense_configurations_agree_with_reference(ref):
+    """the int8 tensor-core dSB path (n >= 256) on random configurations: words within the
+    dense tolerance (measured 0 %)"""
+    from test_gpu_dense import MAX_DENSE_WORD_MISMATCH
+
+    rnd = random.Random(505)
+    s = api.Session(0)
+    s.set_dense_threshold(256)
+    for _ in range(6):
+        n = rnd.choice([256, 272, 320])
+        k = rnd.choice([2, 3])
+        H = k + rnd.choice([1, 2])
+        iseed = rnd.randrange(1000)
+        dens = rnd.choice([0.3, 0.7])
+        batch = rnd.choice([1, 9, 33])
+        T = rnd.choice([5, 50])
+        alpha = rnd.choice([0.15, 0.0])
+        runs = rnd.choice([1, 2])
+        s.generate_uniform_instance(n, dens, k, iseed)
+        ri = ref.generate_uniform(n, dens, k, iseed)
+        nums = ref.das_dennis(k, H)
+        s.set_weights([api.WeightVector(list(r), H) for r in nums])
+        c = make_cfg("dsb", n_iterations=T, batch_size=batch, seed=iseed, threads=16, alpha=alpha)
+        want = ref.run_sampler(ri, nums, H, c, runs)["words"]
+        s.sample(api.SolverConfig(variant=api.SolverVariant.discrete_sb, n_iterations=T, batch_size=batch, seed=iseed,
+                                  alpha=alpha), runs)
+        got = s.pool(stamps=False).words
+        assert got.shape == want.shape
+        assert float(np.mean(np.any(got != want, axis=1))) <= MAX_DENSE_WORD_MISMATCH, dict(
+            n=n, k=k, H=H, seed=iseed, dens=dens, batch=batch, T=T, alpha=alpha, runs=runs)
