@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
 
         // ---- A1: Philox blocks (lane h: blocks h, h+LANES, ...) + fast-attempt mask
         uint64_t F0 = 0, F1 = 0;
-#pragma unroll 2
+#pragma unroll 4
         for (int b = h; b < G::kNB; b += LANES) {
             const uint4 r = philox(k0, k1, static_cast<uint32_t>(b), lo, tr, wl);
             *reinterpret_cast<uint4*>(ub + 4 * b) = r;
