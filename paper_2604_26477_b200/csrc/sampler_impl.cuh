@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
             // its count to 32
             auto from = [](int b) -> uint32_t { return __funnelshift_lc(0u, ~0u, static_cast<uint32_t>(max(b, 0))); };
             int pos = 0, i = 0, cur = 0;  // cur: the word offset of the next fast normal
+#pragma unroll 2
             for (int j = 0; j < m; ++j) {
                 const uint32_t e = en[j * TPC];
                 const int q = static_cast<int>(e & 0xFFu);
