@@ -85,10 +85,15 @@ int momc_b200_generate_correlated_instance(momc_ctx* ctx, int n, double density,
 int momc_b200_measured_correlation(momc_ctx* ctx, int pool_size, uint64_t seed, double* out, char* err, size_t errlen);
 /* copy the resident instance out: edge_i, edge_j (m), w (m x k) */
 int momc_b200_instance_get(momc_ctx* ctx, int32_t* edge_i, int32_t* edge_j, double* w, char* err, size_t errlen);
-/* dSB with integer weights and |H*J(c)| <= 127 uses the int8 tensor-core contraction
- * (exact) with one FP64 rounding of J(c).sgn(X) when n >= n_min (default 256); smaller n
- * keep the bit-exact FP64 order of the reference. */
+/* dSB with integer weights and |H*J(c)| <= 256 uses the fused tensor-core step (exact
+ * int8 / bf16 contraction H*J(c).sgn(X), then one FP64 rounding of c0/H times it) when
+ * n >= n_min (default 256); smaller n keep the bit-exact FP64 order of the reference. */
 int momc_b200_set_dense_threshold(momc_ctx* ctx, int n_min);
+/* Which sampler produced the resident pool: 0 none yet, 1 register-resident (n <= 64,
+ * bit-exact), 2 sequential generic (bit-exact), 3 fused tensor-core dSB with int8 H*J(c),
+ * 4 the same with bf16 H*J(c). Paths 3 and 4 round J(c).sgn(X) once (not bit-exact; see
+ * DESIGN.md §3). */
+int momc_b200_sampler_path(momc_ctx* ctx);
 
 /* Upload L interior weight vectors (numerators, row-major L x k, denominator H) and
  * scalarise every one on the device: build_block_system / scalarize
@@ -211,6 +216,7 @@ typedef struct {
     double reference[16];
     double dedup_s, eval_s, collapse_s, front_s, order_s, reference_s, hv_s;
     int front_method; /* 1 compressed grid, 2 all-pairs */
+    int sampler_path; /* momc_b200_sampler_path() of the sampling stage */
 } momc_bench_report;
 
 /* bench(): instance -> scalarise L weight vectors -> sample runs*L*batch -> filter ->

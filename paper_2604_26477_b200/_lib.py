@@ -57,6 +57,7 @@ class BenchReportC(C.Structure):
         ("reference_s", C.c_double),
         ("hv_s", C.c_double),
         ("front_method", C.c_int),
+        ("sampler_path", C.c_int),
     ]
 
 
@@ -86,6 +87,7 @@ SIGNATURES = [
                                                       C.c_double, C.c_uint64, i64p, C.c_char_p, C.c_size_t]),
     ("momc_b200_instance_get", C.c_int, [vp, i32p, i32p, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_set_dense_threshold", C.c_int, [vp, C.c_int]),
+    ("momc_b200_sampler_path", C.c_int, [vp]),
     ("momc_b200_set_weights", C.c_int, [vp, i32p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     ("momc_b200_get_coupling", C.c_int, [vp, C.c_int, dp, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_sample", C.c_int, [vp, C.POINTER(SolverCfgC), C.c_int, C.c_longlong, C.c_longlong, dp,

@@ -579,6 +579,14 @@ class Session:
     def set_dense_threshold(self, n_min: int):
         self.lib.momc_b200_set_dense_threshold(self.h, n_min)
 
+    SAMPLER_PATHS = ("none", "register", "generic", "dense_i8", "dense_bf16")
+
+    def sampler_path(self) -> str:
+        """which sampler produced the resident pool (momc_b200_sampler_path): "register" and
+        "generic" are bit-exact against the reference; "dense_i8" / "dense_bf16" (the fused
+        tensor-core step) round J(c).sgn(X) once"""
+        return self.SAMPLER_PATHS[int(self.lib.momc_b200_sampler_path(self.h))]
+
     def set_weights(self, weights):
         nums, H = _weights_array(weights, self.inst.k())
         err = _errbuf()

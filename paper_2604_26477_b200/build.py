@@ -76,7 +76,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     stamp = LIB + ".stamp"
     if os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == link_key:
         return LIB
-    cmd = [_nvcc()] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs + ["-lcublasLt", "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    cmd = [_nvcc()] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")

@@ -606,8 +606,10 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         return GenericScratch{c.d_gx.p, c.d_gy.p, c.d_gxn.p, c.d_gnoise.p, cap};
     };
     GenericScratch g{};
-    const bool densepath = !regpath && dense_path_ok(c, cfg->variant);
+    const int dkind = regpath ? 0 : dense_path_kind(c, cfg->variant);
+    const bool densepath = dkind != 0;
     if (!regpath && !densepath) g = scratch(nblocks);
+    c.last_path = regpath ? 1 : densepath ? 2 + dkind : 2;
 
     // the register sampler runs on the low-priority stream, after everything queued so far
     cudaStream_t ss = c.stream;
@@ -1305,6 +1307,7 @@ int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t
         rep->front_s = tm.front_s;
         rep->order_s = tm.order_s;
         rep->front_method = tm.front_method;
+        rep->sampler_path = ctx->last_path;
         const auto tr = clk::now();
         std::vector<double> r(static_cast<size_t>(ctx->k));
         if (fixed_ref) {
@@ -1363,6 +1366,7 @@ int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long
         rep->front_s = tm.front_s;
         rep->order_s = tm.order_s;
         rep->front_method = tm.front_method;
+        rep->sampler_path = ctx->last_path;
         if (do_hv) {
             const auto tr = clk::now();
             std::vector<double> r(static_cast<size_t>(ctx->k));
@@ -1436,6 +1440,8 @@ int momc_b200_instance_get(momc_ctx* ctx, int32_t* edge_i, int32_t* edge_j, doub
         std::copy(ctx->h_w.begin(), ctx->h_w.end(), w);
     });
 }
+
+int momc_b200_sampler_path(momc_ctx* ctx) { return ctx ? ctx->last_path : 0; }
 
 int momc_b200_set_dense_threshold(momc_ctx* ctx, int n_min)
 {

@@ -67,6 +67,7 @@ struct Ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
     long long fallback_blocks = 0;  // sampler blocks re-run on the sequential path
+    int last_path = 0;              // momc_b200_sampler_path of the resident pool
     int fallback_reasons = 0;
 
     // instance
@@ -130,6 +131,7 @@ inline void bind(Ctx& c)
 // dense.cu
 struct SamplerParams;
 bool dense_path_ok(Ctx& c, int variant);
+int dense_path_kind(Ctx& c, int variant);  // 0 none, 1 int8, 2 bf16
 void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblocks);
 bool eval_gemm_ok(const Ctx& c);
 void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, long long U, double* d_out);

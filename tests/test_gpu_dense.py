@@ -104,22 +104,20 @@ def test_dense_reference_point_matches_reference(ref, session):
     assert api.reference_point_sampled(inst, 333, 7, session=session) == ref.reference_point_sampled(ri, 333, 7).tolist()
 
 
-def test_tcgen05_step_matches_cublaslt_path(session):
-    """the fused tcgen05 step (MOMC_DENSE_TC=1) and the cuBLASLt GEMM + update kernels
-    (default) compute the same exact D = (H J) sgn(X) and the same update: identical words"""
-    import os
-    n, H = 384, 4
-    session.generate_uniform_instance(n, 0.6, 3, 21)
-    nums = [[a, b, H - a - b] for a in range(1, H) for b in range(1, H - a)]
+def test_dense_bf16_path_agrees_with_reference(ref, session):
+    """H = 21 (190 weights for K = 3) with |w| <= 10 puts |H*J| up to 210: beyond int8, so the
+    fused kernel runs kind::f16 with bf16 H*J (exact integers <= 256) and FP32 accumulation"""
+    n, H = 320, 21
+    session.generate_uniform_instance(n, 0.4, 3, 31)
+    ri = ref.generate_uniform(n, 0.4, 3, 31)
+    nums = ref.das_dennis(3, H)[::9]  # 24 of the 253 lattice vectors, including boundary ones
+    batch = 9
+    want = ref.run_sampler(ri, nums, H, make_cfg("dsb", batch_size=batch, seed=12, threads=16), 1)["words"]
     session.set_dense_threshold(256)
-    session.set_weights([api.WeightVector(r, H) for r in nums])
-    cfg = api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=200, seed=4)
-    session.sample(cfg, 1)
-    a = session.pool(stamps=False).words.copy()
-    os.environ["MOMC_DENSE_TC"] = "1"
-    try:
-        session.sample(cfg, 1)
-    finally:
-        del os.environ["MOMC_DENSE_TC"]
-    b = session.pool(stamps=False).words
-    assert np.array_equal(a, b)
+    session.set_weights([api.WeightVector(list(r), H) for r in nums])
+    session.sample(api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=batch, seed=12), 1)
+    assert session.sampler_path() == "dense_bf16"
+    got = session.pool(stamps=False).words
+    mm = int(np.sum(np.any(got != want, axis=1)))
+    print(f"dense bf16 dSB n={n}: {mm} of {got.shape[0]} words differ")
+    assert mm <= MAX_DENSE_WORD_MISMATCH * got.shape[0]
