@@ -524,7 +524,8 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     if (runs < 1) usage("runs must be >= 1");
     const int batch = cfg->batch_size;
     const bool regpath = sampler_uses_register_path(c.n, cfg->alpha);
-    const int bt = sampler_block_traj(c.n, cfg->alpha);
+    const int dkind = regpath ? 0 : dense_path_kind(c, cfg->variant);
+    const int bt = dkind ? dense_block_traj() : sampler_block_traj(c.n, cfg->alpha);
     const int chunks = (batch + bt - 1) / bt;
     const long long total_blocks = static_cast<long long>(runs) * c.L * chunks;
     if (b_end < 0 || b_end > total_blocks) b_end = total_blocks;
@@ -606,7 +607,6 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         return GenericScratch{c.d_gx.p, c.d_gy.p, c.d_gxn.p, c.d_gnoise.p, cap};
     };
     GenericScratch g{};
-    const int dkind = regpath ? 0 : dense_path_kind(c, cfg->variant);
     const bool densepath = dkind != 0;
     if (!regpath && !densepath) g = scratch(nblocks);
     c.last_path = regpath ? 1 : densepath ? 2 + dkind : 2;
@@ -680,31 +680,43 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         const int chunkb = static_cast<int>(gb % chunks);
         const long long rl = gb / chunks;
         const int l = static_cast<int>(rl % c.L), run = static_cast<int>(rl / c.L);
-        const int per512 = 512 / bt;  // blocks per reference task (kTrajectoryChunk, solver.hpp:99)
-        const int c512 = chunkb / per512;
-        const long long rb = rl * chunks + static_cast<long long>(per512) * c512;
-        const long long re = std::min<long long>(rl * chunks + chunks, rb + per512);
-        SamplerParams q = p;
-        q.block_begin = rb;
-        q.first_bad_step_task = 1;
-        q.block_end_ns = nullptr;
-        ck(cudaMemsetAsync(c.d_badstep.p, 0x7f, sizeof(int) * (re - rb), c.stream), "memset");
-        // scratch outputs so the pool / flags of the real run are untouched
-        DevBuf<uint64_t> wtmp;
-        const auto tr = rows_of_blocks(batch, bt, rb, re);
-        q.row0 = tr.first;
-        wtmp.reserve(static_cast<size_t>(tr.second - tr.first) * wpc + 1);
-        DevBuf<int> ntmp;
-        ntmp.reserve(static_cast<size_t>(re - rb));
-        q.words = wtmp.p;
-        q.nan_block = ntmp.p;
-        g = scratch(re - rb);  // the sequential path carries the per-step finiteness check
-        const int rc = launch_sampler_generic(q, re - rb, g, c.stream);
-        ck(static_cast<cudaError_t>(rc), "sampler debug launch");
-        std::vector<int> bs(static_cast<size_t>(re - rb));
-        ck(cudaMemcpyAsync(bs.data(), c.d_badstep.p, sizeof(int) * (re - rb), cudaMemcpyDeviceToHost, c.stream), "D2H");
-        ck(cudaStreamSynchronize(c.stream), "sync");
-        int step = *std::min_element(bs.begin(), bs.end());
+        // re-run the reference tasks (512 trajectories, kTrajectoryChunk solver.hpp:99) that
+        // overlap the failing block, in order, on the sequential path in 128-trajectory blocks
+        const int gbt = kSampleBlock, gchunks = (batch + gbt - 1) / gbt, per512 = 512 / gbt;
+        const int tf = chunkb * bt, tl = std::min(tf + bt, batch) - 1;
+        int step = 0x7f7f7f7f;
+        for (int task = tf / 512; task <= tl / 512 && step == 0x7f7f7f7f; ++task) {
+            const long long rb = rl * gchunks + static_cast<long long>(per512) * task;
+            const long long re = std::min<long long>(rl * gchunks + gchunks, rb + per512);
+            SamplerParams q = p;
+            q.block_traj = gbt;
+            q.chunks = gchunks;
+            q.block_begin = rb;
+            q.first_bad_step_task = 1;
+            q.block_end_ns = nullptr;
+            ck(cudaMemsetAsync(c.d_badstep.p, 0x7f, sizeof(int) * (re - rb), c.stream), "memset");
+            // scratch outputs so the pool / flags of the real run are untouched
+            DevBuf<uint64_t> wtmp;
+            const auto tr = rows_of_blocks(batch, gbt, rb, re);
+            q.row0 = tr.first;
+            wtmp.reserve(static_cast<size_t>(tr.second - tr.first) * wpc + 1);
+            DevBuf<int> ntmp;
+            ntmp.reserve(static_cast<size_t>(re - rb));
+            q.words = wtmp.p;
+            q.nan_block = ntmp.p;
+            const long long cap = (re - rb) * gbt;  // the sequential path carries the per-step finiteness check
+            c.d_gx.reserve(static_cast<size_t>(cap) * c.n);
+            c.d_gy.reserve(static_cast<size_t>(cap) * c.n);
+            c.d_gxn.reserve(static_cast<size_t>(cap) * c.n);
+            c.d_gnoise.reserve(static_cast<size_t>(cap) * c.n);
+            const GenericScratch gs{c.d_gx.p, c.d_gy.p, c.d_gxn.p, c.d_gnoise.p, cap};
+            const int rc = launch_sampler_generic(q, re - rb, gs, c.stream);
+            ck(static_cast<cudaError_t>(rc), "sampler debug launch");
+            std::vector<int> bs(static_cast<size_t>(re - rb));
+            ck(cudaMemcpyAsync(bs.data(), c.d_badstep.p, sizeof(int) * (re - rb), cudaMemcpyDeviceToHost, c.stream), "D2H");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            step = *std::min_element(bs.begin(), bs.end());
+        }
         runtime("numerical failure at step " + std::to_string(step) + " (run " + std::to_string(run) + ", weight " +
                 std::to_string(l) + ")");
     }
@@ -1390,7 +1402,9 @@ int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long
 long long momc_b200_num_blocks(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs)
 {
     if (!ctx || !cfg || cfg->batch_size < 1 || runs < 1 || ctx->L < 1) return 0;
-    const int bt = sampler_block_traj(ctx->n, cfg->alpha);
+    bind(*ctx);
+    const bool regpath = sampler_uses_register_path(ctx->n, cfg->alpha);
+    const int bt = !regpath && dense_path_kind(*ctx, cfg->variant) ? dense_block_traj() : sampler_block_traj(ctx->n, cfg->alpha);
     return static_cast<long long>(runs) * ctx->L * ((cfg->batch_size + bt - 1) / bt);
 }
 

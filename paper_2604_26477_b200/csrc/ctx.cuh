@@ -132,6 +132,7 @@ inline void bind(Ctx& c)
 struct SamplerParams;
 bool dense_path_ok(Ctx& c, int variant);
 int dense_path_kind(Ctx& c, int variant);  // 0 none, 1 int8, 2 bf16
+int dense_block_traj();                      // trajectories per block of the dense path
 void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblocks);
 bool eval_gemm_ok(const Ctx& c);
 void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, long long U, double* d_out);

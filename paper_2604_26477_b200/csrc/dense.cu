@@ -13,16 +13,18 @@
 // bit-for-bit; the pool reports the path (Session.sampler_path).
 //
 // One persistent, warp-specialised kernel (k_dense_fused) runs init, all T steps and the
-// readout of one work item = one 128-trajectory block of one (run, weight) pair at a time.
+// readout of one work item = one 120-trajectory block of one (run, weight) pair at a time
+// (MMA rows 120..127 are padding, so the 15 epilogue warps take 8 trajectories each).
 // Per step it walks the spins in tiles of 128:
 //   * the contraction: D_tile (128 traj x 128 spins, TMEM) = Phi (128 x n) . HJ_tile^T with
 //     A = Phi from TMEM and B = the HJ tile from shared memory (TMA, 128-byte swizzle), K in
 //     chunks of 128 bytes, 4 stages; two TMEM accumulators (tile s and s+1 overlap);
+//   * a producer warp: one thread keeps the B TMA up to 4 chunks ahead and issues the
+//     tcgen05.mma of every chunk;
 //   * 4 io warps (one per TMEM lane quarter): expand the packed sign bits of Phi into the A
 //     stage (tcgen05.st) and drain finished accumulators to shared memory (tcgen05.ld ->
-//     64 KB swizzled [traj][spin] int32 tile, double-buffered); one thread of io warp 0 also
-//     issues the B TMA and the tcgen05.mma of every chunk;
-//   * 16 epilogue warps: one warp per trajectory-tile, lanes over spins (32 per window). The
+//     64 KB swizzled [traj][spin] int32 tile, double-buffered);
+//   * 15 epilogue warps: one warp per trajectory-tile, lanes over spins (32 per window). The
 //     (trajectory, step) noise stream (rng.hpp:156-185) is resolved warp-wide: lane L tests
 //     word head + L; slow words (wedge / tail attempts) are tested in parallel and a ballot +
 //     popcount orders the produced normals into a 64-entry ring; each window takes 32. At
@@ -83,15 +85,16 @@ __global__ void k_build_hj(int n, int npad, int k, const int* __restrict__ nums,
 }
 
 // ---- the fused kernel ----------------------------------------------------------------------
-constexpr int kNT = 128;          // trajectories per work item: MMA M, TMEM lanes
+constexpr int kNT = 128;          // MMA M = TMEM lanes = trajectory rows per work item
+constexpr int kNTV = 120;         // trajectories per work item (rows 120..127 are padding)
 constexpr int kNS = 128;          // spins per tile: MMA N, TMEM columns per accumulator
-constexpr int kStages = 4;        // K chunks in flight (A in TMEM, B in shared memory)
-constexpr int kEpiWarps = 16;     // epilogue warps (8 trajectories each per tile)
-constexpr int kEpiWarp0 = 4;      // warps 0..3: io (expand / drain; warp 0 also TMA + MMA); 4..19: epilogue
+constexpr int kStages = 3;        // K chunks in flight (A in TMEM, B in shared memory)
+constexpr int kEpiWarps = 15;     // epilogue warps (8 trajectories each per tile)
+constexpr int kEpiWarp0 = 5;      // warp 0: TMA + MMA; 1..4: io (expand / drain); 5..19: epilogue
 // 20 warps = 5 per SM sub-partition, so each thread may hold 96 registers
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
 constexpr int kRing = 256;        // noise words per epilogue warp
-constexpr int kNBuf = 64;         // buffered normals per epilogue warp
+constexpr int kNBuf = 160;        // normals per epilogue warp: a tile's 128 + one round's overshoot
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColA = 256;   // A stages at TMEM columns [256, 256 + 32 kStages)
 constexpr int kBStage = kNS * 128;  // bytes of one B stage (128 spins x 128 bytes of K)
@@ -133,12 +136,14 @@ __device__ __forceinline__ ItemOf item_of(const FusedArgs& a, long long it)
     ItemOf r;
     r.l = static_cast<int>(rl % a.L);
     r.run = static_cast<int>(rl / a.L);
-    r.traj0 = chunk * kNT;
-    r.count = min(kNT, a.batch - r.traj0);
+    r.traj0 = chunk * kNTV;
+    r.count = min(kNTV, a.batch - r.traj0);
     return r;
 }
 
 __device__ __forceinline__ uint32_t zmag32(uint32_t u) { return static_cast<int32_t>(u) < 0 ? 0u - u : u; }
+
+__device__ __noinline__ bool exp_decides(double lhs, double targ) { return lhs < exp(targ); }
 
 // wedge test of the attempt at word u with uniform words (w1, w2) (rng.hpp:178-183): the FP32
 // exp brackets the FP64 one within 1e-6 relative on [-6, 0]; the FP64 exp decides the band
@@ -151,7 +156,34 @@ __device__ __forceinline__ bool wedge_accept(uint32_t u, uint32_t w1, uint32_t w
     const float ef = __expf(static_cast<float>(targ));
     if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) return true;
     if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) return false;
-    return lhs < exp(targ);
+    return exp_decides(lhs, targ);
+}
+
+// the tail attempt starting at word p0 of the (key, lo, mid, hi) stream (rng.hpp:165-177):
+// (x, y) trials of 4 words until 2y >= x^2; returns the normal and its length in words. Rare
+// (one word in ~1,600), so it lives out of line and reads every word from the ring or Philox.
+struct TailOut {
+    double v;
+    int len;
+};
+__device__ __noinline__ TailOut tail_attempt(const uint32_t* ring, int tail, int p0, uint32_t u, uint32_t k0, uint32_t k1,
+                                             uint32_t lo, uint32_t mid, uint32_t hi)
+{
+    auto word = [&](int p) -> uint32_t {
+        if (p < tail) return ring[p & 255];
+        const uint4 v = philox(k0, k1, static_cast<uint32_t>(p >> 2), lo, mid, hi);
+        const int c = p & 3;
+        return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+    };
+    const double rr = 3.442619855899;
+    int qq = p0 + 1;
+    for (;;) {
+        const double xx = __ddiv_rn(-log(u01_open_from(word(qq), word(qq + 1))), rr);
+        const double yy = -log(u01_open_from(word(qq + 2), word(qq + 3)));
+        qq += 4;
+        if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx))
+            return {static_cast<int32_t>(u) > 0 ? __dadd_rn(rr, xx) : -__dadd_rn(rr, xx), qq - p0};
+    }
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -182,9 +214,16 @@ __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<co
 // epilogue's column-contiguous warp reads are both conflict-free
 __device__ __forceinline__ int dsw(int r, int c) { return r * kNS + (c ^ ((r & 7) << 2)); }
 
+// Named hardware barrier (a waiting warp does not issue): the epilogue warps arrive at
+// kBarDEmpty + b when done with D buffer b, the io warps sync on it before refilling it.
+constexpr int kBarDEmpty = 1;
+constexpr int kBarThreads = (4 + kEpiWarps) * 32;
+__device__ __forceinline__ void named_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kBarThreads) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(kBarThreads) : "memory"); }
+
 struct FusedShared {
     uint64_t b_full[kStages], b_empty[kStages], a_full[kStages], a_empty[kStages];
-    uint64_t d_full[2], d_empty[2], s_full[2], s_empty[2];
+    uint64_t d_full[2], d_empty[2], s_full[2];
     uint32_t tslot;
     int epi_cnt[2], tiles_done, init_cnt, init_done;
 };
@@ -196,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dense_fused(const __grid_consta
                                                              const __grid_constant__ FusedArgs a)
 {
     extern __shared__ uint8_t sm_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     __shared__ FusedShared S;
     ZigTables& z = *reinterpret_cast<ZigTables*>(sm + kOffZig);
     int* pos = reinterpret_cast<int*>(sm + kOffPos);
@@ -231,7 +270,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_dense_fused(const __grid_consta
             tc::mbar_init(&S.d_full[q], 1);
             tc::mbar_init(&S.d_empty[q], 4);
             tc::mbar_init(&S.s_full[q], 4);
-            tc::mbar_init(&S.s_empty[q], kEpiWarps);
             S.epi_cnt[q] = 0;
         }
         S.tiles_done = 0;
@@ -248,36 +286,93 @@ __global__ void __launch_bounds__(kThreads, 1) k_dense_fused(const __grid_consta
     const int nt = a.ntiles, nch = a.nchunks;
     const long long slot = blockIdx.x;
 
-    if (warp < kEpiWarp0) {
-        // ===== io warps (warp = TMEM lane quarter): drain tile s-1, then expand the A chunks of
-        //       tile s; lane 0 of warp 0 also issues the B TMA (two chunks ahead) and the MMAs
-        const int q = warp;
+    if (warp == 0) {
+        // ===== producer: one thread keeps the B TMA up to kStages chunks ahead and issues the
+        //       MMAs of every chunk once its A (io warps) and B (TMA) stages are full
+        if (lane == 0) {
+            const uint32_t idesc = BF16 ? tc::idesc_bf16(kNT, kNS) : tc::idesc_i8(kNT, kNS);
+            const long long my_items = a.nblocks > blockIdx.x ? (a.nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+            const long long g_total = my_items * a.T * nt * nch;
+            long long g_tma = 0;
+            int tma_c = 0, tma_m = 0, tma_t = 0;  // (step, tile, chunk) of chunk g_tma within its item
+            long long tma_it = blockIdx.x;
+            int tma_l = my_items > 0 ? item_of(a, tma_it).l : 0;
+            auto issue = [&]() {
+                const uint32_t st = static_cast<uint32_t>(g_tma % kStages);
+                tc::mbar_expect_tx(&S.b_full[st], kBStage);
+                tc::tma_load_2d(sm + kOffB + st * kBStage, &tmB, tma_c * KC, tma_l * a.n + tma_m * kNS, &S.b_full[st]);
+                ++g_tma;
+                if (++tma_c == nch) {
+                    tma_c = 0;
+                    if (++tma_m == nt) {
+                        tma_m = 0;
+                        if (++tma_t == a.T) {
+                            tma_t = 0;
+                            tma_it += gridDim.x;
+                            if (tma_it < a.nblocks) tma_l = item_of(a, tma_it).l;
+                        }
+                    }
+                }
+            };
+            auto b_free = [&](long long gq) {
+                return tc::mbar_test(&S.b_empty[gq % kStages], (static_cast<uint32_t>(gq / kStages) & 1) ^ 1);
+            };
+            long long g = 0;
+            // TMA of every chunk whose stage is free, up to kStages ahead of the MMA (non-blocking)
+            auto pump = [&]() {
+                while (g_tma < g_total && g_tma < g + kStages && b_free(g_tma)) issue();
+            };
+            uint32_t s = 0;
+            for (long long it = blockIdx.x; it < a.nblocks; it += gridDim.x)
+                for (int t = 0; t < a.T; ++t)
+                    for (int m = 0; m < nt; ++m, ++s) {
+                        const uint32_t buf = s & 1;
+                        while (!tc::mbar_test(&S.d_empty[buf], ((s >> 1) & 1) ^ 1)) {
+                            pump();
+                            __nanosleep(64);
+                        }
+                        tc::fence_after();
+                        const uint32_t dt = tbase + buf * kNS;
+                        for (int c = 0; c < nch; ++c, ++g) {
+                            const uint32_t st = static_cast<uint32_t>(g % kStages), ph = static_cast<uint32_t>(g / kStages) & 1;
+                            pump();
+                            while (g_tma <= g) {  // this chunk's own load (its stage frees with chunk g - kStages)
+                                if (b_free(g_tma)) issue();
+                                else __nanosleep(32);
+                            }
+                            while (!tc::mbar_test(&S.a_full[st], ph) || !tc::mbar_test(&S.b_full[st], ph)) {
+                                pump();
+                                __nanosleep(32);
+                            }
+                            tc::fence_after();
+                            const uint32_t at = tbase + kColA + st * 32;
+                            const uint32_t bs = tc::smem_u32(sm + kOffB + st * kBStage);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                if (BF16) tc::mma_f16_ts(dt, at + 8 * k, tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
+                                else tc::mma_i8_ts(dt, at + 8 * k, tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
+                            }
+                            tc::commit(&S.a_empty[st]);
+                            tc::commit(&S.b_empty[st]);
+                        }
+                        tc::commit(&S.d_full[buf]);
+                    }
+        }
+        __syncwarp();
+    } else if (warp < kEpiWarp0) {
+        // ===== io warps (TMEM lane quarter = warp & 3): drain tile s-1, then expand the A chunks
+        //       of tile s
+        const int q = warp & 3;
         const int r = q * 32 + lane;  // trajectory row of this thread
         const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
         const uint32_t* lut = reinterpret_cast<const uint32_t*>(sm + kOffLut);
-        const uint32_t idesc = BF16 ? tc::idesc_bf16(kNT, kNS) : tc::idesc_i8(kNT, kNS);
-        const long long my_items = a.nblocks > blockIdx.x ? (a.nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-        const long long per_item = static_cast<long long>(a.T) * nt * nch;
-        const long long g_total = my_items * per_item;
-        long long g_tma = 0;
-        auto tma_ahead = [&](long long upto) {  // B chunks [g_tma, upto)
-            for (; g_tma < upto && g_tma < g_total; ++g_tma) {
-                const uint32_t st = static_cast<uint32_t>(g_tma % kStages), ph = static_cast<uint32_t>(g_tma / kStages) & 1;
-                const long long ii2 = g_tma / per_item, rem = g_tma % per_item;
-                const int m2 = static_cast<int>((rem / nch) % nt), c2 = static_cast<int>(rem % nch);
-                const ItemOf io2 = item_of(a, blockIdx.x + ii2 * gridDim.x);
-                tc::mbar_wait(&S.b_empty[st], ph ^ 1);
-                tc::mbar_expect_tx(&S.b_full[st], kBStage);
-                tc::tma_load_2d(sm + kOffB + st * kBStage, &tmB, c2 * KC, io2.l * a.n + m2 * kNS, &S.b_full[st]);
-            }
-        };
         uint32_t s = 0;
         long long g = 0;
         int ii = 0;
         auto drain = [&](uint32_t sd) {
             const uint32_t buf = sd & 1;
-            tc::mbar_wait(&S.d_full[buf], (sd >> 1) & 1);
-            tc::mbar_wait_sleep(&S.s_empty[buf], ((sd >> 1) & 1) ^ 1);
+            tc::mbar_wait_sleep(&S.d_full[buf], (sd >> 1) & 1, 512);
+            if (sd >= 2) named_sync(kBarDEmpty + buf);  // the epilogue is done with tile sd - 2
             tc::fence_after();
             int* D = reinterpret_cast<int*>(sm + kOffD + buf * (kNT * kNS * 4));
 #pragma unroll 1
@@ -307,15 +402,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_dense_fused(const __grid_consta
                     prev = true;
                     for (int c = 0; c < nch; ++c, ++g) {
                         const uint32_t st = static_cast<uint32_t>(g % kStages), ph = static_cast<uint32_t>(g / kStages) & 1;
-                        if (q == 0 && lane == 0) tma_ahead(g + 3);
-                        tc::mbar_wait(&S.a_empty[st], ph ^ 1);
+                        tc::mbar_wait_sleep(&S.a_empty[st], ph ^ 1, 256);
                         // the sign bits of Phi_t for this chunk: written by init (t = 0) or by the
                         // epilogue of step t-1, tile (c KC) / kNS
                         if (t == 0) {
-                            while (vload(&S.init_done) < ii + 1) __nanosleep(32);
+                            while (vload(&S.init_done) < ii + 1) __nanosleep(1000);
                         } else {
                             const int need = static_cast<int>(s) - m - nt + (c * KC) / kNS + 1;
-                            while (vload(&S.tiles_done) < need) __nanosleep(32);
+                            while (vload(&S.tiles_done) < need) __nanosleep(500);
                         }
                         __threadfence_block();
                         uint32_t v[32];
@@ -346,29 +440,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_dense_fused(const __grid_consta
                         tc::fence_before();
                         __syncwarp();
                         if (lane == 0) tc::mbar_arrive(&S.a_full[st]);
-                        if (q == 0 && lane == 0) {  // the MMAs of chunk g
-                            const uint32_t buf = s & 1;
-                            if (c == 0) tc::mbar_wait(&S.d_empty[buf], ((s >> 1) & 1) ^ 1);
-                            tc::mbar_wait(&S.a_full[st], ph);
-                            tc::mbar_wait(&S.b_full[st], ph);
-                            tc::fence_after();
-                            const uint32_t dt = tbase + buf * kNS, at = tbase + kColA + st * 32;
-                            const uint32_t bs = tc::smem_u32(sm + kOffB + st * kBStage);
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                if (BF16) tc::mma_f16_ts(dt, at + 8 * k, tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
-                                else tc::mma_i8_ts(dt, at + 8 * k, tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
-                            }
-                            tc::commit(&S.a_empty[st]);
-                            tc::commit(&S.b_empty[st]);
-                            if (c == nch - 1) tc::commit(&S.d_full[buf]);
-                        }
-                        __syncwarp();
                     }
                 }
             }
         }
         if (prev) drain(s - 1);
+        // the epilogue's arrivals for the last two tiles
+        for (uint32_t sd = s >= 2 ? s - 2 : 0; sd < s; ++sd) named_sync(kBarDEmpty + (sd & 1));
     } else {
         // ===== epilogue warps
         const int e = warp - kEpiWarp0;
@@ -378,7 +456,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_dense_fused(const __grid_consta
         uint32_t s = 0;
         int ii = 0;
         for (long long it = blockIdx.x; it < a.nblocks; it += gridDim.x, ++ii) {
-            const ItemOf io = item_of(a, it);
+            ItemOf io = item_of(a, it);
+            // opaque from here on: the 64-bit item decode must not be re-derived inside the loops
+            asm volatile("" : "+r"(io.l), "+r"(io.run), "+r"(io.traj0), "+r"(io.count));
             const uint64_t key = run_key(a.seed, static_cast<uint32_t>(io.run));
             const uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
             const double c0h = __ddiv_rn(a.c0[io.l], static_cast<double>(a.H));
@@ -386,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dense_fused(const __grid_consta
             // ---- init_state (solver.hpp:108-124): x, y from the init_x / init_y streams, spin
             //      i from words 2i, 2i+1 (block i/2); lanes 0-15 make the x blocks of a 32-spin
             //      window, lanes 16-31 the y blocks
-            for (int jj = e; jj < kNT; jj += kEpiWarps) {
+            for (int jj = e; jj < kNTV; jj += kEpiWarps) {
                 uint32_t* pb0 = a.phib + ((slot * 2 + 0) * kNT + jj) * a.nwp;
                 if (jj >= io.count) continue;
                 const long long rowb = (slot * kNT + jj) * static_cast<long long>(a.n);
@@ -428,145 +508,157 @@ __global__ void __launch_bounds__(kThreads, 1) k_dense_fused(const __grid_consta
                     *reinterpret_cast<volatile int*>(&S.init_done) = ii + 1;
                 }
             }
-            // ---- the T steps
+            // ---- the T steps. This warp's work units (t, tile m, trajectory jj) run in order. A
+            //      unit first produces the tile's normals into nbuf (one loop over rounds), then
+            //      updates its four 32-spin windows in straight-line code; the x / y of the next
+            //      unit are loaded into each window's registers as soon as they are free.
+            double xr[4], yr[4];
+            double* const xs = a.x + slot * kNT * static_cast<long long>(a.n);  // this CTA's state rows
+            double* const ys = a.y + slot * kNT * static_cast<long long>(a.n);
+            if (e < io.count)
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const int sp = 32 * g + lane;
+                    xr[g] = sp < a.n ? xs[e * a.n + sp] : 0.0;
+                    yr[g] = sp < a.n ? ys[e * a.n + sp] : 0.0;
+                }
             for (int t = 0; t < a.T; ++t) {
                 const double neg_drift = -__dsub_rn(a.a0, __ddiv_rn(static_cast<double>(t + 1), static_cast<double>(a.T)));
                 const uint32_t lo = tag_word(kTagStepNoise, static_cast<uint32_t>(t));
                 const bool last = t == a.T - 1;
-                for (int jj = e; jj < kNT; jj += kEpiWarps) pos[jj] = 0;  // own rows only
+                for (int jj = e; jj < kNTV; jj += kEpiWarps) pos[jj] = 0;  // own rows only
                 for (int m = 0; m < nt; ++m, ++s) {
                     const uint32_t buf = s & 1;
-                    tc::mbar_wait(&S.s_full[buf], (s >> 1) & 1);
+                    tc::mbar_wait_sleep(&S.s_full[buf], (s >> 1) & 1, 128);  // the drain of tile s is complete
                     const int* D = reinterpret_cast<const int*>(sm + kOffD + buf * (kNT * kNS * 4));
                     const int sb = m * kNS;
+                    const int ns = min(kNS, a.n - sb);  // spins of this tile
                     for (int jj = e; jj < io.count; jj += kEpiWarps) {
-                        const long long rowb = (slot * kNT + jj) * static_cast<long long>(a.n);
-                        double xr[4], yr[4];
-#pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            const int sp = sb + 32 * g + lane;
-                            xr[g] = sp < a.n ? a.x[rowb + sp] : 0.0;
-                            yr[g] = sp < a.n ? a.y[rowb + sp] : 0.0;
+                        // the next unit of this warp
+                        int nm = m, nj = jj + kEpiWarps;
+                        bool has_next = true;
+                        if (nj >= io.count) {
+                            nj = e;
+                            if (++nm == nt) {
+                                nm = 0;
+                                has_next = !last;
+                            }
                         }
-                        // noise stream of (trajectory, step t) from the position kept at the last tile
-                        const uint32_t mid = static_cast<uint32_t>(io.traj0 + jj), hi = static_cast<uint32_t>(io.l);
-                        int head = pos[jj], tail = head & ~3, nh = 0, ntl = 0, hlast = 0;
-                        uint32_t plast = 0;
-                        auto gen = [&]() {
-                            const uint4 v = philox(k0, k1, static_cast<uint32_t>(tail >> 2) + static_cast<uint32_t>(lane), lo, mid, hi);
-                            *reinterpret_cast<uint4*>(&ring[(tail + 4 * lane) & (kRing - 1)]) = v;
-                            tail += 128;
-                            __syncwarp();
-                        };
-                        auto word = [&](int p) -> uint32_t {
-                            if (p < tail) return ring[p & (kRing - 1)];
-                            const uint4 v = philox(k0, k1, static_cast<uint32_t>(p >> 2), lo, mid, hi);
-                            const int c = p & 3;
-                            return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
-                        };
-                        // one round: test 32 words from head, append the normals they produce
-                        auto round = [&]() {
-                            if (tail - head < 96) gen();
-                            const int H0 = head;
-                            const uint32_t u = ring[(H0 + lane) & (kRing - 1)];
-                            const bool slow = !(zmag32(u) < z.kn[u & 127u]);
-                            const uint32_t smk = __ballot_sync(0xffffffffu, slow);
-                            double v = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), z.wn[u & 127u]);
-                            uint32_t prod = 0xffffffffu;
-                            int end = 32;
-                            if (smk) {
-                                bool good = !slow;
-                                int len = 1;
-                                if (slow) {
-                                    if (u & 127u) {
-                                        good = wedge_accept(u, ring[(H0 + lane + 1) & (kRing - 1)], ring[(H0 + lane + 2) & (kRing - 1)], z);
-                                        len = 3;
-                                    } else {  // tail: (x, y) trials of 4 words, always a normal
-                                        const double rr = 3.442619855899;
-                                        int qq = H0 + lane + 1;
-                                        for (;;) {
-                                            const double xx = __ddiv_rn(-log(u01_open_from(word(qq), word(qq + 1))), rr);
-                                            const double yy = -log(u01_open_from(word(qq + 2), word(qq + 3)));
-                                            qq += 4;
-                                            if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) {
-                                                v = static_cast<int32_t>(u) > 0 ? __dadd_rn(rr, xx) : -__dadd_rn(rr, xx);
-                                                break;
-                                            }
+                        if (NOISY) {
+                            // ---- the normals of this tile: (trajectory, step t) stream from the
+                            //      position kept at the last tile (rng.hpp:156-185)
+                            const uint32_t mid = static_cast<uint32_t>(io.traj0 + jj), hi = static_cast<uint32_t>(io.l);
+                            int head = pos[jj], tail = head & ~3, ntl = 0, hlast = 0;
+                            uint32_t plast = 0;
+                            while (ntl < ns) {
+                                if (tail - head < 40) {  // 32 Philox blocks: 128 words (a round reads <= 34 ahead)
+                                    const uint4 v = philox(k0, k1, static_cast<uint32_t>(tail >> 2) + static_cast<uint32_t>(lane), lo, mid, hi);
+                                    *reinterpret_cast<uint4*>(&ring[(tail + 4 * lane) & (kRing - 1)]) = v;
+                                    tail += 128;
+                                    __syncwarp();
+                                }
+                                // one round: lane L tests word head + L
+                                const int H0 = head;
+                                const uint32_t u = ring[(H0 + lane) & (kRing - 1)];
+                                const bool slow = !(zmag32(u) < z.kn[u & 127u]);
+                                const uint32_t smk = __ballot_sync(0xffffffffu, slow);
+                                double v = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), z.wn[u & 127u]);
+                                uint32_t prod = 0xffffffffu;
+                                int end = 32;
+                                if (smk) {
+                                    // every slow word is tested as if it started an attempt (the ones inside
+                                    // an earlier attempt are dropped below): wedges take 3 words, tails 1 + 4k
+                                    bool good = !slow;
+                                    int len = 1;
+                                    if (slow) {
+                                        if (u & 127u) {
+                                            good = wedge_accept(u, ring[(H0 + lane + 1) & (kRing - 1)], ring[(H0 + lane + 2) & (kRing - 1)], z);
+                                            len = 3;
+                                        } else {  // tail: always a normal
+                                            const TailOut to = tail_attempt(ring, tail, H0 + lane, u, k0, k1, lo, mid, hi);
+                                            v = to.v;
+                                            len = to.len;
+                                            good = true;
                                         }
-                                        len = qq - (H0 + lane);
-                                        good = true;
                                     }
+                                    const uint32_t gm = __ballot_sync(0xffffffffu, good);
+                                    uint32_t cons = 0, rem = smk;
+                                    while (rem) {  // the attempts in order; their extra words are consumed
+                                        const int qb = __ffs(rem) - 1;
+                                        const int lq = __shfl_sync(0xffffffffu, len, qb);
+                                        const uint32_t span = qb + lq >= 32 ? ~0u << qb : ((1u << lq) - 1u) << qb;
+                                        cons |= span & ~(1u << qb);
+                                        rem &= ~span;
+                                        end = qb + lq > end ? qb + lq : end;
+                                    }
+                                    prod = gm & ~cons;
                                 }
-                                const uint32_t gm = __ballot_sync(0xffffffffu, good);
-                                uint32_t cons = 0, rem = smk;
-                                while (rem) {  // the attempts in order; their extra words are consumed
-                                    const int qb = __ffs(rem) - 1;
-                                    const int lq = __shfl_sync(0xffffffffu, len, qb);
-                                    const uint32_t span = qb + lq >= 32 ? ~0u << qb : ((1u << lq) - 1u) << qb;
-                                    cons |= span & ~(1u << qb);
-                                    rem &= ~span;
-                                    end = qb + lq > end ? qb + lq : end;
-                                }
-                                prod = gm & ~cons;
+                                if ((prod >> lane) & 1u) nbuf[ntl + __popc(prod & lt)] = v;
+                                ntl += __popc(prod);
+                                head = H0 + end;
+                                hlast = H0;
+                                plast = prod;
                             }
-                            if ((prod >> lane) & 1u) nbuf[(ntl + __popc(prod & lt)) & (kNBuf - 1)] = v;
-                            ntl += __popc(prod);
-                            head = H0 + end;
-                            hlast = H0;
-                            plast = prod;
-                        };
-                        uint32_t bits[4];
+                            const int left = ntl - ns;
+                            if (left > 0) {  // next tile starts at the (k - left)-th producing word of the last round
+                                const int idx = __popc(plast & lt);
+                                const uint32_t hit = __ballot_sync(0xffffffffu, ((plast >> lane) & 1u) && idx == __popc(plast) - left);
+                                head = hlast + __ffs(hit) - 1;
+                            }
+                            if (lane == 0) pos[jj] = head;
+                            __syncwarp();
+                        }
+                        // ---- the updates (sb_step solver.hpp:159-181, phi = sgn(x)) of the four windows
+                        double* xp = xs + jj * a.n + sb;
+                        double* yp = ys + jj * a.n + sb;
+                        const double* xnp = xs + nj * a.n + nm * kNS;
+                        const double* ynp = ys + nj * a.n + nm * kNS;
+                        const int nsn = min(kNS, a.n - nm * kNS);
+                        uint32_t mybits = 0;  // lane g keeps the sign bits of window g
 #pragma unroll
                         for (int g = 0; g < 4; ++g) {
-                            const int s0 = sb + 32 * g;
-                            const int cnt = min(32, a.n - s0);
-                            if (cnt <= 0) {
-                                bits[g] = 0;
-                                continue;
-                            }
-                            double eta = 0.0;
-                            if (NOISY) {
-                                while (ntl - nh < cnt) round();
-                                __syncwarp();
-                                eta = nbuf[(nh + lane) & (kNBuf - 1)];
-                                __syncwarp();
-                                nh += cnt;
-                            }
-                            bool plus = false;
-                            if (lane < cnt) {
-                                const int dq = D[dsw(jj, 32 * g + lane)];
-                                double xi = xr[g], yi = yr[g];
-                                double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0h, static_cast<double>(dq)));
-                                if (NOISY) d = __dadd_rn(d, __dmul_rn(a.alpha, eta));
-                                yi = __dadd_rn(yi, UDT ? d : __dmul_rn(a.dt, d));
-                                xi = __dadd_rn(xi, UDT ? yi : __dmul_rn(a.sdt, yi));
-                                if (fabs(xi) > 1.0) {  // wall + clamp (both fire exactly when |x| > 1)
-                                    yi = 0.0;
-                                    xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
+                            const int cnt = ns - 32 * g;
+                            if (cnt > 0) {
+                                bool plus = false;
+                                if (lane < cnt) {
+                                    const int dq = D[dsw(jj, 32 * g + lane)];
+                                    double xi = xr[g], yi = yr[g];
+                                    double d = __dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0h, static_cast<double>(dq)));
+                                    if (NOISY) d = __dadd_rn(d, __dmul_rn(a.alpha, nbuf[32 * g + lane]));
+                                    yi = __dadd_rn(yi, UDT ? d : __dmul_rn(a.dt, d));
+                                    xi = __dadd_rn(xi, UDT ? yi : __dmul_rn(a.sdt, yi));
+                                    if (fabs(xi) > 1.0) {  // wall + clamp (both fire exactly when |x| > 1)
+                                        yi = 0.0;
+                                        xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
+                                    }
+                                    // the first step with a non-finite x or y has a non-finite y
+                                    nonfinite |= !(fabs(yi) <= 1.7976931348623157e308);
+                                    xp[32 * g + lane] = xi;
+                                    yp[32 * g + lane] = yi;
+                                    plus = !(xi < 0.0);
                                 }
-                                // the first step with a non-finite x or y has a non-finite y
-                                nonfinite |= !(fabs(yi) <= 1.7976931348623157e308);
-                                a.x[rowb + s0 + lane] = xi;
-                                a.y[rowb + s0 + lane] = yi;
-                                plus = !(xi < 0.0);
-                            }
-                            bits[g] = __ballot_sync(0xffffffffu, plus);
-                        }
-                        if (NOISY) {  // stream position of the first normal this tile did not use
-                            const int left = ntl - nh;
-                            pos[jj] = left > 0 ? hlast + static_cast<int>(__fns(plast, 0, __popc(plast) - left + 1)) : head;
-                        }
-                        if (lane == 0) {
-                            if (!last) {
-                                uint32_t* pbn = a.phib + ((slot * 2 + ((t + 1) & 1)) * kNT + jj) * a.nwp;
-                                *reinterpret_cast<uint4*>(pbn + 4 * m) = make_uint4(bits[0], bits[1], bits[2], bits[3]);
-                            } else {  // read_spins + pack (solver.hpp:237-244, :288-297)
-                                const long long row = (static_cast<long long>(io.run) * a.L + io.l) * a.batch + io.traj0 + jj - a.row0;
-                                uint64_t* wr = a.words + row * a.wpc;
-                                if (2 * m < a.wpc) wr[2 * m] = bits[0] | (static_cast<uint64_t>(bits[1]) << 32);
-                                if (2 * m + 1 < a.wpc) wr[2 * m + 1] = bits[2] | (static_cast<uint64_t>(bits[3]) << 32);
+                                const uint32_t b = __ballot_sync(0xffffffffu, plus);
+                                if (lane == g) mybits = b;
                             }
                         }
+                        // the next unit's x / y, all eight loads together: the next unit's noise phase
+                        // covers their latency, and no wait of this unit shares a scoreboard with them
+                        if (has_next)
+#pragma unroll
+                            for (int g = 0; g < 4; ++g)
+                                if (32 * g + lane < nsn) {
+                                    xr[g] = xnp[32 * g + lane];
+                                    yr[g] = ynp[32 * g + lane];
+                                }
+                        if (!last) {
+                            uint32_t* pbn = a.phib + ((slot * 2 + ((t + 1) & 1)) * kNT + jj) * a.nwp;
+                            if (lane < 4) pbn[4 * m + lane] = mybits;
+                        } else {  // read_spins + pack (solver.hpp:237-244, :288-297): 32-bit halves of the words
+                            const long long row = (static_cast<long long>(io.run) * a.L + io.l) * a.batch + io.traj0 + jj - a.row0;
+                            uint32_t* wr = reinterpret_cast<uint32_t*>(a.words + row * a.wpc);
+                            if (lane < 4 && 4 * m + lane < 2 * a.wpc) wr[4 * m + lane] = mybits;
+                        }
+                        __syncwarp();  // nbuf is rewritten by the next unit
                     }
                     // tile done for this warp
                     __syncwarp();
@@ -578,8 +670,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_dense_fused(const __grid_consta
                             *reinterpret_cast<volatile int*>(&S.tiles_done) = static_cast<int>(s) + 1;
                             if (last && m == nt - 1 && a.block_end_ns) a.block_end_ns[it] = gtimer();
                         }
-                        tc::mbar_arrive(&S.s_empty[buf]);
                     }
+                    named_arrive(kBarDEmpty + buf);  // this warp is done with the D tile
                 }
             }
             if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&a.nan_block[it], 1);
@@ -697,7 +789,7 @@ __global__ void __launch_bounds__(kEvWarps * 32, 1) k_eval_tc(const __grid_const
                                                              const __grid_constant__ EvalArgs a)
 {
     extern __shared__ uint8_t sm_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     __shared__ uint64_t b_full[kStages], b_empty[kStages], a_full[kStages], a_empty[kStages], d_full[2], d_empty[2];
     __shared__ uint32_t tslot;
     uint32_t* lut = reinterpret_cast<uint32_t*>(sm + kStages * kBStage);
@@ -857,11 +949,13 @@ int dense_path_kind(Ctx& c, int variant)
 }
 bool dense_path_ok(Ctx& c, int variant) { return dense_path_kind(c, variant) != 0; }
 
-// Samples the flattened (run, weight, chunk) blocks [b0, b0+nblocks) of 128 trajectories
+int dense_block_traj() { return kNTV; }
+
+// Samples the flattened (run, weight, chunk) blocks [b0, b0+nblocks) of 120 trajectories
 // (p.block_traj) with the fused tensor-core kernel.
 void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblocks)
 {
-    if (p.block_traj != kNT) runtime("dense path: block size must be 128 trajectories");
+    if (p.block_traj != kNTV) runtime("dense path: block size must be " + std::to_string(kNTV) + " trajectories");
     DenseScratch& d = dscratch(c);
     const int kind = dense_path_kind(c, p.variant);
     if (!kind) runtime("dense path not applicable");

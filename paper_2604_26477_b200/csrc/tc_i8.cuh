@@ -73,14 +73,18 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(count));
 }
 
+// the waiting thread is suspended until the phase completes (or this many ns pass), so a
+// waiter does not spin on the issue slots the compute warps need
+constexpr uint32_t kSuspendHintNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase)
 {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
-        "r"(phase));
+        "r"(phase), "r"(kSuspendHintNs)
+        : "memory");
 }
 
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
@@ -227,20 +231,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* mbar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
 }
 
-// mbarrier wait with a nanosleep back-off (for waiters that are not on the critical path)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* mbar, uint32_t phase)
+// mbarrier wait with a nanosleep back-off (for waiters that are not on the critical path:
+// their polling would otherwise take issue slots from the compute warps of their SM
+// sub-partition)
+__device__ __forceinline__ bool mbar_test(uint64_t* mbar, uint32_t phase)
 {
-    uint32_t done = 0;
-    for (;;) {
-        asm volatile(
-            "{\n\t.reg .pred P1;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, P1;\n\t}\n"
-            : "=r"(done)
-            : "r"(smem_u32(mbar)), "r"(phase)
-            : "memory");
-        if (done) return;
-        __nanosleep(64);
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(mbar)), "r"(phase)
+        : "memory");
+    return done != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* mbar, uint32_t phase, uint32_t max_ns = 2048)
+{
+    uint32_t ns = 64;
+    while (!mbar_test(mbar, phase)) {
+        __nanosleep(ns);
+        ns = ns < max_ns ? 2 * ns : max_ns;
     }
 }
 
