@@ -14,11 +14,11 @@
 //
 // Per step, two kernels over the (run, weight) pairs of a group:
 //   * k_dense_gemm: D (trajectories x spins, int32) = Phi . (H J)^T on the tensor cores.
-//     Warp-specialised and persistent: one thread streams 128-byte K chunks of Phi (128
+//     Warp-specialised and persistent: one thread streams 128-byte K chunks of Phi (256
 //     trajectories) and of the H*J(c) tile (256 spins) with TMA into a 3-stage ring, one
-//     thread issues tcgen05.mma (M = 128, N = 256) into one of two TMEM accumulators, and four
-//     epilogue warps move finished tiles TMEM -> registers -> swizzled shared memory -> TMA
-//     store, so tile i+1's MMAs overlap tile i's epilogue.
+//     thread issues tcgen05.mma (two M = 128, N = 256 products per chunk, both reading the
+//     same H*J chunk, into all 512 TMEM columns), and eight epilogue warps move the finished
+//     item TMEM -> registers -> swizzled shared memory -> TMA store.
 //   * k_dense_warp: the FP64 update, one warp per trajectory, 32 spins per window, the
 //     (trajectory, step) noise stream resolved warp-wide (below).
 // State: Phi [pair][traj][ldp] (int8 or bf16), D [pair][traj][ldp] int32, x / y
@@ -89,8 +89,10 @@ template <>
 __device__ __forceinline__ uint16_t phi_of<uint16_t>(bool neg) { return neg ? 0xBF80 : 0x3F80; }
 
 // init_state (solver.hpp:108-124), trajectory-major: one warp per trajectory, lanes over
-// spins; spin i takes words 2i, 2i+1 of the init_x / init_y streams (block i/2, half i%2),
-// so every store of a warp is one contiguous run. Padding trajectories get Phi = +1 rows.
+// spins; spin i takes words 2i, 2i+1 of the init_x / init_y streams (block i/2, half i%2).
+// Per 32-spin window lanes 0-15 make the 16 init_x blocks and lanes 16-31 the init_y blocks
+// (one Philox block per lane), shuffled to the lanes of their spins; every store of a warp is
+// one contiguous run. Padding trajectories get Phi = +1 rows; K padding (H*J zero) too.
 template <typename PhiT>
 __global__ void __launch_bounds__(256) k_dense_init_t(int n, int ldp, int batch_pad, const PairOf* __restrict__ pairs,
                                                       uint64_t seed, double h, double* x, double* y, PhiT* phi)
@@ -108,19 +110,29 @@ __global__ void __launch_bounds__(256) k_dense_init_t(int n, int ldp, int batch_
     const uint64_t key = run_key(seed, static_cast<uint32_t>(pr.run));
     const uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
     const uint32_t tr = static_cast<uint32_t>(pr.traj0 + t), wl = static_cast<uint32_t>(pr.l);
-    for (int i = lane; i < ldp; i += 32) {
-        if (i >= n) {
-            ph[i] = phi_of<PhiT>(false);  // K padding (H*J is zero there)
+    const uint32_t tag = tag_word(lane < 16 ? kTagInitX : kTagInitY, 0);
+    const int src = lane >> 1;
+    const bool odd = lane & 1;
+    for (int s0 = 0; s0 < ldp; s0 += 32) {
+        const int i = s0 + lane;
+        if (s0 >= n) {
+            if (i < ldp) ph[i] = phi_of<PhiT>(false);
             continue;
         }
-        const uint4 rx = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitX, 0), tr, wl);
-        const uint4 ry = philox(k0, k1, static_cast<uint32_t>(i >> 1), tag_word(kTagInitY, 0), tr, wl);
-        const bool odd = i & 1;
-        const double xv = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(rx.z, rx.w) : u01_from(rx.x, rx.y)), 1.0));
-        const double yv = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(ry.z, ry.w) : u01_from(ry.x, ry.y)), 1.0));
-        x[trow * n + i] = xv;
-        y[trow * n + i] = yv;
-        ph[i] = phi_of<PhiT>(xv < 0.0);
+        const uint4 pv = philox(k0, k1, static_cast<uint32_t>(s0 / 2 + (lane & 15)), tag, tr, wl);
+        const uint32_t xa = __shfl_sync(0xffffffffu, pv.x, src), xb = __shfl_sync(0xffffffffu, pv.y, src);
+        const uint32_t xc = __shfl_sync(0xffffffffu, pv.z, src), xd = __shfl_sync(0xffffffffu, pv.w, src);
+        const uint32_t ya = __shfl_sync(0xffffffffu, pv.x, src + 16), yb = __shfl_sync(0xffffffffu, pv.y, src + 16);
+        const uint32_t yc = __shfl_sync(0xffffffffu, pv.z, src + 16), yd = __shfl_sync(0xffffffffu, pv.w, src + 16);
+        if (i < n) {
+            const double xv = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(xc, xd) : u01_from(xa, xb)), 1.0));
+            const double yv = __dmul_rn(h, __dsub_rn(__dmul_rn(2.0, odd ? u01_from(yc, yd) : u01_from(ya, yb)), 1.0));
+            x[trow * n + i] = xv;
+            y[trow * n + i] = yv;
+            ph[i] = phi_of<PhiT>(xv < 0.0);
+        } else if (i < ldp) {
+            ph[i] = phi_of<PhiT>(false);
+        }
     }
 }
 
@@ -136,7 +148,9 @@ __device__ __forceinline__ uint32_t zmag32(uint32_t u) { return static_cast<int3
 __device__ __noinline__ bool exp_decides(double lhs, double targ) { return lhs < exp(targ); }
 
 // wedge test of the attempt at word u with uniform words (w1, w2) (rng.hpp:178-183): the FP32
-// exp brackets the FP64 one within 1e-6 relative on [-6, 0]; the FP64 exp decides the band
+// exp brackets the FP64 one within 1e-6 relative on [-6, 0], so outside a +-1e-5 band around
+// it the decision is taken in FP32 (lhs rounded to FP32 moves by < 1e-7 relative); the FP64
+// exp decides inside the band
 __device__ __forceinline__ bool wedge_accept(uint32_t u, uint32_t w1, uint32_t w2, const ZigTables& z)
 {
     const uint32_t iz = u & 127u;
@@ -144,50 +158,10 @@ __device__ __forceinline__ bool wedge_accept(uint32_t u, uint32_t w1, uint32_t w
     const double lhs = __dadd_rn(z.fn[iz], __dmul_rn(u01_from(w1, w2), __dsub_rn(z.fn[iz - 1], z.fn[iz])));
     const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
     const float ef = __expf(static_cast<float>(targ));
-    if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) return true;
-    if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) return false;
+    const float lf = static_cast<float>(lhs);
+    if (lf < ef * (1.0f - 2e-5f)) return true;
+    if (lf > ef * (1.0f + 2e-5f)) return false;
     return exp_decides(lhs, targ);
-}
-
-// the tail attempt starting at word p0 of the (key, lo, mid, hi) stream (rng.hpp:165-177):
-// (x, y) trials of 4 words until 2y >= x^2; returns the normal and its length in words. Rare
-// (one word in ~1,600), so it lives out of line and reads every word from the ring or Philox.
-struct TailOut {
-    double v;
-    int len;
-};
-__device__ __noinline__ TailOut tail_attempt(const uint32_t* ring, int tail, int p0, uint32_t u, uint32_t k0, uint32_t k1,
-                                             uint32_t lo, uint32_t mid, uint32_t hi)
-{
-    auto word = [&](int p) -> uint32_t {
-        if (p < tail) return ring[p & 255];
-        const uint4 v = philox(k0, k1, static_cast<uint32_t>(p >> 2), lo, mid, hi);
-        const int c = p & 3;
-        return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
-    };
-    const double rr = 3.442619855899;
-    int qq = p0 + 1;
-    for (;;) {
-        const double xx = __ddiv_rn(-log(u01_open_from(word(qq), word(qq + 1))), rr);
-        const double yy = -log(u01_open_from(word(qq + 2), word(qq + 3)));
-        qq += 4;
-        if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx))
-            return {static_cast<int32_t>(u) > 0 ? __dadd_rn(rr, xx) : -__dadd_rn(rr, xx), qq - p0};
-    }
-}
-
-__device__ __forceinline__ uint4 ldcg4(const uint32_t* p)
-{
-    uint4 v;
-    asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-    return v;
-}
-
-__device__ __forceinline__ unsigned long long gtimer()
-{
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
 }
 
 // ---- warp-per-trajectory dSB update. x, y and D are stored
@@ -254,6 +228,7 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
     double* val = vals[warp];
     const uint32_t k0 = pr.k0, k1 = pr.k1, lo = tag_word(kTagStepNoise, static_cast<uint32_t>(a.t_step));
     const uint32_t mid = static_cast<uint32_t>(pr.traj0 + t), hi = static_cast<uint32_t>(pr.l);
+    const double c0h = pr.c0h;
     const uint32_t lt = lanemask_lt();
     int head = 0, tail = 0;  // next unread word / words generated (warp-uniform)
     auto gen = [&]() {       // 128 words: block tail/4 + lane on each lane
@@ -361,7 +336,7 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
         asm volatile("" : "+r"(dq)::"memory");  // keep the conversion (a wait on the load) here
         // ---- the update of spin s0 + lane (sb_step solver.hpp:159-181, phi = sgn(x))
         if (upd) {
-            double d = __dsub_rn(__dmul_rn(a.neg_drift, xi), __dmul_rn(pr.c0h, static_cast<double>(dq)));
+            double d = __dsub_rn(__dmul_rn(a.neg_drift, xi), __dmul_rn(c0h, static_cast<double>(dq)));
             if constexpr (NOISY) d = __dadd_rn(d, __dmul_rn(a.alpha, eta));
             yi = __dadd_rn(yi, UDT ? d : __dmul_rn(a.dt, d));
             xi = __dadd_rn(xi, UDT ? yi : __dmul_rn(a.sdt, yi));
@@ -383,18 +358,21 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
 }
 
 // ---- D = Phi . (H J)^T on the tensor cores (persistent, warp-specialised) -------------------
-constexpr int kGM = 128;              // trajectories per tile (MMA M, TMEM lanes)
-constexpr int kGN = 256;              // spins per tile (MMA N, TMEM columns per accumulator)
+constexpr int kGM = 128;              // trajectories per MMA (M, TMEM lanes)
+constexpr int kGH = 2;                // trajectory tiles per item: both share every B chunk
+constexpr int kGN = 256;              // spins per item (MMA N, TMEM columns per accumulator)
 constexpr int kGStages = 3;
-constexpr int kGStageA = kGM * 128;   // bytes: 128 rows x 128 bytes of K
+constexpr int kGStageA = kGH * kGM * 128;  // bytes: 256 rows x 128 bytes of K
 constexpr int kGStageB = kGN * 128;
 constexpr int kGStage = kGStageA + kGStageB;
 constexpr int kGOut = 32 * 32 * 4;    // one epilogue store box: 32 trajectories x 32 spins int32
-constexpr int kGSmem = kGStages * kGStage + 4 * 2 * kGOut + 1024;
-constexpr int kGThreads = 6 * 32;     // 0: TMA, 1: MMA (+ TMEM), 2..5: epilogue
+constexpr int kGEpi = 8;              // epilogue warps: TMEM lane quarter = warp & 3, column half = (warp - 2) / 4
+constexpr int kGSmem = kGStages * kGStage + kGEpi * kGOut + 1024;
+constexpr int kGThreads = (2 + kGEpi) * 32;  // 0: TMA, 1: MMA (+ TMEM), 2..9: epilogue
 
 struct GemmArgs {
-    int n, ldp, batch_pad, ntn, nch, tiles_per_pair;
+    int n, ldp, batch_pad, ntn, nch, tiles_per_pair;  // tiles_per_pair: items of kGH x 128 trajectories
+    int pair_begin;           // first pair (of the group's state arrays) of this launch
     long long items;          // pairs x tiles_per_pair x ntn, spin tiles fastest
     const PairOf* pairs;
 };
@@ -432,7 +410,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_dense_gemm(const __grid_consta
         }
         for (int q = 0; q < 2; ++q) {
             tc::mbar_init(&d_full[q], 1);
-            tc::mbar_init(&d_empty[q], 4);
+            tc::mbar_init(&d_empty[q], kGEpi);
         }
         tc::fence_mbar_init();
         tc::prefetch_tmap(&tmA);
@@ -450,8 +428,8 @@ __global__ void __launch_bounds__(kGThreads, 1) k_dense_gemm(const __grid_consta
             for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
                 const int j = static_cast<int>(it % a.ntn);
                 const long long pt = it / a.ntn;
-                const int q = static_cast<int>(pt / a.tiles_per_pair), i = static_cast<int>(pt % a.tiles_per_pair);
-                const int arow = q * a.batch_pad + i * kGM, brow = a.pairs[q].l * a.n + j * kGN;
+                const int q = a.pair_begin + static_cast<int>(pt / a.tiles_per_pair), i = static_cast<int>(pt % a.tiles_per_pair);
+                const int arow = q * a.batch_pad + i * kGH * kGM, brow = a.pairs[q].l * a.n + j * kGN;
                 for (int c = 0; c < a.nch; ++c, ++g) {
                     const uint32_t st = g % kGStages, ph = (g / kGStages) & 1;
                     tc::mbar_wait(&empty[st], ph ^ 1);
@@ -467,8 +445,8 @@ __global__ void __launch_bounds__(kGThreads, 1) k_dense_gemm(const __grid_consta
             const uint32_t idesc = BF16 ? tc::idesc_bf16(kGM, kGN) : tc::idesc_i8(kGM, kGN);
             uint32_t g = 0, s = 0;
             for (long long it = blockIdx.x; it < a.items; it += gridDim.x, ++s) {
-                const uint32_t buf = s & 1;
-                tc::mbar_wait(&d_empty[buf], ((s >> 1) & 1) ^ 1);
+                // one accumulator pair (all 512 TMEM columns): wait until the last item is drained
+                tc::mbar_wait(&d_empty[0], (s & 1) ^ 1);
                 tc::fence_after();
                 for (int c = 0; c < a.nch; ++c, ++g) {
                     const uint32_t st = g % kGStages, ph = (g / kGStages) & 1;
@@ -476,42 +454,45 @@ __global__ void __launch_bounds__(kGThreads, 1) k_dense_gemm(const __grid_consta
                     tc::fence_after();
                     const uint32_t as = tc::smem_u32(sm + st * kGStage), bs = as + kGStageA;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (BF16) tc::mma_f16(tbase + buf * kGN, tc::smem_desc_sw128(as + 32 * k), tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
-                        else tc::mma_i8(tbase + buf * kGN, tc::smem_desc_sw128(as + 32 * k), tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
+                    for (int h = 0; h < kGH; ++h) {
+                        const uint32_t dt = tbase + h * kGN, ah = as + h * (kGM * 128);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            if (BF16) tc::mma_f16(dt, tc::smem_desc_sw128(ah + 32 * k), tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
+                            else tc::mma_i8(dt, tc::smem_desc_sw128(ah + 32 * k), tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
+                        }
                     }
                     tc::commit(&empty[st]);
                 }
-                tc::commit(&d_full[buf]);
+                tc::commit(&d_full[0]);
             }
         }
         __syncwarp();
     } else {
-        // epilogue warp: TMEM lane quarter q = its 32 trajectories of the tile; per 32-spin
-        // column group TMEM -> registers -> 128-byte-swizzled box -> TMA store (double-buffered)
-        const int q = warp & 3;
+        // epilogue warp: TMEM lane quarter q = 32 trajectories of each half, column half ch;
+        // per 32-spin column group TMEM -> registers -> 128-byte-swizzled box -> TMA store
+        const int q = warp & 3, ch = (warp - 2) / 4;
         const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
-        uint8_t* outb = sm + kGStages * kGStage + (warp - 2) * 2 * kGOut;
+        uint8_t* ob = sm + kGStages * kGStage + (warp - 2) * kGOut;
         uint32_t s = 0, nst = 0;
         for (long long it = blockIdx.x; it < a.items; it += gridDim.x, ++s) {
             const int j = static_cast<int>(it % a.ntn);
             const long long pt = it / a.ntn;
-            const int qq = static_cast<int>(pt / a.tiles_per_pair), i = static_cast<int>(pt % a.tiles_per_pair);
-            const int row0 = qq * a.batch_pad + i * kGM + q * 32;
-            const uint32_t buf = s & 1;
-            tc::mbar_wait(&d_full[buf], (s >> 1) & 1);
+            const int qq = a.pair_begin + static_cast<int>(pt / a.tiles_per_pair), i = static_cast<int>(pt % a.tiles_per_pair);
+            tc::mbar_wait(&d_full[0], s & 1);
             tc::fence_after();
 #pragma unroll 1
-            for (int cg = 0; cg < kGN / 32; ++cg) {
+            for (int hc = 0; hc < kGH * 4; ++hc) {
+                const int h = hc >> 2, cg = ch * 4 + (hc & 3);
+                const int row0 = qq * a.batch_pad + (i * kGH + h) * kGM + q * 32;
                 const int col0 = j * kGN + cg * 32;
-                if (col0 >= a.n) break;
+                if (col0 >= a.n) continue;
                 uint32_t v[32];
-                tc::tmem_ld32(tbase + lane_addr + buf * kGN + cg * 32, v);
+                tc::tmem_ld32(tbase + lane_addr + h * kGN + cg * 32, v);
                 if (BF16)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) v[e] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(v[e])));
-                uint8_t* ob = outb + (nst & 1) * kGOut;
-                if (lane == 0 && nst >= 2) bulk_wait_read<1>();  // the store that last read this box
+                if (lane == 0 && nst >= 1) bulk_wait_read<0>();  // the previous store has read the box
                 __syncwarp();
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
@@ -524,7 +505,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_dense_gemm(const __grid_consta
             }
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&d_empty[buf]);
+            if (lane == 0) tc::mbar_arrive(&d_empty[0]);
         }
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
@@ -774,6 +755,20 @@ struct DenseScratch {
     long long bound_inst = -1, bound_weights = -1, bound = 0;  // cached hj_bound
     DevBuf<uint8_t> wk;     // the K weight layers, dense int8, per instance (evaluate_cuts)
     long long wk_gen = -1;
+    cudaStream_t s2 = nullptr;  // second stream (the other half of the pairs)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t stream2(Ctx& c)
+    {
+        if (!s2) {
+            int lo = 0, hi = 0;
+            ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+            ck(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi), "stream");
+            ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+        }
+        (void)c;
+        return s2;
+    }
 };
 
 DenseScratch& dscratch(Ctx& c)
@@ -782,6 +777,9 @@ DenseScratch& dscratch(Ctx& c)
         auto* d = static_cast<DenseScratch*>(p);
         d->hj.release(); d->phi.release(); d->D.release(); d->flags.release(); d->x.release(); d->y.release();
         d->pairs.release(); d->wk.release();
+        if (d->s2) cudaStreamDestroy(d->s2);
+        if (d->ev_fork) cudaEventDestroy(d->ev_fork);
+        if (d->ev_join) cudaEventDestroy(d->ev_join);
         delete d;
     });
     return *static_cast<DenseScratch*>(c.dense_scratch.get());
@@ -876,7 +874,7 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
     ck(cudaStreamSynchronize(c.stream), "c0");
     int maxc = 0;
     for (auto& q : pairs) maxc = std::max(maxc, q.count);
-    const int batch_pad = (maxc + kGM - 1) / kGM * kGM;  // GEMM tiles never span two pairs
+    const int batch_pad = (maxc + kGH * kGM - 1) / (kGH * kGM) * (kGH * kGM);  // GEMM items never span two pairs
     int dev = 0, sms = 0;
     ck(cudaGetDevice(&dev), "device");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
@@ -906,59 +904,84 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
                                                                 d.y.p, reinterpret_cast<int8_t*>(d.phi.p));
         c.launches++;
         const int KC = bf16 ? 64 : 128;
-        const CUtensorMap tmA = make_tmap(d.phi.p, static_cast<long long>(rows), npad, npad, esize, KC, kGM);
+        const CUtensorMap tmA = make_tmap(d.phi.p, static_cast<long long>(rows), npad, npad, esize, KC, kGH * kGM);
         const CUtensorMap tmB = make_tmap(d.hj.p, static_cast<long long>(L) * n, npad, npad, esize, KC, kGN);
         const CUtensorMap tmD = make_tmap(d.D.p, static_cast<long long>(rows), n, npad, 4, 32, 32);
-        GemmArgs ga{};
-        ga.n = n;
-        ga.ldp = npad;
-        ga.batch_pad = batch_pad;
-        ga.ntn = (n + kGN - 1) / kGN;
-        ga.nch = (npad + KC - 1) / KC;
-        ga.tiles_per_pair = batch_pad / kGM;
-        ga.items = static_cast<long long>(G) * ga.tiles_per_pair * ga.ntn;
-        ga.pairs = d.pairs.p;
-        const int ggrid = static_cast<int>(std::min<long long>(ga.items, sms));
-        // 8 KB of launch arguments, per call (contexts may sample from several host threads)
-        const auto step_args_p = std::make_unique<DenseStepArgs>();
-        DenseStepArgs& sa = *step_args_p;
-        sa.n = n;
-        sa.ldp = npad;
-        sa.batch_pad = batch_pad;
-        sa.dt = p.dt;
-        sa.alpha = p.alpha;
-        sa.sdt = p.s_dt_a0;
-        sa.zig = p.zig;
-        sa.D = d.D.p;
-        sa.x = d.x.p;
-        sa.y = d.y.p;
-        sa.phi = d.phi.p;
-        sa.bad = d.flags.p;
+        // One stream: GEMM(t) then update(t) over all pairs of the group. (Two pair halves on
+        // two streams did not overlap: the update kernel fills every SM, so a GEMM CTA of the
+        // other half never finds the shared memory it needs.)
+        const int halves = 1;
+        cudaStream_t hs[2] = {c.stream, d.stream2(c)};
+        if (halves == 2) {
+            ck(cudaEventRecord(d.ev_fork, c.stream), "event");
+            ck(cudaStreamWaitEvent(hs[1], d.ev_fork, 0), "event wait");
+        }
+        GemmArgs ga[2];
+        // 8 KB of launch arguments per half, per call (contexts may sample from several host threads)
+        const auto step_args_p = std::make_unique<DenseStepArgs[]>(2);
+        int hb[3] = {0, halves == 2 ? G / 2 : G, G};
+        for (int hh = 0; hh < halves; ++hh) {
+            GemmArgs& g = ga[hh];
+            g.n = n;
+            g.ldp = npad;
+            g.batch_pad = batch_pad;
+            g.ntn = (n + kGN - 1) / kGN;
+            g.nch = (npad + KC - 1) / KC;
+            g.tiles_per_pair = batch_pad / (kGH * kGM);
+            g.pair_begin = hb[hh];
+            g.items = static_cast<long long>(hb[hh + 1] - hb[hh]) * g.tiles_per_pair * g.ntn;
+            g.pairs = d.pairs.p;
+            DenseStepArgs& sa = step_args_p[hh];
+            sa.n = n;
+            sa.ldp = npad;
+            sa.batch_pad = batch_pad;
+            sa.dt = p.dt;
+            sa.alpha = p.alpha;
+            sa.sdt = p.s_dt_a0;
+            sa.zig = p.zig;
+            sa.D = d.D.p;
+            sa.x = d.x.p;
+            sa.y = d.y.p;
+            sa.phi = d.phi.p;
+            sa.bad = d.flags.p;
+        }
         const bool udt = p.dt == 1.0 && p.s_dt_a0 == 1.0, noisy = p.alpha > 0.0;
-        for (int t = 0; t < p.T; ++t) {
-            gemm<<<ggrid, kGThreads, kGSmem, c.stream>>>(tmA, tmB, tmD, ga);
-            c.launches++;
-            for (int s0 = 0; s0 < G; s0 += kDensePairsPerLaunch) {
-                const int np = std::min(kDensePairsPerLaunch, G - s0);
-                sa.t_step = t;
-                sa.pair0 = s0;
-                sa.neg_drift = -(p.a0 - static_cast<double>(t + 1) / static_cast<double>(p.T));
-                for (int q = 0; q < np; ++q) {
-                    const PairOf& pq = pairs[g0 + s0 + q];
-                    const uint64_t key = run_key(p.seed, static_cast<uint32_t>(pq.run));
-                    sa.pair[q] = {static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32), pq.l, pq.traj0, pq.count, 0,
-                                  c0_host[static_cast<size_t>(pq.l)] / static_cast<double>(c.H)};
-                }
-                const dim3 wgrid(static_cast<unsigned>((maxc + kWWarps - 1) / kWWarps), static_cast<unsigned>(np));
-                if (bf16) {
-                    if (noisy) udt ? launch_warp<true, true, uint16_t>(sa, wgrid, c.stream) : launch_warp<true, false, uint16_t>(sa, wgrid, c.stream);
-                    else udt ? launch_warp<false, true, uint16_t>(sa, wgrid, c.stream) : launch_warp<false, false, uint16_t>(sa, wgrid, c.stream);
-                } else {
-                    if (noisy) udt ? launch_warp<true, true, int8_t>(sa, wgrid, c.stream) : launch_warp<true, false, int8_t>(sa, wgrid, c.stream);
-                    else udt ? launch_warp<false, true, int8_t>(sa, wgrid, c.stream) : launch_warp<false, false, int8_t>(sa, wgrid, c.stream);
-                }
+        for (int t = 0; t < p.T; ++t)
+            for (int hh = 0; hh < halves; ++hh) {
+                const cudaStream_t st = hs[hh];
+                const int ggrid = static_cast<int>(std::min<long long>(ga[hh].items, sms));
+                gemm<<<ggrid, kGThreads, kGSmem, st>>>(tmA, tmB, tmD, ga[hh]);
                 c.launches++;
+                if (halves == 2 && t == 0 && hh == 0) {  // half B starts one GEMM later: out of phase
+                    ck(cudaEventRecord(d.ev_fork, st), "event");
+                    ck(cudaStreamWaitEvent(hs[1], d.ev_fork, 0), "event wait");
+                }
+                DenseStepArgs& sa = step_args_p[hh];
+                for (int s0 = hb[hh]; s0 < hb[hh + 1]; s0 += kDensePairsPerLaunch) {
+                    const int np = std::min(kDensePairsPerLaunch, hb[hh + 1] - s0);
+                    sa.t_step = t;
+                    sa.pair0 = s0;
+                    sa.neg_drift = -(p.a0 - static_cast<double>(t + 1) / static_cast<double>(p.T));
+                    for (int q = 0; q < np; ++q) {
+                        const PairOf& pq = pairs[g0 + s0 + q];
+                        const uint64_t key = run_key(p.seed, static_cast<uint32_t>(pq.run));
+                        sa.pair[q] = {static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32), pq.l, pq.traj0, pq.count, 0,
+                                      c0_host[static_cast<size_t>(pq.l)] / static_cast<double>(c.H)};
+                    }
+                    const dim3 wgrid(static_cast<unsigned>((maxc + kWWarps - 1) / kWWarps), static_cast<unsigned>(np));
+                    if (bf16) {
+                        if (noisy) udt ? launch_warp<true, true, uint16_t>(sa, wgrid, st) : launch_warp<true, false, uint16_t>(sa, wgrid, st);
+                        else udt ? launch_warp<false, true, uint16_t>(sa, wgrid, st) : launch_warp<false, false, uint16_t>(sa, wgrid, st);
+                    } else {
+                        if (noisy) udt ? launch_warp<true, true, int8_t>(sa, wgrid, st) : launch_warp<true, false, int8_t>(sa, wgrid, st);
+                        else udt ? launch_warp<false, true, int8_t>(sa, wgrid, st) : launch_warp<false, false, int8_t>(sa, wgrid, st);
+                    }
+                    c.launches++;
+                }
             }
+        if (halves == 2) {
+            ck(cudaEventRecord(d.ev_join, hs[1]), "event");
+            ck(cudaStreamWaitEvent(c.stream, d.ev_join, 0), "event wait");
         }
         const dim3 rgrid(static_cast<unsigned>((batch_pad + 127) / 128), static_cast<unsigned>(G));
         k_dense_readout<<<rgrid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, p.row0, d.flags.p + 1);
