@@ -87,7 +87,8 @@ int momc_b200_measured_correlation(momc_ctx* ctx, int pool_size, uint64_t seed, 
 int momc_b200_instance_get(momc_ctx* ctx, int32_t* edge_i, int32_t* edge_j, double* w, char* err, size_t errlen);
 /* dSB with integer weights and |H*J(c)| <= 256 uses the fused tensor-core step (exact
  * int8 / bf16 contraction H*J(c).sgn(X), then one FP64 rounding of c0/H times it) when
- * n >= n_min (default 256); smaller n keep the bit-exact FP64 order of the reference. */
+ * n >= n_min (default 256; INT_MAX turns it off); smaller n keep the bit-exact FP64 order of
+ * the reference. */
 int momc_b200_set_dense_threshold(momc_ctx* ctx, int n_min);
 /* Which sampler produced the resident pool: 0 none yet, 1 register-resident (n <= 64,
  * bit-exact), 2 sequential generic (bit-exact), 3 fused tensor-core dSB with int8 H*J(c),

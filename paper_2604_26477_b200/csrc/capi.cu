@@ -694,6 +694,7 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
             q.block_begin = rb;
             q.first_bad_step_task = 1;
             q.block_end_ns = nullptr;
+            c.d_badstep.reserve(static_cast<size_t>(re - rb));
             ck(cudaMemsetAsync(c.d_badstep.p, 0x7f, sizeof(int) * (re - rb), c.stream), "memset");
             // scratch outputs so the pool / flags of the real run are untouched
             DevBuf<uint64_t> wtmp;

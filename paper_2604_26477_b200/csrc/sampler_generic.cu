@@ -122,7 +122,10 @@ __global__ void gen_step(WaveCtx w, int t, const double* __restrict__ x, double*
         atomicMin(&w.p.bad_step[w.wave_block0 + wb], t + 1);
 }
 
-__global__ void gen_readout(WaveCtx w, const double* __restrict__ x)
+// check_finite (solver.hpp:138-143) on the final state: a non-finite x never heals (NaN
+// passes the clamp), and a non-finite y survives to the end for SimCIM (no reset); for SB the
+// wall zeroes y whenever x overflowed, as in the reference's post-wall check.
+__global__ void gen_readout(WaveCtx w, const double* __restrict__ x, const double* __restrict__ y)
 {
     const long long wt = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (wt >= w.W) return;
@@ -139,7 +142,7 @@ __global__ void gen_readout(WaveCtx w, const double* __restrict__ x)
         for (int b = 0; b < 64 && wd * 64 + b < n; ++b) {
             const double v = x[(wd * 64 + b) * w.W + wt];
             word |= static_cast<uint64_t>(!(v < 0.0)) << b;
-            bad |= v != v;
+            bad |= !isfinite(v) || !isfinite(y[(wd * 64 + b) * w.W + wt]);
         }
         w.p.words[(idx - w.p.row0) * wpc + wd] = word;
     }
@@ -177,7 +180,7 @@ int launch_sampler_generic(const SamplerParams& p, long long nblocks, const Gene
             xa = xb;
             xb = tmp;
         }
-        gen_readout<<<grid1, 128, 0, st>>>(w, xa);
+        gen_readout<<<grid1, 128, 0, st>>>(w, xa, g.y);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
         const int i = s0 + s;
         if (i < n) {
             word |= static_cast<uint64_t>(!(x[s] < 0.0)) << i;
-            bad |= x[s] != x[s];
+            bad |= !isfinite(x[s]) || !isfinite(y[s]);  // check_finite (solver.hpp:138-143)
         }
     }
     word = lane_or<LANES>(wmask, word);

@@ -19,19 +19,28 @@ import torch
 from . import distributed as mdist
 
 
+def _reached(hv: float, hv_target) -> bool:
+    """samples_to_reach's stopping rule (pareto.hpp:771-779): hv >= target - 1e-9 max(1, |target|).
+    hv_target None (or +inf) never stops: the stream spends max_runs."""
+    if hv_target is None or hv_target == float("inf"):
+        return False
+    return hv >= hv_target - 1e-9 * max(1.0, abs(hv_target))
+
+
 def _packed_front(session, device):
     """resident archive -> one int64 tensor [F, K + wpc] (values as bit patterns)"""
     vals, words = mdist.local_archive_tensors(session, device)
     return torch.cat([vals.view(torch.int64), words], dim=1)
 
 
-def time_to_target(session, cfg, reference, hv_target: float, max_runs: int, world: int = 1, rank: int = 0,
+def time_to_target(session, cfg, reference, hv_target, max_runs: int, world: int = 1, rank: int = 0,
                    device=None, trace: list | None = None, runs_per_step: int = 1) -> dict:
-    """Runs rounds until the running archive's HV at `reference` equals `hv_target` (exact
-    arithmetic for integer weights) or `max_runs` runs are spent. Returns the number of
+    """Runs rounds until the running archive's HV at `reference` reaches `hv_target` (the
+    reference's tolerance, `_reached`; None = never) or `max_runs` runs are spent. Returns the number of
     runs / samples used, the wall time (device-synchronised, this rank) and the final HV.
-    The caller times the whole call as the end-to-end figure (model build included: every
-    round re-scalarises its weight blocks, pipeline.hpp:337-341).
+    The caller times the whole call as the end-to-end figure (model build included: the
+    weight blocks are scalarised once, on the first round, pipeline.hpp:337-341; later rounds
+    reuse the resident J(c)). The last round samples only the runs left below max_runs.
 
     One GPU: one C-ABI call per run (momc_b200_stream_step: sample -> front -> merge into the
     context's running archive -> HV). N ranks: each rank's run front is all-gathered (NCCL)
@@ -48,30 +57,37 @@ def time_to_target(session, cfg, reference, hv_target: float, max_runs: int, wor
     R = max(1, int(runs_per_step))
     rounds = (max_runs + world * R - 1) // (world * R)
     for q in range(rounds):
-        run = (q * world + rank) * R  # this rank's first run of the round
+        # round q covers runs [q*world*R, min((q+1)*world*R, max_runs)); rank r takes its R-slice
+        lo, hi = q * world * R, min((q + 1) * world * R, max_runs)
+        run = min(lo + rank * R, hi)  # this rank's first run of the round
+        run_end = min(run + R, hi)
         if world == 1:
-            hv, F, _ = session.stream_step(cfg, run + R, run * per_run, (run + R) * per_run, reference)
+            hv, F, _ = session.stream_step(cfg, run_end, run * per_run, run_end * per_run, reference)
         else:
-            session.stream_step(cfg, run + R, run * per_run, (run + R) * per_run, None, merge=False)
-            rows = mdist.allgather_rows(_packed_front(session, device))
+            if run_end > run:
+                session.stream_step(cfg, run_end, run * per_run, run_end * per_run, None, merge=False)
+                front = _packed_front(session, device)
+            else:  # the last round left this rank no run: contribute an empty front
+                front = torch.empty((0, k + (session.inst.n() + 63) // 64), dtype=torch.int64, device=device)
+            rows = mdist.allgather_rows(front)
             vals = rows[:, :k].contiguous().view(torch.float64)
             words = rows[:, k:].contiguous()
             torch.cuda.current_stream(device).synchronize()
             hv, F = session.running_merge_values(vals.data_ptr(), words.data_ptr(), words.shape[1], vals.shape[0], k,
                                                  reference)
-        runs_done = (q + 1) * world * R
+        runs_done = hi
         if trace is not None:
             trace.append({"runs": runs_done, "samples": runs_done * samples_per_run, "archive": F, "hv": hv,
                           "wall_s": time.perf_counter() - t0})
-        if hv == hv_target:
+        if _reached(hv, hv_target):
             break
     torch.cuda.synchronize(device)
     session.running_to_archive()
-    return {"reached": hv == hv_target, "runs": runs_done, "samples": runs_done * samples_per_run,
+    return {"reached": _reached(hv, hv_target), "runs": runs_done, "samples": runs_done * samples_per_run,
             "seconds": time.perf_counter() - t0, "hv": hv, "archive": F}
 
 
-def time_to_target_overlapped(sessions: list, merger, cfg, reference, hv_target: float, max_runs: int,
+def time_to_target_overlapped(sessions: list, merger, cfg, reference, hv_target, max_runs: int,
                               trace: list | None = None) -> dict:
     """One GPU, several sampling contexts in host threads plus one merging context: run r is
     sampled and filtered by sessions[r % S] (the register sampler on its low-priority stream)
@@ -110,7 +126,7 @@ def time_to_target_overlapped(sessions: list, merger, cfg, reference, hv_target:
                         trace.append({"runs": run + 1, "samples": (run + 1) * samples_per_run, "archive": st["F"],
                                       "hv": st["hv"], "wall_s": time.perf_counter() - t0})
                     st["next"] = run + 1
-                    if st["hv"] == hv_target:
+                    if _reached(st["hv"], hv_target):
                         st["done"] = True
                     cv.notify_all()
         except BaseException as ex:  # surface worker errors in the caller
@@ -127,5 +143,5 @@ def time_to_target_overlapped(sessions: list, merger, cfg, reference, hv_target:
     if st["error"] is not None:
         raise st["error"]
     merger.running_to_archive()
-    return {"reached": st["hv"] == hv_target, "runs": st["runs"], "samples": st["runs"] * samples_per_run,
+    return {"reached": _reached(st["hv"], hv_target), "runs": st["runs"], "samples": st["runs"] * samples_per_run,
             "seconds": time.perf_counter() - t0, "hv": st["hv"], "archive": st["F"]}

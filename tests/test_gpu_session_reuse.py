@@ -46,7 +46,7 @@ def test_streaming_and_enumeration_after_other_work():
         s.set_instance(load_heavy_hex(3))
         s.set_weights(api.build_weights(3, resolution=7))
         cfg = api.SolverConfig(variant=api.SolverVariant.ballistic_sb, batch_size=60, seed=9)
-        res = streaming.time_to_target(s, cfg, [-60.0, -60.0, -60.0], -1.0, 3)
+        res = streaming.time_to_target(s, cfg, [-60.0, -60.0, -60.0], None, 3)
         return res["hv"], s.archive().values.copy()
 
     shared = api.Session(0)

@@ -41,7 +41,7 @@ def test_c5_scale_pool_filter_equals_streaming_merge():
     st = api.Session(0)
     st.set_instance(inst)
     st.set_weights(w)
-    res = streaming.time_to_target(st, cfg, r, -1.0, RUNS)  # unreachable target: all RUNS runs
+    res = streaming.time_to_target(st, cfg, r, None, RUNS)  # no target: all RUNS runs
     assert res["runs"] == RUNS
     b = st.archive()
     assert np.array_equal(a.values, b.values) and np.array_equal(a.configs, b.configs)
