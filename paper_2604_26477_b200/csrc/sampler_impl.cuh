@@ -135,10 +135,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     // DMAX == 0: rp[NP+1] | cv[nnz] | cc[nnz];  DMAX == 3: one 48-byte record per spin,
     // {J_i,j0, J_i,j1 | J_i,j2, off_j0, off_j1 | off_j2, -, -, -} (off = byte offset of phi_j
     // in a trajectory's row), three LDS.128 per spin
+    //                DMAX == 3 and dSB (TAB): a 16-byte record {off_j0, off_j1, off_j2, -} per
+    // spin, then per spin the 8 values c0 * coupled_i of its 2^3 neighbour sign patterns
+    // (table entry f0 + 2 f1 + 4 f2, f_k = 1 iff x_jk < 0), each summed j-ascending from +0.0
+    // and multiplied by c0 exactly as the reference does per trajectory (bit-identical)
     int* rp = reinterpret_cast<int*>(csr);
     double* cv = reinterpret_cast<double*>(csr + ((NP + 1) * 4 + 15) / 16 * 16);
     int* cc = reinterpret_cast<int*>(cv + p.nnz);
     static_assert(DMAX == 0 || DMAX == 3, "padded rows are 3 wide");
+    constexpr bool TAB = VAR == 1 && DMAX == 3;
 
     const int n = p.n;
     const long long gblock = p.block_begin + blockIdx.x;
@@ -160,6 +165,24 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
             for (int i = tid; i < p.nnz; i += kThreads) {
                 cv[i] = v[i];
                 cc[i] = p.col[i];
+            }
+        } else if constexpr (TAB) {
+            const double* v = p.pad_vals + static_cast<long long>(l) * n * DMAX;
+            const double c0l = p.c0[l];
+            for (int i = tid; i < NP; i += kThreads) {  // phantom rows: zero couplings to themselves
+                int* ro = reinterpret_cast<int*>(csr + i * 16);
+                for (int d = 0; d < 3; ++d) ro[d] = (i < n ? p.pad_col[i * 3 + d] : i) * G::kPhiW;
+                ro[3] = 0;
+            }
+            double* tab = reinterpret_cast<double*>(csr + NP * 16);
+            for (int e = tid; e < NP * 8; e += kThreads) {
+                const int i = e >> 3, pat = e & 7;
+                double coupled = 0.0;
+                for (int d = 0; d < 3; ++d) {
+                    const double jv = i < n ? v[i * 3 + d] : 0.0;
+                    coupled = __dadd_rn(coupled, (pat >> d) & 1 ? -jv : jv);  // J_ij sgn(x_j): a sign flip
+                }
+                tab[e] = __dmul_rn(c0l, coupled);
             }
         } else {
             const double* v = p.pad_vals + static_cast<long long>(l) * n * DMAX;
@@ -222,7 +245,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     unsigned char* phb = phis + t_loc * G::kPStr * G::kPhiW;  // this trajectory's phi row
     // dSB: phi = (x < 0 ? -1 : +1) (solver.hpp:161-165) kept as the sign mask of the product
     auto put_phi = [&](int j, double xv) {
-        if constexpr (VAR == 1) reinterpret_cast<uint32_t*>(phb)[j] = xv < 0.0 ? 0x80000000u : 0u;
+        if constexpr (TAB) reinterpret_cast<uint32_t*>(phb)[j] = xv < 0.0 ? 8u : 0u;  // table byte step
+        else if constexpr (VAR == 1) reinterpret_cast<uint32_t*>(phb)[j] = xv < 0.0 ? 0x80000000u : 0u;
         else reinterpret_cast<double*>(phb)[j] = xv;
     };
     // J_ij * phi_j for the phi entry at byte offset o: exact (a sign flip for dSB)
@@ -240,7 +264,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
     const double* fn = zig->fn;
     uint32_t* ub = ubuf + t_loc * US;  // this trajectory's word row
     uint32_t* en = ent + t_loc;   // this trajectory's event column, stride TPC
-    const uint4* recs = reinterpret_cast<const uint4*>(csr) + s0 * 3;  // this lane's coupling records
+    const uint4* recs = reinterpret_cast<const uint4*>(csr) + s0 * (TAB ? 1 : 3);  // this lane's coupling records
+    const unsigned char* tabl = csr + NP * 16 + s0 * 64;  // TAB: this lane's c0 * coupled tables
     bool overflow = false;
     int ovf_code = 0;  // which buffer overflowed (diagnostics)
     __syncwarp(wmask);
@@ -469,7 +494,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
             if (specm & (1u << s)) eta = __hiloint2double(static_cast<int>(wp[-1]), static_cast<int>(u));
             // coupled_i = sum_j J_ij phi(x_j), j ascending, from +0.0 (shim GEMM order)
             double coupled = 0.0;
-            if constexpr (DMAX > 0) {
+            double c0c = 0.0;  // TAB: c0 * coupled_i from the sign-pattern table
+            if constexpr (TAB) {
+                const uint4 rc = recs[s];
+                const uint32_t f0 = *reinterpret_cast<const uint32_t*>(phb + rc.x);
+                const uint32_t f1 = *reinterpret_cast<const uint32_t*>(phb + rc.y);
+                const uint32_t f2 = *reinterpret_cast<const uint32_t*>(phb + rc.z);
+                c0c = *reinterpret_cast<const double*>(tabl + s * 64 + (f0 + 2 * f1 + 4 * f2));
+            } else if constexpr (DMAX > 0) {
                 const uint4 r0 = recs[3 * s], r1 = recs[3 * s + 1], r2 = recs[3 * s + 2];
                 coupled = __dadd_rn(coupled, term(__hiloint2double(r0.y, r0.x), static_cast<int>(r1.z)));
                 coupled = __dadd_rn(coupled, term(__hiloint2double(r0.w, r0.z), static_cast<int>(r1.w)));
@@ -485,8 +517,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LANES>()) sb_small_kernel
                 yi = __dadd_rn(__dmul_rn(0.9, yi), __dmul_rn(1.0 - 0.9, d));
                 xi = __dadd_rn(xi, UDT ? yi : __dmul_rn(dt, yi));
             } else {
-                const double d =
-                    __dadd_rn(__dsub_rn(__dmul_rn(neg_drift, xi), __dmul_rn(c0, coupled)), __dmul_rn(alpha, eta));
+                if constexpr (!TAB) c0c = __dmul_rn(c0, coupled);
+                const double d = __dadd_rn(__dsub_rn(__dmul_rn(neg_drift, xi), c0c), __dmul_rn(alpha, eta));
                 yi = __dadd_rn(yi, UDT ? d : __dmul_rn(dt, d));
                 xi = __dadd_rn(xi, UDT ? yi : __dmul_rn(sdt, yi));
             }
@@ -533,7 +565,8 @@ template <int NMAX, int LANES, int VAR, int DMAX, bool UDT>
 int launch_small_u(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
     using G = Geo<NMAX, LANES, VAR>;
-    const int csr_bytes = DMAX == 0 ? ((G::kNP + 1) * 4 + 15) / 16 * 16 + p.nnz * 12 : G::kNP * 48;
+    const int csr_bytes = DMAX == 0 ? ((G::kNP + 1) * 4 + 15) / 16 * 16 + p.nnz * 12
+                          : (VAR == 1 ? G::kNP * (16 + 64) : G::kNP * 48);
     const int smem = G::csr + csr_bytes + 16;
     auto kern = sb_small_kernel<NMAX, LANES, VAR, DMAX, UDT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
