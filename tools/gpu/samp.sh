@@ -1,0 +1,3 @@
+set -x
+timeout 600 python -m pytest tests/test_gpu_sampler.py tests/test_gpu_fuzz.py -x -q 2>&1 | tail -4
+timeout 300 python tools/quick_sampler_bench.py
