@@ -21,8 +21,16 @@ scaling), filters it locally, and the fronts are merged with an NCCL all-gather.
           reference point; N ranks sample N runs per round and merge over NCCL. The same
           for the C1 shape (K=3 bSB) is reported beside it.
 
+Beside the headline the line carries the other BASELINE configs, each timed by bench.py on
+the same box (N ranks shard the blocks; the fronts merge over NCCL):
+  c4 : synthetic N=2000 dense K=3 dSB (55 weights x 3000 = 165,000 samples), tensor-core
+       H*J(c).sgn(X) steps; roofline of the FP64 update kernel (HBM) and of the GEMM
+  c5 : Pareto stress, 100 runs of the C2 lattice = 1.0e8 4-objective samples through dedup,
+       evaluation, the non-dominated filter and HV (strong scaling over ranks)
+
 `--impl reference` times the reference itself (oracle/_ref/libmomc_ref.so, the unmodified
-reference headers) on the host cores on a bounded sample of the same workload.
+reference headers) on the host cores: one full C2 step (1,000,120 samples, same config as
+ours), all host threads.
 """
 from __future__ import annotations
 
@@ -48,7 +56,13 @@ TTO_MAX_RUNS = {4: 512, 3: 64}  # bound on the streaming run (K=4 needs ~104 run
 # runs sampled per streaming step (one launch, one merge, one HV check): the K=4 stream
 # checks every 2 runs (merge + HV ~1.2 ms against a 10.7 ms run), the short K=3 one every run
 TTO_RUNS_PER_STEP = {4: 2, 3: 1}
-CPU_SAMPLE_BATCH = 512  # reference arm / cpu_baseline: 220 x 512 = 112,640 samples per step
+CPU_SAMPLE_BATCH = 512  # cpu_baseline leg of our arm: 220 x 512 = 112,640 samples (bounded sample)
+REF_ARM_BATCH = 4546    # reference arm: the full C2 pool (same config as ours)
+C4_BATCH, C4_N, C4_H = 3000, 2000, 12
+C5_RUNS = 100
+# FP64 update kernel of the dense path, per spin-update: read D (int32) + x + y, write x + y +
+# the sign operand (int8)
+C4_UPDATE_BYTES = 4 + 16 + 16 + 1
 
 # Algorithmic lane-operations of one SB sample at n=42, |E|=45, T=50:
 # Philox4x32-10 blocks (42 init + ~550 noise) x 40, ziggurat fast path 2100 x 7,
@@ -140,13 +154,15 @@ def measured_peaks():
         return {}
 
 
-def profile_traffic():
-    """dram bytes per sampler launch from the committed ncu --set full summary, if any."""
+def profile_traffic(name="sampler_ncu_summary.json"):
+    """dram bytes per launch of a kernel from its committed `ncu --set full` summary under
+    profiles/ (captured from the same kernel build; ncu never runs inside the bench: the
+    profiling recipe forbids profiling the timed program), with the file it came from."""
     try:
-        with open(os.path.join(ROOT, "profiles", "sampler_ncu_summary.json")) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh).get("dram_bytes_per_launch"), "profiles/" + name
     except Exception:
-        return None
+        return None, None
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -182,23 +198,157 @@ def run_reference_arm(args):
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
-    steps = max(1, min(args.steps, 3))
-    warmup = min(args.warmup, 1)
-    m = cpu_reference_measure(steps, warmup)
-    sample = (f"C2 shape with batch {CPU_SAMPLE_BATCH} (220 x {CPU_SAMPLE_BATCH} = {m['pool']} samples) per step: "
+    # one full-size C2 step (~40 s on 16 cores): the same pool as our arm, so the ratio the
+    # driver forms compares equal work
+    steps, warmup = 1, 0
+    m = cpu_reference_measure(steps, warmup, batch=REF_ARM_BATCH)
+    sample = (f"the full C2 step (220 x {REF_ARM_BATCH} = {m['pool']} samples): "
               f"run_sampler(threads={m['threads']}) + non_dominated_filter + reference_point_sampled(4096) + "
-              f"hypervolume")
+              f"hypervolume; hv {m['hv']:.0f}, archive {m['archive']}")
     line = {"metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
             "warmup": warmup, "ms_per_step": m["seconds_per_step"] * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": WORKLOAD + f" (bounded CPU sample: batch {CPU_SAMPLE_BATCH})",
+            "config": {"workload": WORKLOAD, "samples_per_step": m["pool"], "same_config": True,
                        "parallelism": f"{m['threads']} host threads"},
             "cpu_baseline": {"value": m["value"], "unit": UNIT, "cores": m["threads"], "kind": "reference",
                              "sample": sample},
             "e2e": {"value": m["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ----------------------------------------------------------------------------- other configs
+def sharded_pipeline(api, mdist, torch, s, inst, cfg, runs, world, rank, local, ref_count, fixed_reference=None):
+    """one pass of the hot path over `runs` runs: this rank's block share -> local front ->
+    NCCL all-gather + device merge (N > 1) -> reference point -> HV"""
+    b0, b1 = mdist.shard_range(s.num_blocks(cfg, runs), world, rank)
+    rep = s.pipeline(cfg, runs, b0, b1, do_hv=(world == 1), ref_count=ref_count, fixed_reference=fixed_reference)
+    if world > 1:
+        vals, words = mdist.local_archive_tensors(s, torch.device("cuda", local))
+        av, aw = mdist.gather_fronts(vals, words)
+        mdist.merge_on_device(s, av, aw)
+        if fixed_reference is not None:
+            r = list(fixed_reference)
+        else:
+            r = api.clamp_reference(api.reference_point_sampled(inst, ref_count, cfg.seed, session=s),
+                                    s.archive(with_configs=False))
+        rep["hv"] = s.archive_hypervolume(r)
+        rep["archive_size"] = s.archive_size()
+    return rep
+
+
+def timed_steps(fn, steps, stream, torch, flush, sync_all, max_over_ranks, world):
+    """device time of `steps` calls (CUDA events on the context's stream, L2 flushed between
+    steps, max over ranks)"""
+    ms, reps = [], []
+    for _ in range(steps):
+        flush.zero_()
+        sync_all()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        reps.append(fn())
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    sync_all()
+    mean = float(np.mean(ms))
+    if world > 1:
+        mean = max_over_ranks(mean)
+    return mean, ms, reps
+
+
+def measure_c4(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, flush, steps):
+    """BASELINE config 4: synthetic N=2000 dense 3-objective MO-MaxCut
+    (generate_uniform_instance(2000, 1.0, 3, WeightSpec{}, 3), built on the device), dSB,
+    55 weights (H=12) x 3000 trajectories, T=50, on the tensor-core path."""
+    s = api.Session(local)
+    t0 = time.perf_counter()
+    inst = s.generate_uniform_instance(C4_N, 1.0, 3, 3)
+    t_gen = time.perf_counter() - t0
+    w = api.build_weights(3, resolution=C4_H)
+    s.set_weights(w)
+    cfg = api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=C4_BATCH, seed=3)
+    stream = torch.cuda.ExternalStream(s.stream(), device=f"cuda:{local}")
+    step = lambda: sharded_pipeline(api, mdist, torch, s, inst, cfg, 1, world, rank, local, 1000)  # noqa: E731
+    step()  # warm-up: state buffers, tensor maps
+    l0 = s.launches()
+    mean_ms, ms, reps = timed_steps(step, steps, stream, torch, flush, sync_all, max_over_ranks, world)
+    launches = (s.launches() - l0) // steps
+    samples = len(w) * C4_BATCH
+    rep = reps[-1]
+    # roofline pass (not timed above): per-kernel device times with event brackets
+    s.set_kernel_timing(True)
+    s.kernel_times(reset=True)
+    rk = sharded_pipeline(api, mdist, torch, s, inst, cfg, 1, world, rank, local, 1000)
+    kt = s.kernel_times(reset=True)
+    s.set_kernel_timing(False)
+    local_samples = rk["pool_size"]
+    upd_ms, upd_n = kt["dense_update"]
+    gemm_ms, gemm_n = kt["dense_gemm"]
+    ev_ms, ev_n = kt["eval_gemm"]
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    upd_bytes = 50 * local_samples * C4_N * C4_UPDATE_BYTES
+    gemm_ops = 2.0 * C4_N * C4_N * local_samples * 50
+    upd_gbs = upd_bytes / (upd_ms * 1e-3) / 1e9 if upd_ms else None
+    traffic, tsrc = profile_traffic("c4_dense_warp_ncu_summary.json")
+    return {
+        "workload": f"C4: synthetic N={C4_N} dense K=3 MO-MaxCut (generate_uniform_instance(2000, 1.0, 3, seed 3), "
+                    f"{inst.num_edges()} edges), dSB, {len(w)} weights (H={C4_H}) x {C4_BATCH}, T=50, alpha=0.15",
+        "samples_per_step": samples, "steps": steps, "warmup": 1, "ms_per_step": mean_ms,
+        "step_ms": [round(float(x), 3) for x in ms], "value": samples / (mean_ms * 1e-3), "unit": UNIT,
+        "scaling": "weak" if world == 1 else "strong (weights x trajectories sharded over ranks)",
+        "sampler_path": s.sampler_path(), "instance_generation_s": t_gen, "gpu_launches": int(launches),
+        "sampling_s": rep["sampling_s"], "pareto_filtering_s": rep["pareto_filtering_s"],
+        "archive": int(rep["archive_size"]), "hv": rep["hv"],
+        "stages_s": {k: rep[k] for k in ("model_construction_s", "dedup_s", "eval_s", "collapse_s", "front_s",
+                                         "order_s", "reference_s", "hv_s")},
+        "roofline": {
+            "bound": "hbm", "kernel": "k_dense_warp (FP64 dSB update, dominant)",
+            "achieved": upd_gbs, "peak": hbm, "unit": "GB/s", "frac": upd_gbs / hbm if upd_gbs else None,
+            "traffic": traffic, "traffic_source": tsrc,
+            "bytes_per_spin_update": C4_UPDATE_BYTES, "launches": upd_n, "ms": upd_ms,
+            "gemm": {"kernel": "k_dense_gemm (tcgen05 kind::i8, H*J(c).sgn(X))", "ms": gemm_ms, "launches": gemm_n,
+                     "achieved_tops": gemm_ops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
+                     "peak_note": "int8 dense nominal 4500 TOP/s (no measured int8 peak); bf16 measured "
+                                  f"{peaks.get('bf16_tflops')} TF/s"},
+            "eval_gemm": {"kernel": "k_eval_tc (tcgen05 evaluate_cuts)", "ms": ev_ms, "launches": ev_n},
+            "kernel_share_of_step": (upd_ms + gemm_ms) / mean_ms if mean_ms else None},
+    }
+
+
+def measure_c5(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, flush, inst, weights, cfg, r):
+    """BASELINE config 5: Pareto stress, 100 runs of the C2 lattice = 100,012,000 sampled
+    4-objective vectors through dedup + evaluation + non-dominated filter + HV at the C2
+    golden reference point; the runs' blocks are sharded over ranks (strong scaling)."""
+    s = api.Session(local)
+    s.set_instance(inst)
+    s.set_weights(weights)
+    stream = torch.cuda.ExternalStream(s.stream(), device=f"cuda:{local}")
+    step = lambda: sharded_pipeline(api, mdist, torch, s, inst, cfg, C5_RUNS, world, rank, local, 4096,  # noqa: E731
+                                    fixed_reference=r)
+    step()  # warm-up: pool-sized buffers
+    mean_ms, ms, reps = timed_steps(step, 2, stream, torch, flush, sync_all, max_over_ranks, world)
+    rep = reps[-1]
+    samples = C5_RUNS * len(weights) * cfg.batch_size
+    local_m = rep["pool_size"]
+    dd = rep["dedup_s"]
+    return {
+        "workload": f"C5: Pareto stress, {C5_RUNS} runs of the C2 lattice (220 x 4546) = {samples} 4-objective "
+                    "vectors: dedup + evaluation + non-dominated filter + HV at the C2 golden reference point",
+        "samples_per_step": samples, "steps": 2, "warmup": 1, "ms_per_step": mean_ms,
+        "step_ms": [round(float(x), 3) for x in ms], "value": samples / (mean_ms * 1e-3), "unit": UNIT,
+        "scaling": "strong", "sampling_s": rep["sampling_s"], "pareto_filtering_s": rep["pareto_filtering_s"],
+        "pareto_vectors_per_s": local_m / rep["pareto_filtering_s"] if rep["pareto_filtering_s"] else None,
+        "unique_configs": int(rep["unique_configs"]), "unique_vectors": int(rep["unique_vectors"]),
+        "archive": int(rep["archive_size"]), "hv": rep["hv"],
+        "stages_s": {k: rep[k] for k in ("dedup_s", "eval_s", "collapse_s", "front_s", "order_s", "hv_s")},
+        "dedup": {"kernel": "k_dedup", "configs": local_m, "seconds": dd,
+                  "achieved_gbs": local_m * 8 / dd / 1e9 if dd else None,
+                  "note": "algorithmic bytes = 8 B packed config read per sample (the hash table is extra)"},
+    }
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -210,6 +360,7 @@ def main():
     ap.add_argument("--no-tto", action="store_true", help="skip the streaming time-to-optimal run")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C4 / C5 measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -396,6 +547,15 @@ def main():
                             "shape": "C2 (K=4 dSB, 220 x 4546)" if k == 4 else "C1 (K=3 bSB, 190 x 3000)"}
             del sessions
 
+    # ---- the other BASELINE configs: C4 (dense tensor-core dSB) and C5 (1e8-sample Pareto
+    #      stress); every rank samples its share of the blocks, fronts merge over NCCL
+    extra = {}
+    if not args.no_extra:
+        extra["c4"] = measure_c4(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, flush,
+                                 max(args.steps // 3, 2))
+        extra["c5"] = measure_c5(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, flush,
+                                 inst, weights, cfg, ref_golden)
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -408,9 +568,10 @@ def main():
     peak_ops = n_sm * 128 * sm_clk * 1e6  # lane-ops/s: 4 schedulers x 32 lanes per SM per clock
     sampling_s = float(np.mean([r["sampling_s"] for r in reps]))
     achieved = ALG_OPS_PER_SAMPLE * (samples_total / world) / sampling_s
+    traffic, traffic_src = profile_traffic()
     roofline = {"bound": "issue", "kernel": "sb_small_kernel<42,4,1,3,true> (SB sampler, dominant)",
                 "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tlane-op/s",
-                "frac": achieved / peak_ops, "traffic": profile_traffic(),
+                "frac": achieved / peak_ops, "traffic": traffic, "traffic_source": traffic_src,
                 "note": "neither HBM- nor tensor-bound: integer Philox + FP64 update; peak = SMs x 128 lanes "
                         "x sm_max_mhz dispatch rate; algorithmic ops/sample in DESIGN.md",
                 "kernel_share_of_step": sampling_s / (ms_per_step * 1e-3)}
@@ -464,6 +625,7 @@ def main():
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

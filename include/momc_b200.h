@@ -90,6 +90,14 @@ int momc_b200_instance_get(momc_ctx* ctx, int32_t* edge_i, int32_t* edge_j, doub
  * n >= n_min (default 256; INT_MAX turns it off); smaller n keep the bit-exact FP64 order of
  * the reference. */
 int momc_b200_set_dense_threshold(momc_ctx* ctx, int n_min);
+/* Per-kernel device times (diagnostics for roofline figures; no reference counterpart).
+ * With timing on, every launch of the register sampler (class 0), the dense tensor-core GEMM
+ * (1), the dense FP64 update (2) and the tensor-core evaluate_cuts (3) is bracketed by CUDA
+ * events on its stream. momc_b200_kernel_times synchronises the context's streams and
+ * returns the summed milliseconds and launch counts per class (4 entries each; NULL skips),
+ * zeroing them when `reset` is non-zero. */
+int momc_b200_set_kernel_timing(momc_ctx* ctx, int on);
+int momc_b200_kernel_times(momc_ctx* ctx, double* ms, long long* counts, int reset);
 /* Which sampler produced the resident pool: 0 none yet, 1 register-resident (n <= 64,
  * bit-exact), 2 sequential generic (bit-exact), 3 fused tensor-core dSB with int8 H*J(c),
  * 4 the same with bf16 H*J(c). Paths 3 and 4 round J(c).sgn(X) once (not bit-exact; see

@@ -88,6 +88,8 @@ SIGNATURES = [
     ("momc_b200_instance_get", C.c_int, [vp, i32p, i32p, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_set_dense_threshold", C.c_int, [vp, C.c_int]),
     ("momc_b200_sampler_path", C.c_int, [vp]),
+    ("momc_b200_set_kernel_timing", C.c_int, [vp, C.c_int]),
+    ("momc_b200_kernel_times", C.c_int, [vp, dp, C.POINTER(C.c_longlong), C.c_int]),
     ("momc_b200_set_weights", C.c_int, [vp, i32p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     ("momc_b200_get_coupling", C.c_int, [vp, C.c_int, dp, dp, C.c_char_p, C.c_size_t]),
     ("momc_b200_sample", C.c_int, [vp, C.POINTER(SolverCfgC), C.c_int, C.c_longlong, C.c_longlong, dp,

@@ -580,6 +580,20 @@ class Session:
         self.lib.momc_b200_set_dense_threshold(self.h, n_min)
 
     SAMPLER_PATHS = ("none", "register", "generic", "dense_i8", "dense_bf16")
+    KERNEL_CLASSES = ("sampler", "dense_gemm", "dense_update", "eval_gemm")
+
+    def set_kernel_timing(self, on: bool):
+        """bracket every sampler / dense GEMM / dense update / tensor-core evaluation launch
+        with CUDA events (momc_b200_set_kernel_timing); a diagnostic for roofline figures"""
+        self.lib.momc_b200_set_kernel_timing(self.h, int(bool(on)))
+
+    def kernel_times(self, reset: bool = True) -> dict:
+        """{class: (summed ms, launches)} since the last reset (momc_b200_kernel_times)"""
+        ms = (C.c_double * 4)()
+        cnt = (C.c_longlong * 4)()
+        if self.lib.momc_b200_kernel_times(self.h, ms, cnt, int(bool(reset))) != 0:
+            raise RuntimeError("momc_b200_kernel_times failed")
+        return {name: (ms[i], cnt[i]) for i, name in enumerate(self.KERNEL_CLASSES)}
 
     def sampler_path(self) -> str:
         """which sampler produced the resident pool (momc_b200_sampler_path): "register" and

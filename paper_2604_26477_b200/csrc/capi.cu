@@ -625,7 +625,9 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
         if (densepath) {
             sample_dense(c, p, b_begin, nblocks);  // tensor-core J sgn(X) (dense.cu)
         } else {
+            const int kt = regpath ? c.ktimer.begin(ss) : -1;
             const int rc = regpath ? launch_sampler(p, nblocks, ss) : launch_sampler_generic(p, nblocks, g, c.stream);
+            c.ktimer.end(kt, kKSampler, ss);
             ck(static_cast<cudaError_t>(rc), "sampler launch");
             c.launches += regpath ? 1 : 2 + (long long)p.T * (cfg->alpha > 0 ? 2 : 1);
         }
@@ -639,6 +641,7 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     ck(cudaStreamSynchronize(ss), "sampler");
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, c.ev0, c.ev1), "event");
+    c.ktimer.collect();
     // test hook: MOMC_TEST_FORCE_FALLBACK=k re-runs every k-th register-path block on the
     // sequential path (its words must be identical); never set in production
     if (regpath) {
@@ -1457,6 +1460,35 @@ int momc_b200_instance_get(momc_ctx* ctx, int32_t* edge_i, int32_t* edge_j, doub
 }
 
 int momc_b200_sampler_path(momc_ctx* ctx) { return ctx ? ctx->last_path : 0; }
+
+int momc_b200_set_kernel_timing(momc_ctx* ctx, int on)
+{
+    if (!ctx) return MOMC_EUSAGE;
+    ctx->ktimer.on = on != 0;
+    return MOMC_OK;
+}
+
+int momc_b200_kernel_times(momc_ctx* ctx, double* ms, long long* counts, int reset)
+{
+    if (!ctx) return MOMC_EUSAGE;
+    bind(*ctx);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess || cudaStreamSynchronize(ctx->sample_stream) != cudaSuccess)
+        return MOMC_ERUNTIME;
+    try {
+        ctx->ktimer.collect();
+    } catch (const std::exception&) {
+        return MOMC_ERUNTIME;
+    }
+    for (int i = 0; i < kKClasses; ++i) {
+        if (ms) ms[i] = ctx->ktimer.ms[i];
+        if (counts) counts[i] = ctx->ktimer.count[i];
+        if (reset) {
+            ctx->ktimer.ms[i] = 0;
+            ctx->ktimer.count[i] = 0;
+        }
+    }
+    return MOMC_OK;
+}
 
 int momc_b200_set_dense_threshold(momc_ctx* ctx, int n_min)
 {

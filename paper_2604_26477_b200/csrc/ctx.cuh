@@ -58,6 +58,54 @@ struct DevBuf {
     }
 };
 
+// Optional per-kernel-class device timing (momc_b200_set_kernel_timing): an event pair around
+// each timed launch on its own stream, summed after the caller's synchronisation. Off by
+// default; bench.py turns it on for a separate roofline pass, never for the timed value.
+enum KernelClass { kKSampler = 0, kKDenseGemm = 1, kKDenseUpdate = 2, kKEvalGemm = 3, kKClasses = 4 };
+struct KernelTimer {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;  // 2 per recorded launch
+    std::vector<int> cls;
+    size_t used = 0;
+    double ms[kKClasses] = {};
+    long long count[kKClasses] = {};
+    int begin(cudaStream_t st)
+    {
+        if (!on) return -1;
+        if (2 * used + 2 > ev.size()) {
+            cudaEvent_t a, b;
+            ck(cudaEventCreate(&a), "event");
+            ck(cudaEventCreate(&b), "event");
+            ev.push_back(a);
+            ev.push_back(b);
+            cls.push_back(0);
+        }
+        ck(cudaEventRecord(ev[2 * used], st), "event");
+        return static_cast<int>(used++);
+    }
+    void end(int i, int k, cudaStream_t st)
+    {
+        if (i < 0) return;
+        cls[static_cast<size_t>(i)] = k;
+        ck(cudaEventRecord(ev[2 * static_cast<size_t>(i) + 1], st), "event");
+    }
+    // call after the launches' stream has been synchronised
+    void collect()
+    {
+        for (size_t i = 0; i < used; ++i) {
+            float t = 0;
+            ck(cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]), "event");
+            ms[cls[i]] += t;
+            count[cls[i]]++;
+        }
+        used = 0;
+    }
+    ~KernelTimer()
+    {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;         // highest priority: everything but the register sampler
@@ -116,7 +164,8 @@ struct Ctx {
     std::shared_ptr<void> running;                // streaming: running archive (unordered)
     double running_hv = 0.0;                      // its HV at running_hv_ref (cached)
     std::vector<double> running_hv_ref;
-    bool skip_order = false;                      // fronts for internal use: no archive order                // resident DevArchive (pareto.cuh)
+    bool skip_order = false;                      // fronts for internal use: no archive order
+    KernelTimer ktimer;                           // optional per-kernel-class device times
 
     ~Ctx();
 };

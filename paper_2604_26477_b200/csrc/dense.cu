@@ -950,7 +950,9 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
             for (int hh = 0; hh < halves; ++hh) {
                 const cudaStream_t st = hs[hh];
                 const int ggrid = static_cast<int>(std::min<long long>(ga[hh].items, sms));
+                const int kg = c.ktimer.begin(st);
                 gemm<<<ggrid, kGThreads, kGSmem, st>>>(tmA, tmB, tmD, ga[hh]);
+                c.ktimer.end(kg, kKDenseGemm, st);
                 c.launches++;
                 if (halves == 2 && t == 0 && hh == 0) {  // half B starts one GEMM later: out of phase
                     ck(cudaEventRecord(d.ev_fork, st), "event");
@@ -969,6 +971,7 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
                                       c0_host[static_cast<size_t>(pq.l)] / static_cast<double>(c.H)};
                     }
                     const dim3 wgrid(static_cast<unsigned>((maxc + kWWarps - 1) / kWWarps), static_cast<unsigned>(np));
+                    const int ku = c.ktimer.begin(st);
                     if (bf16) {
                         if (noisy) udt ? launch_warp<true, true, uint16_t>(sa, wgrid, st) : launch_warp<true, false, uint16_t>(sa, wgrid, st);
                         else udt ? launch_warp<false, true, uint16_t>(sa, wgrid, st) : launch_warp<false, false, uint16_t>(sa, wgrid, st);
@@ -976,6 +979,7 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
                         if (noisy) udt ? launch_warp<true, true, int8_t>(sa, wgrid, st) : launch_warp<true, false, int8_t>(sa, wgrid, st);
                         else udt ? launch_warp<false, true, int8_t>(sa, wgrid, st) : launch_warp<false, false, int8_t>(sa, wgrid, st);
                     }
+                    c.ktimer.end(ku, kKDenseUpdate, st);
                     c.launches++;
                 }
             }
@@ -990,6 +994,7 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
         int fl[2] = {0, 0};
         ck(cudaMemcpyAsync(fl, d.flags.p, sizeof fl, cudaMemcpyDeviceToHost, c.stream), "D2H");
         ck(cudaStreamSynchronize(c.stream), "dense sampler");
+        c.ktimer.collect();
         if (fl[0] != 0x7f7f7f7f)
             runtime("numerical failure at step " + std::to_string(fl[0]) + " (run " + std::to_string(pairs[g0].run) +
                     ", weight " + std::to_string(pairs[g0].l) + ")");
@@ -1044,7 +1049,9 @@ void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, 
     const long long items = (U + kEvM - 1) / kEvM;
     const int grid = static_cast<int>(std::min<long long>(items, sms));
     ck(cudaFuncSetAttribute(k_eval_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kEvSmem), "smem attribute");
+    const int ke = c.ktimer.begin(c.stream);
     k_eval_tc<<<grid, kEvWarps * 32, kEvSmem, c.stream>>>(tm, ea);
+    c.ktimer.end(ke, kKEvalGemm, c.stream);
     c.launches++;
     ck(cudaGetLastError(), "evaluate_cuts (tensor cores)");
     dW.release();
