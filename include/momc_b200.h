@@ -265,6 +265,43 @@ int momc_b200_running_to_archive(momc_ctx* ctx, int64_t* out_F, char* err, size_
  * sharding unit (the reference's (run, weight, 512-trajectory) tasks, solver.hpp:455-499) */
 long long momc_b200_num_blocks(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs);
 
+/* ---------------------------------------------------------------- device groups (several GPUs)
+ * Replaces the reference's task pool (run_sampler solver.hpp:455-522: (run, weight,
+ * 512-trajectory chunk) tasks on `threads` host threads) by one context per device. Blocks
+ * are split into contiguous shares (the RNG streams are position-independent,
+ * solver.hpp:86-94, so the pool is the single-device pool bit for bit); each device filters
+ * its share to a local front; the fronts are gathered on member 0 (NCCL all-gather when the
+ * devices are distinct, peer copies otherwise) and merged by the same filter, so the archive
+ * equals the single-device one (lex-min owners, pareto.hpp:390-398). */
+typedef struct momc_group momc_group;
+#define MOMC_GROUP_SINGLE 0 /* one device */
+#define MOMC_GROUP_NCCL 1   /* ncclCommInitAll over the devices, ncclAllGather of the fronts */
+#define MOMC_GROUP_COPY 2   /* cudaMemcpyPeer into member 0 (repeated devices, MOMC_GROUP_TRANSPORT=copy) */
+/* devices == NULL or ndev <= 0: from MOMC_GPUS ("N" = devices 0..N-1, or a list "0,2,5");
+ * unset: device 0 */
+int momc_b200_group_create(const int* devices, int ndev, momc_group** out, char* err, size_t errlen);
+void momc_b200_group_destroy(momc_group* g);
+int momc_b200_group_size(momc_group* g);
+momc_ctx* momc_b200_group_ctx(momc_group* g, int i); /* member i's context (per-device calls) */
+int momc_b200_group_transport(momc_group* g);       /* MOMC_GROUP_* */
+int momc_b200_group_set_instance(momc_group* g, const momc_instance_view* inst, char* err, size_t errlen);
+int momc_b200_group_set_weights(momc_group* g, const int32_t* nums, int L, int H, char* err, size_t errlen);
+/* momc_b200_run_sampler over the group: the whole pool in canonical order (each shard's
+ * timestamps count from its own device's start) */
+int momc_b200_group_run_sampler(momc_group* g, const momc_instance_view* inst, const int32_t* nums, int L, int H,
+                                const momc_solver_cfg* cfg, int runs, uint64_t* out_words, int64_t* out_stamps_ns,
+                                double* out_seconds, char* err, size_t errlen);
+/* momc_b200_filter_pool over the group: row shares filtered per device, fronts merged; the
+ * archive is resident on member 0 (momc_b200_archive_get(momc_b200_group_ctx(g, 0), ...)) */
+int momc_b200_group_filter_pool(momc_group* g, const uint64_t* words, size_t M, int64_t* out_F, double* filtering_s,
+                                char* err, size_t errlen);
+/* momc_b200_bench over the group (pool and stamps copied out when non-NULL); the archive is
+ * resident on member 0; sampling_s and the stage times are the slowest member's */
+int momc_b200_group_bench(momc_group* g, const momc_instance_view* inst, const int32_t* nums, int L, int H,
+                          const momc_solver_cfg* cfg, int runs, int ref_count, const double* fixed_ref,
+                          uint64_t* out_pool, int64_t* out_stamps_ns, momc_bench_report* report, char* err,
+                          size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,6 +89,19 @@ SIGNATURES = [
     ("momc_b200_set_dense_threshold", C.c_int, [vp, C.c_int]),
     ("momc_b200_sampler_path", C.c_int, [vp]),
     ("momc_b200_set_kernel_timing", C.c_int, [vp, C.c_int]),
+    ("momc_b200_group_create", C.c_int, [i32p, C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
+    ("momc_b200_group_destroy", None, [vp]),
+    ("momc_b200_group_size", C.c_int, [vp]),
+    ("momc_b200_group_ctx", vp, [vp, C.c_int]),
+    ("momc_b200_group_transport", C.c_int, [vp]),
+    ("momc_b200_group_set_instance", C.c_int, [vp, C.POINTER(InstanceViewC), C.c_char_p, C.c_size_t]),
+    ("momc_b200_group_set_weights", C.c_int, [vp, i32p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
+    ("momc_b200_group_run_sampler", C.c_int, [vp, C.POINTER(InstanceViewC), i32p, C.c_int, C.c_int,
+                                              C.POINTER(SolverCfgC), C.c_int, u64p, i64p, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_group_filter_pool", C.c_int, [vp, u64p, C.c_size_t, i64p, dp, C.c_char_p, C.c_size_t]),
+    ("momc_b200_group_bench", C.c_int, [vp, C.POINTER(InstanceViewC), i32p, C.c_int, C.c_int, C.POINTER(SolverCfgC),
+                                        C.c_int, C.c_int, dp, u64p, i64p, C.POINTER(BenchReportC), C.c_char_p,
+                                        C.c_size_t]),
     ("momc_b200_kernel_times", C.c_int, [vp, dp, C.POINTER(C.c_longlong), C.c_int]),
     ("momc_b200_set_weights", C.c_int, [vp, i32p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     ("momc_b200_get_coupling", C.c_int, [vp, C.c_int, dp, dp, C.c_char_p, C.c_size_t]),

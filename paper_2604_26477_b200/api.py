@@ -866,6 +866,106 @@ def _session_for(inst, session):
     return s
 
 
+class DeviceGroup:
+    """Several devices behind one handle (momc_b200_group_*): the blocks of run_sampler /
+    bench are split across the devices, every device filters its share, the fronts are
+    merged on member 0 (NCCL all-gather for distinct devices, peer copies otherwise).
+    ``devices`` None: MOMC_GPUS, else device 0. ``member(0)`` is a Session view of the
+    context holding the merged archive."""
+
+    TRANSPORTS = ("single", "nccl", "copy")
+
+    def __init__(self, devices=None):
+        self.lib = _lib.load()
+        h = _lib.vp()
+        err = _errbuf()
+        arr = None if not devices else np.ascontiguousarray(devices, np.int32)
+        _raise(self.lib.momc_b200_group_create(arr.ctypes.data_as(_lib.i32p) if arr is not None else None,
+                                               0 if arr is None else len(arr), C.byref(h), err, 2048), err)
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.momc_b200_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def size(self) -> int:
+        return int(self.lib.momc_b200_group_size(self.h))
+
+    def transport(self) -> str:
+        return self.TRANSPORTS[int(self.lib.momc_b200_group_transport(self.h))]
+
+    def member(self, i: int) -> Session:
+        """a non-owning Session over member i's context"""
+        s = Session.__new__(Session)
+        s.lib = self.lib
+        s.h = _lib.vp(self.lib.momc_b200_group_ctx(self.h, i))
+        s.device = None
+        s.inst = None
+        s._owner = self  # keeps the group alive
+        s.close = lambda: None
+        return s
+
+    def run_sampler(self, inst: MultiObjectiveInstance, weights, config: SolverConfig, runs: int) -> "SamplePool":
+        config.validate()
+        nums, H = _weights_array(weights, inst.k())
+        L = nums.shape[0]
+        M = runs * L * config.batch_size
+        wpc = (inst.n() + 63) // 64
+        words = np.empty((M, wpc), np.uint64)
+        stamps = np.empty(M, np.int64)
+        secs = np.zeros(2, np.float64)
+        cfg = config.c()
+        v = inst.view()
+        err = _errbuf()
+        _raise(self.lib.momc_b200_group_run_sampler(self.h, C.byref(v), nums.ctypes.data_as(_lib.i32p), L, H,
+                                                    C.byref(cfg), runs, words.ctypes.data_as(_lib.u64p),
+                                                    stamps.ctypes.data_as(_lib.i64p), secs.ctypes.data_as(_lib.dp),
+                                                    err, 2048), err)
+        pool = SamplePool(inst.n(), words, runs, L, config.batch_size)
+        pool.stamps = stamps
+        return pool
+
+    def non_dominated_filter(self, pool, inst: MultiObjectiveInstance) -> ParetoArchive:
+        words = np.ascontiguousarray(pool.words if hasattr(pool, "words") else pool, np.uint64)
+        err = _errbuf()
+        v = inst.view()
+        _raise(self.lib.momc_b200_group_set_instance(self.h, C.byref(v), err, 2048), err)
+        F = C.c_int64()
+        fs = C.c_double()
+        _raise(self.lib.momc_b200_group_filter_pool(self.h, words.ctypes.data_as(_lib.u64p), words.shape[0],
+                                                    C.byref(F), C.byref(fs), err, 2048), err)
+        return _fetch_archive(self.member(0), inst.k(), inst.n(), True)
+
+    def bench(self, inst: MultiObjectiveInstance, weights, config: SolverConfig, runs: int = 1,
+              ref_count: int = 1000, fixed_reference=None) -> "BenchResult":
+        config.validate()
+        nums, H = _weights_array(weights, inst.k())
+        L = nums.shape[0]
+        M = runs * L * config.batch_size
+        wpc = (inst.n() + 63) // 64
+        words = np.empty((M, wpc), np.uint64)
+        rep = _lib.BenchReportC()
+        cfg = config.c()
+        v = inst.view()
+        fr = np.ascontiguousarray(fixed_reference, np.float64) if fixed_reference is not None else None
+        err = _errbuf()
+        _raise(self.lib.momc_b200_group_bench(self.h, C.byref(v), nums.ctypes.data_as(_lib.i32p), L, H, C.byref(cfg),
+                                              runs, ref_count, fr.ctypes.data_as(_lib.dp) if fr is not None else None,
+                                              words.ctypes.data_as(_lib.u64p), None, C.byref(rep), err, 2048), err)
+        report = {name: getattr(rep, name) for name, _ in _lib.BenchReportC._fields_}
+        report["reference"] = list(rep.reference)[: inst.k()]
+        archive = _fetch_archive(self.member(0), inst.k(), inst.n(), True)
+        archive.reference = report["reference"]
+        return BenchResult(report, SamplePool(inst.n(), words, runs, L, config.batch_size), archive)
+
+
 def _fetch_archive(s: Session, k: int, n: int, with_configs: bool) -> ParetoArchive:
     F = int(s.lib.momc_b200_archive_size(s.h))
     vals = np.zeros((F, k), np.float64)

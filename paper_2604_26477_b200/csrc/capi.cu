@@ -12,13 +12,12 @@
 #include <vector>
 
 #include "../../include/momc_b200.h"
+#include "capi_internal.cuh"
 #include "ctx.cuh"
 #include "pareto.cuh"
 #include "sampler.cuh"
 
 using namespace momc_b200;
-
-struct momc_ctx : Ctx {};
 
 namespace momc_b200 {
 
@@ -109,31 +108,6 @@ long long running_merge(Ctx& c, const double* d_vals, const uint64_t* d_words, l
     cv.release();
     cw.release();
     return R.F;
-}
-
-namespace {
-
-void put_err(char* err, size_t errlen, const char* msg)
-{
-    if (err && errlen) {
-        std::strncpy(err, msg, errlen - 1);
-        err[errlen - 1] = 0;
-    }
-}
-
-template <class F>
-int guarded(char* err, size_t errlen, F&& f)
-{
-    try {
-        f();
-        return MOMC_OK;
-    } catch (const ApiError& e) {
-        put_err(err, errlen, e.what());
-        return e.code;
-    } catch (const std::exception& e) {
-        put_err(err, errlen, e.what());
-        return MOMC_ERUNTIME;
-    }
 }
 
 // rng.hpp:62-89 ZigguratTables, same libm calls in the same order (bit-identical tables).
@@ -516,7 +490,7 @@ std::pair<long long, long long> rows_of_blocks(int batch, int bt, long long b0, 
 
 // compact: d_words holds only the rows of the sampled blocks (pool_row0 = first row)
 void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, long long b_end, double* seconds,
-            bool compact = false)
+            bool compact)
 {
     validate_cfg(cfg);
     if (c.n == 0) usage("no instance set");
@@ -761,8 +735,6 @@ void upload_words(Ctx& c, const uint64_t* words, size_t M)
     c.d_upload.reserve(M * wpc + 1);
     ck(cudaMemcpyAsync(c.d_upload.p, words, sizeof(uint64_t) * M * wpc, cudaMemcpyHostToDevice, c.stream), "H2D");
 }
-
-}  // namespace
 
 const ZigTables* device_zig(Ctx& c)
 {
