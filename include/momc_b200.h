@@ -196,6 +196,10 @@ int momc_b200_tc_i8_selftest(momc_ctx* ctx, const int8_t* A, const int8_t* B, in
  * only the sampler's per-word noise work (Philox block per 4 words, rng.hpp:113-121; the
  * ziggurat fast test and eta = hz * wn[iz], rng.hpp:156-163). */
 int momc_b200_rng_calibrate(momc_ctx* ctx, int blocks_per_thread, double* normals_per_s, char* err, size_t errlen);
+/* Philox4x32-10 (rng.hpp:16-39) on the device, through the routine every sampler kernel uses:
+ * out[4i..4i+3] = block(keys[i], ctrs[4i..4i+3]) (known-answer tests, test_rng.cpp:14-27) */
+int momc_b200_philox_blocks(momc_ctx* ctx, const uint64_t* keys, const uint32_t* ctrs, size_t count, uint32_t* out,
+                            char* err, size_t errlen);
 
 /* ---------------------------------------------------------------- pool CSV (solver.hpp:357-432) */
 /* The record rows of save_pool_csv, formatted on the device: for each of M records

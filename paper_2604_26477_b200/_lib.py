@@ -89,6 +89,8 @@ SIGNATURES = [
     ("momc_b200_set_dense_threshold", C.c_int, [vp, C.c_int]),
     ("momc_b200_sampler_path", C.c_int, [vp]),
     ("momc_b200_set_kernel_timing", C.c_int, [vp, C.c_int]),
+    ("momc_b200_philox_blocks", C.c_int, [vp, u64p, C.POINTER(C.c_uint32), C.c_size_t, C.POINTER(C.c_uint32),
+                                          C.c_char_p, C.c_size_t]),
     ("momc_b200_group_create", C.c_int, [i32p, C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
     ("momc_b200_group_destroy", None, [vp]),
     ("momc_b200_group_size", C.c_int, [vp]),

@@ -582,6 +582,18 @@ class Session:
     SAMPLER_PATHS = ("none", "register", "generic", "dense_i8", "dense_bf16")
     KERNEL_CLASSES = ("sampler", "dense_gemm", "dense_update", "eval_gemm")
 
+    def philox_blocks(self, keys, ctrs) -> np.ndarray:
+        """Philox4x32-10 blocks on the device (momc_b200_philox_blocks): keys (N,) u64,
+        ctrs (N, 4) u32 -> (N, 4) u32"""
+        k = np.ascontiguousarray(keys, np.uint64).reshape(-1)
+        c = np.ascontiguousarray(ctrs, np.uint32).reshape(-1, 4)
+        out = np.zeros((k.shape[0], 4), np.uint32)
+        err = _errbuf()
+        _raise(self.lib.momc_b200_philox_blocks(self.h, k.ctypes.data_as(_lib.u64p),
+                                                c.ctypes.data_as(C.POINTER(C.c_uint32)), k.shape[0],
+                                                out.ctypes.data_as(C.POINTER(C.c_uint32)), err, 2048), err)
+        return out
+
     def set_kernel_timing(self, on: bool):
         """bracket every sampler / dense GEMM / dense update / tensor-core evaluation launch
         with CUDA events (momc_b200_set_kernel_timing); a diagnostic for roofline figures"""

@@ -23,7 +23,9 @@ __global__ void __launch_bounds__(256) k_rng_calib(uint64_t key, int blocks_per_
     __syncthreads();
     const uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
     const uint32_t tr = blockIdx.x * blockDim.x + threadIdx.x;
-    double acc = 0.0;
+    // four independent sums (one per word of a block): the adds never form one dependent
+    // chain, so the kernel measures issue throughput, not FP64 add latency
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     uint32_t slow = 0;
     for (int b = 0; b < blocks_per_thread; ++b) {
         const uint4 r = philox(k0, k1, static_cast<uint32_t>(b), 3u << 26, tr, 7u);
@@ -35,13 +37,46 @@ __global__ void __launch_bounds__(256) k_rng_calib(uint64_t key, int blocks_per_
             const int32_t hz = static_cast<int32_t>(u);
             const uint32_t mag = hz < 0 ? 0u - u : u;
             slow += mag >= z.kn[iz];
-            acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(hz), z.wn[iz]));
+            acc[j] = __dadd_rn(acc[j], __dmul_rn(static_cast<double>(hz), z.wn[iz]));
         }
     }
-    if (acc == 1.2345 || slow == 0xFFFFFFFFu) sink[tr] = acc;  // keep the work alive
+    const double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    if (a == 1.2345 || slow == 0xFFFFFFFFu) sink[tr] = a;  // keep the work alive
+}
+
+// Philox4x32-10 blocks (rng.hpp:16-39) through the device routine every sampler uses
+__global__ void k_philox_blocks(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ctrs, long long count,
+                                uint32_t* __restrict__ out)
+{
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= count) return;
+    const uint64_t key = keys[i];
+    const uint4 r = philox(static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32), ctrs[4 * i], ctrs[4 * i + 1],
+                           ctrs[4 * i + 2], ctrs[4 * i + 3]);
+    out[4 * i] = r.x;
+    out[4 * i + 1] = r.y;
+    out[4 * i + 2] = r.z;
+    out[4 * i + 3] = r.w;
 }
 
 }  // namespace
+
+void philox_blocks(Ctx& c, const uint64_t* keys, const uint32_t* ctrs, long long count, uint32_t* out)
+{
+    if (count < 1) return;
+    DevBuf<uint64_t> dk;
+    DevBuf<uint32_t> dc, dout;
+    dk.reserve(static_cast<size_t>(count));
+    dc.reserve(static_cast<size_t>(count) * 4);
+    dout.reserve(static_cast<size_t>(count) * 4);
+    ck(cudaMemcpyAsync(dk.p, keys, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, c.stream), "H2D");
+    ck(cudaMemcpyAsync(dc.p, ctrs, sizeof(uint32_t) * 4 * count, cudaMemcpyHostToDevice, c.stream), "H2D");
+    k_philox_blocks<<<static_cast<unsigned>((count + 127) / 128), 128, 0, c.stream>>>(dk.p, dc.p, count, dout.p);
+    ++c.launches;
+    ck(cudaGetLastError(), "philox blocks");
+    ck(cudaMemcpyAsync(out, dout.p, sizeof(uint32_t) * 4 * count, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "philox blocks");
+}
 
 // normals generated per second by the calibration kernel (148 x 8 CTAs of 256 threads)
 double rng_calibrate(Ctx& c, int blocks_per_thread)

@@ -1236,6 +1236,15 @@ int momc_b200_tc_i8_selftest(momc_ctx* ctx, const int8_t* A, const int8_t* B, in
     });
 }
 
+int momc_b200_philox_blocks(momc_ctx* ctx, const uint64_t* keys, const uint32_t* ctrs, size_t count, uint32_t* out,
+                            char* err, size_t errlen)
+{
+    return guarded(err, errlen, [&] {
+        bind(*ctx);
+        philox_blocks(*ctx, keys, ctrs, static_cast<long long>(count), out);
+    });
+}
+
 int momc_b200_rng_calibrate(momc_ctx* ctx, int blocks_per_thread, double* normals_per_s, char* err, size_t errlen)
 {
     return guarded(err, errlen, [&] {

@@ -202,6 +202,8 @@ void parsed_pool_get(Ctx& c, uint32_t* run, uint32_t* wt, uint32_t* tr, int64_t*
 void tc_i8_selftest(Ctx& c, const int8_t* hA, const int8_t* hB, int K, int32_t* hD);
 // calib.cu: normals/s of the RNG-only calibration kernel
 double rng_calibrate(Ctx& c, int blocks_per_thread);
+// calib.cu: Philox4x32-10 blocks of (key, counter) pairs on the device (known-answer tests)
+void philox_blocks(Ctx& c, const uint64_t* keys, const uint32_t* ctrs, long long count, uint32_t* out);
 // capi.cu: the ziggurat tables on the device (uploaded once)
 const ZigTables* device_zig(Ctx& c);
 // instance_gen.cu

@@ -2,8 +2,8 @@
 generate_uniform_instance; the int8 tensor-core dSB path agrees with the reference within
 the stated tolerance (coupled = (H*J)·sgn(x)/H is one correctly rounded
 division, the reference sums rounded FP64 products, so trajectories may differ at ulp level;
-asserted: <= 1% differing words, reported exactly); evaluate_cuts through int8 GEMMs is
-exact."""
+asserted: the measured value, 0 differing words, reported as a count); evaluate_cuts through
+int8 GEMMs is exact."""
 import numpy as np
 import pytest
 
@@ -11,7 +11,7 @@ from oracle.refbind import make_cfg
 from paper_2604_26477_b200 import api
 
 pytestmark = pytest.mark.gpu
-MAX_DENSE_WORD_MISMATCH = 0.01
+MAX_DENSE_WORD_MISMATCH = 0.0  # measured; the path rounds J(c).sgn(X) once
 
 
 @pytest.mark.parametrize("n,density,k,kind,lo,hi", [(300, 0.3, 3, "int", 1, 10), (120, 0.8, 2, "real", 0.0, 1.0),
@@ -37,7 +37,7 @@ def test_dense_dsb_agrees_with_reference(ref, session, n, batch, seed):
     session.sample(api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=batch, seed=9), 1)
     got = session.pool(stamps=False).words
     mm = float(np.mean(np.any(got != want, axis=1)))
-    print(f"dense dSB n={n}: {mm * 100:.3f}% words differ ({got.shape[0]} samples)")
+    print(f"dense dSB n={n}: {int(round(mm * got.shape[0]))} of {got.shape[0]} pool rows differ")
     assert mm <= MAX_DENSE_WORD_MISMATCH
 
 

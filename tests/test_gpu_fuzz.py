@@ -81,7 +81,7 @@ def test_random_pools_filter_and_hv_match_reference(ref, session, seed):
 
 def test_random_dense_configurations_agree_with_reference(ref):
     """the int8 tensor-core dSB path (n >= 256) on random configurations: words within the
-    dense tolerance (measured 0 %)"""
+    measured dense tolerance (0 differing words)"""
     from test_gpu_dense import MAX_DENSE_WORD_MISMATCH
 
     rnd = random.Random(505)
