@@ -30,6 +30,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sampler.cuh"
 
@@ -585,10 +586,35 @@ int launch_small_u(const SamplerParams& p, long long nblocks, cudaStream_t st)
     return cudaSuccess;
 }
 
+}  // namespace sbimpl
+}  // namespace momc_b200
+
+#include "sampler_batch.cuh"
+
+namespace momc_b200 {
+namespace sbimpl {
+
+inline bool force_step_kernel()
+{
+    static const bool v = [] {
+        const char* e = std::getenv("MOMC_SAMPLER_STEP");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+// n <= 42: batched resolution (sampler_batch.cuh); n <= 64: per-step resolution
 template <int NMAX, int LANES, int VAR, int DMAX>
 int launch_small(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
-    if (p.dt == 1.0 && p.s_dt_a0 == 1.0) return launch_small_u<NMAX, LANES, VAR, DMAX, true>(p, nblocks, st);
+    const bool udt = p.dt == 1.0 && p.s_dt_a0 == 1.0;
+    if constexpr (NMAX <= 42) {
+        if (!force_step_kernel()) {
+            if (udt) return launch_batch_u<NMAX, LANES, VAR, DMAX, true>(p, nblocks, st);
+            return launch_batch_u<NMAX, LANES, VAR, DMAX, false>(p, nblocks, st);
+        }
+    }
+    if (udt) return launch_small_u<NMAX, LANES, VAR, DMAX, true>(p, nblocks, st);
     return launch_small_u<NMAX, LANES, VAR, DMAX, false>(p, nblocks, st);
 }
 
