@@ -33,15 +33,32 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sampler.cuh"
 
 namespace momc_b200 {
 namespace sbimpl {
 
-template <int NMAX, int LANES, int VAR>
+// CTA shapes of the batch kernel (threads, CTAs per SM): (128, 5) = 20 warps at <= 96
+// registers; (192, 3) = 18 warps at <= 112; (128, 4) = 16 warps at <= 128. Chosen by
+// batch_cta() (MOMC_SB_CTA, default 2: the 96-register shapes spill x / y across the noise
+// phase and measured slower, 7.51 / 7.56 vs 7.31 ms at C2).
+constexpr int kCtaBT[3] = {128, 192, 128};
+constexpr int kCtaMin[3] = {5, 3, 4};
+inline int batch_cta()
+{
+    static const int v = [] {
+        const char* e = std::getenv("MOMC_SB_CTA");
+        const int c = e ? std::atoi(e) : 2;
+        return c >= 0 && c < 3 ? c : 2;
+    }();
+    return v;
+}
+
+template <int NMAX, int LANES, int VAR, int BT = 128>
 struct BGeo {
-    static constexpr int kTPC = kThreads / LANES;           // trajectories per CTA
+    static constexpr int kTPC = BT / LANES;           // trajectories per CTA
     static constexpr int kNQ = (NMAX + LANES - 1) / LANES;  // spins per lane
     static constexpr int kNP = kNQ * LANES;                 // integrated spins (>= n)
     static constexpr int kC = 56;                           // words per stream row
@@ -49,7 +66,9 @@ struct BGeo {
     // distinct bank quads), trajectory rows at kTS == 4 mod 32 (B's reads: 4 k + NQ h distinct)
     static constexpr int kSS = kC;
     static constexpr int kTS = LANES * kSS + 4;
-    static constexpr int kNB0 = (NMAX + 6 + 3) / 4;        // blocks generated before the walk
+    // Philox blocks per stream row (kNBU unrolled at a time); more is sequential resolution
+    static constexpr int kNB = (NMAX + 14 + 3) / 4 < kC / 4 ? (NMAX + 14 + 3) / 4 : kC / 4;
+    static constexpr int kNBU = (kNB + 1) / 2;
     // offset table per stream: 16 words of lane-major offset bytes, 4 half-words of tail bits
     // (lane h's at half-word h), 2 pad; per trajectory LANES streams (stride == 16 mod 32)
     static constexpr int kWS = 20;
@@ -60,15 +79,15 @@ struct BGeo {
     static constexpr bool kTab = VAR == 1;  // (with DMAX == 3, see the kernel)
     static constexpr int kMK = 5;           // sign of x_j at mask bit j + kMK (shift counts >= 0)
     static_assert(kNP + kMK <= 64, "sign mask fits 64 bits");
-    static constexpr int zig = 0;                                   // ZigTables (2560 B)
-    static constexpr int words = 2560;                              // kTPC x kTS u32
+    // (the ziggurat tables live in static shared memory: their addresses are immediates)
+    static constexpr int words = 0;                                 // kTPC x kTS u32
     static constexpr int wofs = words + kTPC * kTS * 4;             // kTPC x kWT u32
     static constexpr int phi = wofs + kTPC * kWT * 4;               // kTPC x kPStr phi entries
     static constexpr int csr = (phi + kTPC * kPStr * kPhiW + 15) / 16 * 16;
     static_assert(LANES == 4, "one stream per lane and step of a 4-step batch");
     static_assert(kNQ <= 16, "16 offset bytes per lane");
     static_assert(NMAX + 14 <= kC, "sequential resolution packs n normals and up to 14 tails");
-    static_assert(kNB0 * 4 <= kC, "initial blocks fit the row");
+    static_assert(kNB * 4 <= kC && kNB * 4 < 64, "generated blocks fit the row and the mask");
 };
 
 // wedge test of rng.hpp:164-168 for the attempt with words u, u1, u2: accept iff
@@ -158,11 +177,19 @@ __device__ __noinline__ bool seq_resolve(uint32_t* us, uint32_t* wr, int n, uint
 }
 
 // phi-row bytes of the batch kernel (none for the sign-mask path)
-template <int NMAX, int LANES, int VAR, int DMAX>
+template <int NMAX, int LANES, int VAR, int DMAX, int BT>
 __host__ __device__ constexpr int batch_phi_bytes()
 {
-    using G = BGeo<NMAX, LANES, VAR>;
+    using G = BGeo<NMAX, LANES, VAR, BT>;
     return VAR == 1 && DMAX == 3 ? 0 : G::kTPC * G::kPStr * G::kPhiW;
+}
+
+// (a & b) | c in one LOP3
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c)
+{
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
 }
 
 __device__ __forceinline__ double lds_f64(uint32_t a)
@@ -172,20 +199,21 @@ __device__ __forceinline__ double lds_f64(uint32_t a)
     return v;
 }
 
-template <int NMAX, int LANES, int VAR, int DMAX, bool UDT>
-__global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerParams p)
+template <int NMAX, int LANES, int VAR, int DMAX, bool UDT, int BT, int MINB>
+__global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams p)
 {
-    using G = BGeo<NMAX, LANES, VAR>;
+    using G = BGeo<NMAX, LANES, VAR, BT>;
     constexpr int TPC = G::kTPC;
     constexpr int NQ = G::kNQ;
     constexpr int NP = G::kNP;
     constexpr int kC = G::kC;
     extern __shared__ __align__(16) unsigned char smem[];
-    ZigTables* zig = reinterpret_cast<ZigTables*>(smem + G::zig);
+    __shared__ ZigTables zig_s;
+    ZigTables* zig = &zig_s;
     uint32_t* wbuf = reinterpret_cast<uint32_t*>(smem + G::words);
     uint32_t* wofs = reinterpret_cast<uint32_t*>(smem + G::wofs);
     unsigned char* phis = smem + G::phi;
-    constexpr int kCsr = (G::phi + batch_phi_bytes<NMAX, LANES, VAR, DMAX>() + 15) / 16 * 16;
+    constexpr int kCsr = (G::phi + batch_phi_bytes<NMAX, LANES, VAR, DMAX, BT>() + 15) / 16 * 16;
     unsigned char* csr = smem + kCsr;
     // coupling records as in sb_small_kernel, except TAB: {sh0, sh1, sh2, -} with
     // sh_d = j_d + kMK - 3 - d, so (M >> sh_d) has x_{j_d}'s sign bit at bit 3 + d
@@ -208,24 +236,24 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
     {  // CTA setup (identical to sb_small_kernel)
         const uint32_t* src = reinterpret_cast<const uint32_t*>(p.zig);
         uint32_t* dst = reinterpret_cast<uint32_t*>(zig);
-        for (int i = tid; i < static_cast<int>(sizeof(ZigTables) / 4); i += kThreads) dst[i] = src[i];
+        for (int i = tid; i < static_cast<int>(sizeof(ZigTables) / 4); i += BT) dst[i] = src[i];
         if constexpr (DMAX == 0) {
-            for (int i = tid; i <= NP; i += kThreads) rp[i] = p.row_ptr[i < n ? i : n];
+            for (int i = tid; i <= NP; i += BT) rp[i] = p.row_ptr[i < n ? i : n];
             const double* v = p.vals + static_cast<long long>(l) * p.nnz;
-            for (int i = tid; i < p.nnz; i += kThreads) {
+            for (int i = tid; i < p.nnz; i += BT) {
                 cv[i] = v[i];
                 cc[i] = p.col[i];
             }
         } else if constexpr (TAB) {
             const double* v = p.pad_vals + static_cast<long long>(l) * n * DMAX;
             const double c0l = p.c0[l];
-            for (int i = tid; i < NP; i += kThreads) {
+            for (int i = tid; i < NP; i += BT) {
                 int* ro = reinterpret_cast<int*>(csr + i * 16);
                 for (int d = 0; d < 3; ++d) ro[d] = (i < n ? p.pad_col[i * 3 + d] : i) + G::kMK - 3 - d;
                 ro[3] = 0;
             }
             double* tab = reinterpret_cast<double*>(csr + NP * 16);
-            for (int e = tid; e < NP * 8; e += kThreads) {
+            for (int e = tid; e < NP * 8; e += BT) {
                 const int i = e >> 3, pat = e & 7;
                 double coupled = 0.0;
                 for (int d = 0; d < 3; ++d) {
@@ -236,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
             }
         } else {
             const double* v = p.pad_vals + static_cast<long long>(l) * n * DMAX;
-            for (int i = tid; i < NP; i += kThreads) {
+            for (int i = tid; i < NP; i += BT) {
                 double* rv = reinterpret_cast<double*>(csr + i * 48);
                 int* ro = reinterpret_cast<int*>(csr + i * 48 + 24);
                 for (int d = 0; d < 3; ++d) {
@@ -258,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
     const uint32_t wl = static_cast<uint32_t>(l), tr = static_cast<uint32_t>(traj);
     const double c0 = p.c0[l];
     const double alpha = p.alpha, dt = p.dt, sdt = p.s_dt_a0;
+    const bool pos_init = p.init_scale > 0.0;
     const int s0 = h * NQ;
 
     // ---- init_state (solver.hpp:108-124), as sb_small_kernel
@@ -324,42 +353,59 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
             const uint32_t lo = tag_word(kTagStepNoise, static_cast<uint32_t>(tb + h));
 #pragma unroll
             for (int c = 0; c < G::kWS / 4; ++c) reinterpret_cast<uint4*>(wr)[c] = make_uint4(0u, 0u, 0u, 0u);
-            uint32_t F0 = 0, F1 = 0;  // fast-path mask, words 0..31 / 32..63
-            int gen = 0;              // words generated
-            auto gen_block = [&]() {
-                const uint4 r = philox(k0, k1, static_cast<uint32_t>(gen >> 2), lo, tr, wl);
-                *reinterpret_cast<uint4*>(us + gen) = r;
-                // fast iff |hz| < kn[iz]: both <= 2^31 and kn >= 1, so the sign of the
-                // difference decides; shifted in from word 3 down to word 0
-                uint32_t f = (zmag(r.w) - kn[r.w & 127u]) >> 31;
-                f = __funnelshift_l(zmag(r.z) - kn[r.z & 127u], f, 1);
-                f = __funnelshift_l(zmag(r.y) - kn[r.y & 127u], f, 1);
-                f = __funnelshift_l(zmag(r.x) - kn[r.x & 127u], f, 1);
-                if (gen < 32) F0 |= f << gen;
-                else F1 |= f << (gen - 32);
-                gen += 4;
+            // Philox blocks 0 .. kNB-1 of the stream into the row, and the fast-path mask F
+            // (bit p: word p's attempt would take the fast path); kNB * 4 words cover the
+            // stream unless it needs more (P ~ 1e-3 at n = 42: sequential resolution below)
+            uint64_t F = 0;
+#pragma unroll 1
+            constexpr int kU = MINB >= 5 ? 2 : G::kNBU;  // blocks per unrolled group
+            for (int c = 0; c < G::kNB; c += kU) {
+                uint32_t fc = 0;
+#pragma unroll
+                for (int b = 0; b < kU; ++b) {
+                    if (c + b < G::kNB) {
+                        const uint4 r = philox(k0, k1, static_cast<uint32_t>(c + b), lo, tr, wl);
+                        *reinterpret_cast<uint4*>(us + 4 * (c + b)) = r;
+                        // fast iff |hz| < kn[iz]: both <= 2^31 and kn >= 1, so the sign of the
+                        // difference decides; shifted in from word 3 down to word 0
+                        uint32_t f = (zmag(r.w) - kn[r.w & 127u]) >> 31;
+                        f = __funnelshift_l(zmag(r.z) - kn[r.z & 127u], f, 1);
+                        f = __funnelshift_l(zmag(r.y) - kn[r.y & 127u], f, 1);
+                        f = __funnelshift_l(zmag(r.x) - kn[r.x & 127u], f, 1);
+                        fc |= f << (4 * b);
+                    }
+                }
+                F |= static_cast<uint64_t>(fc) << (4 * c);
+            }
+            constexpr int kGen = 4 * G::kNB;
+            // slow words, and among them the attempt starts: a wedge attempt at q takes words q,
+            // q+1, q+2 whatever its outcome, so the starts are the fixpoint Y = S & ~cov(Y) (a
+            // slow word is a start iff no start lies 1 or 2 words before it; unique, found by
+            // iteration from the left, converging in one or two rounds). Tails take 1 + 4k words
+            // and restart the computation after them.
+            const uint64_t S = ~F & ((1ull << kGen) - 1);
+            auto starts = [](uint64_t s) {
+                // round k settles every position whose chain of slow words 1-2 apart is shorter
+                // than k, so this ends within kGen rounds
+                uint64_t y = s & ~((s << 1) | (s << 2));
+                for (;;) {
+                    const uint64_t yn = s & ~((y << 1) | (y << 2));
+                    if (yn == y) return y;
+                    y = yn;
+                }
             };
-#pragma unroll 4
-            for (int b = 0; b < G::kNB0; ++b) gen_block();
+            uint64_t Y = starts(S);
 
             unsigned char* wb = reinterpret_cast<unsigned char*>(wr);
             unsigned short* tbits = reinterpret_cast<unsigned short*>(wr + 16);
-            int slow = 0, pos = 0;  // words taken by slow attempts beyond their normals; next attempt
+            int slow = 0;  // words taken by the slow attempts so far beyond their normals
             bool seq = false;
-            for (;;) {
-                const int lastq = n - 1 + slow;  // attempts at q <= lastq yield normals < n
-                const uint64_t F = static_cast<uint64_t>(F1) << 32 | F0;
-                uint64_t rem = ~F & (gen >= 64 ? ~0ull : (1ull << gen) - 1);
-                rem = pos >= 64 ? 0ull : rem & (~0ull << pos);
-                const int q = rem ? __ffsll(static_cast<long long>(rem)) - 1 : gen;
-                if (q > lastq) break;
-                if (q + 2 >= gen) {  // words up to lastq, or the wedge's two words, not generated yet
-                    if (gen + 4 > kC) {
-                        seq = true;
-                        break;
-                    }
-                    gen_block();
-                    continue;
+            while (Y) {
+                const int q = __ffsll(static_cast<long long>(Y)) - 1;
+                if (q > n - 1 + slow) break;  // the n normals end before this attempt
+                if (q + 2 >= kGen) {
+                    seq = true;
+                    break;
                 }
                 const uint32_t u = us[q];
                 const int i = q - slow;  // the attempt's normal index
@@ -368,8 +414,7 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
                     int qq = q + 1;
                     double sval = 0.0;
                     for (;;) {
-                        while (qq + 4 > gen && gen + 4 <= kC) gen_block();
-                        if (qq + 4 > gen) {
+                        if (qq + 4 > kGen) {
                             seq = true;
                             break;
                         }
@@ -385,16 +430,17 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
                     e = i;
                     d = qq - q - 1;
                     if (i < NP) tbits[i / NQ] |= static_cast<unsigned short>(1u << (i % NQ));
-                    pos = qq;
+                    Y = qq >= 64 ? 0ull : starts(S & (~0ull << qq));
                 } else {
                     const bool acc = wedge_accept(u, us[q + 1], us[q + 2], wn, zig->fn);
                     e = acc ? i + 1 : i;
                     d = acc ? 2 : 3;
-                    pos = q + 3;
+                    Y &= Y - 1;
                 }
                 slow += d;
                 if (e < NP) wb[16 * (e / NQ) + e % NQ] += static_cast<unsigned char>(4 * d);
             }
+            if (n - 1 + slow >= kGen) seq = true;  // the last normals lie past the generated words
             if (seq) {
 #pragma unroll
                 for (int c = 0; c < G::kWS / 4; ++c) reinterpret_cast<uint4*>(wr)[c] = make_uint4(0u, 0u, 0u, 0u);
@@ -431,8 +477,16 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
             uint64_t M = 0;  // TAB: phi(t) as signs, x_j < 0 at bit j + kMK
             if constexpr (TAB) {
                 uint32_t lm = 0;
+                if (pos_init) {
+                    // init_scale > 0: x is never -0.0 (x_0 = s (2u - 1) gives +0.0 at most,
+                    // x + y is -0.0 only if both are, the clamp gives +-1), so x < 0 is the
+                    // sign bit (a NaN trajectory is reported as a failure either way)
 #pragma unroll
-                for (int s = 0; s < NQ; ++s) lm |= static_cast<uint32_t>(x[s] < 0.0) << s;
+                    for (int s = NQ - 1; s >= 0; --s) lm = __funnelshift_l(__double2hiint(x[s]), lm, 1);
+                } else {
+#pragma unroll
+                    for (int s = 0; s < NQ; ++s) lm |= static_cast<uint32_t>(x[s] < 0.0) << s;
+                }
                 M = static_cast<uint64_t>(lm) << (s0 + G::kMK);
                 M = lane_or<LANES>(wmask, M);
             }
@@ -440,6 +494,9 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
             // ---- B: spin updates (sb_step solver.hpp:159-181 / simcim_step :196-210)
 #pragma unroll
             for (int s = 0; s < NQ; ++s) {
+                // loads of the second half are not hoisted above the first half's updates
+                // (register pressure at 5 CTAs per SM)
+                if (MINB >= 5 && s == NQ / 2) asm volatile("" ::: "memory");
                 const uint32_t Wq = s < 4 ? Wv.x : s < 8 ? Wv.y : s < 12 ? Wv.z : Wv.w;
                 const uint32_t boff = __byte_perm(Wq, 0u, 0x4440u + static_cast<uint32_t>(s & 3));
                 const uint32_t* wp =
@@ -455,9 +512,9 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
                 if constexpr (TAB) {
                     // table entry f0 + 2 f1 + 4 f2 (f_d = x_{j_d} < 0) at byte 8 f0 + 16 f1 + 32 f2
                     const uint4 rc = recs[s];
-                    uint32_t a = (static_cast<uint32_t>(M >> rc.x) & 8u) | tabs;
-                    a |= static_cast<uint32_t>(M >> rc.y) & 16u;
-                    a |= static_cast<uint32_t>(M >> rc.z) & 32u;
+                    uint32_t a = lop3_and_or(static_cast<uint32_t>(M >> rc.x), 8u, tabs);
+                    a = lop3_and_or(static_cast<uint32_t>(M >> rc.y), 16u, a);
+                    a = lop3_and_or(static_cast<uint32_t>(M >> rc.z), 32u, a);
                     c0c = lds_f64(a + s * 64);
                 } else if constexpr (DMAX > 0) {
                     const uint4 r0 = recs[3 * s], r1 = recs[3 * s + 1], r2 = recs[3 * s + 2];
@@ -520,14 +577,14 @@ __global__ void __launch_bounds__(kThreads, 2) sb_batch_kernel(const SamplerPara
     if (p.block_end_ns && (tid & 31) == 0) atomicMax(&p.block_end_ns[blockIdx.x], globaltimer());
 }
 
-template <int NMAX, int LANES, int VAR, int DMAX, bool UDT>
-int launch_batch_u(const SamplerParams& p, long long nblocks, cudaStream_t st)
+template <int NMAX, int LANES, int VAR, int DMAX, bool UDT, int BT, int MINB>
+int launch_batch_c(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
-    using G = BGeo<NMAX, LANES, VAR>;
+    using G = BGeo<NMAX, LANES, VAR, BT>;
     const int csr_bytes = DMAX == 0 ? ((G::kNP + 1) * 4 + 15) / 16 * 16 + p.nnz * 12
                           : (VAR == 1 ? G::kNP * (16 + 64) : G::kNP * 48);
-    const int smem = (G::phi + batch_phi_bytes<NMAX, LANES, VAR, DMAX>() + 15) / 16 * 16 + csr_bytes + 16;
-    auto kern = sb_batch_kernel<NMAX, LANES, VAR, DMAX, UDT>;
+    const int smem = (G::phi + batch_phi_bytes<NMAX, LANES, VAR, DMAX, BT>() + 15) / 16 * 16 + csr_bytes + 16;
+    auto kern = sb_batch_kernel<NMAX, LANES, VAR, DMAX, UDT, BT, MINB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const long long kMaxGrid = 1ll << 30;
@@ -537,11 +594,21 @@ int launch_batch_u(const SamplerParams& p, long long nblocks, cudaStream_t st)
         const long long nb = nblocks - b0 < kMaxGrid ? nblocks - b0 : kMaxGrid;
         q.nan_block = p.nan_block + b0;
         if (p.block_end_ns) q.block_end_ns = p.block_end_ns + b0;
-        kern<<<static_cast<unsigned>(nb), kThreads, smem, st>>>(q);
+        kern<<<static_cast<unsigned>(nb), BT, smem, st>>>(q);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+
+template <int NMAX, int LANES, int VAR, int DMAX, bool UDT>
+int launch_batch_u(const SamplerParams& p, long long nblocks, cudaStream_t st)
+{
+    switch (batch_cta()) {
+        case 1: return launch_batch_c<NMAX, LANES, VAR, DMAX, UDT, kCtaBT[1], kCtaMin[1]>(p, nblocks, st);
+        case 2: return launch_batch_c<NMAX, LANES, VAR, DMAX, UDT, kCtaBT[2], kCtaMin[2]>(p, nblocks, st);
+        default: return launch_batch_c<NMAX, LANES, VAR, DMAX, UDT, kCtaBT[0], kCtaMin[0]>(p, nblocks, st);
+    }
 }
 
 }  // namespace sbimpl
