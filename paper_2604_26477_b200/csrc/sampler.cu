@@ -10,7 +10,7 @@ bool sampler_uses_register_path(int n, double alpha) { return n >= 1 && n <= 64 
 int sampler_block_traj(int n, double alpha)
 {
     if (!sampler_uses_register_path(n, alpha)) return kSampleBlock;
-    return n <= 42 && !sbimpl::force_step_kernel() ? sbimpl::kCtaBT[sbimpl::batch_cta()] / 4 : sbimpl::kThreads / 4;
+    return n <= 42 && !sbimpl::force_step_kernel() ? sbimpl::kBT / 4 : sbimpl::kThreads / 4;
 }
 
 int launch_sampler(const SamplerParams& p, long long nblocks, void* stream)

@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstddef>
 #include <cstdint>
 #include <cstdlib>
 
@@ -40,21 +41,12 @@
 namespace momc_b200 {
 namespace sbimpl {
 
-// CTA shapes of the batch kernel (threads, CTAs per SM): (128, 5) = 20 warps at <= 96
-// registers; (192, 3) = 18 warps at <= 112; (128, 4) = 16 warps at <= 128. Chosen by
-// batch_cta() (MOMC_SB_CTA, default 2: the 96-register shapes spill x / y across the noise
-// phase and measured slower, 7.51 / 7.56 vs 7.31 ms at C2).
-constexpr int kCtaBT[3] = {128, 192, 128};
-constexpr int kCtaMin[3] = {5, 3, 4};
-inline int batch_cta()
-{
-    static const int v = [] {
-        const char* e = std::getenv("MOMC_SB_CTA");
-        const int c = e ? std::atoi(e) : 2;
-        return c >= 0 && c < 3 ? c : 2;
-    }();
-    return v;
-}
+// CTA shape of the batch kernel: 128 threads (32 trajectories), 4 CTAs per SM (123 registers,
+// ~48 KB shared memory each): 16 resident warps. Measured at C2: (128, 5) and (192, 3) force
+// 96 registers and spill x / y across the noise phase (7.51 / 7.56 ms), (192 threads, 112
+// registers) ran 8.33 ms; this shape 7.31 ms.
+constexpr int kBT = 128;
+constexpr int kBMin = 4;
 
 template <int NMAX, int LANES, int VAR, int BT = 128>
 struct BGeo {
@@ -90,34 +82,64 @@ struct BGeo {
     static_assert(kNB * 4 <= kC && kNB * 4 < 64, "generated blocks fit the row and the mask");
 };
 
-// wedge test of rng.hpp:164-168 for the attempt with words u, u1, u2: accept iff
-// fn[iz] + u01 (fn[iz-1] - fn[iz]) < exp(-x^2 / 2); FP32 exp brackets the FP64 one within
-// 1e-6 relative on [-6, 0] and decides unless lhs falls in the +-1e-5 band
-__device__ __forceinline__ bool wedge_accept(uint32_t u, uint32_t u1, uint32_t u2, const double* wn,
-                                             const double* fn)
+// Ziggurat tables of the batch kernel in static shared memory (their addresses are immediates),
+// plus FP32 copies of wn / fn for the wedge and tail brackets.
+struct BatchZig {
+    uint32_t kn[128];
+    double wn[128];
+    double fn[128];
+    float wnf[128];
+    float fnf[128];
+};
+static __shared__ BatchZig g_bz;
+
+// Wedge test of rng.hpp:164-168 for the attempt with words u, u1, u2: accept iff
+// fn[iz] + u01 (fn[iz-1] - fn[iz]) < exp(-x^2 / 2), x = hz wn[iz], in FP64. Decided in FP32
+// unless the two sides are within 4e-5 relative: the FP32 x carries <= 3 roundings (1.8e-7), so
+// -x^2/2 (|.| <= r^2/2 < 6) is off by <= 3e-6 absolute and __expf adds <= 6e-7; the FP32 lhs
+// (u01 truncated to 24 bits, fn rounded) is within 5e-7 relative (adjacent fn within a factor
+// 2.2). Both sides are > 2e-3, so a 4e-5 band leaves a 10x margin.
+__device__ __forceinline__ bool wedge_accept(uint32_t u, uint32_t u1, uint32_t u2)
 {
     const uint32_t iz = u & 127u;
-    const double xv = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), wn[iz]);
-    const double lhs = __dadd_rn(fn[iz], __dmul_rn(u01_from(u1, u2), __dsub_rn(fn[iz - 1], fn[iz])));
-    const double targ = __dmul_rn(__dmul_rn(-0.5, xv), xv);
-    const float ef = __expf(static_cast<float>(targ));
-    if (lhs < static_cast<double>(ef) * (1.0 - 1e-5)) return true;
-    if (lhs > static_cast<double>(ef) * (1.0 + 1e-5)) return false;
-    return lhs < exp(targ);
+    const float xf = __int2float_rn(static_cast<int32_t>(u)) * g_bz.wnf[iz];
+    const float ef = __expf(-0.5f * xf * xf);
+    const float uf = __uint2float_rz(u2 >> 8) * 0x1.0p-24f;  // the top 24 bits of u01, exact
+    const float lf = __fmaf_rn(uf, g_bz.fnf[iz - 1] - g_bz.fnf[iz], g_bz.fnf[iz]);
+    if (lf < ef * (1.0f - 4e-5f)) return true;
+    if (lf > ef * (1.0f + 4e-5f)) return false;
+    const double xv = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), g_bz.wn[iz]);
+    const double lhs =
+        __dadd_rn(g_bz.fn[iz], __dmul_rn(u01_from(u1, u2), __dsub_rn(g_bz.fn[iz - 1], g_bz.fn[iz])));
+    return lhs < exp(__dmul_rn(__dmul_rn(-0.5, xv), xv));
 }
 
-// one tail trial of rng.hpp:172-178 from words a0..a3: returns true (and the value) on accept
+// One tail trial of rng.hpp:172-178 from words a0..a3: true (and the value r + x, signed by
+// hz) on accept. The decision 2y >= x^2 is taken in FP32 unless within 1e-5 relative + 4e-6
+// absolute (__logf of the 53-bit u01 rounded to FP32 is within ~4e-7 absolute); the accepted
+// value is always the FP64 one.
 __device__ __forceinline__ bool tail_trial(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t u,
                                            double& val)
 {
     const double r = 3.442619855899;
-    const double xx = __ddiv_rn(-log(u01_open_from(a0, a1)), r);
-    const double yy = -log(u01_open_from(a2, a3));
-    if (__dadd_rn(yy, yy) >= __dmul_rn(xx, xx)) {
-        val = static_cast<int32_t>(u) > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
-        return true;
+    const uint64_t v1 = (static_cast<uint64_t>(a1) << 32) | a0, v2 = (static_cast<uint64_t>(a3) << 32) | a2;
+    const float xf = -__logf(__ull2float_rn((v1 >> 11) + 1) * 0x1.0p-53f) * (1.0f / 3.442619855899f);
+    const float yf = -__logf(__ull2float_rn((v2 >> 11) + 1) * 0x1.0p-53f);
+    const float lf = yf + yf, rf = xf * xf;
+    const float band = 1e-5f * (lf + rf) + 4e-6f;
+    bool acc;
+    if (lf - rf > band) acc = true;
+    else if (rf - lf > band) acc = false;
+    else {
+        const double xx = __ddiv_rn(-log(u01_open_from(a0, a1)), r);
+        const double yy = -log(u01_open_from(a2, a3));
+        acc = __dadd_rn(yy, yy) >= __dmul_rn(xx, xx);
     }
-    return false;
+    if (acc) {
+        const double xx = __ddiv_rn(-log(u01_open_from(a0, a1)), r);
+        val = static_cast<int32_t>(u) > 0 ? __dadd_rn(r, xx) : -__dadd_rn(r, xx);
+    }
+    return acc;
 }
 
 // Sequential resolution of one stream (the reference's next_normal loop, rng.hpp:156-185) for
@@ -126,7 +148,7 @@ __device__ __forceinline__ bool tail_trial(uint32_t a0, uint32_t a1, uint32_t a2
 // bits into the stream's table (zeroed by the caller). Returns false if the row overflows.
 template <int NQ, int kC>
 __device__ __noinline__ bool seq_resolve(uint32_t* us, uint32_t* wr, int n, uint32_t k0, uint32_t k1, uint32_t lo,
-                                         uint32_t tr, uint32_t wl, const ZigTables* zig)
+                                         uint32_t tr, uint32_t wl)
 {
     uint32_t blk = 0, buf[4];
     int bp = 4;
@@ -149,7 +171,7 @@ __device__ __noinline__ bool seq_resolve(uint32_t* us, uint32_t* wr, int n, uint
         for (;;) {
             const uint32_t u = next();
             const uint32_t iz = u & 127u;
-            if (zmag(u) < zig->kn[iz]) {
+            if (zmag(u) < g_bz.kn[iz]) {
                 us[slot++] = u;
                 break;
             }
@@ -162,12 +184,12 @@ __device__ __noinline__ bool seq_resolve(uint32_t* us, uint32_t* wr, int n, uint
                 us[slot] = static_cast<uint32_t>(__double2hiint(v));
                 us[slot + 1] = static_cast<uint32_t>(__double2loint(v));
                 slot += 2;
-                wb[16 * (i / NQ) + i % NQ] += 4;
+                wb[i + (16 - NQ) * (i / NQ)] += 4;
                 tb[i / NQ] |= static_cast<unsigned short>(1u << (i % NQ));
                 break;
             }
             const uint32_t a = next(), b = next();
-            if (wedge_accept(u, a, b, zig->wn, zig->fn)) {
+            if (wedge_accept(u, a, b)) {
                 us[slot++] = u;
                 break;
             }
@@ -200,7 +222,7 @@ __device__ __forceinline__ double lds_f64(uint32_t a)
 }
 
 template <int NMAX, int LANES, int VAR, int DMAX, bool UDT, int BT, int MINB>
-__global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams p)
+__device__ __forceinline__ void sb_batch_body(const SamplerParams& p)
 {
     using G = BGeo<NMAX, LANES, VAR, BT>;
     constexpr int TPC = G::kTPC;
@@ -208,8 +230,6 @@ __global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams 
     constexpr int NP = G::kNP;
     constexpr int kC = G::kC;
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ ZigTables zig_s;
-    ZigTables* zig = &zig_s;
     uint32_t* wbuf = reinterpret_cast<uint32_t*>(smem + G::words);
     uint32_t* wofs = reinterpret_cast<uint32_t*>(smem + G::wofs);
     unsigned char* phis = smem + G::phi;
@@ -234,9 +254,14 @@ __global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams 
     const int h = tid % LANES;
 
     {  // CTA setup (identical to sb_small_kernel)
+        static_assert(sizeof(ZigTables) == offsetof(BatchZig, wnf), "BatchZig extends ZigTables");
         const uint32_t* src = reinterpret_cast<const uint32_t*>(p.zig);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(zig);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&g_bz);
         for (int i = tid; i < static_cast<int>(sizeof(ZigTables) / 4); i += BT) dst[i] = src[i];
+        for (int i = tid; i < 128; i += BT) {
+            g_bz.wnf[i] = static_cast<float>(p.zig->wn[i]);
+            g_bz.fnf[i] = static_cast<float>(p.zig->fn[i]);
+        }
         if constexpr (DMAX == 0) {
             for (int i = tid; i <= NP; i += BT) rp[i] = p.row_ptr[i < n ? i : n];
             const double* v = p.vals + static_cast<long long>(l) * p.nnz;
@@ -334,8 +359,8 @@ __global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams 
         for (int s = 0; s < NQ; ++s) put_phi(s0 + s, x[s]);
     }
 
-    const uint32_t* kn = zig->kn;
-    const double* wn = zig->wn;
+    const uint32_t* kn = g_bz.kn;
+    const double* wn = g_bz.wn;
     uint32_t* trow = wbuf + t_loc * G::kTS;   // this trajectory's LANES stream rows
     uint32_t* twr = wofs + t_loc * G::kWT;    // and their offset tables
     const uint4* recs = reinterpret_cast<const uint4*>(csr) + s0 * (TAB ? 1 : 3);
@@ -358,7 +383,7 @@ __global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams 
             // stream unless it needs more (P ~ 1e-3 at n = 42: sequential resolution below)
             uint64_t F = 0;
 #pragma unroll 1
-            constexpr int kU = MINB >= 5 ? 2 : G::kNBU;  // blocks per unrolled group
+            constexpr int kU = G::kNBU;  // blocks per unrolled group
             for (int c = 0; c < G::kNB; c += kU) {
                 uint32_t fc = 0;
 #pragma unroll
@@ -395,13 +420,23 @@ __global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams 
                 }
             };
             uint64_t Y = starts(S);
+            uint32_t ylo = static_cast<uint32_t>(Y), yhi = static_cast<uint32_t>(Y >> 32);
 
             unsigned char* wb = reinterpret_cast<unsigned char*>(wr);
             unsigned short* tbits = reinterpret_cast<unsigned short*>(wr + 16);
             int slow = 0;  // words taken by the slow attempts so far beyond their normals
             bool seq = false;
-            while (Y) {
-                const int q = __ffsll(static_cast<long long>(Y)) - 1;
+            for (;;) {
+                int q;  // next attempt start
+                if (ylo) {
+                    q = __ffs(ylo) - 1;
+                    ylo &= ylo - 1;
+                } else if (yhi) {
+                    q = 31 + __ffs(yhi);
+                    yhi &= yhi - 1;
+                } else {
+                    break;
+                }
                 if (q > n - 1 + slow) break;  // the n normals end before this attempt
                 if (q + 2 >= kGen) {
                     seq = true;
@@ -431,20 +466,24 @@ __global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams 
                     d = qq - q - 1;
                     if (i < NP) tbits[i / NQ] |= static_cast<unsigned short>(1u << (i % NQ));
                     Y = qq >= 64 ? 0ull : starts(S & (~0ull << qq));
+                    ylo = static_cast<uint32_t>(Y);
+                    yhi = static_cast<uint32_t>(Y >> 32);
                 } else {
-                    const bool acc = wedge_accept(u, us[q + 1], us[q + 2], wn, zig->fn);
+                    const bool acc = wedge_accept(u, us[q + 1], us[q + 2]);
                     e = acc ? i + 1 : i;
                     d = acc ? 2 : 3;
-                    Y &= Y - 1;
                 }
                 slow += d;
-                if (e < NP) wb[16 * (e / NQ) + e % NQ] += static_cast<unsigned char>(4 * d);
+                if (e < NP) {  // lane-major byte of normal e: 16 (e / NQ) + e % NQ
+                    const uint32_t ue = static_cast<uint32_t>(e);
+                    wb[ue + (16 - NQ) * (ue / NQ)] += static_cast<unsigned char>(4 * d);
+                }
             }
             if (n - 1 + slow >= kGen) seq = true;  // the last normals lie past the generated words
             if (seq) {
 #pragma unroll
                 for (int c = 0; c < G::kWS / 4; ++c) reinterpret_cast<uint4*>(wr)[c] = make_uint4(0u, 0u, 0u, 0u);
-                if (!seq_resolve<NQ, kC>(us, wr, n, k0, k1, lo, tr, wl, zig)) {
+                if (!seq_resolve<NQ, kC>(us, wr, n, k0, k1, lo, tr, wl)) {
                     overflow = true;
                     ovf_code |= 4;
                 }
@@ -494,9 +533,6 @@ __global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams 
             // ---- B: spin updates (sb_step solver.hpp:159-181 / simcim_step :196-210)
 #pragma unroll
             for (int s = 0; s < NQ; ++s) {
-                // loads of the second half are not hoisted above the first half's updates
-                // (register pressure at 5 CTAs per SM)
-                if (MINB >= 5 && s == NQ / 2) asm volatile("" ::: "memory");
                 const uint32_t Wq = s < 4 ? Wv.x : s < 8 ? Wv.y : s < 12 ? Wv.z : Wv.w;
                 const uint32_t boff = __byte_perm(Wq, 0u, 0x4440u + static_cast<uint32_t>(s & 3));
                 const uint32_t* wp =
@@ -578,6 +614,12 @@ __global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams 
 }
 
 template <int NMAX, int LANES, int VAR, int DMAX, bool UDT, int BT, int MINB>
+__global__ void __launch_bounds__(BT, MINB) sb_batch_kernel(const SamplerParams p)
+{
+    sb_batch_body<NMAX, LANES, VAR, DMAX, UDT, BT, MINB>(p);
+}
+
+template <int NMAX, int LANES, int VAR, int DMAX, bool UDT, int BT, int MINB>
 int launch_batch_c(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
     using G = BGeo<NMAX, LANES, VAR, BT>;
@@ -604,11 +646,7 @@ int launch_batch_c(const SamplerParams& p, long long nblocks, cudaStream_t st)
 template <int NMAX, int LANES, int VAR, int DMAX, bool UDT>
 int launch_batch_u(const SamplerParams& p, long long nblocks, cudaStream_t st)
 {
-    switch (batch_cta()) {
-        case 1: return launch_batch_c<NMAX, LANES, VAR, DMAX, UDT, kCtaBT[1], kCtaMin[1]>(p, nblocks, st);
-        case 2: return launch_batch_c<NMAX, LANES, VAR, DMAX, UDT, kCtaBT[2], kCtaMin[2]>(p, nblocks, st);
-        default: return launch_batch_c<NMAX, LANES, VAR, DMAX, UDT, kCtaBT[0], kCtaMin[0]>(p, nblocks, st);
-    }
+    return launch_batch_c<NMAX, LANES, VAR, DMAX, UDT, kBT, kBMin>(p, nblocks, st);
 }
 
 }  // namespace sbimpl
