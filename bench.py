@@ -569,7 +569,7 @@ def main():
     sampling_s = float(np.mean([r["sampling_s"] for r in reps]))
     achieved = ALG_OPS_PER_SAMPLE * (samples_total / world) / sampling_s
     traffic, traffic_src = profile_traffic()
-    roofline = {"bound": "issue", "kernel": "sb_small_kernel<42,4,1,3,true> (SB sampler, dominant)",
+    roofline = {"bound": "issue", "kernel": "sb_batch_kernel<42,4,1,3,true,128,4> (SB sampler, dominant)",
                 "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tlane-op/s",
                 "frac": achieved / peak_ops, "traffic": traffic, "traffic_source": traffic_src,
                 "note": "neither HBM- nor tensor-bound: integer Philox + FP64 update; peak = SMs x 128 lanes "

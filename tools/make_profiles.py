@@ -4,7 +4,7 @@
 
 LAUNCH_CSV : `ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ...
              python tools/profile_step.py` (two C2 steps; the second is summarised)
-NCU_REP    : `ncu --set full --import-source on --clock-control none -k regex:sb_small -c 1
+NCU_REP    : `ncu --set full --import-source on --clock-control none -k regex:sb_batch -c 1
              -o ... python tools/profile_sampler.py dsb`
 """
 import csv
@@ -69,8 +69,8 @@ def sampler(rep, out):
         scale = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(u, 1)
         return m.get(k, 0.0) * scale
     dram = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
-    data = {"kernel": "sb_small_kernel<42,4,1,3,true> (dSB, heavy-hex K=4, 220 x 4546 = 1,000,120 samples)",
-            "source": f"ncu --set full --import-source on --clock-control none -k regex:sb_small -c 1, "
+    data = {"kernel": "sb_batch_kernel<42,4,1,3,true,128,4> (dSB, heavy-hex K=4, 220 x 4546 = 1,000,120 samples)",
+            "source": f"ncu --set full --import-source on --clock-control none -k regex:sb_batch -c 1, "
                       f"python tools/profile_sampler.py dsb ({rep})",
             "metrics": m, "units": {k: units.get(k, "") for k in m},
             "dram_bytes_per_launch": dram, "algorithmic_bytes_per_launch": 8 * 1000120}
