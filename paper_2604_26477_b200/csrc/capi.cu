@@ -1171,7 +1171,7 @@ int momc_b200_stream_step(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, l
             // the HV of an unchanged value set at the same r is the cached one
             const std::vector<double> rv(r, r + ctx->k);
             if (changed || rv != ctx->running_hv_ref) {
-                ctx->running_hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, rv);
+                ctx->running_hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, rv, true);
                 ctx->running_hv_ref = rv;
             }
             *hv = ctx->running_hv;
@@ -1194,7 +1194,7 @@ int momc_b200_running_merge_values(momc_ctx* ctx, const double* d_vals, const ui
             const std::vector<double> rv(r, r + k);
             if (changed || rv != ctx->running_hv_ref) {
                 const DevArchive& R = running_archive(*ctx);
-                ctx->running_hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, rv);
+                ctx->running_hv = hypervolume_device(*ctx, R.vals.p, R.F, R.K, rv, true);
                 ctx->running_hv_ref = rv;
             }
             *hv = ctx->running_hv;
@@ -1315,7 +1315,7 @@ int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t
         }
         const auto th = clk::now();
         rep->reference_s = std::chrono::duration<double>(th - tr).count();
-        rep->hv = hypervolume_device(*ctx, a.vals.p, a.F, a.K, r);
+        rep->hv = hypervolume_device(*ctx, a.vals.p, a.F, a.K, r, true);
         const auto te = clk::now();
         rep->hv_s = std::chrono::duration<double>(te - th).count();
         for (int l = 0; l < ctx->k && l < 16; ++l) rep->reference[l] = r[static_cast<size_t>(l)];
@@ -1375,7 +1375,7 @@ int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long
             }
             const auto th = clk::now();
             rep->reference_s = std::chrono::duration<double>(th - tr).count();
-            rep->hv = hypervolume_device(*ctx, a.vals.p, a.F, a.K, r);
+            rep->hv = hypervolume_device(*ctx, a.vals.p, a.F, a.K, r, true);
             rep->hv_s = std::chrono::duration<double>(clk::now() - th).count();
             for (int l = 0; l < ctx->k && l < 16; ++l) rep->reference[l] = r[static_cast<size_t>(l)];
         }

@@ -165,6 +165,13 @@ struct Ctx {
     double running_hv = 0.0;                      // its HV at running_hv_ref (cached)
     std::vector<double> running_hv_ref;
     bool skip_order = false;                      // fronts for internal use: no archive order
+    // the compressed grid in pareto_scratch (built by the front of the last filter) covers the
+    // archive at (grid_archive, grid_rows): its dominated region is the archive's, so the
+    // hypervolume reuses it instead of rebuilding one (pareto.cu); any other grid build bumps
+    // grid_gen and invalidates it
+    unsigned long long grid_gen = 0, front_grid_gen = ~0ull;
+    const double* grid_archive = nullptr;
+    long long grid_rows = -1;
     KernelTimer ktimer;                           // optional per-kernel-class device times
 
     ~Ctx();

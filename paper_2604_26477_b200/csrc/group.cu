@@ -457,7 +457,7 @@ int momc_b200_group_bench(momc_group* g, const momc_instance_view* inst, const i
         else r = reference_point_sampled_device(root, ref_count, cfg->seed, a.vals.p, a.F);
         const auto th = clk::now();
         rep->reference_s = std::chrono::duration<double>(th - tr).count();
-        rep->hv = hypervolume_device(root, a.vals.p, a.F, a.K, r);
+        rep->hv = hypervolume_device(root, a.vals.p, a.F, a.K, r, true);
         const auto te = clk::now();
         rep->hv_s = std::chrono::duration<double>(te - th).count();
         for (int l = 0; l < root.k && l < 16; ++l) rep->reference[l] = r[static_cast<size_t>(l)];

@@ -525,36 +525,56 @@ __global__ void k_col_min(const double* __restrict__ vals, long long rows, int K
         atomicMin(&rmin[i % K], dkey(vals[i]));
 }
 
-// ---- K8: hypervolume over the compressed grid of the front (gains g = v - r)
+// ---- K8: hypervolume over a compressed grid (gains g = v - r). One warp per line of the
+// innermost grid axis: the other axes' widths are a per-line product, the lanes stride the
+// line's cells (coalesced S loads). Widths are clamped at r, so a grid built over more vectors
+// than the archive (the front's grid over every distinct vector, whose dominated region is the
+// archive's) gives the same exact value; over the archive's own grid (values >= r) the clamp is
+// the identity. Both sums are formed: the exact __int128 one (valid when every gain is an
+// integer, decided on the host from k_hv_stats) and the Kahan FP64 one.
 __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, GridGeo g, const double* __restrict__ r,
-                           bool integral, __int128* ipart, double* dpart, double* dcomp)
+                           __int128* ipart, double* dpart)
 {
+    const int lane = threadIdx.x & 31;
+    const int da = g.dims - 1;  // the innermost grid axis (stride 1)
+    const long long len = g.D[da];
+    const long long lines = cells / len;
+    const long long warps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     __int128 iacc = 0;
     double dacc = 0.0, dc = 0.0;
-    for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < cells;
-         c += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const uint32_t top = S[c];
-        if (!top) continue;
-        const double hgain = g.axis[g.dims][top - 1] - r[g.dims];
-        if (!(hgain > 0.0)) continue;
-        long long rem = c;
-        if (integral) {
-            __int128 vol = static_cast<long long>(hgain);
-            for (int a = 0; a < g.dims; ++a) {
-                const int ra = static_cast<int>(rem / g.stride[a]);
-                rem -= ra * g.stride[a];
-                const double lo = ra ? g.axis[a][ra - 1] : r[a];
-                vol *= static_cast<long long>(g.axis[a][ra] - lo);
-            }
-            iacc += vol;
-        } else {
-            double vol = hgain;
-            for (int a = 0; a < g.dims; ++a) {
-                const int ra = static_cast<int>(rem / g.stride[a]);
-                rem -= ra * g.stride[a];
-                const double lo = ra ? g.axis[a][ra - 1] : r[a];
-                vol *= g.axis[a][ra] - lo;
-            }
+    const double rl = r[g.dims];
+    for (long long line = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; line < lines;
+         line += warps) {
+        // widths of the outer axes of this line
+        long long rem = line * len;
+        double pw = 1.0;
+        long long pwi = 1;
+        bool empty = false;
+        for (int a = 0; a < da; ++a) {
+            const long long ra = rem / g.stride[a];
+            rem -= ra * g.stride[a];
+            const double lo = fmax(ra ? g.axis[a][ra - 1] : r[a], r[a]);
+            const double w = g.axis[a][ra] - lo;
+            if (!(w > 0.0)) empty = true;
+            pw *= w;
+            pwi *= static_cast<long long>(w);
+        }
+        if (empty) continue;
+        const double* ax = g.axis[da];
+        const double rd = r[da];
+        const uint32_t* Sl = S + line * len;
+        for (long long q = lane; q < len; q += 32) {
+            const uint32_t top = Sl[q];
+            if (!top) continue;
+            const double hgain = g.axis[g.dims][top - 1] - rl;
+            if (!(hgain > 0.0)) continue;
+            const double w = ax[q] - fmax(q ? ax[q - 1] : rd, rd);
+            if (!(w > 0.0)) continue;
+            __int128 ivol = pwi;
+            ivol *= static_cast<long long>(w);
+            ivol *= static_cast<long long>(hgain);
+            iacc += ivol;
+            const double vol = hgain * pw * w;
             const double y = vol - dc;  // Kahan
             const double t = dacc + y;
             dc = (t - dacc) - y;
@@ -575,7 +595,6 @@ __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, Grid
         }
         ipart[blockIdx.x] = a;
         dpart[blockIdx.x] = b;
-        (void)dcomp;
     }
 }
 
@@ -651,6 +670,8 @@ struct Scratch {
     DevBuf<long long> rank;
     DevBuf<__int128> ipart;
     DevBuf<double> dpart;
+    GridGeo front_geo{};        // the grid of the last filter's front (see Ctx::grid_gen)
+    long long front_cells = 0;
 };
 Scratch& scratch(Ctx& c)
 {
@@ -678,6 +699,7 @@ bool build_grid(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, Gr
                 std::vector<std::vector<double>>* host_axes = nullptr)
 {
     g.dims = K - 1;
+    ++c.grid_gen;
     const uint64_t tsize = pow2_at_least(2ull * static_cast<uint64_t>(V) + 16);
     // the K axes' distinct values in one pass of launches and one read-back (tables and
     // counters per axis; counters from slot 8 on)
@@ -901,6 +923,8 @@ int front_keep(Ctx& c, Scratch& s, const double* d_vals, long long V, int K)
         if (build_grid(c, s, d_vals, V, K, g, cells)) {
             k_grid_test<<<grid_blocks(V), 256, 0, c.stream>>>(d_vals, V, K, g, s.T.p, s.S.p, s.keep.p);
             c.launches++;
+            s.front_geo = g;
+            s.front_cells = cells;
             return 1;
         }
     }
@@ -1078,6 +1102,11 @@ void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, 
                                                          d_own ? out.words.p : nullptr);
     c.launches++;
     cudaEventRecord(e2, c.stream);
+    if (method == 1) {  // the front's grid covers this archive (hypervolume_device)
+        c.front_grid_gen = c.grid_gen;
+        c.grid_archive = out.vals.p;
+        c.grid_rows = F;
+    }
     ck(cudaStreamSynchronize(c.stream), "archive");
     if (tm) {
         tm->front_s = seconds_between(e0, e1);
@@ -1356,7 +1385,8 @@ std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t s
     return r;
 }
 
-double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, const std::vector<double>& r)
+double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, const std::vector<double>& r,
+                          bool reuse_front_grid)
 {
     if (F <= 0) usage("hypervolume of an empty archive");
     if (static_cast<int>(r.size()) != K) usage("reference point length does not match archive");
@@ -1366,31 +1396,31 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
     s.counters.reserve(8);
     ck(cudaMemcpyAsync(s.rdev.p, r.data(), sizeof(double) * K, cudaMemcpyHostToDevice, c.stream), "H2D");
     const unsigned long long none = ~0ull;
-    ck(cudaMemcpyAsync(s.counters.p + 3, &none, sizeof none, cudaMemcpyHostToDevice, c.stream), "H2D");
-    const unsigned long long stats_init[2] = {~0ull, dkey(0.0)};
-    ck(cudaMemcpyAsync(s.counters.p + 4, stats_init, sizeof stats_init, cudaMemcpyHostToDevice, c.stream), "H2D");
+    const unsigned long long init[3] = {none, ~0ull, dkey(0.0)};
+    ck(cudaMemcpyAsync(s.counters.p + 3, init, sizeof init, cudaMemcpyHostToDevice, c.stream), "H2D");
     k_ref_check<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, F, K, s.rdev.p, s.counters.p + 3);
     // gains are exact integers when every value and r is integral (n=42 configs): then the
     // __int128 cell sum is the exact hypervolume, i.e. the reference's exact double result
     k_hv_stats<<<grid_blocks(F * K), 256, 0, c.stream>>>(d_vals, F, K, s.rdev.p, s.counters.p + 4);
     c.launches += 2;
-    unsigned long long st[3];
-    ck(cudaMemcpyAsync(st, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
-    ck(cudaStreamSynchronize(c.stream), "sync");
-    const unsigned long long bad = st[0];
-    if (bad != none)
-        usage("reference point not dominated by archive entry " + std::to_string(bad / K) + " (objective " +
-              std::to_string(bad % K) + ")");
-    bool integral = st[1] != 0;
-    double maxg;
-    {
+    auto finish_checks = [&](const unsigned long long* st, bool& integral) {
+        if (st[0] != none)
+            usage("reference point not dominated by archive entry " + std::to_string(st[0] / K) + " (objective " +
+                  std::to_string(st[0] % K) + ")");
+        integral = st[1] != 0;
+        double maxg;
         const uint64_t key = st[2];
         const uint64_t b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
         std::memcpy(&maxg, &b, 8);
-    }
-    for (int k = 0; k < K; ++k) integral &= std::floor(r[static_cast<size_t>(k)]) == r[static_cast<size_t>(k)];
-    if (integral && K * std::log2(std::max(maxg, 1.0)) > 120.0) integral = false;  // keep __int128 exact
+        for (int k = 0; k < K; ++k) integral &= std::floor(r[static_cast<size_t>(k)]) == r[static_cast<size_t>(k)];
+        if (integral && K * std::log2(std::max(maxg, 1.0)) > 120.0) integral = false;  // keep __int128 exact
+    };
     if (K == 1) {
+        unsigned long long st[3];
+        ck(cudaMemcpyAsync(st, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+        bool integral;
+        finish_checks(st, integral);
         double best = 0;  // pareto.hpp:544-548
         std::vector<double> hv(static_cast<size_t>(F));
         ck(cudaMemcpyAsync(hv.data(), d_vals, sizeof(double) * F, cudaMemcpyDeviceToHost, c.stream), "D2H");
@@ -1400,19 +1430,29 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
     }
     GridGeo g{};
     long long cells = 0;
-    if (!build_grid(c, s, d_vals, F, K, g, cells))
+    if (reuse_front_grid && c.front_grid_gen == c.grid_gen && c.grid_archive == d_vals && c.grid_rows == F) {
+        g = s.front_geo;  // built over every distinct vector of the pool: the same dominated region
+        cells = s.front_cells;
+    } else if (!build_grid(c, s, d_vals, F, K, g, cells)) {
         runtime("hypervolume: front too large for the compressed-grid method (" + std::to_string(F) + " points)");
-    const int blocks = grid_blocks(cells);
+    }
+    const long long lines = cells / g.D[g.dims - 1];
+    const int blocks = grid_blocks(lines * 32);
     s.ipart.reserve(static_cast<size_t>(blocks));
     s.dpart.reserve(static_cast<size_t>(blocks));
-    k_hv_cells<<<blocks, 256, 0, c.stream>>>(s.S.p, cells, g, s.rdev.p, integral, s.ipart.p, s.dpart.p, nullptr);
+    // both sums (the integral one is exact only when the checks below say so): one read-back
+    k_hv_cells<<<blocks, 256, 0, c.stream>>>(s.S.p, cells, g, s.rdev.p, s.ipart.p, s.dpart.p);
     c.launches++;
     ck(cudaGetLastError(), "hv");
     std::vector<__int128> ip(static_cast<size_t>(blocks));
     std::vector<double> dp(static_cast<size_t>(blocks));
+    unsigned long long st[3];
+    ck(cudaMemcpyAsync(st, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
     ck(cudaMemcpyAsync(ip.data(), s.ipart.p, sizeof(__int128) * blocks, cudaMemcpyDeviceToHost, c.stream), "D2H");
     ck(cudaMemcpyAsync(dp.data(), s.dpart.p, sizeof(double) * blocks, cudaMemcpyDeviceToHost, c.stream), "D2H");
     ck(cudaStreamSynchronize(c.stream), "hv");
+    bool integral;
+    finish_checks(st, integral);
     if (integral) {
         __int128 tot = 0;
         for (auto v : ip) tot += v;

@@ -54,6 +54,9 @@ std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t s
 
 // hypervolume (pareto.hpp:540-552) of F x K values (device) against r (host); validates r
 // (pareto.hpp:103-118) and throws the reference's messages.
-double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, const std::vector<double>& r);
+// reuse_front_grid: the archive is the output of the last filter on this context, whose front
+// grid (if the grid method ran and nothing rebuilt a grid since) covers it
+double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, const std::vector<double>& r,
+                          bool reuse_front_grid = false);
 
 }  // namespace momc_b200
