@@ -37,6 +37,7 @@ Ctx::~Ctx()
     if (ev_dep) cudaEventDestroy(ev_dep);
     if (sample_stream) cudaStreamDestroy(sample_stream);
     if (stream) cudaStreamDestroy(stream);
+    if (pinned) cudaFreeHost(pinned);
 }
 
 DevArchive& resident_archive(Ctx& c)

@@ -169,6 +169,10 @@ struct Ctx {
     // archive at (grid_archive, grid_rows): its dominated region is the archive's, so the
     // hypervolume reuses it instead of rebuilding one (pareto.cu); any other grid build bumps
     // grid_gen and invalidates it
+    // page-locked staging for the small host <-> device transfers of the Pareto stage (a
+    // pageable cudaMemcpyAsync stages through a driver buffer and blocks); see pinned_buf()
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
     unsigned long long grid_gen = 0, front_grid_gen = ~0ull;
     const double* grid_archive = nullptr;
     long long grid_rows = -1;
@@ -176,6 +180,24 @@ struct Ctx {
 
     ~Ctx();
 };
+
+// At least `bytes` of ctx's page-locked staging buffer (grown on demand; contents not kept).
+inline void* pinned_buf(Ctx& c, size_t bytes)
+{
+    if (c.pinned_bytes < bytes) {
+        if (c.pinned) {
+            cudaStreamSynchronize(c.stream);
+            cudaFreeHost(c.pinned);
+            c.pinned = nullptr;
+            c.pinned_bytes = 0;
+        }
+        size_t b = 256 * 1024;
+        while (b < bytes) b <<= 1;
+        if (cudaMallocHost(&c.pinned, b) != cudaSuccess) throw std::runtime_error("cudaMallocHost failed");
+        c.pinned_bytes = b;
+    }
+    return c.pinned;
+}
 
 // Makes ctx's device current and its stream the allocation stream of this thread.
 inline void bind(Ctx& c)

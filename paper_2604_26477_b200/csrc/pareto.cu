@@ -97,6 +97,153 @@ __device__ __forceinline__ void warp_append(bool flag, uint32_t value, uint32_t*
     if (flag) out[base + __popc(b & ((1u << lane) - 1))] = value;
 }
 
+// warp_append that returns each flagged lane's slot (undefined for the others)
+__device__ __forceinline__ unsigned long long warp_append_index(bool flag, unsigned long long* count)
+{
+    const unsigned mask = __activemask();
+    const unsigned b = __ballot_sync(mask, flag);
+    if (!b) return 0;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(b) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(count, static_cast<unsigned long long>(__popc(b)));
+    base = __shfl_sync(mask, base, leader);
+    return base + __popc(b & ((1u << lane) - 1));
+}
+
+// ---- K5+K4+K6 fused, one word per config, n <= 63, integer weights (the C1 / C2 pools):
+// dedup on the config words themselves (64-bit keys, empty = ~0, which no n <= 63 config
+// equals), the cut values of each fresh config (exact int32, instance.hpp:183-194) evaluated
+// by the thread that inserted it, then the value vector collapsed (table of rows into vals,
+// pareto.hpp:383-387) with the lexicographically smallest config kept by a 64-bit atomicMin
+// on the bit-reversed word (config_less order). Counts in cnt[0] (unique configs) and cnt[2]
+// (distinct vectors); reps lists the distinct vectors' slots. The vals row is written and
+// fenced before it is published in t2; readers go through L2 (__ldcg).
+// shared-memory edge table of the fused kernel: per edge one int (ei | ej << 16) and KM
+// weights (KM = 2, 4, 8 or 16 >= K, padded with zeros; 16-byte rows for KM >= 4)
+template <int KM>
+__device__ __forceinline__ void cut_values_int(uint64_t w, int m, const int* __restrict__ epair,
+                                               const int* __restrict__ ew, int (&acc)[KM])
+{
+#pragma unroll
+    for (int k = 0; k < KM; ++k) acc[k] = 0;
+    for (int e = 0; e < m; ++e) {
+        const int pr = epair[e];
+        const uint64_t d = (w >> (pr & 0xFFFF)) ^ (w >> (pr >> 16));
+        const int cut = -static_cast<int>(d & 1ull);
+        if constexpr (KM >= 4) {
+#pragma unroll
+            for (int k = 0; k < KM; k += 4) {
+                const int4 q = *reinterpret_cast<const int4*>(ew + e * KM + k);
+                acc[k] += q.x & cut;
+                acc[k + 1] += q.y & cut;
+                acc[k + 2] += q.z & cut;
+                acc[k + 3] += q.w & cut;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < KM; ++k) acc[k] += ew[e * KM + k] & cut;
+        }
+    }
+}
+
+template <int KM>
+__global__ void __launch_bounds__(256) k_dedup_eval_collapse(
+    const uint64_t* __restrict__ words, long long M, int m, int K, const int* __restrict__ ei,
+    const int* __restrict__ ej, const int* __restrict__ wi, unsigned long long* t1, uint64_t m1, uint32_t* t2,
+    unsigned long long* own, uint64_t m2, double* vals, uint32_t* reps, unsigned long long* cnt)
+{
+    extern __shared__ __align__(16) int sm[];  // weights (m x KM) | edge pairs (m)
+    int* ew = sm;
+    int* epair = sm + m * KM;
+    for (int e = threadIdx.x; e < m; e += blockDim.x) epair[e] = ei[e] | (ej[e] << 16);
+    for (int q = threadIdx.x; q < m * KM; q += blockDim.x) {
+        const int e = q / KM, k = q % KM;
+        ew[q] = k < K ? wi[e * K + k] : 0;
+    }
+    __syncthreads();
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x); i0 < M;
+         i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        bool fresh = false;
+        uint64_t w = 0;
+        if (i < M) {
+            w = words[i];
+            uint64_t h = mix64(w) & m1;
+            for (;;) {
+                const unsigned long long old = atomicCAS(&t1[h], ~0ull, static_cast<unsigned long long>(w));
+                if (old == ~0ull) {
+                    fresh = true;
+                    break;
+                }
+                if (old == w) break;
+                h = (h + 1) & m1;
+            }
+        }
+        const unsigned long long u = warp_append_index(fresh, cnt);
+        bool vfresh = false;
+        uint32_t slot = 0;
+        if (fresh) {
+            int acc[KM];
+            cut_values_int<KM>(w, m, epair, ew, acc);
+            double v[KM];
+#pragma unroll
+            for (int k = 0; k < KM; ++k)
+                if (k < K) {
+                    v[k] = static_cast<double>(acc[k]);
+                    vals[u * K + k] = v[k];
+                }
+            __threadfence();
+            uint64_t hv = 0x243F6A8885A308D3ull;
+#pragma unroll
+            for (int k = 0; k < KM; ++k)
+                if (k < K) hv ^= mix64(dkey(v[k]) + hv);
+            hv &= m2;
+            for (;;) {
+                const uint32_t sidx = atomicCAS(&t2[hv], kEmpty, static_cast<uint32_t>(u));
+                if (sidx == kEmpty) {
+                    vfresh = true;
+                    break;
+                }
+                bool eq = true;
+#pragma unroll
+                for (int k = 0; k < KM; ++k)
+                    if (k < K) eq &= __ldcg(vals + static_cast<long long>(sidx) * K + k) == v[k];
+                if (eq) break;
+                hv = (hv + 1) & m2;
+            }
+            atomicMin(&own[hv], static_cast<unsigned long long>(__brevll(w)));
+            slot = static_cast<uint32_t>(hv);
+        }
+        warp_append(vfresh, slot, reps, cnt + 2);
+    }
+}
+
+// distinct vectors of the fused path -> (row into vals, lex-min config word, identity owner)
+__global__ void k_slots_fused(const uint32_t* __restrict__ reps, const unsigned long long* __restrict__ dV,
+                              const uint32_t* __restrict__ t2, const unsigned long long* __restrict__ own,
+                              uint32_t* rows, uint64_t* cfg, uint32_t* ident)
+{
+    const long long V = static_cast<long long>(*dV);
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const uint32_t sl = reps[i];
+        rows[i] = t2[sl];
+        cfg[i] = __brevll(own[sl]);
+        ident[i] = static_cast<uint32_t>(i);
+    }
+}
+
+// k_gather_vals with the row count on the device
+__global__ void k_gather_vals_dev(const double* __restrict__ src, const uint32_t* __restrict__ rows,
+                                  const unsigned long long* __restrict__ dV, int K, double* dst)
+{
+    const long long n = static_cast<long long>(*dV) * K;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        dst[i] = src[static_cast<long long>(rows[i / K]) * K + i % K];
+}
+
 // ---- K5: dedup of packed configs (pareto.hpp:309-326)
 __global__ void k_dedup(const uint64_t* __restrict__ words, long long M, int wpc, uint32_t* table, uint64_t tmask,
                         uint32_t* uniq, unsigned long long* ucount)
@@ -249,17 +396,33 @@ __global__ void k_collapse(const double* __restrict__ vals, long long U, int K, 
     }
 }
 
-// ---- distinct values of one axis (hash set of keys), then ascending order by rank count
-__global__ void k_distinct(const double* __restrict__ vals, long long V, int K, int axis, unsigned long long* table,
-                           uint64_t tmask, double* out, unsigned long long* count, long long cap)
+// ---- distinct values of every axis (blockIdx.y = axis; hash set of keys per axis), then
+// ascending order by rank count. The row count is *dV when given. A full table (more
+// distinct values than it holds) stops probing and reports count > cap (no grid).
+__global__ void k_distinct(const double* __restrict__ vals, long long V, const unsigned long long* __restrict__ dV,
+                           int K, unsigned long long* tables, uint64_t tsize, double* outs, unsigned long long* counts,
+                           long long cap)
 {
+    const int axis = blockIdx.y;
+    if (dV) V = static_cast<long long>(*dV);
+    unsigned long long* table = tables + tsize * axis;
+    double* out = outs + cap * axis;
+    unsigned long long* count = counts + axis;
+    const uint64_t tmask = tsize - 1;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const double v = vals[i * K + axis];
         const unsigned long long key = dkey(v);
         uint64_t h = mix64(key) & tmask;
-        for (;;) {
-            unsigned long long s = atomicCAS(&table[h], 0ull, key);
+        for (uint64_t probe = 0;; ++probe) {
+            if (probe > tmask) {  // full: more distinct values than any grid takes
+                atomicMax(count, static_cast<unsigned long long>(cap) + 1);
+                break;
+            }
+            // a plain read first: most rows repeat one of the few values already present
+            unsigned long long s = __ldcg(&table[h]);
+            if (s == key) break;
+            if (s == 0ull) s = atomicCAS(&table[h], 0ull, key);
             if (s == 0ull) {
                 const unsigned long long at = atomicAdd(count, 1ull);
                 if (static_cast<long long>(at) < cap) out[at] = v + 0.0;
@@ -271,9 +434,20 @@ __global__ void k_distinct(const double* __restrict__ vals, long long V, int K, 
     }
 }
 
-__global__ void k_rank_sort_asc(const double* __restrict__ in, int D, double* out)
-{  // distinct values: rank = #smaller
+struct RPoint {  // the reference point, by value
+    double v[kMaxK];
+};
+
+struct AxisCounts {
+    int d[kMaxK];
+};
+
+__global__ void k_rank_sort_asc(const double* __restrict__ ins, AxisCounts Ds, long long cap, double* outs)
+{  // distinct values: rank = #smaller (blockIdx.y = axis)
     extern __shared__ double tile[];
+    const int D = Ds.d[blockIdx.y];
+    const double* in = ins + cap * blockIdx.y;
+    double* out = outs + cap * blockIdx.y;
     for (int base = blockIdx.x * blockDim.x; base < D; base += gridDim.x * blockDim.x) {
         const int i = base + threadIdx.x;
         const double v = i < D ? in[i] : 0.0;
@@ -532,7 +706,7 @@ __global__ void k_col_min(const double* __restrict__ vals, long long rows, int K
 // archive's) gives the same exact value; over the archive's own grid (values >= r) the clamp is
 // the identity. Both sums are formed: the exact __int128 one (valid when every gain is an
 // integer, decided on the host from k_hv_stats) and the Kahan FP64 one.
-__global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, GridGeo g, const double* __restrict__ r,
+__global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, GridGeo g, const RPoint rp,
                            __int128* ipart, double* dpart)
 {
     const int lane = threadIdx.x & 31;
@@ -542,17 +716,19 @@ __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, Grid
     const long long warps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     __int128 iacc = 0;
     double dacc = 0.0, dc = 0.0;
+    const double* r = rp.v;
     const double rl = r[g.dims];
     for (long long line = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; line < lines;
          line += warps) {
-        // widths of the outer axes of this line
-        long long rem = line * len;
+        // widths of the outer axes of this line (cells < 2^27: 32-bit index arithmetic)
+        uint32_t rem = static_cast<uint32_t>(line * len);
         double pw = 1.0;
         long long pwi = 1;
         bool empty = false;
         for (int a = 0; a < da; ++a) {
-            const long long ra = rem / g.stride[a];
-            rem -= ra * g.stride[a];
+            const uint32_t sa = static_cast<uint32_t>(g.stride[a]);
+            const uint32_t ra = rem / sa;
+            rem -= ra * sa;
             const double lo = fmax(ra ? g.axis[a][ra - 1] : r[a], r[a]);
             const double w = g.axis[a][ra] - lo;
             if (!(w > 0.0)) empty = true;
@@ -598,9 +774,10 @@ __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, Grid
     }
 }
 
-__global__ void k_ref_check(const double* __restrict__ vals, long long F, int K, const double* __restrict__ r,
+__global__ void k_ref_check(const double* __restrict__ vals, long long F, int K, const RPoint rp,
                             unsigned long long* first)
 {
+    const double* r = rp.v;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
         for (int k = 0; k < K; ++k)
@@ -609,9 +786,10 @@ __global__ void k_ref_check(const double* __restrict__ vals, long long F, int K,
 
 // integrality of the archive values and the largest gain v - r (decides the exact __int128 HV
 // sum): flags[0] &= every value is an integer below 9e15, flags[1] = max dkey(gain)
-__global__ void k_hv_stats(const double* __restrict__ vals, long long F, int K, const double* __restrict__ r,
+__global__ void k_hv_stats(const double* __restrict__ vals, long long F, int K, const RPoint rp,
                            unsigned long long* flags)
 {
+    const double* r = rp.v;
     bool integral = true;
     unsigned long long gmax = dkey(0.0);
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F * K;
@@ -663,7 +841,7 @@ double seconds_between(cudaEvent_t a, cudaEvent_t b)
 // scratch reused across calls
 struct Scratch {
     DevBuf<uint32_t> table, uniq, table2, owner, reps, rows, cfgrows;
-    DevBuf<unsigned long long> counters, dtable;
+    DevBuf<unsigned long long> counters, dtable, dtab64;
     DevBuf<double> vals, axisbuf, axis_sorted, rdev;
     DevBuf<uint32_t> T, S;
     DevBuf<unsigned char> keep;
@@ -680,6 +858,7 @@ Scratch& scratch(Ctx& c)
         s->table.release(); s->uniq.release(); s->table2.release(); s->owner.release(); s->reps.release();
         s->rows.release(); s->cfgrows.release(); s->counters.release(); s->dtable.release(); s->vals.release();
         s->axisbuf.release(); s->axis_sorted.release(); s->rdev.release(); s->T.release(); s->S.release();
+        s->dtab64.release();
         s->keep.release(); s->rank.release(); s->ipart.release(); s->dpart.release();
         delete s;
     });
@@ -688,55 +867,61 @@ Scratch& scratch(Ctx& c)
 
 unsigned long long read_counter(Ctx& c, unsigned long long* d)
 {
-    unsigned long long h = 0;
-    ck(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    auto* h = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long)));
+    ck(cudaMemcpyAsync(h, d, sizeof *h, cudaMemcpyDeviceToHost, c.stream), "D2H");
     ck(cudaStreamSynchronize(c.stream), "sync");
-    return h;
+    return *h;
 }
 
-// Builds the compressed grid over V vectors (K >= 2). Returns false when it would not fit.
-bool build_grid(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, GridGeo& g, long long& cells,
-                std::vector<std::vector<double>>* host_axes = nullptr)
+// Compressed grid over V vectors (K >= 2), in two phases around the one read-back of the
+// per-axis distinct counts. grid_distinct: the distinct values of every axis (V rows, or *dV
+// rows when dV is given; Vcap bounds them), counts at counters[8 .. 8+K).
+void grid_distinct(Ctx& c, Scratch& s, const double* d_vals, long long Vcap, const unsigned long long* dV, int K)
 {
-    g.dims = K - 1;
     ++c.grid_gen;
-    const uint64_t tsize = pow2_at_least(2ull * static_cast<uint64_t>(V) + 16);
-    // the K axes' distinct values in one pass of launches and one read-back (tables and
-    // counters per axis; counters from slot 8 on)
+    const uint64_t tsize =
+        pow2_at_least(2ull * static_cast<uint64_t>(std::min<long long>(Vcap, kDistinctCap)) + 16);
     s.dtable.reserve(tsize * K);
     s.axisbuf.reserve(static_cast<size_t>(kDistinctCap) * K);
     s.axis_sorted.reserve(static_cast<size_t>(kDistinctCap) * K);
     s.counters.reserve(8 + kMaxK);
     ck(cudaMemsetAsync(s.dtable.p, 0, sizeof(unsigned long long) * tsize * K, c.stream), "memset");
     ck(cudaMemsetAsync(s.counters.p + 8, 0, sizeof(unsigned long long) * K, c.stream), "memset");
-    for (int a = 0; a < K; ++a) {
-        k_distinct<<<grid_blocks(V), 256, 0, c.stream>>>(d_vals, V, K, a, s.dtable.p + tsize * a, tsize - 1,
-                                                           s.axisbuf.p + static_cast<size_t>(kDistinctCap) * a,
-                                                           s.counters.p + 8 + a, kDistinctCap);
-        c.launches++;
-    }
-    std::vector<unsigned long long> dcount(static_cast<size_t>(K));
-    ck(cudaMemcpyAsync(dcount.data(), s.counters.p + 8, sizeof(unsigned long long) * K, cudaMemcpyDeviceToHost,
-                       c.stream),
-       "D2H");
-    ck(cudaStreamSynchronize(c.stream), "sync");
+    k_distinct<<<dim3(grid_blocks(Vcap), K), 256, 0, c.stream>>>(d_vals, Vcap, dV, K, s.dtable.p, tsize, s.axisbuf.p,
+                                                                 s.counters.p + 8, kDistinctCap);
+    c.launches++;
+}
+
+// grid_finish: with the distinct counts on the host, sort the axes and build the cell table
+// T (max last-axis rank + 1 per cell) and its suffix max S. Returns false when it would not fit.
+bool grid_finish(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, const unsigned long long* dcount,
+                 GridGeo& g, long long& cells, std::vector<std::vector<double>>* host_axes = nullptr)
+{
+    g.dims = K - 1;
     long long prod = 1;
+    AxisCounts dc{};
+    int maxD = 1;
     for (int a = 0; a < K; ++a) {
-        const long long D = static_cast<long long>(dcount[static_cast<size_t>(a)]);
+        const long long D = static_cast<long long>(dcount[a]);
         if (D > kDistinctCap) return false;
         g.D[a] = static_cast<int>(D);
-        double* sorted = s.axis_sorted.p + static_cast<size_t>(a) * kDistinctCap;
-        k_rank_sort_asc<<<grid_blocks(D, 256), 256, 256 * sizeof(double), c.stream>>>(
-            s.axisbuf.p + static_cast<size_t>(kDistinctCap) * a, static_cast<int>(D), sorted);
-        c.launches++;
-        g.axis[a] = sorted;
+        dc.d[a] = static_cast<int>(D);
+        maxD = std::max(maxD, static_cast<int>(D));
+        g.axis[a] = s.axis_sorted.p + static_cast<size_t>(a) * kDistinctCap;
         if (a < K - 1) {
             prod *= D;
             if (prod > kGridCap) return false;
         }
-        if (host_axes) {
-            std::vector<double> hv(static_cast<size_t>(D));
-            ck(cudaMemcpyAsync(hv.data(), sorted, sizeof(double) * D, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    }
+    k_rank_sort_asc<<<dim3(grid_blocks(maxD, 256), K), 256, 256 * sizeof(double), c.stream>>>(s.axisbuf.p, dc,
+                                                                                             kDistinctCap,
+                                                                                             s.axis_sorted.p);
+    c.launches++;
+    if (host_axes) {
+        for (int a = 0; a < K; ++a) {
+            std::vector<double> hv(static_cast<size_t>(g.D[a]));
+            ck(cudaMemcpyAsync(hv.data(), g.axis[a], sizeof(double) * g.D[a], cudaMemcpyDeviceToHost, c.stream),
+               "D2H");
             ck(cudaStreamSynchronize(c.stream), "sync");
             host_axes->push_back(std::move(hv));
         }
@@ -762,6 +947,17 @@ bool build_grid(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, Gr
         c.launches++;
     }
     return true;
+}
+
+bool build_grid(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, GridGeo& g, long long& cells,
+                std::vector<std::vector<double>>* host_axes = nullptr)
+{
+    grid_distinct(c, s, d_vals, V, nullptr, K);
+    auto* pc = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long) * K));
+    ck(cudaMemcpyAsync(pc, s.counters.p + 8, sizeof(unsigned long long) * K, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    const std::vector<unsigned long long> dcount(pc, pc + K);
+    return grid_finish(c, s, d_vals, V, K, dcount.data(), g, cells, host_axes);
 }
 
 // ---- sieve front for large value sets the compressed grid cannot hold: a front F0 of a
@@ -914,13 +1110,14 @@ void sieve_front(Ctx& c, Scratch& s, const double* d_vals, long long V, int K)
 }
 
 // front of V distinct vectors (device rows); keep[i] set for non-dominated rows
-int front_keep(Ctx& c, Scratch& s, const double* d_vals, long long V, int K)
+int front_keep(Ctx& c, Scratch& s, const double* d_vals, long long V, int K,
+               const unsigned long long* dcount = nullptr)
 {
     s.keep.reserve(static_cast<size_t>(V) + 1);
     if (K >= 2) {
         GridGeo g{};
         long long cells = 0;
-        if (build_grid(c, s, d_vals, V, K, g, cells)) {
+        if (dcount ? grid_finish(c, s, d_vals, V, K, dcount, g, cells) : build_grid(c, s, d_vals, V, K, g, cells)) {
             k_grid_test<<<grid_blocks(V), 256, 0, c.stream>>>(d_vals, V, K, g, s.T.p, s.S.p, s.keep.p);
             c.launches++;
             s.front_geo = g;
@@ -1063,14 +1260,15 @@ void lex_desc_rank(Ctx& c, const double* d_vals, long long F, int K, long long* 
 // Shared tail of both filters: V distinct vectors (d_vv, V x K) with owner configs
 // (row index into `words` via d_own, or none) -> front -> archive (lex-descending).
 void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, const uint64_t* words,
-                    const uint32_t* d_own, int wpc, DevArchive& out, ParetoTimings* tm)
+                    const uint32_t* d_own, int wpc, DevArchive& out, ParetoTimings* tm,
+                    const unsigned long long* dcount = nullptr)
 {
     cudaEvent_t e0, e1, e2;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventCreate(&e2);
     cudaEventRecord(e0, c.stream);
-    const int method = front_keep(c, s, d_vv, V, K);
+    const int method = front_keep(c, s, d_vv, V, K, dcount);
     trace("finish_archive: front launched");
     s.rows.reserve(static_cast<size_t>(V) + 1);
     ck(cudaMemsetAsync(s.counters.p + 1, 0, sizeof(unsigned long long), c.stream), "memset");
@@ -1155,6 +1353,76 @@ void evaluate_cuts_rows(Ctx& c, const uint64_t* d_words, const uint32_t* idx, lo
     ck(cudaGetLastError(), "evaluate_cuts");
 }
 
+// filter_pool_device for one-word configs with integer weights: dedup + evaluation + collapse
+// in one kernel, the distinct values of the grid axes right after, and a single read-back of
+// the counts before the front (three fewer host round trips than the staged path below)
+void filter_pool_fused(Ctx& c, Scratch& s, const uint64_t* d_words, long long M, DevArchive& out, ParetoTimings* tm)
+{
+    const int K = c.k;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c.stream);
+    const uint64_t t1 = pow2_at_least(2ull * static_cast<uint64_t>(M) + 16);
+    s.dtab64.reserve(t1 * 2);           // dedup keys | collapse owners
+    s.table2.reserve(t1);               // collapse rows
+    s.vals.reserve(static_cast<size_t>(M) * K + 1);
+    s.reps.reserve(static_cast<size_t>(M) + 1);
+    s.counters.reserve(8 + kMaxK);
+    ck(cudaMemsetAsync(s.dtab64.p, 0xFF, sizeof(unsigned long long) * t1 * 2, c.stream), "memset");
+    ck(cudaMemsetAsync(s.table2.p, 0xFF, sizeof(uint32_t) * t1, c.stream), "memset");
+    ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long) * 8, c.stream), "memset");
+    const int KM = K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : 16;
+    const int sm = c.m * (1 + KM) * 4;
+    auto kern = KM == 2 ? k_dedup_eval_collapse<2> : KM == 4 ? k_dedup_eval_collapse<4>
+                : KM == 8 ? k_dedup_eval_collapse<8> : k_dedup_eval_collapse<16>;
+    kern<<<grid_blocks(M), 256, sm, c.stream>>>(d_words, M, c.m, K, c.d_ei.p, c.d_ej.p, c.d_wi.p, s.dtab64.p, t1 - 1,
+                                                 s.table2.p, s.dtab64.p + t1, t1 - 1, s.vals.p, s.reps.p, s.counters.p);
+    c.launches++;
+    ck(cudaGetLastError(), "dedup+eval+collapse");
+    DevBuf<uint32_t> vrow, vown;
+    DevBuf<uint64_t> vcfg;
+    vrow.reserve(static_cast<size_t>(M) + 1);
+    vown.reserve(static_cast<size_t>(M) + 1);
+    vcfg.reserve(static_cast<size_t>(M) + 1);
+    const unsigned long long* dV = s.counters.p + 2;
+    k_slots_fused<<<grid_blocks(M), 256, 0, c.stream>>>(s.reps.p, dV, s.table2.p, s.dtab64.p + t1, vrow.p, vcfg.p,
+                                                          vown.p);
+    DevBuf<double> vv;
+    vv.reserve(static_cast<size_t>(M) * K + 1);
+    k_gather_vals_dev<<<grid_blocks(M * K), 256, 0, c.stream>>>(s.vals.p, vrow.p, dV, K, vv.p);
+    c.launches += 2;
+    grid_distinct(c, s, vv.p, M, dV, K);
+    cudaEventRecord(e1, c.stream);
+    auto* ph = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long) * (8 + K)));
+    ck(cudaMemcpyAsync(ph, s.counters.p, sizeof(unsigned long long) * (8 + K), cudaMemcpyDeviceToHost, c.stream),
+       "D2H");
+    ck(cudaStreamSynchronize(c.stream), "counts");
+    unsigned long long h[8 + kMaxK];
+    std::memcpy(h, ph, sizeof(unsigned long long) * (8 + K));
+    const long long U = static_cast<long long>(h[0]), V = static_cast<long long>(h[2]);
+    if (tm) {
+        tm->unique_configs = U;
+        tm->dedup_s = seconds_between(e0, e1);  // dedup + evaluation + collapse + axis values
+        tm->eval_s = 0;
+        tm->collapse_s = 0;
+    }
+    c.values_are_cuts = true;
+    try {
+        finish_archive(c, s, vv.p, V, K, vcfg.p, vown.p, 1, out, tm, h + 8);
+    } catch (...) {
+        c.values_are_cuts = false;
+        throw;
+    }
+    c.values_are_cuts = false;
+    vrow.release();
+    vown.release();
+    vcfg.release();
+    vv.release();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+}
+
 void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive& out, ParetoTimings* tm)
 {
     if (M <= 0) usage("non-dominated filter needs a non-empty pool");
@@ -1165,6 +1433,10 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     Scratch& s = scratch(c);
     const int wpc = (c.n + 63) / 64;
     const int K = c.k;
+    if (c.n <= 63 && K >= 2 && c.integer_weights && !eval_gemm_ok(c) && c.m * 17 <= 12000) {
+        filter_pool_fused(c, s, d_words, M, out, tm);
+        return;
+    }
     cudaEvent_t e0, e1, e2, e3;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -1348,8 +1620,7 @@ std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t s
     s.counters.reserve(8 + kMaxK);
     DevBuf<unsigned long long> rmin;
     rmin.reserve(static_cast<size_t>(c.k));
-    std::vector<unsigned long long> init(static_cast<size_t>(c.k), ~0ull);
-    ck(cudaMemcpyAsync(rmin.p, init.data(), sizeof(unsigned long long) * c.k, cudaMemcpyHostToDevice, c.stream), "H2D");
+    ck(cudaMemsetAsync(rmin.p, 0xFF, sizeof(unsigned long long) * c.k, c.stream), "memset");
     if (eval_gemm_ok(c)) {  // cut_values == evaluate_cuts exactly for integer weights
         const int wpc = (c.n + 63) / 64;
         DevBuf<uint64_t> wd;
@@ -1372,9 +1643,10 @@ std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t s
         k_col_min<<<grid_blocks(clamp_rows * c.k), 256, 0, c.stream>>>(clamp_vals, clamp_rows, c.k, rmin.p);
         c.launches++;
     }
-    std::vector<unsigned long long> h(static_cast<size_t>(c.k));
-    ck(cudaMemcpyAsync(h.data(), rmin.p, sizeof(unsigned long long) * c.k, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    auto* ph = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long) * c.k));
+    ck(cudaMemcpyAsync(ph, rmin.p, sizeof(unsigned long long) * c.k, cudaMemcpyDeviceToHost, c.stream), "D2H");
     ck(cudaStreamSynchronize(c.stream), "reference point");
+    const std::vector<unsigned long long> h(ph, ph + c.k);
     rmin.release();
     std::vector<double> r(static_cast<size_t>(c.k));
     for (int k = 0; k < c.k; ++k) {
@@ -1392,16 +1664,18 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
     if (static_cast<int>(r.size()) != K) usage("reference point length does not match archive");
     if (K > kMaxK) usage("the GPU path supports at most 16 objectives");
     Scratch& s = scratch(c);
-    s.rdev.reserve(static_cast<size_t>(K));
     s.counters.reserve(8);
-    ck(cudaMemcpyAsync(s.rdev.p, r.data(), sizeof(double) * K, cudaMemcpyHostToDevice, c.stream), "H2D");
+    RPoint rp{};
+    for (int k = 0; k < K; ++k) rp.v[k] = r[static_cast<size_t>(k)];
     const unsigned long long none = ~0ull;
-    const unsigned long long init[3] = {none, ~0ull, dkey(0.0)};
-    ck(cudaMemcpyAsync(s.counters.p + 3, init, sizeof init, cudaMemcpyHostToDevice, c.stream), "H2D");
-    k_ref_check<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, F, K, s.rdev.p, s.counters.p + 3);
+    // counters[3] first bad entry (none), [4] integral flag (all ones), [5] max dkey(gain)
+    // (0: below every gain's key; the host floors it at 1 anyway)
+    ck(cudaMemsetAsync(s.counters.p + 3, 0xFF, sizeof(unsigned long long) * 2, c.stream), "memset");
+    ck(cudaMemsetAsync(s.counters.p + 5, 0, sizeof(unsigned long long), c.stream), "memset");
+    k_ref_check<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, F, K, rp, s.counters.p + 3);
     // gains are exact integers when every value and r is integral (n=42 configs): then the
     // __int128 cell sum is the exact hypervolume, i.e. the reference's exact double result
-    k_hv_stats<<<grid_blocks(F * K), 256, 0, c.stream>>>(d_vals, F, K, s.rdev.p, s.counters.p + 4);
+    k_hv_stats<<<grid_blocks(F * K), 256, 0, c.stream>>>(d_vals, F, K, rp, s.counters.p + 4);
     c.launches += 2;
     auto finish_checks = [&](const unsigned long long* st, bool& integral) {
         if (st[0] != none)
@@ -1417,8 +1691,10 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
     };
     if (K == 1) {
         unsigned long long st[3];
-        ck(cudaMemcpyAsync(st, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        auto* pst = static_cast<unsigned long long*>(pinned_buf(c, sizeof st));
+        ck(cudaMemcpyAsync(pst, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
         ck(cudaStreamSynchronize(c.stream), "sync");
+        std::memcpy(st, pst, sizeof st);
         bool integral;
         finish_checks(st, integral);
         double best = 0;  // pareto.hpp:544-548
@@ -1441,16 +1717,24 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
     s.ipart.reserve(static_cast<size_t>(blocks));
     s.dpart.reserve(static_cast<size_t>(blocks));
     // both sums (the integral one is exact only when the checks below say so): one read-back
-    k_hv_cells<<<blocks, 256, 0, c.stream>>>(s.S.p, cells, g, s.rdev.p, s.ipart.p, s.dpart.p);
+    k_hv_cells<<<blocks, 256, 0, c.stream>>>(s.S.p, cells, g, rp, s.ipart.p, s.dpart.p);
     c.launches++;
     ck(cudaGetLastError(), "hv");
-    std::vector<__int128> ip(static_cast<size_t>(blocks));
-    std::vector<double> dp(static_cast<size_t>(blocks));
     unsigned long long st[3];
-    ck(cudaMemcpyAsync(st, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
-    ck(cudaMemcpyAsync(ip.data(), s.ipart.p, sizeof(__int128) * blocks, cudaMemcpyDeviceToHost, c.stream), "D2H");
-    ck(cudaMemcpyAsync(dp.data(), s.dpart.p, sizeof(double) * blocks, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    // one page-locked read-back: checks | __int128 partials | FP64 partials
+    const size_t nb = static_cast<size_t>(blocks);
+    unsigned char* pb = static_cast<unsigned char*>(pinned_buf(c, 32 + nb * (sizeof(__int128) + sizeof(double))));
+    ck(cudaMemcpyAsync(pb, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaMemcpyAsync(pb + 32, s.ipart.p, sizeof(__int128) * nb, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaMemcpyAsync(pb + 32 + sizeof(__int128) * nb, s.dpart.p, sizeof(double) * nb, cudaMemcpyDeviceToHost,
+                       c.stream),
+       "D2H");
     ck(cudaStreamSynchronize(c.stream), "hv");
+    std::memcpy(st, pb, sizeof st);
+    std::vector<__int128> ip(nb);
+    std::vector<double> dp(nb);
+    std::memcpy(ip.data(), pb + 32, sizeof(__int128) * nb);
+    std::memcpy(dp.data(), pb + 32 + sizeof(__int128) * nb, sizeof(double) * nb);
     bool integral;
     finish_checks(st, integral);
     if (integral) {
