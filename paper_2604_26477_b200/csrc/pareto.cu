@@ -274,7 +274,9 @@ __global__ void k_dedup(const uint64_t* __restrict__ words, long long M, int wpc
     }
 }
 
-// ---- K4: exact integer cut values, instance.hpp:183-194 (== evaluate_cuts for integer weights)
+// ---- K4: exact integer cut values, instance.hpp:183-194 (== evaluate_cuts for integer weights);
+// KM >= K objectives unrolled (2, 4, 8 or 16)
+template <int KM>
 __global__ void k_eval_int(const uint64_t* __restrict__ words, const uint32_t* __restrict__ idx, long long U, int wpc,
                            int m, int K, const int* __restrict__ ei, const int* __restrict__ ej,
                            const int* __restrict__ wi, double* out)
@@ -295,16 +297,16 @@ __global__ void k_eval_int(const uint64_t* __restrict__ words, const uint32_t* _
     for (long long u = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; u < U;
          u += static_cast<long long>(gridDim.x) * blockDim.x) {
         const uint64_t* w = words + static_cast<long long>(idx ? idx[u] : u) * wpc;
-        int acc[kMaxK];
+        int acc[KM];
 #pragma unroll
-        for (int k = 0; k < kMaxK; ++k) acc[k] = 0;
+        for (int k = 0; k < KM; ++k) acc[k] = 0;
         if (wpc == 1) {
             const uint64_t w0 = w[0];
             for (int e = 0; e < m; ++e) {
                 const uint64_t d = (w0 >> sei[e]) ^ (w0 >> sej[e]);
                 const int cut = -static_cast<int>(d & 1ull);  // all-ones when the edge is cut
 #pragma unroll
-                for (int k = 0; k < kMaxK; ++k)
+                for (int k = 0; k < KM; ++k)
                     if (k < K) acc[k] += swi[e * K + k] & cut;
             }
         } else {
@@ -313,15 +315,16 @@ __global__ void k_eval_int(const uint64_t* __restrict__ words, const uint32_t* _
                 const uint64_t d = (w[a >> 6] >> (a & 63)) ^ (w[b >> 6] >> (b & 63));
                 const int cut = -static_cast<int>(d & 1ull);
 #pragma unroll
-                for (int k = 0; k < kMaxK; ++k)
+                for (int k = 0; k < KM; ++k)
                     if (k < K) acc[k] += swi[e * K + k] & cut;
             }
         }
 #pragma unroll
-        for (int k = 0; k < kMaxK; ++k)
+        for (int k = 0; k < KM; ++k)
             if (k < K) out[u * K + k] = static_cast<double>(acc[k]);
     }
 }
+
 
 // ---- K4 general: evaluate_cuts' FP64 order in the shim (pareto.hpp:346-359):
 //      JS_i = sum_j J_k(i,j) s_j (j ascending, from +0.0); h = 0.5 * sum_i s_i JS_i; C = 0.5 (W - h)
@@ -831,6 +834,14 @@ int grid_blocks(long long n, int threads = 256)
     return static_cast<int>(b);
 }
 
+void launch_eval_int(Ctx& c, const uint64_t* words, const uint32_t* idx, long long U, int wpc, double* out)
+{
+    const int K = c.k;
+    const int sm = c.m * (2 + K) <= 12000 ? c.m * (2 + K) * 4 : 0;
+    auto kern = K <= 2 ? k_eval_int<2> : K <= 4 ? k_eval_int<4> : K <= 8 ? k_eval_int<8> : k_eval_int<16>;
+    kern<<<grid_blocks(U), 256, sm, c.stream>>>(words, idx, U, wpc, c.m, K, c.d_ei.p, c.d_ej.p, c.d_wi.p, out);
+}
+
 double seconds_between(cudaEvent_t a, cudaEvent_t b)
 {
     float ms = 0;
@@ -1334,9 +1345,7 @@ void evaluate_cuts_rows(Ctx& c, const uint64_t* d_words, const uint32_t* idx, lo
     if (eval_gemm_ok(c)) {
         evaluate_cuts_gemm(c, d_words, idx, U, d_out);
     } else if (c.integer_weights) {
-        const int sm = c.m * (2 + c.k) <= 12000 ? c.m * (2 + c.k) * 4 : 0;
-        k_eval_int<<<grid_blocks(U), 256, sm, c.stream>>>(d_words, idx, U, wpc, c.m, c.k, c.d_ei.p, c.d_ej.p,
-                                                           c.d_wi.p, d_out);
+        launch_eval_int(c, d_words, idx, U, wpc, d_out);
     } else {
         std::vector<double> W(static_cast<size_t>(c.k), 0.0);
         for (int e = 0; e < c.m; ++e)
@@ -1433,7 +1442,8 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     Scratch& s = scratch(c);
     const int wpc = (c.n + 63) / 64;
     const int K = c.k;
-    if (c.n <= 63 && K >= 2 && c.integer_weights && !eval_gemm_ok(c) && c.m * 17 <= 12000) {
+    // (tables sized by M: pools beyond 2^24 configs take the staged path, sized by the counts)
+    if (c.n <= 63 && K >= 2 && c.integer_weights && !eval_gemm_ok(c) && c.m * 17 <= 12000 && M <= (1ll << 24)) {
         filter_pool_fused(c, s, d_words, M, out, tm);
         return;
     }
@@ -1460,9 +1470,7 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     if (eval_gemm_ok(c)) {  // large dense instances: exact int8 tensor-core form
         evaluate_cuts_gemm(c, d_words, s.uniq.p, U, s.vals.p);
     } else if (c.integer_weights) {
-        const int sm = c.m * (2 + K) <= 12000 ? c.m * (2 + K) * 4 : 0;
-        k_eval_int<<<grid_blocks(U), 256, sm, c.stream>>>(d_words, s.uniq.p, U, wpc, c.m, K, c.d_ei.p, c.d_ej.p,
-                                                           c.d_wi.p, s.vals.p);
+        launch_eval_int(c, d_words, s.uniq.p, U, wpc, s.vals.p);
         c.launches++;
     } else {
         std::vector<double> W(static_cast<size_t>(K), 0.0);
