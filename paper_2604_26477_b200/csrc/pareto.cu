@@ -414,11 +414,13 @@ __global__ void k_distinct(const double* __restrict__ vals, long long V, const u
     const uint64_t tmask = tsize - 1;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        // more distinct values than a grid takes: this axis is done (no grid)
+        if (static_cast<long long>(__ldcg(count)) > cap) break;
         const double v = vals[i * K + axis];
         const unsigned long long key = dkey(v);
         uint64_t h = mix64(key) & tmask;
         for (uint64_t probe = 0;; ++probe) {
-            if (probe > tmask) {  // full: more distinct values than any grid takes
+            if (probe > 1024) {  // the table (>= 4 x cap slots) is crowded: too many values
                 atomicMax(count, static_cast<unsigned long long>(cap) + 1);
                 break;
             }
@@ -891,7 +893,7 @@ void grid_distinct(Ctx& c, Scratch& s, const double* d_vals, long long Vcap, con
 {
     ++c.grid_gen;
     const uint64_t tsize =
-        pow2_at_least(2ull * static_cast<uint64_t>(std::min<long long>(Vcap, kDistinctCap)) + 16);
+        pow2_at_least(4ull * static_cast<uint64_t>(std::min<long long>(Vcap, kDistinctCap)) + 16);
     s.dtable.reserve(tsize * K);
     s.axisbuf.reserve(static_cast<size_t>(kDistinctCap) * K);
     s.axis_sorted.reserve(static_cast<size_t>(kDistinctCap) * K);
