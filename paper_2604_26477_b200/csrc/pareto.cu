@@ -244,6 +244,42 @@ __global__ void k_gather_vals_dev(const double* __restrict__ src, const uint32_t
         dst[i] = src[static_cast<long long>(rows[i / K]) * K + i % K];
 }
 
+// ---- K5 for one-word configs with n <= 63: the config word is the key (empty = ~0, which no
+// such config equals); one CAS per config and no re-read of the pool for the comparison
+// A table smaller than the pool (L2-sized) may fill up: past `limit` keys or 256 probes the
+// kernel raises ucount[1] and stops inserting; the host then redoes the dedup at full size.
+__global__ void k_dedup64(const uint64_t* __restrict__ words, long long M, unsigned long long* table, uint64_t tmask,
+                          uint32_t* uniq, unsigned long long* ucount, unsigned long long limit)
+{
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x); i0 < M;
+         i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        bool fresh = false;
+        if (i < M) {
+            const uint64_t w = words[i];
+            uint64_t h = mix64(w) & tmask;
+            for (int probe = 0;; ++probe) {
+                if (probe == 256) {
+                    atomicExch(ucount + 1, 1ull);
+                    break;
+                }
+                const unsigned long long old = atomicCAS(&table[h], ~0ull, static_cast<unsigned long long>(w));
+                if (old == ~0ull) {
+                    fresh = true;
+                    break;
+                }
+                if (old == w) break;
+                h = (h + 1) & tmask;
+            }
+        }
+        const unsigned long long at = warp_append_index(fresh, ucount);
+        if (fresh) {
+            if (at < limit) uniq[at] = static_cast<uint32_t>(i);
+            else atomicExch(ucount + 1, 1ull);  // (the table is redone at full size)
+        }
+    }
+}
+
 // ---- K5: dedup of packed configs (pareto.hpp:309-326)
 __global__ void k_dedup(const uint64_t* __restrict__ words, long long M, int wpc, uint32_t* table, uint64_t tmask,
                         uint32_t* uniq, unsigned long long* ucount)
@@ -1457,12 +1493,32 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     cudaEventRecord(e0, c.stream);
     // K5 dedup
     const uint64_t tsize = pow2_at_least(2ull * static_cast<uint64_t>(M));
-    s.table.reserve(tsize);
     s.uniq.reserve(static_cast<size_t>(M));
     s.counters.reserve(8);
-    ck(cudaMemsetAsync(s.table.p, 0xFF, sizeof(uint32_t) * tsize, c.stream), "memset");
     ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long) * 8, c.stream), "memset");
-    k_dedup<<<grid_blocks(M), 256, 0, c.stream>>>(d_words, M, wpc, s.table.p, tsize - 1, s.uniq.p, s.counters.p);
+    if (c.n <= 63) {
+        // an L2-sized table first (2^24 keys, 128 MB; a pool of 1e8 configs has ~7e6 distinct
+        // ones), the full 2M-slot table only if it fills to 3/4
+        const uint64_t small = std::min<uint64_t>(tsize, 1ull << 24);
+        for (uint64_t ts : {small, tsize}) {
+            s.dtab64.reserve(ts);
+            ck(cudaMemsetAsync(s.dtab64.p, 0xFF, sizeof(unsigned long long) * ts, c.stream), "memset");
+            ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long) * 2, c.stream), "memset");
+            k_dedup64<<<grid_blocks(M), 256, 0, c.stream>>>(d_words, M, s.dtab64.p, ts - 1, s.uniq.p, s.counters.p,
+                                                             ts / 4 * 3);
+            if (ts == tsize) break;
+            auto* pf = static_cast<unsigned long long*>(pinned_buf(c, 2 * sizeof(unsigned long long)));
+            ck(cudaMemcpyAsync(pf, s.counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream),
+               "D2H");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            if (!pf[1]) break;
+            c.launches++;
+        }
+    } else {
+        s.table.reserve(tsize);
+        ck(cudaMemsetAsync(s.table.p, 0xFF, sizeof(uint32_t) * tsize, c.stream), "memset");
+        k_dedup<<<grid_blocks(M), 256, 0, c.stream>>>(d_words, M, wpc, s.table.p, tsize - 1, s.uniq.p, s.counters.p);
+    }
     c.launches++;
     const long long U = static_cast<long long>(read_counter(c, s.counters.p));
     trace("filter_pool: dedup done");
