@@ -574,9 +574,26 @@ __device__ __forceinline__ void sb_batch_body(const SamplerParams& p)
                     yi = __dadd_rn(yi, UDT ? d : __dmul_rn(dt, d));
                     xi = __dadd_rn(xi, UDT ? yi : __dmul_rn(sdt, yi));
                 }
-                if (fabs(xi) > 1.0) {
-                    if constexpr (VAR != 2) yi = 0.0;
-                    xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
+                // y <- 0 where |x| > 1 (strict, SB only), then the clamp to +-1 with x's sign: both
+                // fire exactly when |x| > 1 (never for NaN, which propagates). In place under one
+                // predicate: x.hi = (x.hi & sign) | hi(1.0), x.lo = 0, y = 0
+                {
+                    uint32_t xl = static_cast<uint32_t>(__double2loint(xi)), xh = static_cast<uint32_t>(__double2hiint(xi));
+                    uint32_t yl = static_cast<uint32_t>(__double2loint(yi)), yh = static_cast<uint32_t>(__double2hiint(yi));
+                    if constexpr (VAR != 2) {
+                        asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %4, 0d3FF0000000000000;\n\t"
+                            "@p lop3.b32 %1, %1, 0x80000000, %5, 0xEA;\n\t@p mov.b32 %0, 0;\n\t"
+                            "@p mov.b32 %2, 0;\n\t@p mov.b32 %3, 0;\n\t}"
+                            : "+r"(xl), "+r"(xh), "+r"(yl), "+r"(yh)
+                            : "d"(fabs(xi)), "r"(0x3FF00000u));
+                    } else {
+                        asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %2, 0d3FF0000000000000;\n\t"
+                            "@p lop3.b32 %1, %1, 0x80000000, %3, 0xEA;\n\t@p mov.b32 %0, 0;\n\t}"
+                            : "+r"(xl), "+r"(xh)
+                            : "d"(fabs(xi)), "r"(0x3FF00000u));
+                    }
+                    xi = __hiloint2double(static_cast<int>(xh), static_cast<int>(xl));
+                    yi = __hiloint2double(static_cast<int>(yh), static_cast<int>(yl));
                 }
                 x[s] = xi;
                 y[s] = yi;
