@@ -571,6 +571,11 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     p.nan_block = c.d_nan.p;
     p.first_bad_step_task = -1;
     p.bad_step = c.d_badstep.p;
+    {  // test hook: MOMC_TEST_SEQ_STREAMS=k resolves every k-th noise stream of the batch
+       // kernel on its sequential in-kernel path (the words must be identical)
+        const char* f = std::getenv("MOMC_TEST_SEQ_STREAMS");
+        p.test_seq_every = f ? std::atoi(f) : 0;
+    }
 
     auto scratch = [&](long long blocks) {
         long long cap = std::min<long long>(blocks, 4096) * bt;

@@ -1499,7 +1499,9 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     if (c.n <= 63) {
         // an L2-sized table first (2^24 keys, 128 MB; a pool of 1e8 configs has ~7e6 distinct
         // ones), the full 2M-slot table only if it fills to 3/4
-        const uint64_t small = std::min<uint64_t>(tsize, 1ull << 24);
+        uint64_t small = std::min<uint64_t>(tsize, 1ull << 24);
+        // test hook: MOMC_TEST_DEDUP_SLOTS=s starts with an s-slot table (forces the redo)
+        if (const char* f = std::getenv("MOMC_TEST_DEDUP_SLOTS")) small = std::min<uint64_t>(small, pow2_at_least(std::atoll(f)));
         for (uint64_t ts : {small, tsize}) {
             s.dtab64.reserve(ts);
             ck(cudaMemsetAsync(s.dtab64.p, 0xFF, sizeof(unsigned long long) * ts, c.stream), "memset");

@@ -38,6 +38,8 @@ struct SamplerParams {
     unsigned long long* block_end_ns;  // per launched block (optional)
     int* nan_block;           // per launched block: 1 if any trajectory went non-finite
     int first_bad_step_task;  // debug rerun: -1, else records first bad step per block
+    int test_seq_every;       // test hook: > 0 resolves every k-th (trajectory, step) stream of the
+                              // batch kernel sequentially (seq_resolve); 0 in production
     int* bad_step;            // per launched block: min first non-finite step (debug rerun)
 };
 

@@ -480,6 +480,7 @@ __device__ __forceinline__ void sb_batch_body(const SamplerParams& p)
                 }
             }
             if (n - 1 + slow >= kGen) seq = true;  // the last normals lie past the generated words
+            if (p.test_seq_every > 0 && (tr + static_cast<uint32_t>(tb + h)) % p.test_seq_every == 0) seq = true;
             if (seq) {
 #pragma unroll
                 for (int c = 0; c < G::kWS / 4; ++c) reinterpret_cast<uint4*>(wr)[c] = make_uint4(0u, 0u, 0u, 0u);

@@ -81,6 +81,21 @@ def test_filter_real_weights(ref, session):
     check_archive(got, ref.filter_pool(ri, words))
 
 
+def test_filter_dedup_table_redo(ref, session):
+    """the staged path's dedup starts with an L2-sized key table and redoes the dedup at full
+    size when it fills; forced here with a 1024-slot first table (MOMC_TEST_DEDUP_SLOTS), the
+    archive must still equal the reference's (real weights take the staged path)"""
+    ri = ref.generate_uniform(14, 0.6, 3, 9, kind="real", lo=0.0, hi=1.0)
+    inst = inst_from_ref(ri)
+    words = random_words(14, 20000, 3)
+    os.environ["MOMC_TEST_DEDUP_SLOTS"] = "1024"
+    try:
+        got = api.non_dominated_filter(api.SamplePool(14, words), inst, session=session)
+    finally:
+        del os.environ["MOMC_TEST_DEDUP_SLOTS"]
+    check_archive(got, ref.filter_pool(ri, words))
+
+
 def test_filter_lex_tiebreak(ref, session):
     """test_pareto.cpp:160-176: equal vectors keep the lexicographically smallest config."""
     inst = api.MultiObjectiveInstance(4, 2, [(0, 1, [1.0, 1.0]), (2, 3, [1.0, 1.0])])

@@ -184,3 +184,28 @@ def test_register_path_fallback_blocks_are_identical(session, variant):
     b = s.pool(stamps=False).words
     assert (s.fallback_blocks() & ((1 << 40) - 1)) > before
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("variant", ["dsb", "bsb", "simcim"])
+def test_batch_kernel_sequential_streams_are_identical(session, variant):
+    """noise streams resolved on the batch kernel's in-kernel sequential path (seq_resolve,
+    taken by streams that need more than 56 words) give the same words as the walk
+    (MOMC_TEST_SEQ_STREAMS=3 sends every 3rd (trajectory, step) stream there)"""
+    import os
+    from paper_2604_26477_b200.instances import load_heavy_hex
+    inst = load_heavy_hex(4)
+    s = session
+    s.set_instance(inst)
+    s.set_weights(api.build_weights(4, resolution=5))
+    cfg = SolverConfig(variant=api.parse_variant(variant), batch_size=300, seed=12)
+    s.sample(cfg, 1)
+    a = s.pool(stamps=False).words.copy()
+    os.environ["MOMC_TEST_SEQ_STREAMS"] = "3"
+    try:
+        s.sample(cfg, 1)
+    finally:
+        del os.environ["MOMC_TEST_SEQ_STREAMS"]
+    b = s.pool(stamps=False).words
+    diff = int(np.count_nonzero(a != b))
+    print(f"{variant}: {diff} of {a.size} words differ with every 3rd stream resolved sequentially")
+    assert diff == 0
