@@ -134,6 +134,8 @@ struct Ctx {
     std::vector<double> h_w;
     DevBuf<int> d_ei, d_ej, d_rowptr, d_col, d_eidx;
     DevBuf<double> d_w;
+    DevBuf<double> d_wsum;          // per-objective totals of the edge weights (weight_totals())
+    long long wsum_gen = -1;
     DevBuf<int> d_wi;  // integer weights (m x k) when integer_weights
 
     // weights / scalarisation
@@ -197,6 +199,23 @@ inline void* pinned_buf(Ctx& c, size_t bytes)
         c.pinned_bytes = b;
     }
     return c.pinned;
+}
+
+// Device array of the K per-objective sums of all edge weights, W_k = sum_e w_ek in edge
+// order (evaluate_cuts' constant, pareto.hpp:346-361), computed once per instance.
+inline const double* weight_totals(Ctx& c)
+{
+    if (c.wsum_gen != c.inst_gen) {
+        std::vector<double> W(static_cast<size_t>(c.k), 0.0);
+        for (int e = 0; e < c.m; ++e)
+            for (int q = 0; q < c.k; ++q) W[static_cast<size_t>(q)] += c.h_w[static_cast<size_t>(e) * c.k + q];
+        c.d_wsum.reserve(static_cast<size_t>(c.k));
+        if (cudaMemcpyAsync(c.d_wsum.p, W.data(), sizeof(double) * c.k, cudaMemcpyHostToDevice, c.stream) != cudaSuccess ||
+            cudaStreamSynchronize(c.stream) != cudaSuccess)
+            throw std::runtime_error("weight totals upload failed");
+        c.wsum_gen = c.inst_gen;
+    }
+    return c.d_wsum.p;
 }
 
 // Makes ctx's device current and its stream the allocation stream of this thread.

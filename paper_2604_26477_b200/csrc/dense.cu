@@ -1024,13 +1024,7 @@ void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, 
         c.launches++;
         d.wk_gen = c.inst_gen;
     }
-    std::vector<double> W(static_cast<size_t>(K), 0.0);
-    for (int e = 0; e < c.m; ++e)
-        for (int q = 0; q < K; ++q) W[static_cast<size_t>(q)] += c.h_w[static_cast<size_t>(e) * K + q];
     d.flags.reserve(8);
-    DevBuf<double> dW;
-    dW.reserve(static_cast<size_t>(K));
-    ck(cudaMemcpyAsync(dW.p, W.data(), sizeof(double) * K, cudaMemcpyHostToDevice, c.stream), "H2D");
     EvalArgs ea{};
     ea.n = n;
     ea.K = K;
@@ -1040,7 +1034,7 @@ void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, 
     ea.U = U;
     ea.words = d_words;
     ea.idx = d_idx;
-    ea.W = dW.p;
+    ea.W = weight_totals(c);
     ea.out = d_out;
     const CUtensorMap tm = make_tmap(d.wk.p, static_cast<long long>(K) * n, npad, npad, 1, 128, kEvN);
     int dev = 0, sms = 0;
@@ -1054,7 +1048,6 @@ void evaluate_cuts_gemm(Ctx& c, const uint64_t* d_words, const uint32_t* d_idx, 
     c.ktimer.end(ke, kKEvalGemm, c.stream);
     c.launches++;
     ck(cudaGetLastError(), "evaluate_cuts (tensor cores)");
-    dW.release();
 }
 
 }  // namespace momc_b200

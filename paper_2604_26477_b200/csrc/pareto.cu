@@ -1385,16 +1385,8 @@ void evaluate_cuts_rows(Ctx& c, const uint64_t* d_words, const uint32_t* idx, lo
     } else if (c.integer_weights) {
         launch_eval_int(c, d_words, idx, U, wpc, d_out);
     } else {
-        std::vector<double> W(static_cast<size_t>(c.k), 0.0);
-        for (int e = 0; e < c.m; ++e)
-            for (int q = 0; q < c.k; ++q) W[static_cast<size_t>(q)] += c.h_w[static_cast<size_t>(e) * c.k + q];
-        DevBuf<double> dW;
-        dW.reserve(static_cast<size_t>(c.k));
-        ck(cudaMemcpyAsync(dW.p, W.data(), sizeof(double) * c.k, cudaMemcpyHostToDevice, c.stream), "H2D");
         k_eval_dbl<<<grid_blocks(U, 128), 128, 0, c.stream>>>(d_words, idx, U, wpc, c.n, c.k, c.d_rowptr.p,
-                                                               c.d_col.p, c.d_eidx.p, c.d_w.p, dW.p, d_out);
-        ck(cudaStreamSynchronize(c.stream), "eval");
-        dW.release();
+                                                               c.d_col.p, c.d_eidx.p, c.d_w.p, weight_totals(c), d_out);
     }
     c.launches++;
     ck(cudaGetLastError(), "evaluate_cuts");
@@ -1533,13 +1525,9 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
         launch_eval_int(c, d_words, s.uniq.p, U, wpc, s.vals.p);
         c.launches++;
     } else {
-        std::vector<double> W(static_cast<size_t>(K), 0.0);
-        for (int e = 0; e < c.m; ++e)
-            for (int q = 0; q < K; ++q) W[static_cast<size_t>(q)] += c.h_w[static_cast<size_t>(e) * K + q];
-        s.rdev.reserve(static_cast<size_t>(K));
-        ck(cudaMemcpyAsync(s.rdev.p, W.data(), sizeof(double) * K, cudaMemcpyHostToDevice, c.stream), "H2D");
         k_eval_dbl<<<grid_blocks(U, 128), 128, 0, c.stream>>>(d_words, s.uniq.p, U, wpc, c.n, K, c.d_rowptr.p,
-                                                               c.d_col.p, c.d_eidx.p, c.d_w.p, s.rdev.p, s.vals.p);
+                                                               c.d_col.p, c.d_eidx.p, c.d_w.p, weight_totals(c),
+                                                               s.vals.p);
         c.launches++;
     }
     ck(cudaGetLastError(), "eval");
