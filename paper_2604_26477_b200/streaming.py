@@ -88,12 +88,13 @@ def time_to_target(session, cfg, reference, hv_target, max_runs: int, world: int
 
 
 def time_to_target_overlapped(sessions: list, merger, cfg, reference, hv_target, max_runs: int,
-                              trace: list | None = None) -> dict:
+                              trace: list | None = None, runs_per_step: int = 1) -> dict:
     """One GPU, several sampling contexts in host threads plus one merging context: run r is
     sampled and filtered by sessions[r % S] (the register sampler on its low-priority stream)
     while earlier runs' fronts are merged into `merger`'s running archive on its own stream.
     Merges happen strictly in run order, so runs / samples / archive / HV equal the sequential
-    stream's; only the wall time differs."""
+    stream's; only the wall time differs. Step k samples runs [k R, (k+1) R) (R = runs_per_step)
+    in one launch on sessions[k % S] and is merged (one merge, one HV check) after step k - 1."""
     import threading
 
     S = len(sessions)
@@ -106,26 +107,30 @@ def time_to_target_overlapped(sessions: list, merger, cfg, reference, hv_target,
     cv = threading.Condition()
     t0 = time.perf_counter()
 
+    R = max(1, int(runs_per_step))
+    steps = (max_runs + R - 1) // R
+
     def worker(w):
         s = sessions[w]
         try:
-            for run in range(w, max_runs, S):
+            for step in range(w, steps, S):
                 with cv:
                     if st["done"]:
                         return
-                s.stream_step(cfg, run + 1, run * per_run, (run + 1) * per_run, None, merge=False)
+                run, run_end = step * R, min((step + 1) * R, max_runs)
+                s.stream_step(cfg, run_end, run * per_run, run_end * per_run, None, merge=False)
                 with cv:
-                    while st["next"] != run and not st["done"]:
+                    while st["next"] != step and not st["done"]:
                         cv.wait()
                     if st["done"]:
                         return
                     v, wd, F = s.archive_device_ptrs()
                     st["hv"], st["F"] = merger.running_merge_values(v, wd, wpc, F, k, reference)
-                    st["runs"] = run + 1
+                    st["runs"] = run_end
                     if trace is not None:
-                        trace.append({"runs": run + 1, "samples": (run + 1) * samples_per_run, "archive": st["F"],
+                        trace.append({"runs": run_end, "samples": run_end * samples_per_run, "archive": st["F"],
                                       "hv": st["hv"], "wall_s": time.perf_counter() - t0})
-                    st["next"] = run + 1
+                    st["next"] = step + 1
                     if _reached(st["hv"], hv_target):
                         st["done"] = True
                     cv.notify_all()

@@ -23,7 +23,7 @@ def main():
     cfg = api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=4546, seed=7)
     dev = torch.device("cuda", 0)
     out = {}
-    for it, S in enumerate((1, 1, 1, 2)):
+    for it, S in enumerate((1, 1, 2, 2, 3)):
         sessions = [api.Session(0) for _ in range(S)]
         for s in sessions:
             s.set_instance(inst)
@@ -32,13 +32,14 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if S == 1:
-            res = streaming.time_to_target(sessions[0], cfg, r, target, 300, device=dev, runs_per_step=[1, 2, 4, 1][it])
+            res = streaming.time_to_target(sessions[0], cfg, r, target, 300, device=dev, runs_per_step=[1, 2][it])
         else:
             merger = api.Session(0)
             merger.set_instance(inst)
-            res = streaming.time_to_target_overlapped(sessions, merger, cfg, r, target, 300)
+            res = streaming.time_to_target_overlapped(sessions, merger, cfg, r, target, 300,
+                                                      runs_per_step=[0, 0, 1, 2, 2][it])
         res["wall"] = time.perf_counter() - t0
-        out[f"{it}:sessions{S}:R{[1, 2, 4, 1][it] if S == 1 else 1}"] = {"seconds": round(res["seconds"], 4), "runs": res["runs"]}
+        out[f"{it}:sessions{S}:R{[1, 2, 1, 2, 2][it]}"] = {"seconds": round(res["seconds"], 4), "runs": res["runs"]}
         del sessions
     print(json.dumps(out))
 
