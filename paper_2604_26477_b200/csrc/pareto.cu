@@ -436,41 +436,68 @@ __global__ void k_collapse(const double* __restrict__ vals, long long U, int K, 
 }
 
 // ---- distinct values of every axis (blockIdx.y = axis; hash set of keys per axis), then
-// ascending order by rank count. The row count is *dV when given. A full table (more
-// distinct values than it holds) stops probing and reports count > cap (no grid).
+// ascending order by rank count. The row count is *dV when given. Each block first keeps the
+// keys it has seen in a shared-memory set, so only its first sighting of a value reaches the
+// global set (a handful of values repeat across ~10^6 rows; their global slots are otherwise
+// the hottest lines of the stage). A full global table (more distinct values than it holds)
+// stops probing and reports count > cap (no grid).
+__device__ __forceinline__ void distinct_insert_global(unsigned long long key, double v, unsigned long long* table,
+                                                       uint64_t tmask, double* out, unsigned long long* count,
+                                                       long long cap)
+{
+    uint64_t h = mix64(key) & tmask;
+    for (uint64_t probe = 0;; ++probe) {
+        if (probe > 1024) {  // the table (>= 4 x cap slots) is crowded: too many values
+            atomicMax(count, static_cast<unsigned long long>(cap) + 1);
+            return;
+        }
+        unsigned long long s = __ldcg(&table[h]);
+        if (s == key) return;
+        if (s == 0ull) s = atomicCAS(&table[h], 0ull, key);
+        if (s == 0ull) {
+            const unsigned long long at = atomicAdd(count, 1ull);
+            if (static_cast<long long>(at) < cap) out[at] = v + 0.0;
+            return;
+        }
+        if (s == key) return;
+        h = (h + 1) & tmask;
+    }
+}
+
 __global__ void k_distinct(const double* __restrict__ vals, long long V, const unsigned long long* __restrict__ dV,
                            int K, unsigned long long* tables, uint64_t tsize, double* outs, unsigned long long* counts,
                            long long cap)
 {
+    constexpr int kSet = 1024;
+    __shared__ unsigned long long sset[kSet];
     const int axis = blockIdx.y;
     if (dV) V = static_cast<long long>(*dV);
     unsigned long long* table = tables + tsize * axis;
     double* out = outs + cap * axis;
     unsigned long long* count = counts + axis;
     const uint64_t tmask = tsize - 1;
+    for (int q = threadIdx.x; q < kSet; q += blockDim.x) sset[q] = 0ull;
+    __syncthreads();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        // more distinct values than a grid takes: this axis is done (no grid)
-        if (static_cast<long long>(__ldcg(count)) > cap) break;
         const double v = vals[i * K + axis];
         const unsigned long long key = dkey(v);
-        uint64_t h = mix64(key) & tmask;
-        for (uint64_t probe = 0;; ++probe) {
-            if (probe > 1024) {  // the table (>= 4 x cap slots) is crowded: too many values
-                atomicMax(count, static_cast<unsigned long long>(cap) + 1);
+        uint32_t h = static_cast<uint32_t>(mix64(key)) & (kSet - 1);
+        bool fresh = true, seen = false;
+        for (int probe = 0; probe < 32; ++probe) {  // a full set passes the value through
+            const unsigned long long s = atomicCAS(&sset[h], 0ull, key);
+            if (s == 0ull) break;
+            if (s == key) {
+                seen = true;
                 break;
             }
-            // a plain read first: most rows repeat one of the few values already present
-            unsigned long long s = __ldcg(&table[h]);
-            if (s == key) break;
-            if (s == 0ull) s = atomicCAS(&table[h], 0ull, key);
-            if (s == 0ull) {
-                const unsigned long long at = atomicAdd(count, 1ull);
-                if (static_cast<long long>(at) < cap) out[at] = v + 0.0;
-                break;
-            }
-            if (s == key) break;
-            h = (h + 1) & tmask;
+            h = (h + 1) & (kSet - 1);
+        }
+        fresh = !seen;
+        if (fresh) {
+            // more distinct values than a grid takes: this axis is done (no grid)
+            if (static_cast<long long>(__ldcg(count)) > cap) break;
+            distinct_insert_global(key, v, table, tmask, out, count, cap);
         }
     }
 }
@@ -698,13 +725,45 @@ __global__ void k_gather_rows(const double* __restrict__ src_vals, const uint32_
 // order) of `count` configs drawn 64 spins per next_u64 from
 // Stream(derive_key(seed, 0x70617265), c, 0, tag_word(reference_sample)); per-objective min.
 __global__ void k_ref_sample(int count, uint64_t key, int n, int m, int K, const int* __restrict__ ei,
-                             const int* __restrict__ ej, const double* __restrict__ w, unsigned long long* rmin)
+                             const int* __restrict__ ej, const double* __restrict__ w, unsigned long long* rmin,
+                             bool staged)
 {
+    const int wpc = (n + 63) / 64;
+    if (staged) {  // (n <= 64)  // one word per config: register-resident, edges and weights in shared memory
+        extern __shared__ __align__(16) unsigned char sraw[];
+        double* sw = reinterpret_cast<double*>(sraw);                 // m x K
+        int* spair = reinterpret_cast<int*>(sw + static_cast<long long>(m) * K);  // (ei | ej << 16) x m
+        for (int e = threadIdx.x; e < m; e += blockDim.x) spair[e] = ei[e] | (ej[e] << 16);
+        for (int q = threadIdx.x; q < m * K; q += blockDim.x) sw[q] = w[q];
+        __syncthreads();
+        for (int c0 = blockIdx.x * blockDim.x; c0 < count; c0 += gridDim.x * blockDim.x) {
+            const int c = c0 + threadIdx.x;
+            uint64_t w0 = 0;
+            if (c < count) {
+                DevStream s;
+                s.init(key, static_cast<uint32_t>(c), 0u, tag_word(kTagReferenceSample, 0));
+                w0 = s.next_u64();
+            }
+            for (int k = 0; k < K; ++k) {
+                double acc = 0.0;
+                for (int e = 0; e < m; ++e) {
+                    const int pr = spair[e];
+                    if (((w0 >> (pr & 0xFFFF)) ^ (w0 >> (pr >> 16))) & 1ull) acc = __dadd_rn(acc, sw[e * K + k]);
+                }
+                unsigned long long mk = c < count ? dkey(acc) : ~0ull;
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long u = __shfl_xor_sync(0xffffffffu, mk, o);
+                    mk = u < mk ? u : mk;
+                }
+                if ((threadIdx.x & 31) == 0 && mk != ~0ull) atomicMin(&rmin[k], mk);
+            }
+        }
+        return;
+    }
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < count; c += gridDim.x * blockDim.x) {
         DevStream s;
         s.init(key, static_cast<uint32_t>(c), 0u, tag_word(kTagReferenceSample, 0));
         uint64_t wd[64];
-        const int wpc = (n + 63) / 64;
         for (int q = 0; q < wpc && q < 64; ++q) wd[q] = s.next_u64();
         for (int k = 0; k < K; ++k) {
             double acc = 0.0;
@@ -733,11 +792,23 @@ __global__ void k_ref_words(int count, uint64_t key, int n, uint64_t* words)
     }
 }
 
+// per-objective minimum (ordered keys): one thread per row, a warp minimum per objective,
+// then one atomic per warp and objective (the K counters are contended otherwise)
 __global__ void k_col_min(const double* __restrict__ vals, long long rows, int K, unsigned long long* rmin)
 {
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < rows * K;
-         i += static_cast<long long>(gridDim.x) * blockDim.x)
-        atomicMin(&rmin[i % K], dkey(vals[i]));
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long base0 = blockIdx.x * static_cast<long long>(blockDim.x);
+    for (long long b = base0; b < rows; b += stride) {
+        const long long i = b + threadIdx.x;
+        for (int k = 0; k < K; ++k) {
+            unsigned long long m = i < rows ? dkey(vals[i * K + k]) : ~0ull;
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long u = __shfl_xor_sync(0xffffffffu, m, o);
+                m = u < m ? u : m;
+            }
+            if ((threadIdx.x & 31) == 0 && m != ~0ull) atomicMin(&rmin[k], m);
+        }
+    }
 }
 
 // ---- K8: hypervolume over a compressed grid (gains g = v - r). One warp per line of the
@@ -745,10 +816,12 @@ __global__ void k_col_min(const double* __restrict__ vals, long long rows, int K
 // line's cells (coalesced S loads). Widths are clamped at r, so a grid built over more vectors
 // than the archive (the front's grid over every distinct vector, whose dominated region is the
 // archive's) gives the same exact value; over the archive's own grid (values >= r) the clamp is
-// the identity. Both sums are formed: the exact __int128 one (valid when every gain is an
-// integer, decided on the host from k_hv_stats) and the Kahan FP64 one.
+// the identity. The mode comes from k_hv_stats on the device (stats[0]: every value integral,
+// stats[1]: the largest gain's key): integral data and r give the exact __int128 sum (64-bit
+// cell products when gain^K < 2^62), anything else the Kahan FP64 sum; the host reads the
+// matching partials.
 __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, GridGeo g, const RPoint rp,
-                           __int128* ipart, double* dpart)
+                           const unsigned long long* __restrict__ stats, __int128* ipart, double* dpart)
 {
     const int lane = threadIdx.x & 31;
     const int da = g.dims - 1;  // the innermost grid axis (stride 1)
@@ -759,6 +832,17 @@ __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, Grid
     double dacc = 0.0, dc = 0.0;
     const double* r = rp.v;
     const double rl = r[g.dims];
+    bool integral = stats[0] != 0;
+    for (int a = 0; a <= g.dims; ++a) integral &= floor(r[a]) == r[a];
+    bool fit64 = false;
+    if (integral) {  // the host's rule (hypervolume_device): exact while K e <= 120, maxg < 2^e
+        const uint64_t key = stats[1];
+        const uint64_t b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
+        int e = 0;
+        frexp(fmax(__longlong_as_double(static_cast<long long>(b)), 1.0), &e);
+        integral = (g.dims + 1) * e <= 120;
+        fit64 = (g.dims + 1) * e <= 62;
+    }
     for (long long line = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; line < lines;
          line += warps) {
         // widths of the outer axes of this line (cells < 2^27: 32-bit index arithmetic)
@@ -787,26 +871,46 @@ __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, Grid
             if (!(hgain > 0.0)) continue;
             const double w = ax[q] - fmax(q ? ax[q - 1] : rd, rd);
             if (!(w > 0.0)) continue;
-            __int128 ivol = pwi;
-            ivol *= static_cast<long long>(w);
-            ivol *= static_cast<long long>(hgain);
-            iacc += ivol;
-            const double vol = hgain * pw * w;
-            const double y = vol - dc;  // Kahan
-            const double t = dacc + y;
-            dc = (t - dacc) - y;
-            dacc = t;
+            if (integral) {
+                if (fit64) {
+                    iacc += pwi * static_cast<long long>(w) * static_cast<long long>(hgain);
+                } else {
+                    __int128 ivol = pwi;
+                    ivol *= static_cast<long long>(w);
+                    ivol *= static_cast<long long>(hgain);
+                    iacc += ivol;
+                }
+            } else {
+                const double vol = hgain * pw * w;
+                const double y = vol - dc;  // Kahan
+                const double t = dacc + y;
+                dc = (t - dacc) - y;
+                dacc = t;
+            }
         }
     }
-    __shared__ __int128 si[256];
-    __shared__ double sd[256];
-    si[threadIdx.x] = iacc;
-    sd[threadIdx.x] = dacc - dc;
+    // block partials: shuffle sums within each warp (the __int128 as two 64-bit halves with the
+    // carry), then the 8 warp sums by thread 0
+    double dsum = dacc - dc;
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long lo = static_cast<unsigned long long>(iacc);
+        const long long hi = static_cast<long long>(iacc >> 64);
+        const unsigned long long olo = __shfl_down_sync(0xffffffffu, lo, o);
+        const long long ohi = __shfl_down_sync(0xffffffffu, hi, o);
+        iacc += (static_cast<__int128>(ohi) << 64) | static_cast<__int128>(olo);
+        dsum += __shfl_down_sync(0xffffffffu, dsum, o);
+    }
+    __shared__ __int128 si[8];
+    __shared__ double sd[8];
+    if (lane == 0) {
+        si[threadIdx.x >> 5] = iacc;
+        sd[threadIdx.x >> 5] = dsum;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         __int128 a = 0;
         double b = 0.0;
-        for (int q = 0; q < static_cast<int>(blockDim.x); ++q) {
+        for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) {
             a += si[q];
             b += sd[q];
         }
@@ -936,8 +1040,9 @@ void grid_distinct(Ctx& c, Scratch& s, const double* d_vals, long long Vcap, con
     s.counters.reserve(8 + kMaxK);
     ck(cudaMemsetAsync(s.dtable.p, 0, sizeof(unsigned long long) * tsize * K, c.stream), "memset");
     ck(cudaMemsetAsync(s.counters.p + 8, 0, sizeof(unsigned long long) * K, c.stream), "memset");
-    k_distinct<<<dim3(grid_blocks(Vcap), K), 256, 0, c.stream>>>(d_vals, Vcap, dV, K, s.dtable.p, tsize, s.axisbuf.p,
-                                                                 s.counters.p + 8, kDistinctCap);
+    const int gx = std::min(grid_blocks(Vcap), 256);  // long block loops: few first sightings per block
+    k_distinct<<<dim3(gx, K), 256, 0, c.stream>>>(d_vals, Vcap, dV, K, s.dtable.p, tsize, s.axisbuf.p,
+                                                   s.counters.p + 8, kDistinctCap);
     c.launches++;
 }
 
@@ -1686,17 +1791,19 @@ std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t s
         k_ref_words<<<grid_blocks(count, 128), 128, 0, c.stream>>>(count, derive_key(seed, 0x70617265u), c.n, wd.p);
         c.launches++;
         evaluate_cuts_gemm(c, wd.p, nullptr, count, cv.p);
-        k_col_min<<<grid_blocks(static_cast<long long>(count) * c.k), 256, 0, c.stream>>>(cv.p, count, c.k, rmin.p);
+        k_col_min<<<grid_blocks(count), 256, 0, c.stream>>>(cv.p, count, c.k, rmin.p);
         c.launches++;
         wd.release();  // stream-ordered: no host sync needed
         cv.release();
     } else {
-        k_ref_sample<<<grid_blocks(count, 128), 128, 0, c.stream>>>(count, derive_key(seed, 0x70617265u), c.n, c.m, c.k,
-                                                                     c.d_ei.p, c.d_ej.p, c.d_w.p, rmin.p);
+        const size_t sm = static_cast<size_t>(c.m) * (c.k * 8 + 4);
+        const bool staged = c.n <= 64 && sm <= 48 * 1024;
+        k_ref_sample<<<grid_blocks(count, 128), 128, staged ? sm : 0, c.stream>>>(
+            count, derive_key(seed, 0x70617265u), c.n, c.m, c.k, c.d_ei.p, c.d_ej.p, c.d_w.p, rmin.p, staged);
         c.launches++;
     }
     if (clamp_vals && clamp_rows > 0) {  // clamp_reference (pareto.hpp:647-655): min with every archive row
-        k_col_min<<<grid_blocks(clamp_rows * c.k), 256, 0, c.stream>>>(clamp_vals, clamp_rows, c.k, rmin.p);
+        k_col_min<<<grid_blocks(clamp_rows), 256, 0, c.stream>>>(clamp_vals, clamp_rows, c.k, rmin.p);
         c.launches++;
     }
     auto* ph = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long) * c.k));
@@ -1743,7 +1850,9 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
         const uint64_t b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
         std::memcpy(&maxg, &b, 8);
         for (int k = 0; k < K; ++k) integral &= std::floor(r[static_cast<size_t>(k)]) == r[static_cast<size_t>(k)];
-        if (integral && K * std::log2(std::max(maxg, 1.0)) > 120.0) integral = false;  // keep __int128 exact
+        int e = 0;  // keep __int128 exact: maxg < 2^e, K e <= 120 (the same rule as k_hv_cells)
+        std::frexp(std::max(maxg, 1.0), &e);
+        if (integral && K * e > 120) integral = false;
     };
     if (K == 1) {
         unsigned long long st[3];
@@ -1773,7 +1882,7 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
     s.ipart.reserve(static_cast<size_t>(blocks));
     s.dpart.reserve(static_cast<size_t>(blocks));
     // both sums (the integral one is exact only when the checks below say so): one read-back
-    k_hv_cells<<<blocks, 256, 0, c.stream>>>(s.S.p, cells, g, rp, s.ipart.p, s.dpart.p);
+    k_hv_cells<<<blocks, 256, 0, c.stream>>>(s.S.p, cells, g, rp, s.counters.p + 4, s.ipart.p, s.dpart.p);
     c.launches++;
     ck(cudaGetLastError(), "hv");
     unsigned long long st[3];
