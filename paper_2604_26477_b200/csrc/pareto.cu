@@ -166,9 +166,11 @@ __global__ void __launch_bounds__(256) k_dedup_eval_collapse(
          i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long i = i0 + threadIdx.x;
         bool fresh = false;
-        uint64_t w = 0;
-        if (i < M) {
-            w = words[i];
+        uint64_t w = i < M ? words[i] : ~0ull;
+        // lanes holding the same word (neighbouring trajectories often converge to the same
+        // configuration): only the lowest of them probes the table
+        const unsigned same = __match_any_sync(0xffffffffu, w);
+        if (i < M && (threadIdx.x & 31) == __ffs(same) - 1) {
             uint64_t h = mix64(w) & m1;
             for (;;) {
                 const unsigned long long old = atomicCAS(&t1[h], ~0ull, static_cast<unsigned long long>(w));
@@ -216,6 +218,105 @@ __global__ void __launch_bounds__(256) k_dedup_eval_collapse(
             slot = static_cast<uint32_t>(hv);
         }
         warp_append(vfresh, slot, reps, cnt + 2);
+    }
+}
+
+struct AxisBits {  // per objective: (1 << bits) - 1
+    unsigned long long mask[kMaxK];
+};
+
+// packed cut-value key: objective k at bits [shift_k, shift_k + bits_k) as v_k - lo_k
+struct PackGeo {
+    long long lo[kMaxK];
+    int shift[kMaxK];
+};
+
+// The fused kernel when the K cut values pack into at most 63 bits (cut_pack): the collapse
+// table holds the packed vectors themselves (64-bit keys, empty = ~0), so no value row is
+// written, fenced and re-read for the comparison; the distinct vectors are unpacked from the
+// table afterwards. The unique-config count goes to 32 spread counters (cnt[32..63]).
+template <int KM>
+__global__ void __launch_bounds__(256) k_dedup_eval_collapse_packed(
+    const uint64_t* __restrict__ words, long long M, int m, int K, const int* __restrict__ ei,
+    const int* __restrict__ ej, const int* __restrict__ wi, unsigned long long* t1, uint64_t m1,
+    unsigned long long* t2, unsigned long long* own, uint64_t m2, PackGeo g, uint32_t* reps, unsigned long long* cnt)
+{
+    extern __shared__ __align__(16) int sm[];  // weights (m x KM) | edge pairs (m)
+    int* ew = sm;
+    int* epair = sm + m * KM;
+    for (int e = threadIdx.x; e < m; e += blockDim.x) epair[e] = ei[e] | (ej[e] << 16);
+    for (int q = threadIdx.x; q < m * KM; q += blockDim.x) {
+        const int e = q / KM, k = q % KM;
+        ew[q] = k < K ? wi[e * K + k] : 0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    unsigned long long* ucnt = cnt + 32 + ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & 31);
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x); i0 < M;
+         i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        bool fresh = false;
+        uint64_t w = 0;
+        if (i < M) {
+            w = words[i];
+            uint64_t h = mix64(w) & m1;
+            for (;;) {
+                const unsigned long long old = atomicCAS(&t1[h], ~0ull, static_cast<unsigned long long>(w));
+                if (old == ~0ull) {
+                    fresh = true;
+                    break;
+                }
+                if (old == w) break;
+                h = (h + 1) & m1;
+            }
+        }
+        const unsigned fb = __ballot_sync(0xffffffffu, fresh);
+        if (lane == 0 && fb) atomicAdd(ucnt, static_cast<unsigned long long>(__popc(fb)));
+        bool vfresh = false;
+        uint32_t slot = 0;
+        if (fresh) {
+            int acc[KM];
+            cut_values_int<KM>(w, m, epair, ew, acc);
+            unsigned long long key = 0;
+#pragma unroll
+            for (int k = 0; k < KM; ++k)
+                if (k < K) key |= static_cast<unsigned long long>(static_cast<long long>(acc[k]) - g.lo[k]) << g.shift[k];
+            uint64_t hv = mix64(key) & m2;
+            for (;;) {
+                const unsigned long long old = atomicCAS(&t2[hv], ~0ull, key);
+                if (old == ~0ull) {
+                    vfresh = true;
+                    break;
+                }
+                if (old == key) break;
+                hv = (hv + 1) & m2;
+            }
+            atomicMin(&own[hv], static_cast<unsigned long long>(__brevll(w)));
+            slot = static_cast<uint32_t>(hv);
+        }
+        warp_append(vfresh, slot, reps, cnt + 2);
+    }
+}
+
+// distinct vectors of the packed fused path: values unpacked from the keys, lex-min config
+template <int KM>
+__global__ void k_slots_packed(const uint32_t* __restrict__ reps, const unsigned long long* __restrict__ dV,
+                               const unsigned long long* __restrict__ t2, const unsigned long long* __restrict__ own,
+                               int K, PackGeo g, AxisBits b, double* vv, uint64_t* cfg, uint32_t* ident)
+{
+    const long long V = static_cast<long long>(*dV);
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < V;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const uint32_t sl = reps[i];
+        const unsigned long long key = t2[sl];
+        const unsigned long long ow = own[sl];
+#pragma unroll
+        for (int k = 0; k < KM; ++k)
+            if (k < K)
+                vv[i * K + k] =
+                    static_cast<double>(g.lo[k] + static_cast<long long>((key >> g.shift[k]) & b.mask[k]));
+        cfg[i] = __brevll(ow);
+        ident[i] = static_cast<uint32_t>(i);
     }
 }
 
@@ -1324,11 +1425,6 @@ __global__ void k_map_u32(const uint32_t* __restrict__ idx, const uint32_t* __re
         out[i] = map[idx[i]];
 }
 
-// rank[i] = position of row i in the lexicographically descending order (rows distinct)
-struct PackGeo {
-    long long lo[kMaxK];
-    int shift[kMaxK];
-};
 
 // packed lexicographic key: objective 0 in the most significant bits (exact: integer cut
 // values within their ranges)
@@ -1508,43 +1604,79 @@ void filter_pool_fused(Ctx& c, Scratch& s, const uint64_t* d_words, long long M,
     cudaEventCreate(&e1);
     cudaEventRecord(e0, c.stream);
     const uint64_t t1 = pow2_at_least(2ull * static_cast<uint64_t>(M) + 16);
-    s.dtab64.reserve(t1 * 2);           // dedup keys | collapse owners
-    s.table2.reserve(t1);               // collapse rows
-    s.vals.reserve(static_cast<size_t>(M) * K + 1);
+    int pbits = 0;
+    for (int k = 0; k < K; ++k) pbits += c.cut_bits[static_cast<size_t>(k)];
+    const bool packed = c.cut_pack && pbits <= 63;  // ~0 is then no vector's key
+    s.dtab64.reserve(t1 * 2);  // dedup keys | collapse owners
+    if (!packed) {
+        s.table2.reserve(t1);  // collapse rows
+        s.vals.reserve(static_cast<size_t>(M) * K + 1);
+        ck(cudaMemsetAsync(s.table2.p, 0xFF, sizeof(uint32_t) * t1, c.stream), "memset");
+    }
     s.reps.reserve(static_cast<size_t>(M) + 1);
-    s.counters.reserve(8 + kMaxK);
+    s.counters.reserve(64);  // [0] unique configs, [2] distinct vectors, [8, 8+K) axis counts,
+                             // [32, 64) spread unique-config counters (packed path)
     ck(cudaMemsetAsync(s.dtab64.p, 0xFF, sizeof(unsigned long long) * t1 * 2, c.stream), "memset");
-    ck(cudaMemsetAsync(s.table2.p, 0xFF, sizeof(uint32_t) * t1, c.stream), "memset");
-    ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long) * 8, c.stream), "memset");
+    ck(cudaMemsetAsync(s.counters.p, 0, sizeof(unsigned long long) * 64, c.stream), "memset");
     const int KM = K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : 16;
     const int sm = c.m * (1 + KM) * 4;
-    auto kern = KM == 2 ? k_dedup_eval_collapse<2> : KM == 4 ? k_dedup_eval_collapse<4>
-                : KM == 8 ? k_dedup_eval_collapse<8> : k_dedup_eval_collapse<16>;
-    kern<<<grid_blocks(M), 256, sm, c.stream>>>(d_words, M, c.m, K, c.d_ei.p, c.d_ej.p, c.d_wi.p, s.dtab64.p, t1 - 1,
-                                                 s.table2.p, s.dtab64.p + t1, t1 - 1, s.vals.p, s.reps.p, s.counters.p);
-    c.launches++;
-    ck(cudaGetLastError(), "dedup+eval+collapse");
     DevBuf<uint32_t> vrow, vown;
     DevBuf<uint64_t> vcfg;
-    vrow.reserve(static_cast<size_t>(M) + 1);
+    DevBuf<double> vv;
     vown.reserve(static_cast<size_t>(M) + 1);
     vcfg.reserve(static_cast<size_t>(M) + 1);
-    const unsigned long long* dV = s.counters.p + 2;
-    k_slots_fused<<<grid_blocks(M), 256, 0, c.stream>>>(s.reps.p, dV, s.table2.p, s.dtab64.p + t1, vrow.p, vcfg.p,
-                                                          vown.p);
-    DevBuf<double> vv;
     vv.reserve(static_cast<size_t>(M) * K + 1);
-    k_gather_vals_dev<<<grid_blocks(M * K), 256, 0, c.stream>>>(s.vals.p, vrow.p, dV, K, vv.p);
-    c.launches += 2;
+    const unsigned long long* dV = s.counters.p + 2;
+    if (packed) {
+        PackGeo g{};
+        AxisBits b{};
+        int sh = 64;
+        for (int k = 0; k < K; ++k) {
+            const int bits = c.cut_bits[static_cast<size_t>(k)];
+            sh -= bits;
+            g.lo[k] = c.cut_lo[static_cast<size_t>(k)];
+            g.shift[k] = sh;
+            b.mask[k] = bits >= 64 ? ~0ull : (1ull << bits) - 1;
+        }
+        DevBuf<unsigned long long> t2;
+        t2.reserve(t1);
+        ck(cudaMemsetAsync(t2.p, 0xFF, sizeof(unsigned long long) * t1, c.stream), "memset");
+        auto kern = KM == 2 ? k_dedup_eval_collapse_packed<2> : KM == 4 ? k_dedup_eval_collapse_packed<4>
+                    : KM == 8 ? k_dedup_eval_collapse_packed<8> : k_dedup_eval_collapse_packed<16>;
+        kern<<<grid_blocks(M), 256, sm, c.stream>>>(d_words, M, c.m, K, c.d_ei.p, c.d_ej.p, c.d_wi.p, s.dtab64.p,
+                                                     t1 - 1, t2.p, s.dtab64.p + t1, t1 - 1, g, s.reps.p,
+                                                     s.counters.p);
+        ck(cudaGetLastError(), "dedup+eval+collapse");
+        auto ks = KM == 2 ? k_slots_packed<2> : KM == 4 ? k_slots_packed<4>
+                  : KM == 8 ? k_slots_packed<8> : k_slots_packed<16>;
+        ks<<<grid_blocks(M), 256, 0, c.stream>>>(s.reps.p, dV, t2.p, s.dtab64.p + t1, K, g, b, vv.p, vcfg.p, vown.p);
+        t2.release();
+        c.launches += 2;
+    } else {
+        auto kern = KM == 2 ? k_dedup_eval_collapse<2> : KM == 4 ? k_dedup_eval_collapse<4>
+                    : KM == 8 ? k_dedup_eval_collapse<8> : k_dedup_eval_collapse<16>;
+        kern<<<grid_blocks(M), 256, sm, c.stream>>>(d_words, M, c.m, K, c.d_ei.p, c.d_ej.p, c.d_wi.p, s.dtab64.p,
+                                                     t1 - 1, s.table2.p, s.dtab64.p + t1, t1 - 1, s.vals.p, s.reps.p,
+                                                     s.counters.p);
+        c.launches++;
+        ck(cudaGetLastError(), "dedup+eval+collapse");
+        vrow.reserve(static_cast<size_t>(M) + 1);
+        k_slots_fused<<<grid_blocks(M), 256, 0, c.stream>>>(s.reps.p, dV, s.table2.p, s.dtab64.p + t1, vrow.p,
+                                                              vcfg.p, vown.p);
+        k_gather_vals_dev<<<grid_blocks(M * K), 256, 0, c.stream>>>(s.vals.p, vrow.p, dV, K, vv.p);
+        c.launches += 2;
+    }
     grid_distinct(c, s, vv.p, M, dV, K);
     cudaEventRecord(e1, c.stream);
-    auto* ph = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long) * (8 + K)));
-    ck(cudaMemcpyAsync(ph, s.counters.p, sizeof(unsigned long long) * (8 + K), cudaMemcpyDeviceToHost, c.stream),
-       "D2H");
+    auto* ph = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long) * 64));
+    ck(cudaMemcpyAsync(ph, s.counters.p, sizeof(unsigned long long) * 64, cudaMemcpyDeviceToHost, c.stream), "D2H");
     ck(cudaStreamSynchronize(c.stream), "counts");
-    unsigned long long h[8 + kMaxK];
-    std::memcpy(h, ph, sizeof(unsigned long long) * (8 + K));
-    const long long U = static_cast<long long>(h[0]), V = static_cast<long long>(h[2]);
+    unsigned long long h[64];
+    std::memcpy(h, ph, sizeof h);
+    long long U = static_cast<long long>(h[0]);
+    if (packed)
+        for (int q = 32; q < 64; ++q) U += static_cast<long long>(h[q]);
+    const long long V = static_cast<long long>(h[2]);
     if (tm) {
         tm->unique_configs = U;
         tm->dedup_s = seconds_between(e0, e1);  // dedup + evaluation + collapse + axis values
