@@ -605,17 +605,17 @@ def main():
             r_frozen = [float(x) for x in g["reference"]]
             target = float(g["hv_star"])
             ik, wk, ck = shapes[k]
-            sessions = [api.Session(local)]
-            for sk in sessions:
+            tto_sessions = [api.Session(local)]
+            for sk in tto_sessions:
                 sk.set_instance(ik)  # warm the contexts (module load, pools) outside the clock
                 sk.set_weights(wk)
                 sk.pipeline(ck, 1, 0, sk.num_blocks(ck, 1), do_hv=False)
             sync_all()
             t0 = time.perf_counter()
-            for sk in sessions:
+            for sk in tto_sessions:
                 sk.set_instance(ik)  # model build inside the clock
                 sk.set_weights(wk)
-            res = streaming.time_to_target(sessions[0], ck, r_frozen, target, TTO_MAX_RUNS[k], world, rank,
+            res = streaming.time_to_target(tto_sessions[0], ck, r_frozen, target, TTO_MAX_RUNS[k], world, rank,
                                            torch.device("cuda", local), runs_per_step=TTO_RUNS_PER_STEP[k])
             torch.cuda.synchronize(local)
             secs = time.perf_counter() - t0
@@ -626,7 +626,7 @@ def main():
                             "archive": res["archive"], "front_exact": int(g["values"].shape[0]),
                             "reference_frozen": r_frozen, "runs_per_check": TTO_RUNS_PER_STEP[k] * world,
                             "shape": "C2 (K=4 dSB, 220 x 4546)" if k == 4 else "C1 (K=3 bSB, 190 x 3000)"}
-            del sessions
+            del tto_sessions
 
     # ---- the other BASELINE configs: C4 (dense tensor-core dSB) and C5 (1e8-sample Pareto
     #      stress); every rank samples its share of the blocks, fronts merge over NCCL

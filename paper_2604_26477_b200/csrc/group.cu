@@ -453,13 +453,15 @@ int momc_b200_group_bench(momc_group* g, const momc_instance_view* inst, const i
         rep->sampler_path = root.last_path;
         const auto tr = clk::now();
         std::vector<double> r(static_cast<size_t>(root.k));
-        if (fixed_ref) r.assign(fixed_ref, fixed_ref + root.k);
-        else r = reference_point_sampled_device(root, ref_count, cfg->seed, a.vals.p, a.F);
-        const auto th = clk::now();
-        rep->reference_s = std::chrono::duration<double>(th - tr).count();
-        rep->hv = hypervolume_device(root, a.vals.p, a.F, a.K, r, true);
+        if (fixed_ref) {
+            r.assign(fixed_ref, fixed_ref + root.k);
+            rep->hv = hypervolume_device(root, a.vals.p, a.F, a.K, r, true);
+        } else {
+            rep->hv = hv_sampled_reference_device(root, a.vals.p, a.F, a.K, ref_count, cfg->seed, r, true);
+        }
         const auto te = clk::now();
-        rep->hv_s = std::chrono::duration<double>(te - th).count();
+        rep->reference_s = 0;
+        rep->hv_s = std::chrono::duration<double>(te - tr).count();
         for (int l = 0; l < root.k && l < 16; ++l) rep->reference[l] = r[static_cast<size_t>(l)];
         rep->pareto_filtering_s = std::chrono::duration<double>(te - tf).count();
         if (out_pool || out_stamps_ns) gather_pool(*g, out_pool, out_stamps_ns);

@@ -603,10 +603,6 @@ __global__ void k_distinct(const double* __restrict__ vals, long long V, const u
     }
 }
 
-struct RPoint {  // the reference point, by value
-    double v[kMaxK];
-};
-
 struct AxisCounts {
     int d[kMaxK];
 };
@@ -893,6 +889,17 @@ __global__ void k_ref_words(int count, uint64_t key, int n, uint64_t* words)
     }
 }
 
+// ordered keys (dkey) -> the doubles they encode
+__global__ void k_keys_to_vals(const unsigned long long* __restrict__ keys, int K, double* out)
+{
+    const int k = threadIdx.x;
+    if (k < K) {
+        const unsigned long long key = keys[k];
+        const unsigned long long b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
+        out[k] = __longlong_as_double(static_cast<long long>(b));
+    }
+}
+
 // per-objective minimum (ordered keys): one thread per row, a warp minimum per objective,
 // then one atomic per warp and objective (the K counters are contended otherwise)
 __global__ void k_col_min(const double* __restrict__ vals, long long rows, int K, unsigned long long* rmin)
@@ -921,7 +928,7 @@ __global__ void k_col_min(const double* __restrict__ vals, long long rows, int K
 // stats[1]: the largest gain's key): integral data and r give the exact __int128 sum (64-bit
 // cell products when gain^K < 2^62), anything else the Kahan FP64 sum; the host reads the
 // matching partials.
-__global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, GridGeo g, const RPoint rp,
+__global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, GridGeo g, const double* __restrict__ r,
                            const unsigned long long* __restrict__ stats, __int128* ipart, double* dpart)
 {
     const int lane = threadIdx.x & 31;
@@ -931,7 +938,6 @@ __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, Grid
     const long long warps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     __int128 iacc = 0;
     double dacc = 0.0, dc = 0.0;
-    const double* r = rp.v;
     const double rl = r[g.dims];
     bool integral = stats[0] != 0;
     for (int a = 0; a <= g.dims; ++a) integral &= floor(r[a]) == r[a];
@@ -1020,10 +1026,9 @@ __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, Grid
     }
 }
 
-__global__ void k_ref_check(const double* __restrict__ vals, long long F, int K, const RPoint rp,
+__global__ void k_ref_check(const double* __restrict__ vals, long long F, int K, const double* __restrict__ r,
                             unsigned long long* first)
 {
-    const double* r = rp.v;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
         for (int k = 0; k < K; ++k)
@@ -1032,10 +1037,9 @@ __global__ void k_ref_check(const double* __restrict__ vals, long long F, int K,
 
 // integrality of the archive values and the largest gain v - r (decides the exact __int128 HV
 // sum): flags[0] &= every value is an integer below 9e15, flags[1] = max dkey(gain)
-__global__ void k_hv_stats(const double* __restrict__ vals, long long F, int K, const RPoint rp,
+__global__ void k_hv_stats(const double* __restrict__ vals, long long F, int K, const double* __restrict__ r,
                            unsigned long long* flags)
 {
-    const double* r = rp.v;
     bool integral = true;
     unsigned long long gmax = dkey(0.0);
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F * K;
@@ -1904,16 +1908,16 @@ void filter_values_device(Ctx& c, const double* d_vals, const uint64_t* d_words,
     vv.release();
 }
 
-std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed, const double* clamp_vals,
-                                                   long long clamp_rows)
+namespace {
+
+// reference_point_sampled (pareto.hpp:620-642) [+ clamp_reference :647-655] as K ordered keys
+// in d_keys (dkey of each objective's minimum), launches only
+void reference_keys_device(Ctx& c, int count, uint64_t seed, const double* clamp_vals, long long clamp_rows,
+                           unsigned long long* d_keys)
 {
     if (count < 1) usage("sampled reference needs count >= 1");
     if (c.n > 4096) usage("reference sampling on the GPU path supports n <= 4096");
-    Scratch& s = scratch(c);
-    s.counters.reserve(8 + kMaxK);
-    DevBuf<unsigned long long> rmin;
-    rmin.reserve(static_cast<size_t>(c.k));
-    ck(cudaMemsetAsync(rmin.p, 0xFF, sizeof(unsigned long long) * c.k, c.stream), "memset");
+    ck(cudaMemsetAsync(d_keys, 0xFF, sizeof(unsigned long long) * c.k, c.stream), "memset");
     if (eval_gemm_ok(c)) {  // cut_values == evaluate_cuts exactly for integer weights
         const int wpc = (c.n + 63) / 64;
         DevBuf<uint64_t> wd;
@@ -1923,7 +1927,7 @@ std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t s
         k_ref_words<<<grid_blocks(count, 128), 128, 0, c.stream>>>(count, derive_key(seed, 0x70617265u), c.n, wd.p);
         c.launches++;
         evaluate_cuts_gemm(c, wd.p, nullptr, count, cv.p);
-        k_col_min<<<grid_blocks(count), 256, 0, c.stream>>>(cv.p, count, c.k, rmin.p);
+        k_col_min<<<grid_blocks(count), 256, 0, c.stream>>>(cv.p, count, c.k, d_keys);
         c.launches++;
         wd.release();  // stream-ordered: no host sync needed
         cv.release();
@@ -1931,46 +1935,61 @@ std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t s
         const size_t sm = static_cast<size_t>(c.m) * (c.k * 8 + 4);
         const bool staged = c.n <= 64 && sm <= 48 * 1024;
         k_ref_sample<<<grid_blocks(count, 128), 128, staged ? sm : 0, c.stream>>>(
-            count, derive_key(seed, 0x70617265u), c.n, c.m, c.k, c.d_ei.p, c.d_ej.p, c.d_w.p, rmin.p, staged);
+            count, derive_key(seed, 0x70617265u), c.n, c.m, c.k, c.d_ei.p, c.d_ej.p, c.d_w.p, d_keys, staged);
         c.launches++;
     }
     if (clamp_vals && clamp_rows > 0) {  // clamp_reference (pareto.hpp:647-655): min with every archive row
-        k_col_min<<<grid_blocks(clamp_rows), 256, 0, c.stream>>>(clamp_vals, clamp_rows, c.k, rmin.p);
+        k_col_min<<<grid_blocks(clamp_rows), 256, 0, c.stream>>>(clamp_vals, clamp_rows, c.k, d_keys);
         c.launches++;
     }
-    auto* ph = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long) * c.k));
-    ck(cudaMemcpyAsync(ph, rmin.p, sizeof(unsigned long long) * c.k, cudaMemcpyDeviceToHost, c.stream), "D2H");
-    ck(cudaStreamSynchronize(c.stream), "reference point");
-    const std::vector<unsigned long long> h(ph, ph + c.k);
-    rmin.release();
-    std::vector<double> r(static_cast<size_t>(c.k));
-    for (int k = 0; k < c.k; ++k) {
-        const uint64_t key = h[static_cast<size_t>(k)];
+}
+
+std::vector<double> decode_keys(const unsigned long long* h, int K)
+{
+    std::vector<double> r(static_cast<size_t>(K));
+    for (int k = 0; k < K; ++k) {
+        const uint64_t key = h[k];
         const uint64_t b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
         std::memcpy(&r[static_cast<size_t>(k)], &b, 8);
     }
     return r;
 }
 
-double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, const std::vector<double>& r,
-                          bool reuse_front_grid)
+}  // namespace
+
+std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t seed, const double* clamp_vals,
+                                                   long long clamp_rows)
+{
+    DevBuf<unsigned long long> rmin;
+    rmin.reserve(static_cast<size_t>(c.k));
+    reference_keys_device(c, count, seed, clamp_vals, clamp_rows, rmin.p);
+    auto* ph = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long) * c.k));
+    ck(cudaMemcpyAsync(ph, rmin.p, sizeof(unsigned long long) * c.k, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaStreamSynchronize(c.stream), "reference point");
+    const std::vector<double> r = decode_keys(ph, c.k);
+    rmin.release();
+    return r;
+}
+
+namespace {
+
+// Hypervolume of the archive (d_vals, F x K) at the reference point in device memory (d_r).
+// With rkeys (the K ordered keys d_r was decoded from) r is read back with the sums and
+// returned in r; otherwise r holds it already. One read-back: [r keys] | checks | partials.
+double hv_core(Ctx& c, Scratch& s, const double* d_vals, long long F, int K, const double* d_r,
+               std::vector<double>& r, const unsigned long long* rkeys, bool reuse_front_grid)
 {
     if (F <= 0) usage("hypervolume of an empty archive");
-    if (static_cast<int>(r.size()) != K) usage("reference point length does not match archive");
     if (K > kMaxK) usage("the GPU path supports at most 16 objectives");
-    Scratch& s = scratch(c);
-    s.counters.reserve(8);
-    RPoint rp{};
-    for (int k = 0; k < K; ++k) rp.v[k] = r[static_cast<size_t>(k)];
     const unsigned long long none = ~0ull;
     // counters[3] first bad entry (none), [4] integral flag (all ones), [5] max dkey(gain)
     // (0: below every gain's key; the host floors it at 1 anyway)
     ck(cudaMemsetAsync(s.counters.p + 3, 0xFF, sizeof(unsigned long long) * 2, c.stream), "memset");
     ck(cudaMemsetAsync(s.counters.p + 5, 0, sizeof(unsigned long long), c.stream), "memset");
-    k_ref_check<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, F, K, rp, s.counters.p + 3);
+    k_ref_check<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, F, K, d_r, s.counters.p + 3);
     // gains are exact integers when every value and r is integral (n=42 configs): then the
     // __int128 cell sum is the exact hypervolume, i.e. the reference's exact double result
-    k_hv_stats<<<grid_blocks(F * K), 256, 0, c.stream>>>(d_vals, F, K, rp, s.counters.p + 4);
+    k_hv_stats<<<grid_blocks(F * K), 256, 0, c.stream>>>(d_vals, F, K, d_r, s.counters.p + 4);
     c.launches += 2;
     auto finish_checks = [&](const unsigned long long* st, bool& integral) {
         if (st[0] != none)
@@ -1986,12 +2005,15 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
         std::frexp(std::max(maxg, 1.0), &e);
         if (integral && K * e > 120) integral = false;
     };
+    const size_t kb = rkeys ? 16 * sizeof(unsigned long long) : 0;  // r keys lead the read-back
     if (K == 1) {
         unsigned long long st[3];
-        auto* pst = static_cast<unsigned long long*>(pinned_buf(c, sizeof st));
-        ck(cudaMemcpyAsync(pst, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        unsigned char* pb = static_cast<unsigned char*>(pinned_buf(c, kb + sizeof st));
+        if (rkeys) ck(cudaMemcpyAsync(pb, rkeys, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream), "D2H");
+        ck(cudaMemcpyAsync(pb + kb, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
         ck(cudaStreamSynchronize(c.stream), "sync");
-        std::memcpy(st, pst, sizeof st);
+        if (rkeys) r = decode_keys(reinterpret_cast<const unsigned long long*>(pb), 1);
+        std::memcpy(st, pb + kb, sizeof st);
         bool integral;
         finish_checks(st, integral);
         double best = 0;  // pareto.hpp:544-548
@@ -2013,25 +2035,26 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
     const int blocks = grid_blocks(lines * 32);
     s.ipart.reserve(static_cast<size_t>(blocks));
     s.dpart.reserve(static_cast<size_t>(blocks));
-    // both sums (the integral one is exact only when the checks below say so): one read-back
-    k_hv_cells<<<blocks, 256, 0, c.stream>>>(s.S.p, cells, g, rp, s.counters.p + 4, s.ipart.p, s.dpart.p);
+    k_hv_cells<<<blocks, 256, 0, c.stream>>>(s.S.p, cells, g, d_r, s.counters.p + 4, s.ipart.p, s.dpart.p);
     c.launches++;
     ck(cudaGetLastError(), "hv");
     unsigned long long st[3];
-    // one page-locked read-back: checks | __int128 partials | FP64 partials
     const size_t nb = static_cast<size_t>(blocks);
-    unsigned char* pb = static_cast<unsigned char*>(pinned_buf(c, 32 + nb * (sizeof(__int128) + sizeof(double))));
-    ck(cudaMemcpyAsync(pb, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
-    ck(cudaMemcpyAsync(pb + 32, s.ipart.p, sizeof(__int128) * nb, cudaMemcpyDeviceToHost, c.stream), "D2H");
-    ck(cudaMemcpyAsync(pb + 32 + sizeof(__int128) * nb, s.dpart.p, sizeof(double) * nb, cudaMemcpyDeviceToHost,
+    unsigned char* pb =
+        static_cast<unsigned char*>(pinned_buf(c, kb + 32 + nb * (sizeof(__int128) + sizeof(double))));
+    if (rkeys) ck(cudaMemcpyAsync(pb, rkeys, sizeof(unsigned long long) * K, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaMemcpyAsync(pb + kb, s.counters.p + 3, sizeof st, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaMemcpyAsync(pb + kb + 32, s.ipart.p, sizeof(__int128) * nb, cudaMemcpyDeviceToHost, c.stream), "D2H");
+    ck(cudaMemcpyAsync(pb + kb + 32 + sizeof(__int128) * nb, s.dpart.p, sizeof(double) * nb, cudaMemcpyDeviceToHost,
                        c.stream),
        "D2H");
     ck(cudaStreamSynchronize(c.stream), "hv");
-    std::memcpy(st, pb, sizeof st);
+    if (rkeys) r = decode_keys(reinterpret_cast<const unsigned long long*>(pb), K);
+    std::memcpy(st, pb + kb, sizeof st);
     std::vector<__int128> ip(nb);
     std::vector<double> dp(nb);
-    std::memcpy(ip.data(), pb + 32, sizeof(__int128) * nb);
-    std::memcpy(dp.data(), pb + 32 + sizeof(__int128) * nb, sizeof(double) * nb);
+    std::memcpy(ip.data(), pb + kb + 32, sizeof(__int128) * nb);
+    std::memcpy(dp.data(), pb + kb + 32 + sizeof(__int128) * nb, sizeof(double) * nb);
     bool integral;
     finish_checks(st, integral);
     if (integral) {
@@ -2047,6 +2070,41 @@ double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, cons
         tot = t;
     }
     return tot;
+}
+
+}  // namespace
+
+double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, const std::vector<double>& r,
+                          bool reuse_front_grid)
+{
+    if (F <= 0) usage("hypervolume of an empty archive");
+    if (static_cast<int>(r.size()) != K) usage("reference point length does not match archive");
+    if (K > kMaxK) usage("the GPU path supports at most 16 objectives");
+    Scratch& s = scratch(c);
+    s.counters.reserve(8);
+    s.rdev.reserve(static_cast<size_t>(kMaxK));
+    auto* pr = static_cast<double*>(pinned_buf(c, sizeof(double) * K));
+    std::memcpy(pr, r.data(), sizeof(double) * K);
+    ck(cudaMemcpyAsync(s.rdev.p, pr, sizeof(double) * K, cudaMemcpyHostToDevice, c.stream), "H2D");
+    std::vector<double> rr = r;
+    return hv_core(c, s, d_vals, F, K, s.rdev.p, rr, nullptr, reuse_front_grid);
+}
+
+double hv_sampled_reference_device(Ctx& c, const double* d_vals, long long F, int K, int count, uint64_t seed,
+                                   std::vector<double>& r_out, bool reuse_front_grid)
+{
+    if (F <= 0) usage("hypervolume of an empty archive");
+    Scratch& s = scratch(c);
+    s.counters.reserve(8);
+    s.rdev.reserve(static_cast<size_t>(kMaxK));
+    DevBuf<unsigned long long> keys;
+    keys.reserve(static_cast<size_t>(kMaxK));
+    reference_keys_device(c, count, seed, d_vals, F, keys.p);
+    k_keys_to_vals<<<1, 32, 0, c.stream>>>(keys.p, K, s.rdev.p);
+    c.launches++;
+    const double hv = hv_core(c, s, d_vals, F, K, s.rdev.p, r_out, keys.p, reuse_front_grid);
+    keys.release();
+    return hv;
 }
 
 namespace {

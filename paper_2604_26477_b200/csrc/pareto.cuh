@@ -59,4 +59,9 @@ std::vector<double> reference_point_sampled_device(Ctx& c, int count, uint64_t s
 double hypervolume_device(Ctx& c, const double* d_vals, long long F, int K, const std::vector<double>& r,
                           bool reuse_front_grid = false);
 
+// reference_point_sampled clamped under the archive (pareto.hpp:620-655) and the hypervolume
+// at it, with r kept on the device between the two: one host round trip; r_out receives r
+double hv_sampled_reference_device(Ctx& c, const double* d_vals, long long F, int K, int count, uint64_t seed,
+                                   std::vector<double>& r_out, bool reuse_front_grid = false);
+
 }  // namespace momc_b200
