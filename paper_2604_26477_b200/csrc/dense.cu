@@ -151,6 +151,24 @@ __device__ __noinline__ bool exp_decides(double lhs, double targ) { return lhs <
 // exp brackets the FP64 one within 1e-6 relative on [-6, 0], so outside a +-1e-5 band around
 // it the decision is taken in FP32 (lhs rounded to FP32 moves by < 1e-7 relative); the FP64
 // exp decides inside the band
+// the same decision from FP32 copies of wn / fn (the batch sampler's bracket, sampler_batch.cuh:
+// x, -x^2/2 and lhs in FP32 are within ~4e-6 / 5e-7 relative of their FP64 values; a 4e-5 band
+// leaves a 10x margin); the FP64 test only inside the band
+__device__ __forceinline__ bool wedge_accept32(uint32_t u, uint32_t w1, uint32_t w2, const ZigTables& z,
+                                               const float* wnf, const float* fnf)
+{
+    const uint32_t iz = u & 127u;
+    const float xf = __int2float_rn(static_cast<int32_t>(u)) * wnf[iz];
+    const float ef = __expf(-0.5f * xf * xf);
+    const float uf = __uint2float_rz(w2 >> 8) * 0x1.0p-24f;  // the top 24 bits of u01, exact
+    const float lf = __fmaf_rn(uf, fnf[iz - 1] - fnf[iz], fnf[iz]);
+    if (lf < ef * (1.0f - 4e-5f)) return true;
+    if (lf > ef * (1.0f + 4e-5f)) return false;
+    const double xv = __dmul_rn(static_cast<double>(static_cast<int32_t>(u)), z.wn[iz]);
+    const double lhs = __dadd_rn(z.fn[iz], __dmul_rn(u01_from(w1, w2), __dsub_rn(z.fn[iz - 1], z.fn[iz])));
+    return exp_decides(lhs, __dmul_rn(__dmul_rn(-0.5, xv), xv));
+}
+
 __device__ __forceinline__ bool wedge_accept(uint32_t u, uint32_t w1, uint32_t w2, const ZigTables& z)
 {
     const uint32_t iz = u & 127u;
@@ -212,11 +230,16 @@ template <bool NOISY, bool UDT, typename PhiT>
 __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_constant__ DenseStepArgs a)
 {
     __shared__ ZigTables z;
+    __shared__ float zwf[128], zff[128];
     __shared__ __align__(16) uint32_t rings[kWWarps][kWRing];
     __shared__ double vals[kWWarps][32];
     if constexpr (NOISY) {
         for (int q = threadIdx.x; q < static_cast<int>(sizeof(ZigTables) / 4); q += blockDim.x)
             reinterpret_cast<uint32_t*>(&z)[q] = reinterpret_cast<const uint32_t*>(a.zig)[q];
+        for (int q = threadIdx.x; q < 128; q += blockDim.x) {
+            zwf[q] = static_cast<float>(a.zig->wn[q]);
+            zff[q] = static_cast<float>(a.zig->fn[q]);
+        }
         __syncthreads();
     }
     const DensePairArg& pr = a.pair[blockIdx.y];
@@ -275,7 +298,8 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
             int len = 1;
             if (slow) {
                 if (u & 127u) {
-                    good = wedge_accept(u, ring[(H + lane + 1) & (kWRing - 1)], ring[(H + lane + 2) & (kWRing - 1)], z);
+                    good = wedge_accept32(u, ring[(H + lane + 1) & (kWRing - 1)], ring[(H + lane + 2) & (kWRing - 1)], z,
+                                          zwf, zff);
                     len = 3;
                 } else {
                     const double r = 3.442619855899;
@@ -340,9 +364,16 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
             if constexpr (NOISY) d = __dadd_rn(d, __dmul_rn(a.alpha, eta));
             yi = __dadd_rn(yi, UDT ? d : __dmul_rn(a.dt, d));
             xi = __dadd_rn(xi, UDT ? yi : __dmul_rn(a.sdt, yi));
-            if (fabs(xi) > 1.0) {  // wall + clamp (both fire exactly when |x| > 1)
-                yi = 0.0;
-                xi = __hiloint2double((__double2hiint(xi) & static_cast<int>(0x80000000u)) | 0x3FF00000, 0);
+            {  // wall + clamp (both fire exactly when |x| > 1): one predicate, one LOP3 for +-1
+                uint32_t xl = static_cast<uint32_t>(__double2loint(xi)), xh = static_cast<uint32_t>(__double2hiint(xi));
+                uint32_t yl = static_cast<uint32_t>(__double2loint(yi)), yh = static_cast<uint32_t>(__double2hiint(yi));
+                asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %4, 0d3FF0000000000000;\n\t"
+                    "@p lop3.b32 %1, %1, 0x80000000, %5, 0xEA;\n\t@p mov.b32 %0, 0;\n\t"
+                    "@p mov.b32 %2, 0;\n\t@p mov.b32 %3, 0;\n\t}"
+                    : "+r"(xl), "+r"(xh), "+r"(yl), "+r"(yh)
+                    : "d"(fabs(xi)), "r"(0x3FF00000u));
+                xi = __hiloint2double(static_cast<int>(xh), static_cast<int>(xl));
+                yi = __hiloint2double(static_cast<int>(yh), static_cast<int>(yl));
             }
             // the first step with a non-finite x or y has a non-finite y (x = x + dt a0 y, walls)
             nonfinite |= !(fabs(yi) <= 1.7976931348623157e308);
