@@ -21,6 +21,16 @@ using namespace momc_b200;
 
 namespace momc_b200 {
 
+// out row i = -(in row F - 1 - i) (the Hamiltonian-sense archive order, momc_b200_filter_values)
+__global__ void k_negate_reverse_rows(const double* __restrict__ in, long long F, int K, double* __restrict__ out)
+{
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < F * K;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = q / K, k = q % K;
+        out[q] = -in[(F - 1 - i) * K + k];
+    }
+}
+
 Ctx::~Ctx()
 {
     cudaSetDevice(device);
@@ -926,18 +936,18 @@ int momc_b200_filter_values(momc_ctx* ctx, const double* vals, size_t M, int k, 
         filter_values_device(*ctx, dv.p, nullptr, 0, 0, static_cast<long long>(M), k, a, nullptr);
         ck(cudaStreamSynchronize(ctx->stream), "sync");
         dv.release();
-        if (sense) {  // back to Hamiltonian values, archive ordered by them (pareto.hpp:283-289)
-            std::vector<double> f(static_cast<size_t>(a.F) * k);
-            ck(cudaMemcpy(f.data(), a.vals.p, sizeof(double) * f.size(), cudaMemcpyDeviceToHost), "D2H");
-            std::vector<std::vector<double>> rows(static_cast<size_t>(a.F));
-            for (long long i = 0; i < a.F; ++i) {
-                rows[static_cast<size_t>(i)].assign(f.begin() + i * k, f.begin() + (i + 1) * k);
-                for (double& x : rows[static_cast<size_t>(i)]) x = -x;
-            }
-            std::sort(rows.begin(), rows.end(), std::greater<>());
-            for (long long i = 0; i < a.F; ++i)
-                std::copy(rows[static_cast<size_t>(i)].begin(), rows[static_cast<size_t>(i)].end(), f.begin() + i * k);
-            ck(cudaMemcpy(a.vals.p, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice), "H2D");
+        if (sense && a.F > 0) {
+            // back to Hamiltonian values, archive ordered by them (pareto.hpp:283-289): negating
+            // reverses the lexicographic order, so the lex-descending front in maximisation
+            // space becomes lex-descending in Hamiltonian values by negating every value and
+            // reversing the rows (rows are distinct)
+            DevBuf<double> t;
+            t.reserve(static_cast<size_t>(a.F) * k);
+            k_negate_reverse_rows<<<(static_cast<unsigned>(a.F * k) + 255) / 256, 256, 0, ctx->stream>>>(a.vals.p, a.F,
+                                                                                                       k, t.p);
+            ck(cudaMemcpyAsync(a.vals.p, t.p, sizeof(double) * a.F * k, cudaMemcpyDeviceToDevice, ctx->stream), "D2D");
+            ck(cudaStreamSynchronize(ctx->stream), "sync");
+            t.release();
         }
         if (out_F) *out_F = a.F;
     });
