@@ -92,5 +92,36 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     return LIB
 
 
+PROF_SRC = os.path.join(PKG, "prof", "cupti_traffic.cpp")
+PROF_LIB = os.path.join(PKG, "libmomc_b200_prof.so")
+
+
+def build_prof(verbose: bool = False) -> str | None:
+    """libmomc_b200_prof.so: in-process DRAM traffic of kernels through the CUPTI range profiler
+    (bench.py's roofline.traffic). Measurement tooling, separate from the product library; None
+    when CUPTI is not installed."""
+    cuda = os.path.dirname(os.path.dirname(_nvcc()))
+    inc = os.path.join(cuda, "include")
+    if not os.path.exists(os.path.join(inc, "cupti_range_profiler.h")):
+        return None
+    with open(PROF_SRC, "rb") as fh:
+        key = hashlib.sha256(fh.read()).hexdigest()[:16]
+    stamp = PROF_LIB + ".stamp"
+    if os.path.exists(PROF_LIB) and os.path.exists(stamp) and open(stamp).read() == key:
+        return PROF_LIB
+    cmd = ["g++", "-O2", "-fPIC", "-shared", "-std=c++17", "-I" + inc, PROF_SRC, "-o", PROF_LIB + ".tmp",
+           "-L" + os.path.join(cuda, "lib64"), "-Wl,-rpath," + os.path.join(cuda, "lib64"), "-lcupti", "-lcuda"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        if verbose:
+            print(f"  (prof library not built: {res.stderr[-500:]})", file=sys.stderr)
+        return None
+    os.replace(PROF_LIB + ".tmp", PROF_LIB)
+    with open(stamp, "w") as fh:
+        fh.write(key)
+    return PROF_LIB
+
+
 if __name__ == "__main__":
     print(build(verbose=True))
+    print(build_prof(verbose=True))
