@@ -1,9 +1,9 @@
 #pragma once
 // SB sampler, batched noise resolution (n <= 42; included by sampler_impl.cuh).
 //
-// Same thread layout, B phase and rounding as sb_small_kernel (see sampler_impl.cuh): a CTA of
-// 256 threads integrates 64 trajectories of one (run, weight), LANES = 4 consecutive lanes per
-// trajectory, each lane holding NQ spins in registers. What changes is who resolves the
+// Same B phase and rounding as sb_small_kernel (see sampler_impl.cuh): a CTA of 128 threads
+// integrates 32 trajectories of one (run, weight), LANES = 4 lanes per trajectory (lanes t,
+// t + 8, t + 16, t + 24 of a warp), each lane holding NQ spins in registers. What changes is who resolves the
 // (trajectory, step) noise streams of fill_step_noise (solver.hpp:128-136, rng.hpp:156-185).
 // sb_small_kernel resolves one step at a time: the four lanes of a trajectory walk the same
 // stream redundantly and the warp waits for the slowest of its 8 streams every step. Here the
@@ -54,17 +54,19 @@ struct BGeo {
     static constexpr int kNQ = (NMAX + LANES - 1) / LANES;  // spins per lane
     static constexpr int kNP = kNQ * LANES;                 // integrated spins (>= n)
     static constexpr int kC = 56;                           // words per stream row
-    // row strides: lane h's row at h * kSS (== 24 mod 32: the 8 lanes of an STS.128 phase hit
-    // distinct bank quads), trajectory rows at kTS == 4 mod 32 (B's reads: 4 k + NQ h distinct)
+    // row strides: stream h's row at h * kSS, trajectory rows at kTS == 4 mod 32 (the 8 lanes
+    // of an STS.128 phase, 8 trajectories with one h, hit distinct bank quads; B's reads at
+    // 4 t + NQ h are distinct over the warp)
     static constexpr int kSS = kC;
     static constexpr int kTS = LANES * kSS + 4;
     // Philox blocks per stream row (kNBU unrolled at a time); more is sequential resolution
     static constexpr int kNB = (NMAX + 14 + 3) / 4 < kC / 4 ? (NMAX + 14 + 3) / 4 : kC / 4;
     static constexpr int kNBU = (kNB + 1) / 2;
     // offset table per stream: 16 words of lane-major offset bytes, 4 half-words of tail bits
-    // (lane h's at half-word h), 2 pad; per trajectory LANES streams (stride == 16 mod 32)
+    // (lane h's at half-word h), 2 pad; per trajectory LANES streams
     static constexpr int kWS = 20;
-    static constexpr int kWT = LANES * kWS;
+    static constexpr int kWT = LANES * kWS + 20;  // == 4 mod 32: the 8 lanes of a quarter-warp
+                                                 // (8 trajectories, one h) read distinct quads
     static constexpr int kPhiW = VAR == 1 ? 4 : 8;
     static constexpr int kPStr = VAR == 1 ? (kNP + 27) / 32 * 32 + 4 : (kNP + 13) / 16 * 16 + 2;
     // dSB with padded rows (TAB) keeps phi as a sign mask in registers: no phi rows
@@ -81,6 +83,15 @@ struct BGeo {
     static_assert(NMAX + 14 <= kC, "sequential resolution packs n normals and up to 14 tails");
     static_assert(kNB * 4 <= kC && kNB * 4 < 64, "generated blocks fit the row and the mask");
 };
+
+// OR over the LANES lanes of a trajectory (lanes t + 8 h, h < LANES)
+template <int LANES>
+__device__ __forceinline__ uint64_t traj_or(unsigned mask, uint64_t v)
+{
+#pragma unroll
+    for (int o = 32 / LANES; o < 32; o <<= 1) v |= __shfl_xor_sync(mask, v, o);
+    return v;
+}
 
 // Ziggurat tables of the batch kernel in static shared memory (their addresses are immediates),
 // plus FP32 copies of wn / fn for the wedge and tail brackets.
@@ -250,8 +261,12 @@ __device__ __forceinline__ void sb_batch_body(const SamplerParams& p)
     const int l = static_cast<int>(rl % p.L);
     const int run = static_cast<int>(rl / p.L);
     const int tid = threadIdx.x;
-    const int t_loc = tid / LANES;
-    const int h = tid % LANES;
+    // lane 8 h + t of a warp: trajectory t of the warp's 8, spin block h. A half-warp then holds
+    // two spin blocks whose coupling tables (spins 11 h + s) start 16 banks apart, so the
+    // 16 table reads of an LDS.64 phase are conflict-free (lane 4 t + h put h = 0, 2 on the same
+    // banks: 1.3e8 extra wavefronts per C2 launch)
+    const int t_loc = (tid >> 5) * (32 / LANES) + (tid & (32 / LANES - 1));
+    const int h = (tid & 31) / (32 / LANES);
 
     {  // CTA setup (identical to sb_small_kernel)
         static_assert(sizeof(ZigTables) == offsetof(BatchZig, wnf), "BatchZig extends ZigTables");
@@ -528,7 +543,7 @@ __device__ __forceinline__ void sb_batch_body(const SamplerParams& p)
                     for (int s = 0; s < NQ; ++s) lm |= static_cast<uint32_t>(x[s] < 0.0) << s;
                 }
                 M = static_cast<uint64_t>(lm) << (s0 + G::kMK);
-                M = lane_or<LANES>(wmask, M);
+                M = traj_or<LANES>(wmask, M);
             }
 
             // ---- B: spin updates (sb_step solver.hpp:159-181 / simcim_step :196-210)
@@ -621,7 +636,7 @@ __device__ __forceinline__ void sb_batch_body(const SamplerParams& p)
             bad |= !isfinite(x[s]) || !isfinite(y[s]);  // check_finite (solver.hpp:138-143)
         }
     }
-    word = lane_or<LANES>(wmask, word);
+    word = traj_or<LANES>(wmask, word);
     if (h == 0) {
         const long long idx = (static_cast<long long>(run) * p.L + l) * p.batch + traj;
         p.words[idx - p.row0] = word;
