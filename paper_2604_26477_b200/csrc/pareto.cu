@@ -97,6 +97,42 @@ __device__ __forceinline__ void warp_append(bool flag, uint32_t value, uint32_t*
     if (flag) out[base + __popc(b & ((1u << lane) - 1))] = value;
 }
 
+// warp_append through a per-warp shared-memory buffer of CAP entries: one atomicAdd on the
+// global count per flush instead of one per warp and iteration (a single counter taking
+// millions of adds is serialised in L2: C5's 6.6e6 distinct configs). Every lane of the warp
+// calls push (block-uniform loops) and flush once after the loop. Entries at or past `limit`
+// raise *overflow instead of being stored.
+template <int CAP>
+struct WarpBuffer {
+    uint32_t* buf;  // this warp's CAP entries
+    int n;          // warp-uniform fill
+    __device__ __forceinline__ void flush(uint32_t* out, unsigned long long* count, unsigned long long limit,
+                                          unsigned long long* overflow)
+    {
+        __syncwarp();
+        const int lane = threadIdx.x & 31;
+        unsigned long long base = 0;
+        if (lane == 0 && n) base = atomicAdd(count, static_cast<unsigned long long>(n));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int j = lane; j < n; j += 32) {
+            if (base + j < limit) out[base + j] = buf[j];
+            else atomicExch(overflow, 1ull);
+        }
+        __syncwarp();
+        n = 0;
+    }
+    __device__ __forceinline__ void push(bool flag, uint32_t v, uint32_t* out, unsigned long long* count,
+                                         unsigned long long limit, unsigned long long* overflow)
+    {
+        const unsigned b = __ballot_sync(0xffffffffu, flag);
+        const int nf = __popc(b);
+        if (n + nf > CAP) flush(out, count, limit, overflow);
+        if (flag) buf[n + __popc(b & ((1u << (threadIdx.x & 31)) - 1))] = v;
+        n += nf;
+    }
+};
+constexpr int kWBuf = 128;
+
 // warp_append that returns each flagged lane's slot (undefined for the others)
 __device__ __forceinline__ unsigned long long warp_append_index(bool flag, unsigned long long* count)
 {
@@ -261,7 +297,9 @@ __global__ void __launch_bounds__(256) k_dedup_eval_collapse_packed(
             w = words[i];
             uint64_t h = mix64(w) & m1;
             for (;;) {
-                const unsigned long long old = atomicCAS(&t1[h], ~0ull, static_cast<unsigned long long>(w));
+                // a slot goes from empty to its key once: a plain L2 read settles repeats
+                unsigned long long old = __ldcg(&t1[h]);
+                if (old == ~0ull) old = atomicCAS(&t1[h], ~0ull, static_cast<unsigned long long>(w));
                 if (old == ~0ull) {
                     fresh = true;
                     break;
@@ -283,7 +321,8 @@ __global__ void __launch_bounds__(256) k_dedup_eval_collapse_packed(
                 if (k < K) key |= static_cast<unsigned long long>(static_cast<long long>(acc[k]) - g.lo[k]) << g.shift[k];
             uint64_t hv = mix64(key) & m2;
             for (;;) {
-                const unsigned long long old = atomicCAS(&t2[hv], ~0ull, key);
+                unsigned long long old = __ldcg(&t2[hv]);
+                if (old == ~0ull) old = atomicCAS(&t2[hv], ~0ull, key);
                 if (old == ~0ull) {
                     vfresh = true;
                     break;
@@ -349,22 +388,37 @@ __global__ void k_gather_vals_dev(const double* __restrict__ src, const uint32_t
 // such config equals); one CAS per config and no re-read of the pool for the comparison
 // A table smaller than the pool (L2-sized) may fill up: past `limit` keys or 256 probes the
 // kernel raises ucount[1] and stops inserting; the host then redoes the dedup at full size.
+constexpr int kDedupCache = 1024;  // keys per CTA (8 KB)
 __global__ void k_dedup64(const uint64_t* __restrict__ words, long long M, unsigned long long* table, uint64_t tmask,
                           uint32_t* uniq, unsigned long long* ucount, unsigned long long limit)
 {
+    // most configs of a pool are repeats (1e8 samples, ~7e6 distinct at C5), and the popular
+    // ones would send thousands of CASes to one slot, serialised in L2. A direct-mapped cache of
+    // keys this CTA has already settled in the table screens them first; then one lane per
+    // distinct key of the warp goes to the table, where a slot already holding the key is
+    // found by a plain read (a slot goes from empty to its key once)
+    __shared__ unsigned long long seen[kDedupCache];
+    __shared__ uint32_t pend[8][kWBuf];  // 256 threads
+    for (int q = threadIdx.x; q < kDedupCache; q += blockDim.x) seen[q] = ~0ull;
+    __syncthreads();
+    WarpBuffer<kWBuf> wb{pend[threadIdx.x >> 5], 0};
     for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x); i0 < M;
          i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long i = i0 + threadIdx.x;
         bool fresh = false;
-        if (i < M) {
-            const uint64_t w = words[i];
+        uint64_t w = i < M ? words[i] : ~0ull;
+        const uint32_t cs = static_cast<uint32_t>(w ^ (w >> 29)) & (kDedupCache - 1);
+        if (i < M && seen[cs] == w) w = ~0ull;  // settled by this CTA before
+        const unsigned peers = __match_any_sync(0xffffffffu, w);
+        if (w != ~0ull && (threadIdx.x & 31) == __ffs(peers) - 1) {
             uint64_t h = mix64(w) & tmask;
             for (int probe = 0;; ++probe) {
                 if (probe == 256) {
                     atomicExch(ucount + 1, 1ull);
                     break;
                 }
-                const unsigned long long old = atomicCAS(&table[h], ~0ull, static_cast<unsigned long long>(w));
+                unsigned long long old = __ldcg(&table[h]);
+                if (old == ~0ull) old = atomicCAS(&table[h], ~0ull, static_cast<unsigned long long>(w));
                 if (old == ~0ull) {
                     fresh = true;
                     break;
@@ -372,13 +426,11 @@ __global__ void k_dedup64(const uint64_t* __restrict__ words, long long M, unsig
                 if (old == w) break;
                 h = (h + 1) & tmask;
             }
+            seen[cs] = w;  // in the table now (a racing write leaves another settled key)
         }
-        const unsigned long long at = warp_append_index(fresh, ucount);
-        if (fresh) {
-            if (at < limit) uniq[at] = static_cast<uint32_t>(i);
-            else atomicExch(ucount + 1, 1ull);  // (the table is redone at full size)
-        }
+        wb.push(fresh, static_cast<uint32_t>(i), uniq, ucount, limit, ucount + 1);  // past limit: redo
     }
+    wb.flush(uniq, ucount, limit, ucount + 1);
 }
 
 // ---- K5: dedup of packed configs (pareto.hpp:309-326)
@@ -496,6 +548,8 @@ __global__ void k_collapse(const double* __restrict__ vals, long long U, int K, 
                            const uint32_t* __restrict__ cfg_of_row, int wpc, uint32_t* table, uint32_t* owner,
                            uint64_t tmask, uint32_t* reps, unsigned long long* vcount)
 {
+    __shared__ uint32_t pend[8][kWBuf];  // 256 threads
+    WarpBuffer<kWBuf> wb{pend[threadIdx.x >> 5], 0};
     for (long long u0 = blockIdx.x * static_cast<long long>(blockDim.x); u0 < U;
          u0 += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long u = u0 + threadIdx.x;
@@ -532,8 +586,9 @@ __global__ void k_collapse(const double* __restrict__ vals, long long U, int K, 
                 }
             }
         }
-        warp_append(fresh, slot_of, reps, vcount);
+        wb.push(fresh, slot_of, reps, vcount, ~0ull, vcount);
     }
+    wb.flush(reps, vcount, ~0ull, vcount);
 }
 
 // ---- distinct values of every axis (blockIdx.y = axis; hash set of keys per axis), then
