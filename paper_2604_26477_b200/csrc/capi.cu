@@ -1176,10 +1176,12 @@ int momc_b200_stream_step(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, l
         DevArchive& R = running_archive(*ctx);
         const long long X = R.F;
         DevBuf<double> all;
-        filter_pool_merge_device(*ctx, ctx->d_words.p, ctx->pool_size, R.vals.p, R.words.p, X, R, all);
+        const bool fused = filter_pool_merge_device(*ctx, ctx->d_words.p, ctx->pool_size, R.vals.p, R.words.p, X, R, all);
         R.K = ctx->k;
         R.wpc = (ctx->n + 63) / 64;
-        const bool changed = X == 0 || !same_value_set(*ctx, all.p, X, R.vals.p, R.F, ctx->k);
+        // the fused merge recomputes the HV every step: a value-set comparison (two kernels and
+        // a read-back) costs about as much as the HV, and the set changes on most steps
+        const bool changed = fused || X == 0 || !same_value_set(*ctx, all.p, X, R.vals.p, R.F, ctx->k);
         all.release();
         rp->archive_size = R.F;
         if (running_F) *running_F = R.F;

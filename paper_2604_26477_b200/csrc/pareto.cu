@@ -337,6 +337,43 @@ __global__ void __launch_bounds__(256) k_dedup_eval_collapse_packed(
     }
 }
 
+// rows of a running archive (distinct value vectors with their lex-min configs, one word each)
+// into the packed collapse table of k_dedup_eval_collapse_packed: a vector the pool also reached
+// keeps the smaller config (the same atomicMin over bit-reversed words), a new one is appended
+template <int KM>
+__global__ void k_insert_rows_packed(const double* __restrict__ xv, const uint64_t* __restrict__ xw, long long X,
+                                     int K, PackGeo g, unsigned long long* t2, unsigned long long* own, uint64_t m2,
+                                     uint32_t* reps, unsigned long long* cnt)
+{
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x); i0 < X;
+         i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        bool vfresh = false;
+        uint32_t slot = 0;
+        if (i < X) {
+            unsigned long long key = 0;
+#pragma unroll
+            for (int k = 0; k < KM; ++k)
+                if (k < K)
+                    key |= static_cast<unsigned long long>(static_cast<long long>(xv[i * K + k]) - g.lo[k]) << g.shift[k];
+            uint64_t hv = mix64(key) & m2;
+            for (;;) {
+                unsigned long long old = __ldcg(&t2[hv]);
+                if (old == ~0ull) old = atomicCAS(&t2[hv], ~0ull, key);
+                if (old == ~0ull) {
+                    vfresh = true;
+                    break;
+                }
+                if (old == key) break;
+                hv = (hv + 1) & m2;
+            }
+            atomicMin(&own[hv], static_cast<unsigned long long>(__brevll(xw[i])));
+            slot = static_cast<uint32_t>(hv);
+        }
+        warp_append(vfresh, slot, reps, cnt + 2);
+    }
+}
+
 // distinct vectors of the packed fused path: values unpacked from the keys, lex-min config
 template <int KM>
 __global__ void k_slots_packed(const uint32_t* __restrict__ reps, const unsigned long long* __restrict__ dV,
@@ -1614,8 +1651,8 @@ void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, 
         c.grid_archive = out.vals.p;
         c.grid_rows = F;
     }
-    ck(cudaStreamSynchronize(c.stream), "archive");
     if (tm) {
+        ck(cudaStreamSynchronize(c.stream), "archive");
         tm->front_s = seconds_between(e0, e1);
         tm->order_s = seconds_between(e1, e2);
         tm->front_method = method;
@@ -1655,24 +1692,42 @@ void evaluate_cuts_rows(Ctx& c, const uint64_t* d_words, const uint32_t* idx, lo
 // filter_pool_device for one-word configs with integer weights: dedup + evaluation + collapse
 // in one kernel, the distinct values of the grid axes right after, and a single read-back of
 // the counts before the front (three fewer host round trips than the staged path below)
-void filter_pool_fused(Ctx& c, Scratch& s, const uint64_t* d_words, long long M, DevArchive& out, ParetoTimings* tm)
+// the fused dedup + evaluation + collapse pass applies: one-word configs, integer weights, the
+// per-CTA edge tables fit shared memory, tables sized by rows <= 2^24
+bool fused_filter_ok(Ctx& c, long long rows)
+{
+    return c.n <= 63 && c.k >= 2 && c.integer_weights && !eval_gemm_ok(c) && c.m * 17 <= 12000 && rows <= (1ll << 24);
+}
+
+// the K cut values of this instance pack into one 64-bit key below ~0
+bool cuts_pack63(const Ctx& c)
+{
+    int pbits = 0;
+    for (int k = 0; k < c.k; ++k) pbits += c.cut_bits[static_cast<size_t>(k)];
+    return c.cut_pack && pbits <= 63;
+}
+
+// X > 0 (packed only): the X rows (xv: X x K values, xw: one config word each) of a running
+// archive join the collapse, so out = filter(pool U archive) in one pass (stream_step)
+void filter_pool_fused(Ctx& c, Scratch& s, const uint64_t* d_words, long long M, DevArchive& out, ParetoTimings* tm,
+                       const double* xv = nullptr, const uint64_t* xw = nullptr, long long X = 0)
 {
     const int K = c.k;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, c.stream);
-    const uint64_t t1 = pow2_at_least(2ull * static_cast<uint64_t>(M) + 16);
-    int pbits = 0;
-    for (int k = 0; k < K; ++k) pbits += c.cut_bits[static_cast<size_t>(k)];
-    const bool packed = c.cut_pack && pbits <= 63;  // ~0 is then no vector's key
+    const bool packed = cuts_pack63(c);  // ~0 is then no vector's key
+    if (X > 0 && !packed) usage("internal: archive rows need packed keys");
+    const long long MX = M + X;  // bound on the distinct vectors
+    const uint64_t t1 = pow2_at_least(2ull * static_cast<uint64_t>(MX) + 16);
     s.dtab64.reserve(t1 * 2);  // dedup keys | collapse owners
     if (!packed) {
         s.table2.reserve(t1);  // collapse rows
         s.vals.reserve(static_cast<size_t>(M) * K + 1);
         ck(cudaMemsetAsync(s.table2.p, 0xFF, sizeof(uint32_t) * t1, c.stream), "memset");
     }
-    s.reps.reserve(static_cast<size_t>(M) + 1);
+    s.reps.reserve(static_cast<size_t>(MX) + 1);
     s.counters.reserve(64);  // [0] unique configs, [2] distinct vectors, [8, 8+K) axis counts,
                              // [32, 64) spread unique-config counters (packed path)
     ck(cudaMemsetAsync(s.dtab64.p, 0xFF, sizeof(unsigned long long) * t1 * 2, c.stream), "memset");
@@ -1682,9 +1737,9 @@ void filter_pool_fused(Ctx& c, Scratch& s, const uint64_t* d_words, long long M,
     DevBuf<uint32_t> vrow, vown;
     DevBuf<uint64_t> vcfg;
     DevBuf<double> vv;
-    vown.reserve(static_cast<size_t>(M) + 1);
-    vcfg.reserve(static_cast<size_t>(M) + 1);
-    vv.reserve(static_cast<size_t>(M) * K + 1);
+    vown.reserve(static_cast<size_t>(MX) + 1);
+    vcfg.reserve(static_cast<size_t>(MX) + 1);
+    vv.reserve(static_cast<size_t>(MX) * K + 1);
     const unsigned long long* dV = s.counters.p + 2;
     if (packed) {
         PackGeo g{};
@@ -1706,9 +1761,16 @@ void filter_pool_fused(Ctx& c, Scratch& s, const uint64_t* d_words, long long M,
                                                      t1 - 1, t2.p, s.dtab64.p + t1, t1 - 1, g, s.reps.p,
                                                      s.counters.p);
         ck(cudaGetLastError(), "dedup+eval+collapse");
+        if (X > 0) {
+            auto ki = KM == 2 ? k_insert_rows_packed<2> : KM == 4 ? k_insert_rows_packed<4>
+                      : KM == 8 ? k_insert_rows_packed<8> : k_insert_rows_packed<16>;
+            ki<<<grid_blocks(X), 256, 0, c.stream>>>(xv, xw, X, K, g, t2.p, s.dtab64.p + t1, t1 - 1, s.reps.p,
+                                                     s.counters.p);
+            c.launches++;
+        }
         auto ks = KM == 2 ? k_slots_packed<2> : KM == 4 ? k_slots_packed<4>
                   : KM == 8 ? k_slots_packed<8> : k_slots_packed<16>;
-        ks<<<grid_blocks(M), 256, 0, c.stream>>>(s.reps.p, dV, t2.p, s.dtab64.p + t1, K, g, b, vv.p, vcfg.p, vown.p);
+        ks<<<grid_blocks(MX), 256, 0, c.stream>>>(s.reps.p, dV, t2.p, s.dtab64.p + t1, K, g, b, vv.p, vcfg.p, vown.p);
         t2.release();
         c.launches += 2;
     } else {
@@ -1725,7 +1787,7 @@ void filter_pool_fused(Ctx& c, Scratch& s, const uint64_t* d_words, long long M,
         k_gather_vals_dev<<<grid_blocks(M * K), 256, 0, c.stream>>>(s.vals.p, vrow.p, dV, K, vv.p);
         c.launches += 2;
     }
-    grid_distinct(c, s, vv.p, M, dV, K);
+    grid_distinct(c, s, vv.p, MX, dV, K);
     cudaEventRecord(e1, c.stream);
     auto* ph = static_cast<unsigned long long*>(pinned_buf(c, sizeof(unsigned long long) * 64));
     ck(cudaMemcpyAsync(ph, s.counters.p, sizeof(unsigned long long) * 64, cudaMemcpyDeviceToHost, c.stream), "D2H");
@@ -1769,7 +1831,7 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     const int wpc = (c.n + 63) / 64;
     const int K = c.k;
     // (tables sized by M: pools beyond 2^24 configs take the staged path, sized by the counts)
-    if (c.n <= 63 && K >= 2 && c.integer_weights && !eval_gemm_ok(c) && c.m * 17 <= 12000 && M <= (1ll << 24)) {
+    if (fused_filter_ok(c, M)) {
         filter_pool_fused(c, s, d_words, M, out, tm);
         return;
     }
@@ -1891,7 +1953,7 @@ __global__ void k_gather_words(const uint64_t* __restrict__ words, const uint32_
 // front of (the M pool configs U the X rows xv / xw) into `out` in one collapse + front pass:
 // the streaming step's "run front merged into the running archive" without a separate run
 // front. xv / xw may alias `out` (they are copied first).
-void filter_pool_merge_device(Ctx& c, const uint64_t* d_words, long long M, const double* xv, const uint64_t* xw,
+bool filter_pool_merge_device(Ctx& c, const uint64_t* d_words, long long M, const double* xv, const uint64_t* xw,
                               long long X, DevArchive& out, DevBuf<double>& all_vals)
 {
     if (M <= 0) usage("non-dominated filter needs a non-empty pool");
@@ -1900,6 +1962,14 @@ void filter_pool_merge_device(Ctx& c, const uint64_t* d_words, long long M, cons
     Scratch& s = scratch(c);
     const int wpc = (c.n + 63) / 64;
     const int K = c.k;
+    if (fused_filter_ok(c, M + X) && cuts_pack63(c)) {
+        // the fused pool pass with the archive rows inserted into its collapse table; the old
+        // rows go to all_vals first (the caller compares them with the result)
+        all_vals.reserve(static_cast<size_t>(X) * K + 1);
+        if (X) ck(cudaMemcpyAsync(all_vals.p, xv, sizeof(double) * X * K, cudaMemcpyDeviceToDevice, c.stream), "D2D");
+        filter_pool_fused(c, s, d_words, M, out, nullptr, all_vals.p, xw, X);
+        return true;
+    }
     const uint64_t tsize = pow2_at_least(2ull * static_cast<uint64_t>(M));
     s.table.reserve(tsize);
     s.uniq.reserve(static_cast<size_t>(M));
@@ -1923,6 +1993,7 @@ void filter_pool_merge_device(Ctx& c, const uint64_t* d_words, long long M, cons
     c.launches++;
     filter_values_device(c, all_vals.p, aw.p, wpc, c.n, T, K, out, nullptr);
     aw.release();
+    return false;
 }
 
 void filter_values_device(Ctx& c, const double* d_vals, const uint64_t* d_words, int wpc, int n_spins, long long M,

@@ -39,8 +39,9 @@ void filter_values_device(Ctx& c, const double* d_vals, const uint64_t* d_words,
 bool same_value_set(Ctx& c, const double* a, long long Fa, const double* b, long long Fb, int K);
 
 // front of (M pool configs U X extra rows xv/xw) into `out` in one pass (streaming merge);
-// all_vals receives the combined values, the X extra rows first
-void filter_pool_merge_device(Ctx& c, const uint64_t* d_words, long long M, const double* xv, const uint64_t* xw,
+// all_vals receives the combined values, the X extra rows first. True when the fused pool
+// pass ran (all_vals then holds only the X old rows)
+bool filter_pool_merge_device(Ctx& c, const uint64_t* d_words, long long M, const double* xv, const uint64_t* xw,
                               long long X, DevArchive& out, DevBuf<double>& all_vals);
 
 // detail::evaluate_cuts (pareto.hpp:330-363) for U configs: d_out U x K.
