@@ -270,6 +270,25 @@ __global__ void pad_rows_kernel(int n, int nnz, int dmax, const int* __restrict_
     }
 }
 
+// per-block sampler flags -> {OR of all flags, first block with bit 1 (or INT_MAX)} at
+// flags[n], flags[n + 1], so the host reads two words instead of one per block
+__global__ void k_flag_summary(int* flags, long long n)
+{
+    int acc = 0, first = 0x7fffffff;
+    for (long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; b < n;
+         b += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int f = flags[b];
+        acc |= f;
+        if ((f & 1) && b < first) first = static_cast<int>(b);
+    }
+    acc = __reduce_or_sync(0xffffffffu, acc);
+    first = __reduce_min_sync(0xffffffffu, first);
+    if ((threadIdx.x & 31) == 0) {
+        if (acc) atomicOr(flags + n, acc);
+        if (first != 0x7fffffff) atomicMin(flags + n + 1, first);
+    }
+}
+
 __global__ void stamp_t0(unsigned long long* t0)
 {
     unsigned long long t;
@@ -530,12 +549,13 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     c.pool_blocks = nblocks;
     c.pool_block_traj = bt;
     c.d_words.reserve(static_cast<size_t>(c.pool_size) * wpc);
-    c.d_nan.reserve(static_cast<size_t>(nblocks) + 1);
+    c.d_nan.reserve(static_cast<size_t>(nblocks) + 2);
     c.d_badstep.reserve(static_cast<size_t>(nblocks) + 1);
     c.d_block_end.reserve(static_cast<size_t>(nblocks) + 1);
     c.d_t0.reserve(2);
     device_zig(c);
     ck(cudaMemsetAsync(c.d_nan.p, 0, sizeof(int) * (nblocks + 1), c.stream), "memset");
+    ck(cudaMemsetAsync(c.d_nan.p + nblocks + 1, 0x7f, sizeof(int), c.stream), "memset");
     ck(cudaMemsetAsync(c.d_block_end.p, 0, sizeof(unsigned long long) * (nblocks + 1), c.stream), "memset");
 
     SamplerParams p{};
@@ -624,24 +644,40 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     }
     ck(cudaEventRecord(c.ev1, ss), "event");
     // Per-block flags: bit 2 = the register path's noise-event buffer overflowed (re-run the
-    // block on the exact sequential path); bit 1 = some trajectory went non-finite.
-    std::vector<int> flags(static_cast<size_t>(nblocks));
-    if (nblocks > 0)
-        ck(cudaMemcpyAsync(flags.data(), c.d_nan.p, sizeof(int) * nblocks, cudaMemcpyDeviceToHost, ss), "D2H");
-    ck(cudaStreamSynchronize(ss), "sampler");
+    // block on the exact sequential path); bit 1 = some trajectory went non-finite. Reduced on
+    // the device; the per-block words come back only when some block raised a flag.
+    std::vector<int> flags;
+    int summary[2] = {0, 0x7f7f7f7f};
+    if (nblocks > 0) {
+        k_flag_summary<<<static_cast<unsigned>(std::min<long long>((nblocks + 255) / 256, 148)), 256, 0, ss>>>(c.d_nan.p,
+                                                                                                          nblocks);
+        ++c.launches;
+        auto* ph = static_cast<int*>(pinned_buf(c, 2 * sizeof(int)));
+        ck(cudaMemcpyAsync(ph, c.d_nan.p + nblocks, 2 * sizeof(int), cudaMemcpyDeviceToHost, ss), "D2H");
+        ck(cudaStreamSynchronize(ss), "sampler");
+        summary[0] = ph[0];
+        summary[1] = ph[1];
+    } else {
+        ck(cudaStreamSynchronize(ss), "sampler");
+    }
+    const char* force_fb = regpath ? std::getenv("MOMC_TEST_FORCE_FALLBACK") : nullptr;
+    if (summary[0] != 0 || force_fb) {
+        flags.resize(static_cast<size_t>(nblocks));
+        ck(cudaMemcpy(flags.data(), c.d_nan.p, sizeof(int) * nblocks, cudaMemcpyDeviceToHost), "D2H");
+    }
+    const long long nflags = static_cast<long long>(flags.size());  // 0: no block raised a flag
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, c.ev0, c.ev1), "event");
     c.ktimer.collect();
     // test hook: MOMC_TEST_FORCE_FALLBACK=k re-runs every k-th register-path block on the
     // sequential path (its words must be identical); never set in production
-    if (regpath) {
-        const char* f = std::getenv("MOMC_TEST_FORCE_FALLBACK");
-        const long long every = f ? std::atoll(f) : 0;
+    if (force_fb) {
+        const long long every = std::atoll(force_fb);
         if (every > 0)
-            for (long long b = 0; b < nblocks; b += every) flags[static_cast<size_t>(b)] |= 2;
+            for (long long b = 0; b < nflags; b += every) flags[static_cast<size_t>(b)] |= 2;
     }
     bool refixed = false;
-    for (long long b = 0; b < nblocks; ++b) {
+    for (long long b = 0; b < nflags; ++b) {
         if (!(flags[static_cast<size_t>(b)] & 2)) continue;
         if (!refixed) g = scratch(1);
         refixed = true;
@@ -663,7 +699,7 @@ void sample(Ctx& c, const momc_solver_cfg* cfg, int runs, long long b_begin, lon
     // the clamp, so a final-state scan finds every failing trajectory; the step index is
     // recovered by re-running the first failing 512-trajectory task with per-step checks.
     long long h_first = -1;
-    for (long long b = 0; b < nblocks; ++b)
+    for (long long b = 0; b < nflags; ++b)
         if (flags[static_cast<size_t>(b)] & 1) {
             h_first = b;
             break;
