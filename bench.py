@@ -648,9 +648,10 @@ def main():
             ik, wk, ck = shapes[k]
             tto_sessions = [api.Session(local)]
             for sk in tto_sessions:
-                sk.set_instance(ik)  # warm the contexts (module load, pools) outside the clock
-                sk.set_weights(wk)
-                sk.pipeline(ck, 1, 0, sk.num_blocks(ck, 1), do_hv=False)
+                sk.set_instance(ik)  # warm the contexts (module load, pools) outside the clock:
+                sk.set_weights(wk)   # two untimed streaming steps through sample, merge and HV
+                streaming.time_to_target(sk, ck, r_frozen, None, 2 * TTO_RUNS_PER_STEP[k] * world, world, rank,
+                                         torch.device("cuda", local), runs_per_step=TTO_RUNS_PER_STEP[k])
             sync_all()
             t0 = time.perf_counter()
             for sk in tto_sessions:
