@@ -355,7 +355,7 @@ def measure_c4(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, 
             "achieved": upd_gbs, "peak": hbm, "unit": "GB/s", "frac": upd_gbs / hbm if upd_gbs else None,
             "traffic": traffic, "traffic_source": tsrc,
             "bytes_per_spin_update": C4_UPDATE_BYTES, "launches": upd_n, "ms": upd_ms,
-            "gemm": {"kernel": "k_dense_gemm (tcgen05 kind::i8, H*J(c).sgn(X))", "ms": gemm_ms, "launches": gemm_n,
+            "gemm": {"kernel": "k_dense_gemm2 (tcgen05 cta_group::2 kind::i8, H*J(c).sgn(X))", "ms": gemm_ms, "launches": gemm_n,
                      "achieved_tops": gemm_ops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                      "peak_note": "int8 dense nominal 4500 TOP/s (no measured int8 peak); bf16 measured "
                                   f"{peaks.get('bf16_tflops')} TF/s"},

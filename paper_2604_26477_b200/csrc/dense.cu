@@ -13,12 +13,13 @@
 // bit-for-bit; the context reports the path (momc_b200_sampler_path).
 //
 // Per step, two kernels over the (run, weight) pairs of a group:
-//   * k_dense_gemm: D (trajectories x spins, int32) = Phi . (H J)^T on the tensor cores.
-//     Warp-specialised and persistent: one thread streams 128-byte K chunks of Phi (256
-//     trajectories) and of the H*J(c) tile (256 spins) with TMA into a 3-stage ring, one
-//     thread issues tcgen05.mma (two M = 128, N = 256 products per chunk, both reading the
-//     same H*J chunk, into all 512 TMEM columns), and eight epilogue warps move the finished
-//     item TMEM -> registers -> swizzled shared memory -> TMA store.
+//   * k_dense_gemm2: D (trajectories x spins, int32) = Phi . (H J)^T on the tensor cores.
+//     Persistent CTA pairs (cta_group::2), warp-specialised: in each CTA one thread streams
+//     128-byte K chunks of its 128 trajectories of Phi and its halves of the H*J(c) tiles
+//     with TMA into a 4-stage ring, one thread of rank 0 issues tcgen05.mma for the pair
+//     (M = 256, two N = 256 products per chunk into all 512 TMEM columns of both CTAs), and
+//     eight epilogue warps per CTA move the finished item TMEM -> registers -> swizzled
+//     shared memory -> TMA store.
 //   * k_dense_warp: the FP64 update, one warp per trajectory, 32 spins per window, the
 //     (trajectory, step) noise stream resolved warp-wide (below).
 // State: Phi [pair][traj][ldp] (int8 or bf16), D [pair][traj][ldp] int32, x / y
@@ -389,16 +390,11 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
 }
 
 // ---- D = Phi . (H J)^T on the tensor cores (persistent, warp-specialised) -------------------
-constexpr int kGM = 128;              // trajectories per MMA (M, TMEM lanes)
-constexpr int kGH = 2;                // trajectory tiles per item: both share every B chunk
-constexpr int kGN = 256;              // spins per item (MMA N, TMEM columns per accumulator)
-constexpr int kGStages = 3;
-constexpr int kGStageA = kGH * kGM * 128;  // bytes: 256 rows x 128 bytes of K
-constexpr int kGStageB = kGN * 128;
-constexpr int kGStage = kGStageA + kGStageB;
+constexpr int kGM = 128;              // trajectories per CTA (TMEM lanes)
+constexpr int kGH = 2;                // trajectory tiles per item: 256 rows, one per CTA of a pair
+constexpr int kGN = 256;              // spins per MMA (N)
 constexpr int kGOut = 32 * 32 * 4;    // one epilogue store box: 32 trajectories x 32 spins int32
 constexpr int kGEpi = 8;              // epilogue warps: TMEM lane quarter = warp & 3, column half = (warp - 2) / 4
-constexpr int kGSmem = kGStages * kGStage + kGEpi * kGOut + 1024;
 constexpr int kGThreads = (2 + kGEpi) * 32;  // 0: TMA, 1: MMA (+ TMEM), 2..9: epilogue
 
 struct GemmArgs {
@@ -422,104 +418,130 @@ __device__ __forceinline__ void bulk_wait_read()
     asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
 }
 
+// ---- the same product on CTA pairs (cta_group::2): an item is 256 trajectories x 256 kG2NT
+// spins; rank r of the pair stages trajectory rows [128 r, 128 r + 128) and, of each 256-spin
+// product u, spin rows (of H J) [256 u + 128 r, + 128) of every K chunk; rank 0 issues the
+// M = 256, N = 256 MMAs, which read both CTAs' shared memory, and each CTA's TMEM holds its
+// 128 rows x 256 kG2NT spins. The operands come from L2 at (256 + 256 kG2NT) bytes per K
+// step for 65,536 kG2NT outputs: the kernel is bound by that traffic (tensor pipe 50 % busy,
+// L2 at 70 % of its throughput with kG2NT = 1, the same cycles as the single-CTA kernel
+// above), so kG2NT = 2 (12 B per output instead of 16) fills the 512 TMEM columns with one
+// accumulator; with kG2NT = 1 two accumulators alternate and an item's MMAs overlap the
+// previous item's epilogue.
+constexpr int kG2M = 128;                          // trajectories per CTA (MMA M = 256 per pair)
+constexpr int kG2NT = 2;                           // N = 256 products per item (spins 256 kG2NT)
+constexpr int kG2Acc = kG2NT == 1 ? 2 : 1;         // TMEM accumulators (512 columns)
+constexpr int kG2Stages = kG2NT == 1 ? 5 : 4;
+constexpr int kG2StageA = kG2M * 128;              // bytes: 128 rows x 128 bytes of K
+constexpr int kG2StageB = kG2NT * (kGN / 2) * 128;  // this CTA's half of each product's 256 spin rows
+constexpr int kG2Stage = kG2StageA + kG2StageB;
+constexpr int kG2Smem = kG2Stages * kG2Stage + kGEpi * kGOut + 1024;
+static_assert(kG2Smem <= 232448, "shared memory per CTA");
+
 template <bool BF16>
-__global__ void __launch_bounds__(kGThreads, 1) k_dense_gemm(const __grid_constant__ CUtensorMap tmA,
-                                                            const __grid_constant__ CUtensorMap tmB,
-                                                            const __grid_constant__ CUtensorMap tmD,
-                                                            const __grid_constant__ GemmArgs a)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGThreads, 1)
+    k_dense_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const __grid_constant__ CUtensorMap tmD, const __grid_constant__ GemmArgs a)
 {
     extern __shared__ uint8_t sm_raw[];
     uint8_t* sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);
-    __shared__ uint64_t full[kGStages], empty[kGStages], d_full[2], d_empty[2];
+    __shared__ uint64_t full[kG2Stages], empty[kG2Stages], d_full[2], d_empty[2];
     __shared__ uint32_t tslot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_rank();
+    const long long pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     constexpr int KC = BF16 ? 64 : 128;  // K elements per 128-byte chunk
     if (threadIdx.x == 0) {
-        for (int q = 0; q < kGStages; ++q) {
-            tc::mbar_init(&full[q], 1);
-            tc::mbar_init(&empty[q], 1);
+        for (int q = 0; q < kG2Stages; ++q) {
+            tc::mbar_init(&full[q], 1);   // rank 0's: its expect_tx arrival + both CTAs' bytes
+            tc::mbar_init(&empty[q], 1);  // each CTA's: the pair's MMA commit
         }
-        for (int q = 0; q < 2; ++q) {
-            tc::mbar_init(&d_full[q], 1);
-            tc::mbar_init(&d_empty[q], kGEpi);
+        for (int q = 0; q < kG2Acc; ++q) {
+            tc::mbar_init(&d_full[q], 1);           // each CTA's: the pair's MMA commit
+            tc::mbar_init(&d_empty[q], 2 * kGEpi);  // rank 0's: both CTAs' epilogue warps
         }
         tc::fence_mbar_init();
         tc::prefetch_tmap(&tmA);
         tc::prefetch_tmap(&tmB);
         tc::prefetch_tmap(&tmD);
     }
-    if (warp == 1) tc::tmem_alloc<512>(&tslot);
+    if (warp == 1) tc::tmem_alloc_2sm<512>(&tslot);
     tc::fence_before();
-    __syncthreads();
+    tc::cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
     tc::fence_after();
     const uint32_t tbase = tslot;
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer
+        if (lane == 0) {  // TMA producer (both CTAs): this CTA's half of A and of B
             uint32_t g = 0;
-            for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
+            for (long long it = pair_id; it < a.items; it += npairs) {
                 const int j = static_cast<int>(it % a.ntn);
                 const long long pt = it / a.ntn;
                 const int q = a.pair_begin + static_cast<int>(pt / a.tiles_per_pair), i = static_cast<int>(pt % a.tiles_per_pair);
-                const int arow = q * a.batch_pad + i * kGH * kGM, brow = a.pairs[q].l * a.n + j * kGN;
+                const int arow = q * a.batch_pad + i * kGH * kGM + static_cast<int>(rank) * kG2M;
+                const int brow = a.pairs[q].l * a.n + j * kGN * kG2NT + static_cast<int>(rank) * (kGN / 2);
                 for (int c = 0; c < a.nch; ++c, ++g) {
-                    const uint32_t st = g % kGStages, ph = (g / kGStages) & 1;
+                    const uint32_t st = g % kG2Stages, ph = (g / kG2Stages) & 1;
                     tc::mbar_wait(&empty[st], ph ^ 1);
-                    uint8_t* sa = sm + st * kGStage;
-                    tc::mbar_expect_tx(&full[st], kGStage);
-                    tc::tma_load_2d(sa, &tmA, c * KC, arow, &full[st]);
-                    tc::tma_load_2d(sa + kGStageA, &tmB, c * KC, brow, &full[st]);
+                    uint8_t* sa = sm + st * kG2Stage;
+                    const uint32_t fb = tc::mapa(tc::smem_u32(&full[st]), 0);
+                    if (rank == 0) tc::mbar_expect_tx(&full[st], 2 * kG2Stage);
+                    tc::tma_load_2d_2sm(sa, &tmA, c * KC, arow, fb);
+#pragma unroll
+                    for (int u = 0; u < kG2NT; ++u)
+                        tc::tma_load_2d_2sm(sa + kG2StageA + u * (kGN / 2) * 128, &tmB, c * KC, brow + u * kGN, fb);
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer
-            const uint32_t idesc = BF16 ? tc::idesc_bf16(kGM, kGN) : tc::idesc_i8(kGM, kGN);
+        if (lane == 0 && rank == 0) {  // MMA issuer of the pair
+            const uint32_t idesc = BF16 ? tc::idesc_bf16(2 * kG2M, kGN) : tc::idesc_i8(2 * kG2M, kGN);
             uint32_t g = 0, s = 0;
-            for (long long it = blockIdx.x; it < a.items; it += gridDim.x, ++s) {
-                // one accumulator pair (all 512 TMEM columns): wait until the last item is drained
-                tc::mbar_wait(&d_empty[0], (s & 1) ^ 1);
+            for (long long it = pair_id; it < a.items; it += npairs, ++s) {
+                const uint32_t acc = s % kG2Acc, use = s / kG2Acc;
+                tc::mbar_wait(&d_empty[acc], (use & 1) ^ 1);  // both epilogues drained it
                 tc::fence_after();
                 for (int c = 0; c < a.nch; ++c, ++g) {
-                    const uint32_t st = g % kGStages, ph = (g / kGStages) & 1;
+                    const uint32_t st = g % kG2Stages, ph = (g / kG2Stages) & 1;
                     tc::mbar_wait(&full[st], ph);
                     tc::fence_after();
-                    const uint32_t as = tc::smem_u32(sm + st * kGStage), bs = as + kGStageA;
+                    const uint32_t as = tc::smem_u32(sm + st * kG2Stage), bs = as + kG2StageA;
 #pragma unroll
-                    for (int h = 0; h < kGH; ++h) {
-                        const uint32_t dt = tbase + h * kGN, ah = as + h * (kGM * 128);
+                    for (int u = 0; u < kG2NT; ++u) {
+                        const uint32_t dt = tbase + (acc * kG2NT + u) * kGN, bu = bs + u * (kGN / 2) * 128;
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            if (BF16) tc::mma_f16(dt, tc::smem_desc_sw128(ah + 32 * k), tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
-                            else tc::mma_i8(dt, tc::smem_desc_sw128(ah + 32 * k), tc::smem_desc_sw128(bs + 32 * k), idesc, c > 0 || k > 0);
+                            if (BF16) tc::mma_f16_2sm(dt, tc::smem_desc_sw128(as + 32 * k), tc::smem_desc_sw128(bu + 32 * k), idesc, c > 0 || k > 0);
+                            else tc::mma_i8_2sm(dt, tc::smem_desc_sw128(as + 32 * k), tc::smem_desc_sw128(bu + 32 * k), idesc, c > 0 || k > 0);
                         }
                     }
-                    tc::commit(&empty[st]);
+                    tc::commit_2sm(&empty[st], 0x3);
                 }
-                tc::commit(&d_full[0]);
+                tc::commit_2sm(&d_full[acc], 0x3);
             }
         }
         __syncwarp();
     } else {
-        // epilogue warp: TMEM lane quarter q = 32 trajectories of each half, column half ch;
-        // per 32-spin column group TMEM -> registers -> 128-byte-swizzled box -> TMA store
+        // epilogue warp (both CTAs): TMEM lane quarter q = 32 of this CTA's 128 trajectories,
+        // column half ch; per 32-spin column group TMEM -> registers -> swizzled box -> TMA store
         const int q = warp & 3, ch = (warp - 2) / 4;
         const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
-        uint8_t* ob = sm + kGStages * kGStage + (warp - 2) * kGOut;
+        uint8_t* ob = sm + kG2Stages * kG2Stage + (warp - 2) * kGOut;
         uint32_t s = 0, nst = 0;
-        for (long long it = blockIdx.x; it < a.items; it += gridDim.x, ++s) {
+        for (long long it = pair_id; it < a.items; it += npairs, ++s) {
+            const uint32_t acc = s % kG2Acc, use = s / kG2Acc;
             const int j = static_cast<int>(it % a.ntn);
             const long long pt = it / a.ntn;
             const int qq = a.pair_begin + static_cast<int>(pt / a.tiles_per_pair), i = static_cast<int>(pt % a.tiles_per_pair);
-            tc::mbar_wait(&d_full[0], s & 1);
+            tc::mbar_wait(&d_full[acc], use & 1);
             tc::fence_after();
+            const int row0 = qq * a.batch_pad + i * kGH * kGM + static_cast<int>(rank) * kG2M + q * 32;
 #pragma unroll 1
-            for (int hc = 0; hc < kGH * 4; ++hc) {
-                const int h = hc >> 2, cg = ch * 4 + (hc & 3);
-                const int row0 = qq * a.batch_pad + (i * kGH + h) * kGM + q * 32;
-                const int col0 = j * kGN + cg * 32;
+            for (int cc = 0; cc < 4 * kG2NT; ++cc) {
+                const int cg = ch * 4 * kG2NT + cc;  // 32-spin column group of the item
+                const int col0 = j * kGN * kG2NT + cg * 32;
                 if (col0 >= a.n) continue;
                 uint32_t v[32];
-                tc::tmem_ld32(tbase + lane_addr + h * kGN + cg * 32, v);
+                tc::tmem_ld32(tbase + lane_addr + acc * kG2NT * kGN + cg * 32, v);
                 if (BF16)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) v[e] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(v[e])));
@@ -536,14 +558,15 @@ __global__ void __launch_bounds__(kGThreads, 1) k_dense_gemm(const __grid_consta
             }
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&d_empty[0]);
+            if (lane == 0) tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&d_empty[acc]), 0));
         }
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
     }
     tc::fence_before();
-    __syncthreads();
-    if (warp == 1) tc::tmem_free<512>(tbase);
+    tc::cluster_sync();  // the peer's MMAs, arrivals and TMEM use are over
+    tc::fence_after();
+    if (warp == 1) tc::tmem_free_2sm<512>(tbase);
 }
 
 __global__ void k_dense_readout(int n, int batch_pad, int batch, int L, const PairOf* __restrict__ pairs,
@@ -909,8 +932,8 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
     int dev = 0, sms = 0;
     ck(cudaGetDevice(&dev), "device");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
-    auto gemm = bf16 ? k_dense_gemm<true> : k_dense_gemm<false>;
-    ck(cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kGSmem), "smem attribute");
+    auto gemm = bf16 ? k_dense_gemm2<true> : k_dense_gemm2<false>;
+    ck(cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2Smem), "smem attribute");
     // process pairs in groups bounded by memory (~24 GB of state)
     const size_t per_pair = static_cast<size_t>(batch_pad) * (static_cast<size_t>(n) * 16 + static_cast<size_t>(npad) * (4 + esize));
     const size_t group = std::max<size_t>(1, (24ull << 30) / per_pair);
@@ -935,8 +958,8 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
                                                                 d.y.p, reinterpret_cast<int8_t*>(d.phi.p));
         c.launches++;
         const int KC = bf16 ? 64 : 128;
-        const CUtensorMap tmA = make_tmap(d.phi.p, static_cast<long long>(rows), npad, npad, esize, KC, kGH * kGM);
-        const CUtensorMap tmB = make_tmap(d.hj.p, static_cast<long long>(L) * n, npad, npad, esize, KC, kGN);
+        const CUtensorMap tmA = make_tmap(d.phi.p, static_cast<long long>(rows), npad, npad, esize, KC, kG2M);
+        const CUtensorMap tmB = make_tmap(d.hj.p, static_cast<long long>(L) * n, npad, npad, esize, KC, kGN / 2);
         const CUtensorMap tmD = make_tmap(d.D.p, static_cast<long long>(rows), n, npad, 4, 32, 32);
         // One stream: GEMM(t) then update(t) over all pairs of the group. (Two pair halves on
         // two streams did not overlap: the update kernel fills every SM, so a GEMM CTA of the
@@ -956,7 +979,7 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
             g.n = n;
             g.ldp = npad;
             g.batch_pad = batch_pad;
-            g.ntn = (n + kGN - 1) / kGN;
+            g.ntn = (n + kGN * kG2NT - 1) / (kGN * kG2NT);
             g.nch = (npad + KC - 1) / KC;
             g.tiles_per_pair = batch_pad / (kGH * kGM);
             g.pair_begin = hb[hh];
@@ -980,9 +1003,9 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
         for (int t = 0; t < p.T; ++t)
             for (int hh = 0; hh < halves; ++hh) {
                 const cudaStream_t st = hs[hh];
-                const int ggrid = static_cast<int>(std::min<long long>(ga[hh].items, sms));
+                const int ggrid = 2 * static_cast<int>(std::min<long long>(ga[hh].items, sms / 2));  // CTA pairs
                 const int kg = c.ktimer.begin(st);
-                gemm<<<ggrid, kGThreads, kGSmem, st>>>(tmA, tmB, tmD, ga[hh]);
+                gemm<<<ggrid, kGThreads, kG2Smem, st>>>(tmA, tmB, tmD, ga[hh]);
                 c.ktimer.end(kg, kKDenseGemm, st);
                 c.launches++;
                 if (halves == 2 && t == 0 && hh == 0) {  // half B starts one GEMM later: out of phase
