@@ -226,8 +226,12 @@ struct DenseStepArgs {
 
 
 
-// UDT: dt == 1 and dt * a0 == 1, so dt * d and dt a0 * y are exact and skipped
-template <bool NOISY, bool UDT, typename PhiT>
+// UDT: dt == 1 and dt * a0 == 1, so dt * d and dt a0 * y are exact and skipped. CHECK: record
+// the first step with a non-finite y (check_finite, solver.hpp:138-143). Only NaN survives a
+// step (an infinite y makes |x| > 1, and the wall and clamp reset both), and NaN is sticky, so
+// unchecked steps plus a final-state scan find every failing trajectory; the steps are re-run
+// with CHECK only then, for the step index.
+template <bool NOISY, bool UDT, typename PhiT, bool CHECK>
 __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_constant__ DenseStepArgs a)
 {
     __shared__ ZigTables z;
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
                 yi = __hiloint2double(static_cast<int>(yh), static_cast<int>(yl));
             }
             // the first step with a non-finite x or y has a non-finite y (x = x + dt a0 y, walls)
-            nonfinite |= !(fabs(yi) <= 1.7976931348623157e308);
+            if constexpr (CHECK) nonfinite |= !(fabs(yi) <= 1.7976931348623157e308);
             a.x[e] = xi;
             a.y[e] = yi;
             static_cast<PhiT*>(a.phi)[ep] = phi_of<PhiT>(xi < 0.0);
@@ -386,7 +390,8 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
         k = kn;
         eta = etan;
     }
-    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicMin(a.bad, a.t_step + 1);
+    if constexpr (CHECK)
+        if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicMin(a.bad, a.t_step + 1);
 }
 
 // ---- D = Phi . (H J)^T on the tensor cores (persistent, warp-specialised) -------------------
@@ -857,10 +862,13 @@ long long hj_bound(Ctx& c)
     return maxabs;
 }
 
-template <bool NOISY, bool UDT, typename PhiT>
-void launch_warp(const DenseStepArgs& sa, dim3 grid, cudaStream_t st)
+template <typename PhiT, bool CHECK>
+void launch_warp(const DenseStepArgs& sa, dim3 grid, cudaStream_t st, bool noisy, bool udt)
 {
-    k_dense_warp<NOISY, UDT, PhiT><<<grid, kWWarps * 32, 0, st>>>(sa);
+    if (noisy) udt ? k_dense_warp<true, true, PhiT, CHECK><<<grid, kWWarps * 32, 0, st>>>(sa)
+                   : k_dense_warp<true, false, PhiT, CHECK><<<grid, kWWarps * 32, 0, st>>>(sa);
+    else udt ? k_dense_warp<false, true, PhiT, CHECK><<<grid, kWWarps * 32, 0, st>>>(sa)
+             : k_dense_warp<false, false, PhiT, CHECK><<<grid, kWWarps * 32, 0, st>>>(sa);
 }
 
 }  // namespace
@@ -947,111 +955,116 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
         d.D.reserve(rows * npad);
         d.phi.reserve(rows * npad * esize);
         d.flags.reserve(4);
-        ck(cudaMemsetAsync(d.flags.p, 0x7f, sizeof(int), c.stream), "memset");
-        ck(cudaMemsetAsync(d.flags.p + 1, 0, sizeof(int), c.stream), "memset");
-        const dim3 igrid(static_cast<unsigned>((batch_pad + 7) / 8), static_cast<unsigned>(G));
-        if (bf16)
-            k_dense_init_t<uint16_t><<<igrid, 256, 0, c.stream>>>(n, npad, batch_pad, d.pairs.p, p.seed, p.init_scale, d.x.p,
-                                                                  d.y.p, reinterpret_cast<uint16_t*>(d.phi.p));
-        else
-            k_dense_init_t<int8_t><<<igrid, 256, 0, c.stream>>>(n, npad, batch_pad, d.pairs.p, p.seed, p.init_scale, d.x.p,
-                                                                d.y.p, reinterpret_cast<int8_t*>(d.phi.p));
-        c.launches++;
-        const int KC = bf16 ? 64 : 128;
-        const CUtensorMap tmA = make_tmap(d.phi.p, static_cast<long long>(rows), npad, npad, esize, KC, kG2M);
-        const CUtensorMap tmB = make_tmap(d.hj.p, static_cast<long long>(L) * n, npad, npad, esize, KC, kGN / 2);
-        const CUtensorMap tmD = make_tmap(d.D.p, static_cast<long long>(rows), n, npad, 4, 32, 32);
-        // One stream: GEMM(t) then update(t) over all pairs of the group. (Two pair halves on
-        // two streams did not overlap: the update kernel fills every SM, so a GEMM CTA of the
-        // other half never finds the shared memory it needs.)
-        const int halves = 1;
-        cudaStream_t hs[2] = {c.stream, d.stream2(c)};
-        if (halves == 2) {
-            ck(cudaEventRecord(d.ev_fork, c.stream), "event");
-            ck(cudaStreamWaitEvent(hs[1], d.ev_fork, 0), "event wait");
-        }
-        GemmArgs ga[2];
-        // 8 KB of launch arguments per half, per call (contexts may sample from several host threads)
-        const auto step_args_p = std::make_unique<DenseStepArgs[]>(2);
-        int hb[3] = {0, halves == 2 ? G / 2 : G, G};
-        for (int hh = 0; hh < halves; ++hh) {
-            GemmArgs& g = ga[hh];
-            g.n = n;
-            g.ldp = npad;
-            g.batch_pad = batch_pad;
-            g.ntn = (n + kGN * kG2NT - 1) / (kGN * kG2NT);
-            g.nch = (npad + KC - 1) / KC;
-            g.tiles_per_pair = batch_pad / (kGH * kGM);
-            g.pair_begin = hb[hh];
-            g.items = static_cast<long long>(hb[hh + 1] - hb[hh]) * g.tiles_per_pair * g.ntn;
-            g.pairs = d.pairs.p;
-            DenseStepArgs& sa = step_args_p[hh];
-            sa.n = n;
-            sa.ldp = npad;
-            sa.batch_pad = batch_pad;
-            sa.dt = p.dt;
-            sa.alpha = p.alpha;
-            sa.sdt = p.s_dt_a0;
-            sa.zig = p.zig;
-            sa.D = d.D.p;
-            sa.x = d.x.p;
-            sa.y = d.y.p;
-            sa.phi = d.phi.p;
-            sa.bad = d.flags.p;
-        }
-        const bool udt = p.dt == 1.0 && p.s_dt_a0 == 1.0, noisy = p.alpha > 0.0;
-        for (int t = 0; t < p.T; ++t)
-            for (int hh = 0; hh < halves; ++hh) {
-                const cudaStream_t st = hs[hh];
-                const int ggrid = 2 * static_cast<int>(std::min<long long>(ga[hh].items, sms / 2));  // CTA pairs
-                const int kg = c.ktimer.begin(st);
-                gemm<<<ggrid, kGThreads, kG2Smem, st>>>(tmA, tmB, tmD, ga[hh]);
-                c.ktimer.end(kg, kKDenseGemm, st);
-                c.launches++;
-                if (halves == 2 && t == 0 && hh == 0) {  // half B starts one GEMM later: out of phase
-                    ck(cudaEventRecord(d.ev_fork, st), "event");
-                    ck(cudaStreamWaitEvent(hs[1], d.ev_fork, 0), "event wait");
-                }
-                DenseStepArgs& sa = step_args_p[hh];
-                for (int s0 = hb[hh]; s0 < hb[hh + 1]; s0 += kDensePairsPerLaunch) {
-                    const int np = std::min(kDensePairsPerLaunch, hb[hh + 1] - s0);
-                    sa.t_step = t;
-                    sa.pair0 = s0;
-                    sa.neg_drift = -(p.a0 - static_cast<double>(t + 1) / static_cast<double>(p.T));
-                    for (int q = 0; q < np; ++q) {
-                        const PairOf& pq = pairs[g0 + s0 + q];
-                        const uint64_t key = run_key(p.seed, static_cast<uint32_t>(pq.run));
-                        sa.pair[q] = {static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32), pq.l, pq.traj0, pq.count, 0,
-                                      c0_host[static_cast<size_t>(pq.l)] / static_cast<double>(c.H)};
-                    }
-                    const dim3 wgrid(static_cast<unsigned>((maxc + kWWarps - 1) / kWWarps), static_cast<unsigned>(np));
-                    const int ku = c.ktimer.begin(st);
-                    if (bf16) {
-                        if (noisy) udt ? launch_warp<true, true, uint16_t>(sa, wgrid, st) : launch_warp<true, false, uint16_t>(sa, wgrid, st);
-                        else udt ? launch_warp<false, true, uint16_t>(sa, wgrid, st) : launch_warp<false, false, uint16_t>(sa, wgrid, st);
-                    } else {
-                        if (noisy) udt ? launch_warp<true, true, int8_t>(sa, wgrid, st) : launch_warp<true, false, int8_t>(sa, wgrid, st);
-                        else udt ? launch_warp<false, true, int8_t>(sa, wgrid, st) : launch_warp<false, false, int8_t>(sa, wgrid, st);
-                    }
-                    c.ktimer.end(ku, kKDenseUpdate, st);
-                    c.launches++;
-                }
+        // pass 0 unchecked; pass 1 (only when the final state holds a NaN) re-runs the group with
+        // per-step checks for the failing step (test hook MOMC_TEST_DENSE_CHECKED: checked at once)
+        static const bool force_checked = std::getenv("MOMC_TEST_DENSE_CHECKED") != nullptr;
+        for (int pass = force_checked ? 1 : 0; pass < 2; ++pass) {
+            const bool checked = pass == 1;
+            ck(cudaMemsetAsync(d.flags.p, 0x7f, sizeof(int), c.stream), "memset");
+            ck(cudaMemsetAsync(d.flags.p + 1, 0, sizeof(int), c.stream), "memset");
+            const dim3 igrid(static_cast<unsigned>((batch_pad + 7) / 8), static_cast<unsigned>(G));
+            if (bf16)
+                k_dense_init_t<uint16_t><<<igrid, 256, 0, c.stream>>>(n, npad, batch_pad, d.pairs.p, p.seed, p.init_scale, d.x.p,
+                                                                      d.y.p, reinterpret_cast<uint16_t*>(d.phi.p));
+            else
+                k_dense_init_t<int8_t><<<igrid, 256, 0, c.stream>>>(n, npad, batch_pad, d.pairs.p, p.seed, p.init_scale, d.x.p,
+                                                                    d.y.p, reinterpret_cast<int8_t*>(d.phi.p));
+            c.launches++;
+            const int KC = bf16 ? 64 : 128;
+            const CUtensorMap tmA = make_tmap(d.phi.p, static_cast<long long>(rows), npad, npad, esize, KC, kG2M);
+            const CUtensorMap tmB = make_tmap(d.hj.p, static_cast<long long>(L) * n, npad, npad, esize, KC, kGN / 2);
+            const CUtensorMap tmD = make_tmap(d.D.p, static_cast<long long>(rows), n, npad, 4, 32, 32);
+            // One stream: GEMM(t) then update(t) over all pairs of the group. (Two pair halves on
+            // two streams did not overlap: the update kernel fills every SM, so a GEMM CTA of the
+            // other half never finds the shared memory it needs.)
+            const int halves = 1;
+            cudaStream_t hs[2] = {c.stream, d.stream2(c)};
+            if (halves == 2) {
+                ck(cudaEventRecord(d.ev_fork, c.stream), "event");
+                ck(cudaStreamWaitEvent(hs[1], d.ev_fork, 0), "event wait");
             }
-        if (halves == 2) {
-            ck(cudaEventRecord(d.ev_join, hs[1]), "event");
-            ck(cudaStreamWaitEvent(c.stream, d.ev_join, 0), "event wait");
+            GemmArgs ga[2];
+            // 8 KB of launch arguments per half, per call (contexts may sample from several host threads)
+            const auto step_args_p = std::make_unique<DenseStepArgs[]>(2);
+            int hb[3] = {0, halves == 2 ? G / 2 : G, G};
+            for (int hh = 0; hh < halves; ++hh) {
+                GemmArgs& g = ga[hh];
+                g.n = n;
+                g.ldp = npad;
+                g.batch_pad = batch_pad;
+                g.ntn = (n + kGN * kG2NT - 1) / (kGN * kG2NT);
+                g.nch = (npad + KC - 1) / KC;
+                g.tiles_per_pair = batch_pad / (kGH * kGM);
+                g.pair_begin = hb[hh];
+                g.items = static_cast<long long>(hb[hh + 1] - hb[hh]) * g.tiles_per_pair * g.ntn;
+                g.pairs = d.pairs.p;
+                DenseStepArgs& sa = step_args_p[hh];
+                sa.n = n;
+                sa.ldp = npad;
+                sa.batch_pad = batch_pad;
+                sa.dt = p.dt;
+                sa.alpha = p.alpha;
+                sa.sdt = p.s_dt_a0;
+                sa.zig = p.zig;
+                sa.D = d.D.p;
+                sa.x = d.x.p;
+                sa.y = d.y.p;
+                sa.phi = d.phi.p;
+                sa.bad = d.flags.p;
+            }
+            const bool udt = p.dt == 1.0 && p.s_dt_a0 == 1.0, noisy = p.alpha > 0.0;
+            for (int t = 0; t < p.T; ++t)
+                for (int hh = 0; hh < halves; ++hh) {
+                    const cudaStream_t st = hs[hh];
+                    const int ggrid = 2 * static_cast<int>(std::min<long long>(ga[hh].items, sms / 2));  // CTA pairs
+                    const int kg = c.ktimer.begin(st);
+                    gemm<<<ggrid, kGThreads, kG2Smem, st>>>(tmA, tmB, tmD, ga[hh]);
+                    c.ktimer.end(kg, kKDenseGemm, st);
+                    c.launches++;
+                    if (halves == 2 && t == 0 && hh == 0) {  // half B starts one GEMM later: out of phase
+                        ck(cudaEventRecord(d.ev_fork, st), "event");
+                        ck(cudaStreamWaitEvent(hs[1], d.ev_fork, 0), "event wait");
+                    }
+                    DenseStepArgs& sa = step_args_p[hh];
+                    for (int s0 = hb[hh]; s0 < hb[hh + 1]; s0 += kDensePairsPerLaunch) {
+                        const int np = std::min(kDensePairsPerLaunch, hb[hh + 1] - s0);
+                        sa.t_step = t;
+                        sa.pair0 = s0;
+                        sa.neg_drift = -(p.a0 - static_cast<double>(t + 1) / static_cast<double>(p.T));
+                        for (int q = 0; q < np; ++q) {
+                            const PairOf& pq = pairs[g0 + s0 + q];
+                            const uint64_t key = run_key(p.seed, static_cast<uint32_t>(pq.run));
+                            sa.pair[q] = {static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32), pq.l, pq.traj0, pq.count, 0,
+                                          c0_host[static_cast<size_t>(pq.l)] / static_cast<double>(c.H)};
+                        }
+                        const dim3 wgrid(static_cast<unsigned>((maxc + kWWarps - 1) / kWWarps), static_cast<unsigned>(np));
+                        const int ku = c.ktimer.begin(st);
+                        if (bf16) checked ? launch_warp<uint16_t, true>(sa, wgrid, st, noisy, udt)
+                                          : launch_warp<uint16_t, false>(sa, wgrid, st, noisy, udt);
+                        else checked ? launch_warp<int8_t, true>(sa, wgrid, st, noisy, udt)
+                                     : launch_warp<int8_t, false>(sa, wgrid, st, noisy, udt);
+                        c.ktimer.end(ku, kKDenseUpdate, st);
+                        c.launches++;
+                    }
+                }
+            if (halves == 2) {
+                ck(cudaEventRecord(d.ev_join, hs[1]), "event");
+                ck(cudaStreamWaitEvent(c.stream, d.ev_join, 0), "event wait");
+            }
+            const dim3 rgrid(static_cast<unsigned>((batch_pad + 127) / 128), static_cast<unsigned>(G));
+            k_dense_readout<<<rgrid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, p.row0, d.flags.p + 1);
+            c.launches++;
+            ck(cudaGetLastError(), "dense sampler");
+            int fl[2] = {0, 0};
+            ck(cudaMemcpyAsync(fl, d.flags.p, sizeof fl, cudaMemcpyDeviceToHost, c.stream), "D2H");
+            ck(cudaStreamSynchronize(c.stream), "dense sampler");
+            c.ktimer.collect();
+            if (fl[0] != 0x7f7f7f7f)
+                runtime("numerical failure at step " + std::to_string(fl[0]) + " (run " + std::to_string(pairs[g0].run) +
+                        ", weight " + std::to_string(pairs[g0].l) + ")");
+            if (fl[1] == 0) break;  // no trajectory ended non-finite
+            if (checked) runtime("numerical failure (non-finite final state)");
         }
-        const dim3 rgrid(static_cast<unsigned>((batch_pad + 127) / 128), static_cast<unsigned>(G));
-        k_dense_readout<<<rgrid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, p.row0, d.flags.p + 1);
-        c.launches++;
-        ck(cudaGetLastError(), "dense sampler");
-        int fl[2] = {0, 0};
-        ck(cudaMemcpyAsync(fl, d.flags.p, sizeof fl, cudaMemcpyDeviceToHost, c.stream), "D2H");
-        ck(cudaStreamSynchronize(c.stream), "dense sampler");
-        c.ktimer.collect();
-        if (fl[0] != 0x7f7f7f7f)
-            runtime("numerical failure at step " + std::to_string(fl[0]) + " (run " + std::to_string(pairs[g0].run) +
-                    ", weight " + std::to_string(pairs[g0].l) + ")");
     }
 }
 

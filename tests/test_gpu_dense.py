@@ -121,3 +121,40 @@ def test_dense_bf16_path_agrees_with_reference(ref, session):
     mm = int(np.sum(np.any(got != want, axis=1)))
     print(f"dense bf16 dSB n={n}: {mm} of {got.shape[0]} words differ")
     assert mm <= MAX_DENSE_WORD_MISMATCH * got.shape[0]
+
+
+_CHECKED_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2604_26477_b200 import api
+s = api.Session(0)
+s.generate_uniform_instance(288, 0.5, 3, 12)
+s.set_dense_threshold(256)
+s.set_weights(api.build_weights(3, resolution=4))
+s.sample(api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=40, seed=21), 1)
+assert s.sampler_path() == "dense_i8", s.sampler_path()
+np.save({out!r}, s.pool(stamps=False).words)
+"""
+
+
+def test_dense_unchecked_steps_equal_checked_steps(tmp_path):
+    """The update kernel runs without the per-step finiteness check (a final-state scan and a
+    checked re-run on failure replace it); with the checks forced on (MOMC_TEST_DENSE_CHECKED)
+    the pool is the same."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pools = []
+    for checked in (False, True):
+        out = str(tmp_path / f"words_{int(checked)}.npy")
+        env = dict(os.environ)
+        env.pop("MOMC_TEST_DENSE_CHECKED", None)
+        if checked:
+            env["MOMC_TEST_DENSE_CHECKED"] = "1"
+        subprocess.run([sys.executable, "-c", _CHECKED_SCRIPT.format(root=root, out=out)], env=env, check=True,
+                       timeout=300)
+        pools.append(np.load(out))
+    diff = int(np.sum(np.any(pools[0] != pools[1], axis=1)))
+    print(f"checked vs unchecked dense steps: {diff} of {pools[0].shape[0]} pool rows differ")
+    assert pools[0].shape[0] > 0 and diff == 0
