@@ -699,10 +699,15 @@ struct AxisCounts {
     int d[kMaxK];
 };
 
+// axes with at most this many distinct values are ordered by k_rank_sort_asc (every value
+// counts the smaller ones: D^2 compares, ~5 us at the C2 front's ~900); larger ones by a radix sort
+constexpr int kRankSortMax = 2048;
+
 __global__ void k_rank_sort_asc(const double* __restrict__ ins, AxisCounts Ds, long long cap, double* outs)
 {  // distinct values: rank = #smaller (blockIdx.y = axis)
     extern __shared__ double tile[];
     const int D = Ds.d[blockIdx.y];
+    if (D > kRankSortMax) return;  // (radix-sorted by the host)
     const double* in = ins + cap * blockIdx.y;
     double* out = outs + cap * blockIdx.y;
     for (int base = blockIdx.x * blockDim.x; base < D; base += gridDim.x * blockDim.x) {
@@ -1264,10 +1269,24 @@ bool grid_finish(Ctx& c, Scratch& s, const double* d_vals, long long V, int K, c
             if (prod > kGridCap) return false;
         }
     }
-    k_rank_sort_asc<<<dim3(grid_blocks(maxD, 256), K), 256, 256 * sizeof(double), c.stream>>>(s.axisbuf.p, dc,
-                                                                                             kDistinctCap,
-                                                                                             s.axis_sorted.p);
+    k_rank_sort_asc<<<dim3(grid_blocks(std::min(maxD, kRankSortMax), 256), K), 256, 256 * sizeof(double),
+                      c.stream>>>(s.axisbuf.p, dc, kDistinctCap, s.axis_sorted.p);
     c.launches++;
+    if (maxD > kRankSortMax) {  // O(D) per large axis instead of D^2 compares
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tb, s.axisbuf.p, s.axis_sorted.p, maxD, 0, 64, c.stream);
+        DevBuf<unsigned char> tmp;
+        tmp.reserve(tb + 1);
+        for (int a = 0; a < K; ++a)
+            if (g.D[a] > kRankSortMax) {
+                const size_t off = static_cast<size_t>(a) * kDistinctCap;
+                ck(cub::DeviceRadixSort::SortKeys(tmp.p, tb, s.axisbuf.p + off, s.axis_sorted.p + off, g.D[a], 0, 64,
+                                                  c.stream),
+                   "axis sort");
+                c.launches += 4;
+            }
+        tmp.release();
+    }
     if (host_axes) {
         for (int a = 0; a < K; ++a) {
             std::vector<double> hv(static_cast<size_t>(g.D[a]));

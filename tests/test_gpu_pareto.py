@@ -130,6 +130,18 @@ def test_filter_values_sieve_matches_reference(ref, session, k, V):
     assert np.array_equal(got.values, want.values)
 
 
+@pytest.mark.parametrize("k,V", [(2, 20000), (3, 8000)])
+def test_filter_values_grid_with_large_axes_matches_reference(ref, session, k, V):
+    """continuous values with more than 2048 (but at most 32768) distinct values per axis: the
+    compressed grid still fits, and its axes are ordered by the radix-sort branch"""
+    rng = np.random.default_rng(3 * V + k)
+    vals = rng.normal(size=(V, k)) + rng.normal(size=(V, 1))
+    got = api.non_dominated_filter([ObjectiveVector(list(v), Sense.cut) for v in vals], session=session)
+    want = ref.filter_values(vals)
+    print(f"K={k}, V={V}: front {want.values.shape[0]}")
+    assert np.array_equal(got.values, want.values)
+
+
 def test_filter_values_hamiltonian_sense(ref, session):
     vals = grid_vectors(3000, 3, 77)
     got = api.non_dominated_filter([ObjectiveVector(v, Sense.hamiltonian) for v in vals], session=session)
