@@ -199,6 +199,30 @@ __device__ __forceinline__ bool wedge_accept(uint32_t u, uint32_t w1, uint32_t w
 //     that falls short (about 1 in 10) are walked sequentially by the whole warp.
 // The values go through a 32-entry shared buffer to the lanes of their spins.
 constexpr int kWRing = 256;  // words per warp
+
+// shared-memory accesses by 32-bit shared-window address (the per-warp rings and value
+// buffers: through generic pointers the compiler rebuilt their window base every window)
+__device__ __forceinline__ uint32_t lds32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ double ldsf64(uint32_t a)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void stsf64(uint32_t a, double v)
+{
+    asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory");
+}
 constexpr int kWWarps = 8;   // trajectories (warps) per CTA
 
 struct DensePairArg {
@@ -252,8 +276,9 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
     const int t = blockIdx.x * kWWarps + warp;
     if (t >= pr.count) return;  // whole warps; no CTA barrier below
     const int n = a.n;
-    uint32_t* ring = rings[warp];
-    double* val = vals[warp];
+    const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(rings[warp]));
+    const uint32_t val = static_cast<uint32_t>(__cvta_generic_to_shared(vals[warp]));
+    auto rw = [&](int p) { return lds32(ring + 4u * static_cast<uint32_t>(p & (kWRing - 1))); };
     const uint32_t k0 = pr.k0, k1 = pr.k1, lo = tag_word(kTagStepNoise, static_cast<uint32_t>(a.t_step));
     const uint32_t mid = static_cast<uint32_t>(pr.traj0 + t), hi = static_cast<uint32_t>(pr.l);
     const double c0h = pr.c0h;
@@ -261,12 +286,12 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
     int head = 0, tail = 0;  // next unread word / words generated (warp-uniform)
     auto gen = [&]() {       // 128 words: block tail/4 + lane on each lane
         const uint4 v = philox(k0, k1, static_cast<uint32_t>(tail >> 2) + static_cast<uint32_t>(lane), lo, mid, hi);
-        *reinterpret_cast<uint4*>(&ring[(tail + 4 * lane) & (kWRing - 1)]) = v;
+        sts128(ring + 4u * static_cast<uint32_t>((tail + 4 * lane) & (kWRing - 1)), v);
         tail += 128;
         __syncwarp();
     };
     auto word = [&](int p) -> uint32_t {  // any position: the ring, or generated directly (slow path)
-        if (p < tail) return ring[p & (kWRing - 1)];
+        if (p < tail) return rw(p);
         const uint4 v = philox(k0, k1, static_cast<uint32_t>(p >> 2), lo, mid, hi);
         const int c = p & 3;
         return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
@@ -287,7 +312,7 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
         if constexpr (NOISY) {
             if (tail - head < 96) gen();
             const int H = head;
-            const uint32_t u = ring[(H + lane) & (kWRing - 1)];
+            const uint32_t u = rw(H + lane);
             const bool slow = !is_fast(u);
             const uint32_t sm = __ballot_sync(0xffffffffu, slow);
             if (sm == 0) {  // 32 fast words: lane L's normal is its own word
@@ -303,7 +328,7 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
             int len = 1;
             if (slow) {
                 if (u & 127u) {
-                    good = wedge_accept32(u, ring[(H + lane + 1) & (kWRing - 1)], ring[(H + lane + 2) & (kWRing - 1)], z,
+                    good = wedge_accept32(u, rw(H + lane + 1), rw(H + lane + 2), z,
                                           zwf, zff);
                     len = 3;
                 } else {
@@ -338,9 +363,9 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
             const uint32_t prod = gm & ~cons;  // positions that give this window's normals
             k = __popc(prod);
             head = H + end;
-            if ((prod >> lane) & 1u) val[__popc(prod & lt)] = v;
+            if ((prod >> lane) & 1u) stsf64(val + 8u * __popc(prod & lt), v);
             __syncwarp();
-            eta = val[lane];
+            eta = ldsf64(val + 8u * lane);
             __syncwarp();  // read before the next window writes
         }
     };
