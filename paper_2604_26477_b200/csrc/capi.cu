@@ -45,6 +45,10 @@ Ctx::~Ctx()
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev_dep) cudaEventDestroy(ev_dep);
+    if (order_stream) cudaStreamSynchronize(order_stream);
+    if (ev_order_fork) cudaEventDestroy(ev_order_fork);
+    if (ev_order_done) cudaEventDestroy(ev_order_done);
+    if (order_stream) cudaStreamDestroy(order_stream);
     if (sample_stream) cudaStreamDestroy(sample_stream);
     if (stream) cudaStreamDestroy(stream);
     if (pinned) cudaFreeHost(pinned);
@@ -1406,7 +1410,24 @@ int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long
         const auto tf = clk::now();
         ParetoTimings tm;
         DevArchive& a = resident_archive(*ctx);
+        // with HV, the archive order runs on ctx->order_stream beside the reference point and
+        // HV, which read the unordered front (the same value set); joined below, or on error
+        struct OrderJoin {
+            Ctx& c;
+            ~OrderJoin()
+            {
+                c.order_async = false;
+                if (c.order_pending) {
+                    cudaStreamWaitEvent(c.stream, c.ev_order_done, 0);
+                    c.order_pending = false;
+                }
+            }
+        } order_join{*ctx};
+        ctx->order_async = do_hv != 0;
         filter_pool_device(*ctx, ctx->d_words.p, ctx->pool_size, a, &tm);
+        ctx->order_async = false;
+        const bool ordering = ctx->order_pending;
+        const double* hv_vals = ordering ? ctx->order_front : a.vals.p;
         rep->pool_size = ctx->pool_size;
         rep->unique_configs = tm.unique_configs;
         rep->unique_vectors = tm.unique_vectors;
@@ -1423,15 +1444,22 @@ int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long
             std::vector<double> r(static_cast<size_t>(ctx->k));
             if (fixed_ref) {
                 r.assign(fixed_ref, fixed_ref + ctx->k);
-                rep->hv = hypervolume_device(*ctx, a.vals.p, a.F, a.K, r, true);
+                rep->hv = hypervolume_device(*ctx, hv_vals, a.F, a.K, r, true);
             } else {
                 // sampled reference clamped under the archive, kept on the device for the HV:
                 // one read-back for both (reference_s is then folded into hv_s)
-                rep->hv = hv_sampled_reference_device(*ctx, a.vals.p, a.F, a.K, ref_count, cfg->seed, r, true);
+                rep->hv = hv_sampled_reference_device(*ctx, hv_vals, a.F, a.K, ref_count, cfg->seed, r, true);
             }
             rep->reference_s = 0;
             rep->hv_s = std::chrono::duration<double>(clk::now() - tr).count();
             for (int l = 0; l < ctx->k && l < 16; ++l) rep->reference[l] = r[static_cast<size_t>(l)];
+        }
+        if (ordering) {  // the archive is complete when its order is
+            ck(cudaEventSynchronize(ctx->ev_order_done), "archive order");
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, ctx->ev_order_fork, ctx->ev_order_done), "event");
+            rep->order_s = ms * 1e-3;
+            if (ctx->grid_archive == hv_vals) ctx->grid_archive = a.vals.p;  // the same value set
         }
         rep->pareto_filtering_s = std::chrono::duration<double>(clk::now() - tf).count();
         rep->end_to_end_s = std::chrono::duration<double>(clk::now() - t0).count();

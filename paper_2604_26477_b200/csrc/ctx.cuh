@@ -178,6 +178,14 @@ struct Ctx {
     unsigned long long grid_gen = 0, front_grid_gen = ~0ull;
     const double* grid_archive = nullptr;
     long long grid_rows = -1;
+    // momc_b200_pipeline with HV: the archive's lexicographic order runs on order_stream
+    // beside the reference point and HV on `stream` (which read the unordered front, the same
+    // value set); the pipeline joins it before returning
+    cudaStream_t order_stream = nullptr;
+    cudaEvent_t ev_order_fork = nullptr, ev_order_done = nullptr;
+    bool order_async = false;    // the next finish_archive orders on order_stream
+    bool order_pending = false;  // an order is in flight on order_stream
+    const double* order_front = nullptr;  // its unordered front rows (the same value set)
     KernelTimer ktimer;                           // optional per-kernel-class device times
 
     ~Ctx();

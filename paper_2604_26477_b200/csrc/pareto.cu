@@ -986,17 +986,6 @@ __global__ void k_ref_words(int count, uint64_t key, int n, uint64_t* words)
     }
 }
 
-// ordered keys (dkey) -> the doubles they encode
-__global__ void k_keys_to_vals(const unsigned long long* __restrict__ keys, int K, double* out)
-{
-    const int k = threadIdx.x;
-    if (k < K) {
-        const unsigned long long key = keys[k];
-        const unsigned long long b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
-        out[k] = __longlong_as_double(static_cast<long long>(b));
-    }
-}
-
 // per-objective minimum (ordered keys): one thread per row, a warp minimum per objective,
 // then one atomic per warp and objective (the K counters are contended otherwise)
 __global__ void k_col_min(const double* __restrict__ vals, long long rows, int K, unsigned long long* rmin)
@@ -1123,27 +1112,43 @@ __global__ void k_hv_cells(const uint32_t* __restrict__ S, long long cells, Grid
     }
 }
 
-__global__ void k_ref_check(const double* __restrict__ vals, long long F, int K, const double* __restrict__ r,
-                            unsigned long long* first)
-{
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F;
-         i += static_cast<long long>(gridDim.x) * blockDim.x)
-        for (int k = 0; k < K; ++k)
-            if (r[k] > vals[i * K + k]) atomicMin(first, static_cast<unsigned long long>(i * K + k));
-}
 
 // integrality of the archive values and the largest gain v - r (decides the exact __int128 HV
-// sum): flags[0] &= every value is an integer below 9e15, flags[1] = max dkey(gain)
-__global__ void k_hv_stats(const double* __restrict__ vals, long long F, int K, const double* __restrict__ r,
-                           unsigned long long* flags)
+// sum): flags[0] &= every value is an integer below 9e15, flags[1] = max dkey(gain); and
+// validate_reference (pareto.hpp:103-118): *first = the first (entry K + objective) with
+// r > v. With rkeys the reference comes as ordered keys (reference_keys_device): it is decoded
+// here and written to r for the kernels that follow.
+__global__ void k_hv_stats(const double* __restrict__ vals, long long F, int K, double* r,
+                           const unsigned long long* __restrict__ rkeys, unsigned long long* flags,
+                           unsigned long long* first)
 {
+    double rr[kMaxK];
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) {
+        if (k < K) {
+            if (rkeys) {
+                const unsigned long long key = rkeys[k];
+                const unsigned long long b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
+                rr[k] = __longlong_as_double(static_cast<long long>(b));
+            } else {
+                rr[k] = r[k];
+            }
+        }
+    }
+    if (rkeys && blockIdx.x == 0 && threadIdx.x < K) r[threadIdx.x] = rr[threadIdx.x];
     bool integral = true;
     unsigned long long gmax = dkey(0.0);
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < F * K;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const double v = vals[i];
+        const int k = static_cast<int>(i % K);
+        double rk = rr[0];
+#pragma unroll
+        for (int q = 1; q < kMaxK; ++q)
+            if (q == k) rk = rr[q];
         integral &= floor(v) == v && fabs(v) < 9.0e15;
-        const unsigned long long g = dkey(v - r[i % K]);
+        if (rk > v) atomicMin(first, static_cast<unsigned long long>(i));
+        const unsigned long long g = dkey(v - rk);
         gmax = g > gmax ? g : gmax;
     }
     if (!__all_sync(0xffffffffu, integral) && (threadIdx.x & 31) == 0) atomicAnd(&flags[0], 0ull);
@@ -1202,6 +1207,9 @@ struct Scratch {
     DevBuf<unsigned char> keep;
     DevBuf<long long> rank;
     DevBuf<__int128> ipart;
+    DevBuf<double> front_vals;  // unordered front rows kept for an async order (finish_archive)
+    DevBuf<uint32_t> front_own;
+    DevBuf<uint64_t> front_words;
     DevBuf<double> dpart;
     GridGeo front_geo{};        // the grid of the last filter's front (see Ctx::grid_gen)
     long long front_cells = 0;
@@ -1215,6 +1223,7 @@ Scratch& scratch(Ctx& c)
         s->axisbuf.release(); s->axis_sorted.release(); s->rdev.release(); s->T.release(); s->S.release();
         s->dtab64.release();
         s->keep.release(); s->rank.release(); s->ipart.release(); s->dpart.release();
+        s->front_vals.release(); s->front_own.release(); s->front_words.release();
         delete s;
     });
     return *static_cast<Scratch*>(c.pareto_scratch.get());
@@ -1622,6 +1631,14 @@ void lex_desc_rank(Ctx& c, const double* d_vals, long long F, int K, long long* 
     tmp.release();
 }
 
+__global__ void k_gather_words(const uint64_t* __restrict__ words, const uint32_t* __restrict__ idx, long long U, int wpc,
+                               uint64_t* out)
+{
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < U * wpc;
+         q += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[q] = words[static_cast<long long>(idx[q / wpc]) * wpc + q % wpc];
+}
+
 // Shared tail of both filters: V distinct vectors (d_vv, V x K) with owner configs
 // (row index into `words` via d_own, or none) -> front -> archive (lex-descending).
 void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, const uint64_t* words,
@@ -1641,10 +1658,15 @@ void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, 
     c.launches++;
     const long long F = static_cast<long long>(read_counter(c, s.counters.p + 1));
     cudaEventRecord(e1, c.stream);
-    // gather front rows, then order them lexicographically descending
-    DevBuf<double> fv;
+    // gather front rows, then order them lexicographically descending. With c.order_async the
+    // front rows stay in scratch (the caller's HV reads them) and the order runs on
+    // c.order_stream; the caller joins it (momc_b200_pipeline)
+    const bool async = c.order_async && !c.skip_order;
+    DevBuf<double> fv_local;
+    DevBuf<uint32_t> fown_local;
+    DevBuf<double>& fv = async ? s.front_vals : fv_local;
+    DevBuf<uint32_t>& fown = async ? s.front_own : fown_local;
     fv.reserve(static_cast<size_t>(F) * K + 1);
-    DevBuf<uint32_t> fown;
     if (d_own) {
         fown.reserve(static_cast<size_t>(F) + 1);
         k_map_u32<<<grid_blocks(F), 256, 0, c.stream>>>(s.rows.p, d_own, F, fown.p);
@@ -1654,31 +1676,68 @@ void finish_archive(Ctx& c, Scratch& s, const double* d_vv, long long V, int K, 
                                                          nullptr);
     c.launches++;
     s.rank.reserve(static_cast<size_t>(F) + 1);
-    if (!c.skip_order) lex_desc_rank(c, fv.p, F, K, s.rank.p);
     out.F = F;
     out.K = K;
     out.wpc = d_own ? wpc : 0;
     out.vals.reserve(static_cast<size_t>(F) * K + 1);
     if (d_own) out.words.reserve(static_cast<size_t>(F) * wpc + 1);
-    k_gather_rows<<<grid_blocks(F), 256, 0, c.stream>>>(fv.p, nullptr, F, K, words, d_own ? fown.p : nullptr, wpc,
-                                                         c.skip_order ? nullptr : s.rank.p, out.vals.p,
-                                                         d_own ? out.words.p : nullptr);
-    c.launches++;
+    const uint64_t* ow = words;  // the order's config source, rows fown (or the front's own rows)
+    const uint32_t* orows = d_own ? fown.p : nullptr;
+    if (async && d_own) {  // the caller's `words` may be freed on c.stream before the order runs
+        s.front_words.reserve(static_cast<size_t>(F) * wpc + 1);
+        k_gather_words<<<grid_blocks(F * wpc), 256, 0, c.stream>>>(words, fown.p, F, wpc, s.front_words.p);
+        c.launches++;
+        ow = s.front_words.p;
+        orows = nullptr;
+    }
+    auto order = [&] {
+        if (!c.skip_order) lex_desc_rank(c, fv.p, F, K, s.rank.p);
+        k_gather_rows<<<grid_blocks(F), 256, 0, c.stream>>>(fv.p, nullptr, F, K, ow, orows, wpc,
+                                                             c.skip_order ? nullptr : s.rank.p, out.vals.p,
+                                                             d_own ? out.words.p : nullptr);
+        c.launches++;
+    };
+    if (async) {
+        if (!c.order_stream) {
+            int least = 0, greatest = 0;
+            ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "stream priorities");
+            ck(cudaStreamCreateWithPriority(&c.order_stream, cudaStreamNonBlocking, greatest), "stream");
+            ck(cudaEventCreate(&c.ev_order_fork), "event");
+            ck(cudaEventCreate(&c.ev_order_done), "event");
+        }
+        ck(cudaEventRecord(c.ev_order_fork, c.stream), "event");
+        ck(cudaStreamWaitEvent(c.order_stream, c.ev_order_fork, 0), "event wait");
+        struct Swap {  // the order's launches, allocations and frees go to order_stream
+            Ctx& c;
+            cudaStream_t main;
+            explicit Swap(Ctx& cc) : c(cc), main(cc.stream) { c.stream = c.order_stream; g_alloc_stream = c.order_stream; }
+            ~Swap() { c.stream = main; g_alloc_stream = main; }
+        };
+        {
+            Swap swap(c);
+            order();
+            ck(cudaEventRecord(c.ev_order_done, c.stream), "event");
+        }
+        c.order_pending = true;
+        c.order_front = fv.p;
+    } else {
+        order();
+    }
     cudaEventRecord(e2, c.stream);
     if (method == 1) {  // the front's grid covers this archive (hypervolume_device)
         c.front_grid_gen = c.grid_gen;
-        c.grid_archive = out.vals.p;
+        c.grid_archive = async ? fv.p : out.vals.p;  // (the pipeline's join points it at out.vals)
         c.grid_rows = F;
     }
     if (tm) {
         ck(cudaStreamSynchronize(c.stream), "archive");
         tm->front_s = seconds_between(e0, e1);
-        tm->order_s = seconds_between(e1, e2);
+        tm->order_s = async ? 0.0 : seconds_between(e1, e2);  // async: the pipeline times it
         tm->front_method = method;
         tm->unique_vectors = V;
     }
-    fv.release();
-    fown.release();
+    fv_local.release();
+    fown_local.release();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
@@ -1961,13 +2020,6 @@ void filter_pool_device(Ctx& c, const uint64_t* d_words, long long M, DevArchive
     for (auto ev : {e0, e1, e2, e3}) cudaEventDestroy(ev);
 }
 
-__global__ void k_gather_words(const uint64_t* __restrict__ words, const uint32_t* __restrict__ idx, long long U, int wpc,
-                               uint64_t* out)
-{
-    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < U * wpc;
-         q += static_cast<long long>(gridDim.x) * blockDim.x)
-        out[q] = words[static_cast<long long>(idx[q / wpc]) * wpc + q % wpc];
-}
 
 // front of (the M pool configs U the X rows xv / xw) into `out` in one collapse + front pass:
 // the streaming step's "run front merged into the running archive" without a separate run
@@ -2131,11 +2183,11 @@ double hv_core(Ctx& c, Scratch& s, const double* d_vals, long long F, int K, con
     // (0: below every gain's key; the host floors it at 1 anyway)
     ck(cudaMemsetAsync(s.counters.p + 3, 0xFF, sizeof(unsigned long long) * 2, c.stream), "memset");
     ck(cudaMemsetAsync(s.counters.p + 5, 0, sizeof(unsigned long long), c.stream), "memset");
-    k_ref_check<<<grid_blocks(F), 256, 0, c.stream>>>(d_vals, F, K, d_r, s.counters.p + 3);
     // gains are exact integers when every value and r is integral (n=42 configs): then the
     // __int128 cell sum is the exact hypervolume, i.e. the reference's exact double result
-    k_hv_stats<<<grid_blocks(F * K), 256, 0, c.stream>>>(d_vals, F, K, d_r, s.counters.p + 4);
-    c.launches += 2;
+    k_hv_stats<<<grid_blocks(F * K), 256, 0, c.stream>>>(d_vals, F, K, const_cast<double*>(d_r), rkeys,
+                                                          s.counters.p + 4, s.counters.p + 3);
+    c.launches++;
     auto finish_checks = [&](const unsigned long long* st, bool& integral) {
         if (st[0] != none)
             usage("reference point not dominated by archive entry " + std::to_string(st[0] / K) + " (objective " +
@@ -2245,8 +2297,7 @@ double hv_sampled_reference_device(Ctx& c, const double* d_vals, long long F, in
     DevBuf<unsigned long long> keys;
     keys.reserve(static_cast<size_t>(kMaxK));
     reference_keys_device(c, count, seed, d_vals, F, keys.p);
-    k_keys_to_vals<<<1, 32, 0, c.stream>>>(keys.p, K, s.rdev.p);
-    c.launches++;
+    // (k_hv_stats decodes the keys into s.rdev for k_hv_cells)
     const double hv = hv_core(c, s, d_vals, F, K, s.rdev.p, r_out, keys.p, reuse_front_grid);
     keys.release();
     return hv;
