@@ -1325,6 +1325,42 @@ int momc_b200_clamp_reference(momc_ctx* ctx, double* r, char* err, size_t errlen
     });
 }
 
+namespace {
+// With HV, a filter's archive order (finish_archive with order_async) runs on
+// ctx.order_stream beside the reference point and HV, which read the unordered front (the same
+// value set). The order is joined into ctx.stream when this leaves scope, also on error.
+struct OrderJoin {
+    Ctx& c;
+    bool ordering = false;
+    OrderJoin(Ctx& cc, bool async) : c(cc) { c.order_async = async; }
+    // the values the HV reads: the unordered front while the order runs
+    const double* hv_vals(const DevArchive& a)
+    {
+        c.order_async = false;
+        ordering = c.order_pending;
+        return ordering ? c.order_front : a.vals.p;
+    }
+    // after the HV: the archive is complete when its order is
+    void complete(const DevArchive& a, const double* hv_vals, momc_bench_report* rep)
+    {
+        if (!ordering) return;
+        ck(cudaEventSynchronize(c.ev_order_done), "archive order");
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, c.ev_order_fork, c.ev_order_done), "event");
+        rep->order_s = ms * 1e-3;
+        if (c.grid_archive == hv_vals) c.grid_archive = a.vals.p;  // the same value set
+    }
+    ~OrderJoin()
+    {
+        c.order_async = false;
+        if (c.order_pending) {
+            cudaStreamWaitEvent(c.stream, c.ev_order_done, 0);
+            c.order_pending = false;
+        }
+    }
+};
+}  // namespace
+
 int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t* nums, int L, int H,
                     const momc_solver_cfg* cfg, int runs, int ref_count, const double* fixed_ref, uint64_t* out_pool,
                     momc_bench_report* rep, char* err, size_t errlen)
@@ -1352,7 +1388,9 @@ int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t
         const auto tf = clk::now();
         ParetoTimings tm;
         DevArchive& a = resident_archive(*ctx);
+        OrderJoin order_join(*ctx, true);
         filter_pool_device(*ctx, ctx->d_words.p, ctx->pool_size, a, &tm);
+        const double* hv_vals = order_join.hv_vals(a);
         rep->unique_configs = tm.unique_configs;
         rep->unique_vectors = tm.unique_vectors;
         rep->archive_size = a.F;
@@ -1367,12 +1405,13 @@ int momc_b200_bench(momc_ctx* ctx, const momc_instance_view* inst, const int32_t
         std::vector<double> r(static_cast<size_t>(ctx->k));
         if (fixed_ref) {
             r.assign(fixed_ref, fixed_ref + ctx->k);
-            rep->hv = hypervolume_device(*ctx, a.vals.p, a.F, a.K, r, true);
+            rep->hv = hypervolume_device(*ctx, hv_vals, a.F, a.K, r, true);
         } else {
             // sampled reference clamped under the archive, kept on the device for the HV: one
             // read-back for both (reference_s is then folded into hv_s)
-            rep->hv = hv_sampled_reference_device(*ctx, a.vals.p, a.F, a.K, ref_count, cfg->seed, r, true);
+            rep->hv = hv_sampled_reference_device(*ctx, hv_vals, a.F, a.K, ref_count, cfg->seed, r, true);
         }
+        order_join.complete(a, hv_vals, rep);
         const auto te = clk::now();
         rep->reference_s = 0;
         rep->hv_s = std::chrono::duration<double>(te - tr).count();
@@ -1410,24 +1449,9 @@ int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long
         const auto tf = clk::now();
         ParetoTimings tm;
         DevArchive& a = resident_archive(*ctx);
-        // with HV, the archive order runs on ctx->order_stream beside the reference point and
-        // HV, which read the unordered front (the same value set); joined below, or on error
-        struct OrderJoin {
-            Ctx& c;
-            ~OrderJoin()
-            {
-                c.order_async = false;
-                if (c.order_pending) {
-                    cudaStreamWaitEvent(c.stream, c.ev_order_done, 0);
-                    c.order_pending = false;
-                }
-            }
-        } order_join{*ctx};
-        ctx->order_async = do_hv != 0;
+        OrderJoin order_join(*ctx, do_hv != 0);
         filter_pool_device(*ctx, ctx->d_words.p, ctx->pool_size, a, &tm);
-        ctx->order_async = false;
-        const bool ordering = ctx->order_pending;
-        const double* hv_vals = ordering ? ctx->order_front : a.vals.p;
+        const double* hv_vals = order_join.hv_vals(a);
         rep->pool_size = ctx->pool_size;
         rep->unique_configs = tm.unique_configs;
         rep->unique_vectors = tm.unique_vectors;
@@ -1454,13 +1478,7 @@ int momc_b200_pipeline(momc_ctx* ctx, const momc_solver_cfg* cfg, int runs, long
             rep->hv_s = std::chrono::duration<double>(clk::now() - tr).count();
             for (int l = 0; l < ctx->k && l < 16; ++l) rep->reference[l] = r[static_cast<size_t>(l)];
         }
-        if (ordering) {  // the archive is complete when its order is
-            ck(cudaEventSynchronize(ctx->ev_order_done), "archive order");
-            float ms = 0;
-            ck(cudaEventElapsedTime(&ms, ctx->ev_order_fork, ctx->ev_order_done), "event");
-            rep->order_s = ms * 1e-3;
-            if (ctx->grid_archive == hv_vals) ctx->grid_archive = a.vals.p;  // the same value set
-        }
+        order_join.complete(a, hv_vals, rep);
         rep->pareto_filtering_s = std::chrono::duration<double>(clk::now() - tf).count();
         rep->end_to_end_s = std::chrono::duration<double>(clk::now() - t0).count();
     });
