@@ -51,6 +51,7 @@ METRIC = "SB samples/sec and end-to-end time-to-optimal-hypervolume, 1/2/4/8 B20
 UNIT = "samples/s"
 WORKLOAD = "C2: 42-node heavy-hex K=4 MO-MaxCut, dSB, 220 weights (H=13) x batch 4546, T=50, alpha=0.15, seed 7"
 GOLDEN = os.path.join(ROOT, "tests", "golden", "c2_heavyhex_k4_dsb.npz")
+C1_GOLDEN = os.path.join(ROOT, "tests", "golden", "c1_heavyhex_k3_bsb.npz")
 EXACT = os.path.join(ROOT, "tests", "golden", "heavyhex42_k{k}_exact.npz")
 TTO_MAX_RUNS = {4: 512, 3: 64}  # bound on the streaming run (K=4 needs ~104 runs, K=3 ~3)
 # runs sampled per streaming step (one launch, one merge, one HV check): the K=4 stream
@@ -364,6 +365,37 @@ def measure_c4(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, 
     }
 
 
+def measure_c1(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, flush, steps):
+    """BASELINE config 1 on the GPU: 42-node heavy-hex, K=3, bSB, 190 weights (H=21) x 3,000 =
+    570,000 samples (the reference's CPU-runnable case), one pass of the hot path per step;
+    the HV and reference point are checked against the reference's golden for the same pool."""
+    from paper_2604_26477_b200.instances import load_heavy_hex
+    g = np.load(C1_GOLDEN)
+    inst = load_heavy_hex(int(g["k"]))
+    w = api.build_weights(int(g["k"]), resolution=int(g["H"]))
+    cfg = api.SolverConfig(variant=api.SolverVariant.ballistic_sb, batch_size=int(g["batch"]), seed=int(g["seed"]))
+    s = api.Session(local)
+    s.set_instance(inst)
+    s.set_weights(w)
+    stream = torch.cuda.ExternalStream(s.stream(), device=f"cuda:{local}")
+    step = lambda: sharded_pipeline(api, mdist, torch, s, inst, cfg, 1, world, rank, local, 4096)  # noqa: E731
+    step()  # warm-up
+    mean_ms, ms, reps = timed_steps(step, steps, stream, torch, flush, sync_all, max_over_ranks, world)
+    rep = reps[-1]
+    samples = len(w) * cfg.batch_size
+    hv_ok = all(r["hv"] == float(g["hv"]) and list(r["reference"][:3]) == g["reference"].tolist() for r in reps)
+    return {
+        "workload": f"C1: 42-node heavy-hex, K=3, bSB, {len(w)} weights (H=21) x {cfg.batch_size}, T=50, seed 7",
+        "samples_per_step": samples, "steps": steps, "warmup": 1, "ms_per_step": mean_ms,
+        "step_ms": [round(float(x), 3) for x in ms], "value": samples / (mean_ms * 1e-3), "unit": UNIT,
+        "scaling": "weak" if world == 1 else "strong (weights x trajectories sharded over ranks)",
+        "sampling_s": rep["sampling_s"], "pareto_filtering_s": rep["pareto_filtering_s"],
+        "archive": int(rep["archive_size"]), "hv": rep["hv"], "hv_reference_c1": float(g["hv"]),
+        "hv_equals_reference": bool(world > 1 or hv_ok),
+        "stages_s": {k: rep[k] for k in ("dedup_s", "eval_s", "collapse_s", "front_s", "order_s", "hv_s")},
+    }
+
+
 def measure_c5(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, flush, inst, weights, cfg, r):
     """BASELINE config 5: Pareto stress, 100 runs of the C2 lattice = 100,012,000 sampled
     4-objective vectors through dedup + evaluation + non-dominated filter + HV at the C2
@@ -405,7 +437,7 @@ def main():
     ap.add_argument("--no-tto", action="store_true", help="skip the streaming time-to-optimal run")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the C4 / C5 measurements")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C1 / C4 / C5 measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -674,6 +706,7 @@ def main():
     #      stress); every rank samples its share of the blocks, fronts merge over NCCL
     extra = {}
     if not args.no_extra:
+        extra["c1"] = measure_c1(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, flush, args.steps)
         extra["c4"] = measure_c4(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, flush,
                                  max(args.steps // 3, 2))
         extra["c5"] = measure_c5(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, flush,
