@@ -839,20 +839,6 @@ struct DenseScratch {
     long long bound_inst = -1, bound_weights = -1, bound = 0;  // cached hj_bound
     DevBuf<uint8_t> wk;     // the K weight layers, dense int8, per instance (evaluate_cuts)
     long long wk_gen = -1;
-    cudaStream_t s2 = nullptr;  // second stream (the other half of the pairs)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    cudaStream_t stream2(Ctx& c)
-    {
-        if (!s2) {
-            int lo = 0, hi = 0;
-            ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
-            ck(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi), "stream");
-            ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
-            ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
-        }
-        (void)c;
-        return s2;
-    }
 };
 
 DenseScratch& dscratch(Ctx& c)
@@ -861,9 +847,6 @@ DenseScratch& dscratch(Ctx& c)
         auto* d = static_cast<DenseScratch*>(p);
         d->hj.release(); d->phi.release(); d->D.release(); d->flags.release(); d->x.release(); d->y.release();
         d->pairs.release(); d->wk.release();
-        if (d->s2) cudaStreamDestroy(d->s2);
-        if (d->ev_fork) cudaEventDestroy(d->ev_fork);
-        if (d->ev_join) cudaEventDestroy(d->ev_join);
         delete d;
     });
     return *static_cast<DenseScratch*>(c.dense_scratch.get());
@@ -1002,79 +985,59 @@ void sample_dense(Ctx& c, const SamplerParams& p, long long b0, long long nblock
             // One stream: GEMM(t) then update(t) over all pairs of the group. (Two pair halves on
             // two streams did not overlap: the update kernel fills every SM, so a GEMM CTA of the
             // other half never finds the shared memory it needs.)
-            const int halves = 1;
-            cudaStream_t hs[2] = {c.stream, d.stream2(c)};
-            if (halves == 2) {
-                ck(cudaEventRecord(d.ev_fork, c.stream), "event");
-                ck(cudaStreamWaitEvent(hs[1], d.ev_fork, 0), "event wait");
-            }
-            GemmArgs ga[2];
-            // 8 KB of launch arguments per half, per call (contexts may sample from several host threads)
-            const auto step_args_p = std::make_unique<DenseStepArgs[]>(2);
-            int hb[3] = {0, halves == 2 ? G / 2 : G, G};
-            for (int hh = 0; hh < halves; ++hh) {
-                GemmArgs& g = ga[hh];
-                g.n = n;
-                g.ldp = npad;
-                g.batch_pad = batch_pad;
-                g.ntn = (n + kGN * kG2NT - 1) / (kGN * kG2NT);
-                g.nch = (npad + KC - 1) / KC;
-                g.tiles_per_pair = batch_pad / (kGH * kGM);
-                g.pair_begin = hb[hh];
-                g.items = static_cast<long long>(hb[hh + 1] - hb[hh]) * g.tiles_per_pair * g.ntn;
-                g.pairs = d.pairs.p;
-                DenseStepArgs& sa = step_args_p[hh];
-                sa.n = n;
-                sa.ldp = npad;
-                sa.batch_pad = batch_pad;
-                sa.dt = p.dt;
-                sa.alpha = p.alpha;
-                sa.sdt = p.s_dt_a0;
-                sa.zig = p.zig;
-                sa.D = d.D.p;
-                sa.x = d.x.p;
-                sa.y = d.y.p;
-                sa.phi = d.phi.p;
-                sa.bad = d.flags.p;
-            }
+            GemmArgs g;
+            g.n = n;
+            g.ldp = npad;
+            g.batch_pad = batch_pad;
+            g.ntn = (n + kGN * kG2NT - 1) / (kGN * kG2NT);
+            g.nch = (npad + KC - 1) / KC;
+            g.tiles_per_pair = batch_pad / (kGH * kGM);
+            g.pair_begin = 0;
+            g.items = static_cast<long long>(G) * g.tiles_per_pair * g.ntn;
+            g.pairs = d.pairs.p;
+            // 8 KB of launch arguments, per call (contexts may sample from several host threads)
+            const auto sa_p = std::make_unique<DenseStepArgs>();
+            DenseStepArgs& sa = *sa_p;
+            sa.n = n;
+            sa.ldp = npad;
+            sa.batch_pad = batch_pad;
+            sa.dt = p.dt;
+            sa.alpha = p.alpha;
+            sa.sdt = p.s_dt_a0;
+            sa.zig = p.zig;
+            sa.D = d.D.p;
+            sa.x = d.x.p;
+            sa.y = d.y.p;
+            sa.phi = d.phi.p;
+            sa.bad = d.flags.p;
             const bool udt = p.dt == 1.0 && p.s_dt_a0 == 1.0, noisy = p.alpha > 0.0;
-            for (int t = 0; t < p.T; ++t)
-                for (int hh = 0; hh < halves; ++hh) {
-                    const cudaStream_t st = hs[hh];
-                    const int ggrid = 2 * static_cast<int>(std::min<long long>(ga[hh].items, sms / 2));  // CTA pairs
-                    const int kg = c.ktimer.begin(st);
-                    gemm<<<ggrid, kGThreads, kG2Smem, st>>>(tmA, tmB, tmD, ga[hh]);
-                    c.ktimer.end(kg, kKDenseGemm, st);
+            const cudaStream_t st = c.stream;
+            const int ggrid = 2 * static_cast<int>(std::min<long long>(g.items, sms / 2));  // CTA pairs
+            for (int t = 0; t < p.T; ++t) {
+                const int kg = c.ktimer.begin(st);
+                gemm<<<ggrid, kGThreads, kG2Smem, st>>>(tmA, tmB, tmD, g);
+                c.ktimer.end(kg, kKDenseGemm, st);
+                c.launches++;
+                for (int s0 = 0; s0 < G; s0 += kDensePairsPerLaunch) {
+                    const int np = std::min(kDensePairsPerLaunch, G - s0);
+                    sa.t_step = t;
+                    sa.pair0 = s0;
+                    sa.neg_drift = -(p.a0 - static_cast<double>(t + 1) / static_cast<double>(p.T));
+                    for (int q = 0; q < np; ++q) {
+                        const PairOf& pq = pairs[g0 + s0 + q];
+                        const uint64_t key = run_key(p.seed, static_cast<uint32_t>(pq.run));
+                        sa.pair[q] = {static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32), pq.l, pq.traj0, pq.count, 0,
+                                      c0_host[static_cast<size_t>(pq.l)] / static_cast<double>(c.H)};
+                    }
+                    const dim3 wgrid(static_cast<unsigned>((maxc + kWWarps - 1) / kWWarps), static_cast<unsigned>(np));
+                    const int ku = c.ktimer.begin(st);
+                    if (bf16) checked ? launch_warp<uint16_t, true>(sa, wgrid, st, noisy, udt)
+                                      : launch_warp<uint16_t, false>(sa, wgrid, st, noisy, udt);
+                    else checked ? launch_warp<int8_t, true>(sa, wgrid, st, noisy, udt)
+                                 : launch_warp<int8_t, false>(sa, wgrid, st, noisy, udt);
+                    c.ktimer.end(ku, kKDenseUpdate, st);
                     c.launches++;
-                    if (halves == 2 && t == 0 && hh == 0) {  // half B starts one GEMM later: out of phase
-                        ck(cudaEventRecord(d.ev_fork, st), "event");
-                        ck(cudaStreamWaitEvent(hs[1], d.ev_fork, 0), "event wait");
-                    }
-                    DenseStepArgs& sa = step_args_p[hh];
-                    for (int s0 = hb[hh]; s0 < hb[hh + 1]; s0 += kDensePairsPerLaunch) {
-                        const int np = std::min(kDensePairsPerLaunch, hb[hh + 1] - s0);
-                        sa.t_step = t;
-                        sa.pair0 = s0;
-                        sa.neg_drift = -(p.a0 - static_cast<double>(t + 1) / static_cast<double>(p.T));
-                        for (int q = 0; q < np; ++q) {
-                            const PairOf& pq = pairs[g0 + s0 + q];
-                            const uint64_t key = run_key(p.seed, static_cast<uint32_t>(pq.run));
-                            sa.pair[q] = {static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32), pq.l, pq.traj0, pq.count, 0,
-                                          c0_host[static_cast<size_t>(pq.l)] / static_cast<double>(c.H)};
-                        }
-                        const dim3 wgrid(static_cast<unsigned>((maxc + kWWarps - 1) / kWWarps), static_cast<unsigned>(np));
-                        const int ku = c.ktimer.begin(st);
-                        if (bf16) checked ? launch_warp<uint16_t, true>(sa, wgrid, st, noisy, udt)
-                                          : launch_warp<uint16_t, false>(sa, wgrid, st, noisy, udt);
-                        else checked ? launch_warp<int8_t, true>(sa, wgrid, st, noisy, udt)
-                                     : launch_warp<int8_t, false>(sa, wgrid, st, noisy, udt);
-                        c.ktimer.end(ku, kKDenseUpdate, st);
-                        c.launches++;
-                    }
                 }
-            if (halves == 2) {
-                ck(cudaEventRecord(d.ev_join, hs[1]), "event");
-                ck(cudaStreamWaitEvent(c.stream, d.ev_join, 0), "event wait");
             }
             const dim3 rgrid(static_cast<unsigned>((batch_pad + 127) / 128), static_cast<unsigned>(G));
             k_dense_readout<<<rgrid, 128, 0, c.stream>>>(n, batch_pad, p.batch, L, d.pairs.p, d.x.p, p.words, p.row0, d.flags.p + 1);
