@@ -318,7 +318,10 @@ def measure_c4(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, 
     step = lambda: sharded_pipeline(api, mdist, torch, s, inst, cfg, 1, world, rank, local, 1000)  # noqa: E731
     step()  # warm-up: state buffers, tensor maps
     l0 = s.launches()
-    mean_ms, ms, reps = timed_steps(step, steps, stream, torch, flush, sync_all, max_over_ranks, world)
+    pr = torch.cuda.get_device_properties(local)
+    pci = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+    with ClockSampler(local, pci) as clocks:  # the int8 GEMM + FP64 update run near the power cap
+        mean_ms, ms, reps = timed_steps(step, steps, stream, torch, flush, sync_all, max_over_ranks, world)
     launches = (s.launches() - l0) // steps
     samples = len(w) * C4_BATCH
     rep = reps[-1]
@@ -347,6 +350,7 @@ def measure_c4(api, mdist, torch, local, world, rank, sync_all, max_over_ranks, 
         "step_ms": [round(float(x), 3) for x in ms], "value": samples / (mean_ms * 1e-3), "unit": UNIT,
         "scaling": "weak" if world == 1 else "strong (weights x trajectories sharded over ranks)",
         "sampler_path": s.sampler_path(), "instance_generation_s": t_gen, "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
         "sampling_s": rep["sampling_s"], "pareto_filtering_s": rep["pareto_filtering_s"],
         "archive": int(rep["archive_size"]), "hv": rep["hv"],
         "stages_s": {k: rep[k] for k in ("model_construction_s", "dedup_s", "eval_s", "collapse_s", "front_s",
