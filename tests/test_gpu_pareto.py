@@ -231,3 +231,26 @@ def test_full_size_pipeline_matches_reference_golden(session, case):
     assert np.array_equal(res.archive.configs, g["archive_words"])
     assert res.report["reference"] == g["reference"].tolist()
     assert res.report["hv"] == float(g["hv"])
+
+
+def test_pipeline_order_overlap_joins_on_error():
+    """momc_b200_pipeline orders the archive on a side stream beside the HV. When the HV raises
+    (a fixed reference not dominated by the archive) the order is still joined: the archive
+    read afterwards is the complete ordered one, equal to a plain filter of the same pool, and
+    the context keeps working."""
+    from paper_2604_26477_b200.instances import load_heavy_hex
+    inst = load_heavy_hex(4)
+    w = api.build_weights(4, resolution=13)
+    cfg = api.SolverConfig(variant=api.SolverVariant.discrete_sb, batch_size=300, seed=3)
+    s = api.Session(0)
+    s.set_instance(inst)
+    s.set_weights(w)
+    with pytest.raises(InvalidArgument, match="not dominated by archive entry"):
+        s.pipeline(cfg, 1, 0, s.num_blocks(cfg, 1), fixed_reference=[1e9, 1e9, 1e9, 1e9])
+    got = s.archive()
+    ref = api.Session(0)
+    want = api.non_dominated_filter(api.run_sampler(inst, w, cfg, 1, session=ref), inst, session=ref)
+    assert np.array_equal(got.values, want.values) and np.array_equal(got.configs, want.configs)
+    rep = s.pipeline(cfg, 1, 0, s.num_blocks(cfg, 1))
+    assert rep["hv"] == api.hypervolume(want, rep["reference"], session=ref)
+    assert rep["order_s"] > 0
