@@ -260,8 +260,12 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
 {
     __shared__ ZigTables z;
     __shared__ float zwf[128], zff[128];
-    __shared__ __align__(16) uint32_t rings[kWWarps][kWRing];
-    __shared__ double vals[kWWarps][32];
+    // per warp: the word ring, then the 32-entry value buffer at a fixed offset
+    struct __align__(16) WarpRing {
+        uint32_t words[kWRing];
+        double vals[32];
+    };
+    __shared__ WarpRing rings[kWWarps];
     if constexpr (NOISY) {
         for (int q = threadIdx.x; q < static_cast<int>(sizeof(ZigTables) / 4); q += blockDim.x)
             reinterpret_cast<uint32_t*>(&z)[q] = reinterpret_cast<const uint32_t*>(a.zig)[q];
@@ -276,8 +280,11 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
     const int t = blockIdx.x * kWWarps + warp;
     if (t >= pr.count) return;  // whole warps; no CTA barrier below
     const int n = a.n;
-    const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(rings[warp]));
-    const uint32_t val = static_cast<uint32_t>(__cvta_generic_to_shared(vals[warp]));
+    uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(rings[warp].words));
+    // opaque: the compiler would otherwise rebuild it from the generic window at every use (8 %
+    // of the kernel's instructions)
+    asm volatile("" : "+r"(ring));
+    const uint32_t val = ring + 4u * kWRing;
     auto rw = [&](int p) { return lds32(ring + 4u * static_cast<uint32_t>(p & (kWRing - 1))); };
     const uint32_t k0 = pr.k0, k1 = pr.k1, lo = tag_word(kTagStepNoise, static_cast<uint32_t>(a.t_step));
     const uint32_t mid = static_cast<uint32_t>(pr.traj0 + t), hi = static_cast<uint32_t>(pr.l);
