@@ -258,7 +258,7 @@ struct DenseStepArgs {
 template <bool NOISY, bool UDT, typename PhiT, bool CHECK>
 __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_constant__ DenseStepArgs a)
 {
-    __shared__ ZigTables z;
+    __shared__ __align__(16) ZigTables z;
     __shared__ float zwf[128], zff[128];
     // per warp: the word ring, then the 32-entry value buffer at a fixed offset
     struct __align__(16) WarpRing {
@@ -267,8 +267,9 @@ __global__ void __launch_bounds__(kWWarps * 32, 6) k_dense_warp(const __grid_con
     };
     __shared__ WarpRing rings[kWWarps];
     if constexpr (NOISY) {
-        for (int q = threadIdx.x; q < static_cast<int>(sizeof(ZigTables) / 4); q += blockDim.x)
-            reinterpret_cast<uint32_t*>(&z)[q] = reinterpret_cast<const uint32_t*>(a.zig)[q];
+        static_assert(sizeof(ZigTables) % 16 == 0, "16-byte copies");
+        for (int q = threadIdx.x; q < static_cast<int>(sizeof(ZigTables) / 16); q += blockDim.x)
+            reinterpret_cast<uint4*>(&z)[q] = __ldg(reinterpret_cast<const uint4*>(a.zig) + q);
         for (int q = threadIdx.x; q < 128; q += blockDim.x) {
             zwf[q] = static_cast<float>(a.zig->wn[q]);
             zff[q] = static_cast<float>(a.zig->fn[q]);
